@@ -1,0 +1,320 @@
+"""CPU oracle for the TriMe++ hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import this package.  The
+product path (``paper_2309_13824_b200``) never imports it and shares no code
+with it (see ``oracle/oracle.h``).
+
+Thin ctypes wrapper over ``liboracle.so`` (plain C, built with
+``-O2 -ffp-contract=off``); every arithmetic step lives in ``oracle.c`` and
+cites PAPER.md there.  ``build()`` compiles it on demand.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+_DIR = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_DIR, "liboracle.so")
+_lib = None
+
+CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11", "-fPIC", "-shared"]
+
+
+def build(force: bool = False) -> str:
+    src = os.path.join(_DIR, "oracle.c")
+    hdr = os.path.join(_DIR, "oracle.h")
+    if (not force and os.path.exists(_LIB_PATH)
+            and os.path.getmtime(_LIB_PATH) >= max(os.path.getmtime(src), os.path.getmtime(hdr))):
+        return _LIB_PATH
+    tmp = _LIB_PATH + f".tmp{os.getpid()}"
+    subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, src, "-lm"])
+    os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+class Fields(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32),
+                ("x0", ctypes.c_double), ("y0", ctypes.c_double),
+                ("x1", ctypes.c_double), ("y1", ctypes.c_double),
+                ("phi", ctypes.c_void_p), ("mu", ctypes.c_void_p), ("rho", ctypes.c_void_p)]
+
+
+class Params(ctypes.Structure):
+    _fields_ = [("fac_voro_bound", ctypes.c_double), ("fac_pt_mvmt", ctypes.c_double),
+                ("fac_geps", ctypes.c_double), ("fac_end_mvmt", ctypes.c_double),
+                ("newton_damping", ctypes.c_double), ("newton_max", ctypes.c_int32),
+                ("quad_max_level", ctypes.c_int32), ("fscale", ctypes.c_double),
+                ("dt_k", ctypes.c_double), ("keep_tol", ctypes.c_double)]
+
+
+class Info(ctypes.Structure):
+    _fields_ = [("c", ctypes.c_double), ("h_avg", ctypes.c_double), ("fac_mu", ctypes.c_double),
+                ("sum_l2", ctypes.c_double), ("sum_mu2", ctypes.c_double),
+                ("n_delaunay", ctypes.c_int64), ("n_kept", ctypes.c_int64),
+                ("n_edges", ctypes.c_int64), ("n_degenerate", ctypes.c_int64),
+                ("n_hull", ctypes.c_int64)]
+
+
+def default_params(**kw) -> Params:
+    """Table B.1 defaults plus the L3/L10/L13 readings."""
+    p = Params(fac_voro_bound=5.0, fac_pt_mvmt=0.4, fac_geps=0.01, fac_end_mvmt=0.001,
+               newton_damping=1.0, newton_max=10, quad_max_level=10, fscale=1.2, dt_k=0.2,
+               keep_tol=0.0)
+    for k, v in kw.items():
+        setattr(p, k, v)
+    return p
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB_PATH)
+        D = ctypes.POINTER(ctypes.c_double)
+        L.or_orient2d.restype = ctypes.c_int
+        L.or_orient2d.argtypes = [D, D, D]
+        L.or_orient2d_exact.restype = ctypes.c_int
+        L.or_orient2d_exact.argtypes = [D, D, D]
+        L.or_incircle.restype = ctypes.c_int
+        L.or_incircle.argtypes = [D, D, D, D]
+        L.or_incircle_exact.restype = ctypes.c_int
+        L.or_incircle_exact.argtypes = [D, D, D, D]
+        L.or_delaunay.restype = ctypes.c_int64
+        L.or_delaunay.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                  ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]
+        L.or_field_value.restype = ctypes.c_double
+        L.or_field_value.argtypes = [ctypes.POINTER(Fields), ctypes.c_void_p, ctypes.c_double, ctypes.c_double]
+        L.or_field_grad.restype = None
+        L.or_field_grad.argtypes = [ctypes.POINTER(Fields), ctypes.c_void_p, ctypes.c_double, ctypes.c_double,
+                                    D, D]
+        L.or_domain.restype = None
+        L.or_domain.argtypes = [ctypes.POINTER(Fields), ctypes.c_int64, D, D]
+        L.or_cells.restype = ctypes.c_int64
+        L.or_cells.argtypes = [ctypes.POINTER(Fields), ctypes.POINTER(Params), ctypes.c_int64,
+                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                               ctypes.POINTER(Info)]
+        L.or_iteration.restype = ctypes.c_int
+        L.or_iteration.argtypes = [ctypes.POINTER(Fields), ctypes.POINTER(Params), ctypes.c_int64,
+                                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                   ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
+                                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(Info)]
+        L.or_cvd_polygon.restype = None
+        L.or_cvd_polygon.argtypes = [ctypes.POINTER(Fields), ctypes.POINTER(Params), ctypes.c_int,
+                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_double,
+                                     ctypes.c_double, ctypes.c_double, D, D, ctypes.POINTER(ctypes.c_int)]
+        L.or_distmesh.restype = None
+        L.or_distmesh.argtypes = [ctypes.POINTER(Fields), ctypes.POINTER(Params), ctypes.c_int64,
+                                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, D]
+        L.or_treat.restype = ctypes.c_int
+        L.or_treat.argtypes = [ctypes.POINTER(Fields), ctypes.POINTER(Params), ctypes.c_double,
+                               ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                               ctypes.c_double, D, D, D]
+        L.or_triangle_quality.restype = None
+        L.or_triangle_quality.argtypes = [D, D, D, D, D]
+        L.or_stats.restype = None
+        L.or_stats.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                               ctypes.c_void_p]
+        _lib = L
+    return _lib
+
+
+def _p(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _dptr(v):
+    arr = (ctypes.c_double * len(v))(*[float(t) for t in v])
+    return arr
+
+
+class FieldSet:
+    """Keeps the numpy grids alive while the C struct points into them."""
+
+    def __init__(self, box, phi, mu=None, rho=None):
+        self.phi = np.ascontiguousarray(phi, dtype=np.float64)
+        self.mu = None if mu is None else np.ascontiguousarray(mu, dtype=np.float64)
+        self.rho = None if rho is None else np.ascontiguousarray(rho, dtype=np.float64)
+        ny, nx = self.phi.shape
+        self.c = Fields(nx=nx, ny=ny, x0=box[0], y0=box[1], x1=box[2], y1=box[3],
+                        phi=_p(self.phi), mu=_p(self.mu), rho=_p(self.rho))
+
+    @classmethod
+    def from_config(cls, cfg):
+        return cls(cfg.box, cfg.phi, cfg.mu, cfg.rho)
+
+
+# ------------------------------------------------------------------ predicates
+def orient2d(a, b, c, exact=False) -> int:
+    f = lib().or_orient2d_exact if exact else lib().or_orient2d
+    return int(f(_dptr(a), _dptr(b), _dptr(c)))
+
+
+def incircle(a, b, c, d, exact=False) -> int:
+    f = lib().or_incircle_exact if exact else lib().or_incircle
+    return int(f(_dptr(a), _dptr(b), _dptr(c), _dptr(d)))
+
+
+# ------------------------------------------------------------------ O1
+def delaunay(x, y):
+    """Returns (tri int32 [T,3] CCW min-first, n_degenerate)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    n = x.shape[0]
+    cap = 2 * n + 16
+    tri = np.empty((cap, 3), dtype=np.int32)
+    nd = ctypes.c_int64(0)
+    t = lib().or_delaunay(n, _p(x), _p(y), _p(tri), cap, ctypes.byref(nd))
+    if t < 0:
+        raise RuntimeError("oracle Delaunay failed (n<3, collinear or duplicate points)")
+    return tri[:t].copy(), int(nd.value)
+
+
+# ------------------------------------------------------------------ fields
+def field_value(fs: FieldSet, which: str, x: float, y: float) -> float:
+    return float(lib().or_field_value(ctypes.byref(fs.c), _p(getattr(fs, which)), x, y))
+
+
+def field_grad(fs: FieldSet, which: str, x: float, y: float):
+    gx, gy = ctypes.c_double(), ctypes.c_double()
+    lib().or_field_grad(ctypes.byref(fs.c), _p(getattr(fs, which)), x, y, ctypes.byref(gx), ctypes.byref(gy))
+    return gx.value, gy.value
+
+
+def domain(fs: FieldSet, n_total: int):
+    c, h = ctypes.c_double(), ctypes.c_double()
+    lib().or_domain(ctypes.byref(fs.c), n_total, ctypes.byref(c), ctypes.byref(h))
+    return c.value, h.value
+
+
+# ------------------------------------------------------------------ O2
+@dataclass
+class Cells:
+    start: np.ndarray
+    la: np.ndarray
+    lb: np.ndarray
+    vx: np.ndarray   # relative to the generator
+    vy: np.ndarray
+    info: Info
+
+    def cell(self, i):
+        s, e = self.start[i], self.start[i + 1]
+        return self.la[s:e], self.lb[s:e], self.vx[s:e], self.vy[s:e]
+
+
+def cells(fs: FieldSet, x, y, params: Optional[Params] = None) -> Cells:
+    params = params or default_params()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    n = x.shape[0]
+    cap = 16 * n + 64
+    while True:
+        start = np.empty(n + 1, dtype=np.int64)
+        la = np.empty(cap, dtype=np.int32)
+        lb = np.empty(cap, dtype=np.int32)
+        vx = np.empty(cap, dtype=np.float64)
+        vy = np.empty(cap, dtype=np.float64)
+        info = Info()
+        t = lib().or_cells(ctypes.byref(fs.c), ctypes.byref(params), n, _p(x), _p(y), _p(start), _p(la),
+                           _p(lb), _p(vx), _p(vy), cap, ctypes.byref(info))
+        if t >= 0:
+            return Cells(start, la[:t], lb[:t], vx[:t], vy[:t], info)
+        cap = -t
+
+
+# ------------------------------------------------------------------ one iteration
+@dataclass
+class IterResult:
+    tri: np.ndarray          # kept triangles K [T,3], CCW, min index first
+    edges: np.ndarray        # unique kept edges [E,2] (a<b)
+    x_hat: np.ndarray
+    y_hat: np.ndarray
+    x: np.ndarray
+    y: np.ndarray
+    d_prev: np.ndarray
+    status: np.ndarray
+    counts: Optional[np.ndarray]
+    info: Info
+
+
+def iteration(fs: FieldSet, x, y, mode: str, d_prev=None, params: Optional[Params] = None,
+              counts: bool = False) -> IterResult:
+    """One Delaunay + update + treatment iteration (mode 'cvd' or 'dm')."""
+    params = params or default_params()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    n = x.shape[0]
+    tri_cap = 2 * n + 16
+    tri = np.empty((tri_cap, 3), dtype=np.int32)
+    edges = np.empty((3 * n + 16, 2), dtype=np.int32)
+    xh = np.empty(n)
+    yh = np.empty(n)
+    xo = np.empty(n)
+    yo = np.empty(n)
+    dp = np.empty(n)
+    st = np.empty(n, dtype=np.int8)
+    cnt = np.zeros((n, 6), dtype=np.int64) if counts else None
+    dpi = None if d_prev is None else np.ascontiguousarray(d_prev, dtype=np.float64)
+    info = Info()
+    rc = lib().or_iteration(ctypes.byref(fs.c), ctypes.byref(params), n, _p(x), _p(y), _p(dpi),
+                            0 if mode == "cvd" else 1, _p(tri), tri_cap, _p(edges), edges.shape[0],
+                            _p(xh), _p(yh), _p(xo), _p(yo), _p(dp), _p(st), _p(cnt), ctypes.byref(info))
+    if rc != 0:
+        raise RuntimeError(f"oracle iteration failed rc={rc}")
+    return IterResult(tri[:info.n_kept].copy(), edges[:info.n_edges].copy(), xh, yh, xo, yo, dp, st, cnt, info)
+
+
+# ------------------------------------------------------------------ pieces
+def cvd_polygon(fs: FieldSet, px, py, g, h, d_prev=-1.0, params=None):
+    params = params or default_params()
+    px = np.ascontiguousarray(px, dtype=np.float64)
+    py = np.ascontiguousarray(py, dtype=np.float64)
+    cx, cy, lv = ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
+    lib().or_cvd_polygon(ctypes.byref(fs.c), ctypes.byref(params), px.shape[0], _p(px), _p(py), g[0], g[1],
+                         h, d_prev, ctypes.byref(cx), ctypes.byref(cy), ctypes.byref(lv))
+    return cx.value, cy.value, lv.value
+
+
+def distmesh(fs: FieldSet, x, y, edges, fixed=None, params=None):
+    params = params or default_params()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    e = np.ascontiguousarray(edges, dtype=np.int32)
+    fx = None if fixed is None else np.ascontiguousarray(fixed, dtype=np.uint8)
+    xh = np.empty_like(x)
+    yh = np.empty_like(y)
+    fm = ctypes.c_double()
+    lib().or_distmesh(ctypes.byref(fs.c), ctypes.byref(params), x.shape[0], _p(x), _p(y), e.shape[0], _p(e),
+                      _p(fx), _p(xh), _p(yh), ctypes.byref(fm))
+    return xh, yh, fm.value
+
+
+def treat(fs: FieldSet, c, h_avg, old, new, params=None):
+    params = params or default_params()
+    xn, yn, dp = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    st = lib().or_treat(ctypes.byref(fs.c), ctypes.byref(params), c, h_avg, old[0], old[1], new[0], new[1],
+                        ctypes.byref(xn), ctypes.byref(yn), ctypes.byref(dp))
+    return (xn.value, yn.value), dp.value, int(st)
+
+
+def triangle_quality(a, b, c):
+    al, be = ctypes.c_double(), ctypes.c_double()
+    lib().or_triangle_quality(_dptr(a), _dptr(b), _dptr(c), ctypes.byref(al), ctypes.byref(be))
+    return al.value, be.value
+
+
+def stats(tri, x, y):
+    tri = np.ascontiguousarray(tri, dtype=np.int32)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    out = np.zeros(12)
+    lib().or_stats(tri.shape[0], _p(tri), _p(x), _p(y), _p(out))
+    return out
