@@ -1,0 +1,217 @@
+/*
+ * trime_gpu.h -- C ABI of libtrime_gpu.so, the B200 (sm_100a) hot path of one
+ * TriMe++ meshing iteration (arXiv 2309.13824; PAPER.md cited as P:<line>).
+ *
+ * The paper's problem statement (P:117-119 Procedure 1, Alg. 2,
+ * P:168-195 Alg. 1): points + a signed-distance grid + a sizing/density field
+ * go in; the Delaunay triangles of the current points (obtained from
+ * Voronoi cells built by half-plane clipping) and the updated
+ * points (CVD centroid P:203-207, or DistMesh truss force P:139-164, then the
+ * boundary treatment P:570-605) come out.
+ *
+ * CONVENTIONS (all entry points)
+ *  - Pointers are DEVICE pointers unless annotated "host".  The caller owns
+ *    every I/O buffer; the context owns its scratch, its copies of the grids
+ *    and the sorted state of the last tm_grid_bin (freed by tm_destroy).
+ *  - Every call is stream-ordered on the context's stream and never blocks the
+ *    host, except where annotated "synchronises".  Nothing aborts or exits:
+ *    every function returns a tm_status; tm_last_error() explains the last
+ *    failure.  Asynchronous device-side failures (capacity overflow, duplicate
+ *    or outside points, CUDA faults) are latched in the context and reported
+ *    by the next synchronising call (tm_sync, tm_mesh_stats).
+ *  - Point-indexed outputs are in the CALLER's input order; triangle vertex
+ *    indices are caller indices, or gid[] values when gid was given to
+ *    tm_grid_bin.  The DistMesh ELL adjacency (adj/deg) is the exception: it is
+ *    laid out by the context's sorted slot order and holds sorted slots; use
+ *    tm_adjacency_export() to obtain caller-order rows of caller indices.
+ *  - Call order is a state machine (TM_E_STATE otherwise):
+ *      tm_set_domain -> tm_grid_bin -> { tm_voronoi_delaunay | tm_cvd_step }
+ *      -> [ tm_distmesh_sums -> tm_distmesh_step ] -> [ tm_project_sdf ]
+ *    tm_grid_bin must be repeated whenever the points change.
+ *  - Precision: IEEE binary64 round-to-nearest; decision-relevant arithmetic
+ *    is contraction-free (reading L25); exact incircle decisions
+ *    (floating filter + exact expansion arithmetic).  Inputs must be generic
+ *    (no four cocircular Delaunay points, L12); exact predicate zeros are
+ *    counted in tm_stats.n_degenerate.
+ *  - Threading: a context is bound to one device and one stream and is not
+ *    thread-safe; several contexts may coexist.
+ */
+#ifndef TRIME_GPU_H
+#define TRIME_GPU_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tm_ctx tm_ctx;
+
+typedef enum {
+    TM_OK = 0,
+    TM_E_ARG = 1,        /* NULL pointer, N < 3, grid < 2x2, bad size            */
+    TM_E_CUDA = 2,       /* launch / allocation / asynchronous CUDA failure      */
+    TM_E_CAPACITY = 3,   /* tri_cap, adj_stride or cell vertex capacity exceeded */
+    TM_E_DUPLICATE = 4,  /* two bitwise-equal points (bisector undefined, L26)   */
+    TM_E_OUTSIDE = 5,    /* a point is NaN or outside the closed box B           */
+    TM_E_STATE = 6,      /* call out of the documented order                     */
+    TM_E_DEGENERATE = 7  /* inconsistent cell clip (non-generic input, L12)      */
+} tm_status;
+
+/* Node-centred grids over B = [x0,x1] x [y0,y1], row-major [ny][nx], node k at
+ * x0 + k*(x1-x0)/(nx-1) (L15).  Bilinear lookup with cell index clamped
+ * (SURVEY §8.0).  All three are DEVICE pointers; the context copies them. */
+typedef struct {
+    int32_t nx, ny;
+    double x0, y0, x1, y1;
+    const double *phi;   /* required: signed distance, < 0 inside  */
+    const double *mu;    /* relative sizing mu(x); NULL = uniform   */
+    const double *rho;   /* CVD density rho(x);   NULL = uniform    */
+} tm_fields;
+
+/* Defaults = PAPER.md Table B.1 where the paper gives one. */
+typedef struct {
+    double n_opt;              /* 3.3   P:1077 mean points per bin                      */
+    double fac_voro_bound;     /* 5     P:1116 octagon circumradius S = fac*h (L6)      */
+    double fac_pt_mvmt;        /* 0.4   P:1102 move clamp T_pt = fac*h(p_old)           */
+    double fac_geps;           /* 0.01  P:1104 geps = fac*min(h, h_avg)                 */
+    double fac_end_mvmt;       /* 0.001 P:1100 quadrature error floor                   */
+    double newton_damping;     /* 1                                          */
+    int32_t newton_max;        /* 10                                          */
+    int32_t quad_max_level;    /* 10    L13 (paper silent)                              */
+    double fscale;             /* 1.2   P:147 fac_F                                     */
+    double dt_k;               /* 0.2   L3: Delta t * k (paper silent)                  */
+    double keep_tol;           /* 0.0   L10: keep t iff phi~(centroid) < keep_tol       */
+    int32_t adj_stride;        /* 16    ELL row width for DistMesh                      */
+    int32_t max_cell_vertices; /* 32    cell vertex capacity (one warp lane per vertex) */
+    uint32_t flags;            /* TM_F_* below                                          */
+} tm_params;
+
+#define TM_F_TWO_LEVEL_BINS 0x1u  /* split dense bins into 2^r x 2^r sub-bins (adaptive rho) */
+#define TM_F_COUNT_WORK     0x2u  /* accumulate per-cell work counters (tm_work_counts)       */
+
+/* Mesh quality (alpha = R_circ/(2 R_in), beta = l_max/l_min) and
+ * the health counters of the last iteration. */
+typedef struct {
+    int64_t n_tri, n_alpha_lt_1_2, n_alpha_lt_2;
+    int64_t n_degenerate;   /* exact predicate zeros + inconsistent clips        */
+    int64_t n_fallback;     /* points whose projection failed (status & 2)       */
+    int64_t n_overflow;     /* cells that exceeded the vertex capacity           */
+    double sum_sqrt_alpha, sum_sqrt_beta, max_alpha, max_beta;
+    double sum_alpha, sum_alpha2, sum_beta, sum_beta2;
+} tm_stats;
+
+/* Algorithmic work of the last tm_voronoi_delaunay / tm_cvd_step launch
+ * (only with TM_F_COUNT_WORK).  Sums over cells. */
+typedef struct {
+    int64_t n_cells, n_cert, deg, verts, t_own, quad_tris, ell, candidates, clips, exact_calls;
+} tm_work;
+
+void tm_params_default(tm_params *p);
+
+/* Create a context on `device` that issues all work on `cuda_stream`
+ * (a cudaStream_t; NULL = legacy default stream).  *out receives the handle. */
+tm_status tm_create(int device, void *cuda_stream, const tm_params *p, tm_ctx **out);
+void tm_destroy(tm_ctx *ctx);
+const char *tm_last_error(const tm_ctx *ctx);
+/* host: blocks until the stream is idle, then reports latched device errors. synchronises */
+tm_status tm_sync(tm_ctx *ctx);
+
+/* S0: copy the grids, compute
+ * h(x) = c*mu~(x) with c = sqrt( ∫_{phi~<0} mu~^-2 dA / n_total ) (midpoint
+ * rule over grid cells, row-major sequential sum) and h_avg = mean h over those
+ * cells; size the level-0 bins for n_total points.  c_out/h_avg_out are host
+ * pointers (may be NULL).  synchronises */
+tm_status tm_set_domain(tm_ctx *ctx, const tm_fields *f, int64_t n_total, double *c_out, double *h_avg_out);
+
+/* S1 (container insert P:651-655): counting-sort points into the
+ * uniform bin grid (average occupancy n_opt), splitting dense bins when
+ * TM_F_TWO_LEVEL_BINS.  x,y: n_local caller-order coordinates; the first
+ * n_owned are owned, the rest are ghosts (multi-GPU halo) that are binned but
+ * get no cell.  gid: global ids (NULL = identity).  Points must lie in B
+ * (TM_E_OUTSIDE, latched). */
+tm_status tm_grid_bin(tm_ctx *ctx, const double *x, const double *y, int64_t n_local, int64_t n_owned,
+                      const int32_t *gid);
+
+/* S2+S3: bounded Voronoi cell of every owned point by
+ * nearest-first half-plane clipping of B ∩ Oct_i, then Delaunay extraction:
+ * triangle {i,a,b} (i the smallest id) is written once, CCW with the smallest
+ * id first, iff its circumcentre lies strictly inside B and all three octagons
+ * and phi~(centroid) < keep_tol.  tri: int32[3*tri_cap]; n_tri: device int64
+ * receiving the count (required count on overflow, TM_E_CAPACITY latched).
+ * adj/deg (both or neither): DistMesh ELL rows (sorted-slot layout, width
+ * adj_stride).  If x_out is non-NULL the CVD update is fused (S4a+S5, Alg. 2):
+ * d_prev (caller order, NULL => first iteration, eps_c = fac_pt_mvmt, L13) in,
+ * treated positions x_out/y_out, d_prev_out and status out (caller order;
+ * status 0 accepted, 1 projected, 2 fallback to p_old, +4 move clamped). */
+tm_status tm_voronoi_delaunay(tm_ctx *ctx, int32_t *tri, int64_t tri_cap, int64_t *n_tri,
+                              int32_t *adj, uint8_t *deg,
+                              const double *d_prev, double *x_out, double *y_out,
+                              double *d_prev_out, int8_t *status);
+
+/* S4a alone: density-weighted centroid x_hat of every
+ * owned cell (recomputes the cells of the last tm_grid_bin), caller order. */
+tm_status tm_cvd_step(tm_ctx *ctx, const double *d_prev, double *x_hat, double *y_hat);
+
+/* S4b pass 1 (Eq. size scaling P:150-153, L1-L2): sums2[0] = Σ l_e^2,
+ * sums2[1] = Σ mu~(m_e)^2 over unique kept edges owned by this rank (edge owned
+ * by its smaller-id endpoint), deterministic fixed-order reduction. sums2: device
+ * double[2].  For multi-GPU, all-reduce sums2 before pass 2. */
+tm_status tm_distmesh_sums(tm_ctx *ctx, const int32_t *adj, const uint8_t *deg, double *sums2);
+
+/* S4b pass 2 + S5 (Eqs. spring force, Euler P:141-163): per-point
+ * gather F_i = Σ_a max(l0-l,0)(p_i-p_a)/l with l0 = mu~(m)*fscale*sqrt(s0/s1),
+ * x_hat = p + dt_k*F (p if fixed[i], caller order, NULL = none), then the
+ * treatment as in tm_voronoi_delaunay.  Outputs caller order. */
+tm_status tm_distmesh_step(tm_ctx *ctx, const int32_t *adj, const uint8_t *deg, const double *sums2,
+                           const uint8_t *fixed, const double *d_prev,
+                           double *x_out, double *y_out, double *d_prev_out, int8_t *status);
+
+/* S5 alone (L20-L22): clamp the move to
+ * fac_pt_mvmt*h(p_old), clamp into B, accept if phi~ <= geps, else <= newton_max
+ * gradient-Newton steps q -= phi~ grad/|grad|^2 (clamped into B) until
+ * |phi~| <= geps, else fall back to p_old.  All arrays length n, any order. */
+tm_status tm_project_sdf(tm_ctx *ctx, const double *x_old, const double *y_old, const double *x_hat,
+                         const double *y_hat, int64_t n, double *x_out, double *y_out, double *d_prev_out,
+                         int8_t *status);
+
+/* S6: quality of n_tri triangles (caller indices into x,y) and the
+ * health counters of the last iteration.  out: host.  synchronises */
+tm_status tm_mesh_stats(tm_ctx *ctx, const double *x, const double *y, const int32_t *tri, int64_t n_tri,
+                        tm_stats *out);
+
+/* Copy of the ELL adjacency in caller order with caller ids (tests/export):
+ * adj_out int32[n_owned*adj_stride], deg_out uint8[n_owned] (device). */
+tm_status tm_adjacency_export(tm_ctx *ctx, const int32_t *adj, const uint8_t *deg, int32_t *adj_out,
+                              uint8_t *deg_out);
+
+/* Work counters of the last cell launch (TM_F_COUNT_WORK).  out: host. synchronises */
+tm_status tm_work_counts(tm_ctx *ctx, tm_work *out);
+
+/* ---- S7 multi-GPU strips; the exchange itself is NCCL ------ */
+/* Pack the owned points with x < strip_lo + width into send_lo and those with
+ * x >= strip_hi - width into send_hi, each as SoA segments [x | y | gid] of
+ * capacity cap (doubles, doubles, int32).  Counts go to cnt2 (device int64[2]). */
+tm_status tm_halo_pack(tm_ctx *ctx, const double *x, const double *y, const int32_t *gid, int64_t n_owned,
+                       double strip_lo, double strip_hi, double width, double *send_lo, double *send_hi,
+                       int64_t cap, int64_t *cnt2);
+/* Partition owned points after an update: points with x < strip_lo go to
+ * out_lo, x >= strip_hi to out_hi (SoA [x|y|gid|d_prev] segments of capacity
+ * cap), the rest are compacted in place at the front of x/y/gid/d_prev.
+ * cnt3 (device int64[3]) = kept, to_lo, to_hi. */
+tm_status tm_migrate_pack(tm_ctx *ctx, double *x, double *y, int32_t *gid, double *d_prev, int64_t n_owned,
+                          double strip_lo, double strip_hi, double *out_lo, double *out_hi, int64_t cap,
+                          int64_t *cnt3);
+
+/* ---- host-side predicate hooks (no GPU needed; same code as the kernels) -- */
+/* sign of incircle(a,b,c,d) (>0: d inside circle(a,b,c), a,b,c CCW) by the
+ * kernels' exact expansion arithmetic, and by the kernels' full filtered path */
+int tm_host_incircle_exact(const double *a, const double *b, const double *c, const double *d);
+/* kernels' canonical Cramer vertex and keep-rule arithmetic, for CPU tests */
+void tm_host_cramer(const double *A3, const double *B3, double *xy);
+double tm_host_bilinear(int32_t nx, int32_t ny, double x0, double y0, double x1, double y1, const double *F,
+                        double x, double y);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,272 @@
+"""paper_2309_13824_b200 -- B200-native hot path of TriMe++ iterative meshing.
+
+Thin ctypes binding over ``libtrime_gpu.so`` (``include/trime_gpu.h``): the
+functions below keep the C names and only marshal arguments (torch CUDA
+tensors -> device pointers, the current torch stream -> the context stream).
+Every step of the iteration runs in the library's sm_100a kernels; there is
+no CPU fallback -- importing this package on a machine without the built
+library raises immediately, and calls fail loudly on a non-zero status.
+
+PyTorch supplies device memory, streams and process groups only.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+from . import build as _build
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libtrime_gpu.so")
+
+TM_OK, TM_E_ARG, TM_E_CUDA, TM_E_CAPACITY, TM_E_DUPLICATE, TM_E_OUTSIDE, TM_E_STATE, TM_E_DEGENERATE = range(8)
+STATUS_NAMES = ["TM_OK", "TM_E_ARG", "TM_E_CUDA", "TM_E_CAPACITY", "TM_E_DUPLICATE", "TM_E_OUTSIDE",
+                "TM_E_STATE", "TM_E_DEGENERATE"]
+TM_F_TWO_LEVEL_BINS = 0x1
+TM_F_COUNT_WORK = 0x2
+
+
+class TmError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{STATUS_NAMES[code] if 0 <= code < len(STATUS_NAMES) else code}: {msg}")
+        self.code = code
+
+
+class tm_fields(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32),
+                ("x0", ctypes.c_double), ("y0", ctypes.c_double),
+                ("x1", ctypes.c_double), ("y1", ctypes.c_double),
+                ("phi", ctypes.c_void_p), ("mu", ctypes.c_void_p), ("rho", ctypes.c_void_p)]
+
+
+class tm_params(ctypes.Structure):
+    _fields_ = [("n_opt", ctypes.c_double), ("fac_voro_bound", ctypes.c_double),
+                ("fac_pt_mvmt", ctypes.c_double), ("fac_geps", ctypes.c_double),
+                ("fac_end_mvmt", ctypes.c_double), ("newton_damping", ctypes.c_double),
+                ("newton_max", ctypes.c_int32), ("quad_max_level", ctypes.c_int32),
+                ("fscale", ctypes.c_double), ("dt_k", ctypes.c_double), ("keep_tol", ctypes.c_double),
+                ("adj_stride", ctypes.c_int32), ("max_cell_vertices", ctypes.c_int32),
+                ("flags", ctypes.c_uint32)]
+
+
+class tm_stats(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in ("n_tri", "n_alpha_lt_1_2", "n_alpha_lt_2", "n_degenerate",
+                                              "n_fallback", "n_overflow")] + \
+               [(n, ctypes.c_double) for n in ("sum_sqrt_alpha", "sum_sqrt_beta", "max_alpha", "max_beta",
+                                               "sum_alpha", "sum_alpha2", "sum_beta", "sum_beta2")]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class tm_work(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in ("n_cells", "n_cert", "deg", "verts", "t_own", "quad_tris", "ell",
+                                              "candidates", "clips", "exact_calls")]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+EXPORTED = ["tm_params_default", "tm_create", "tm_destroy", "tm_last_error", "tm_sync", "tm_set_domain",
+            "tm_grid_bin", "tm_voronoi_delaunay", "tm_cvd_step", "tm_distmesh_sums", "tm_distmesh_step",
+            "tm_project_sdf", "tm_mesh_stats", "tm_adjacency_export", "tm_work_counts", "tm_halo_pack",
+            "tm_migrate_pack", "tm_host_incircle_exact", "tm_host_cramer", "tm_host_bilinear"]
+
+
+def load_library(path: str = LIB_PATH, build_if_missing: bool = True):
+    """Load libtrime_gpu.so (building it with nvcc if absent and allowed)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        if not build_if_missing:
+            raise ImportError(f"{path} missing: run `python -m paper_2309_13824_b200.build`")
+        _build.build()
+    L = ctypes.CDLL(path)
+    vp, i64, i32, dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double
+    st = ctypes.c_int
+    sig = {
+        "tm_params_default": (None, [ctypes.POINTER(tm_params)]),
+        "tm_create": (st, [ctypes.c_int, vp, ctypes.POINTER(tm_params), ctypes.POINTER(vp)]),
+        "tm_destroy": (None, [vp]),
+        "tm_last_error": (ctypes.c_char_p, [vp]),
+        "tm_sync": (st, [vp]),
+        "tm_set_domain": (st, [vp, ctypes.POINTER(tm_fields), i64, ctypes.POINTER(dbl), ctypes.POINTER(dbl)]),
+        "tm_grid_bin": (st, [vp, vp, vp, i64, i64, vp]),
+        "tm_voronoi_delaunay": (st, [vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp]),
+        "tm_cvd_step": (st, [vp, vp, vp, vp]),
+        "tm_distmesh_sums": (st, [vp, vp, vp, vp]),
+        "tm_distmesh_step": (st, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+        "tm_project_sdf": (st, [vp, vp, vp, vp, vp, i64, vp, vp, vp, vp]),
+        "tm_mesh_stats": (st, [vp, vp, vp, vp, i64, ctypes.POINTER(tm_stats)]),
+        "tm_adjacency_export": (st, [vp, vp, vp, vp, vp]),
+        "tm_work_counts": (st, [vp, ctypes.POINTER(tm_work)]),
+        "tm_halo_pack": (st, [vp, vp, vp, vp, i64, dbl, dbl, dbl, vp, vp, i64, vp]),
+        "tm_migrate_pack": (st, [vp, vp, vp, vp, vp, i64, dbl, dbl, vp, vp, i64, vp]),
+        "tm_host_incircle_exact": (ctypes.c_int, [vp, vp, vp, vp]),
+        "tm_host_cramer": (None, [vp, vp, vp]),
+        "tm_host_bilinear": (dbl, [i32, i32, dbl, dbl, dbl, dbl, vp, dbl, dbl]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise TmError(TM_E_ARG, "tensor must live on a CUDA device (no CPU fallback)")
+    if not t.is_contiguous():
+        raise TmError(TM_E_ARG, "tensor must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def default_params(**kw) -> tm_params:
+    p = tm_params()
+    load_library().tm_params_default(ctypes.byref(p))
+    for k, v in kw.items():
+        setattr(p, k, v)
+    return p
+
+
+class Context:
+    """One tm_ctx bound to a CUDA device and a torch stream."""
+
+    def __init__(self, device: int = 0, stream: Optional[torch.cuda.Stream] = None,
+                 params: Optional[tm_params] = None):
+        if not torch.cuda.is_available():
+            raise TmError(TM_E_CUDA, "no CUDA device: the TriMe++ B200 path has no CPU fallback")
+        self.L = load_library()
+        self.device = device
+        self.stream = stream or torch.cuda.current_stream(device)
+        self.params = params or default_params()
+        h = ctypes.c_void_p()
+        rc = self.L.tm_create(device, ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(self.params),
+                              ctypes.byref(h))
+        if rc != TM_OK:
+            raise TmError(rc, "tm_create failed")
+        self.h = h
+        self.c = None
+        self.h_avg = None
+        self._fields_keepalive = None
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.tm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc != TM_OK:
+            msg = self.L.tm_last_error(self.h)
+            raise TmError(rc, msg.decode() if msg else "")
+
+    # ---------------------------------------------------------------- C names
+    def tm_sync(self):
+        self._check(self.L.tm_sync(self.h))
+
+    def tm_set_domain(self, box, phi: torch.Tensor, mu=None, rho=None, n_total: int = 0):
+        ny, nx = phi.shape
+        f = tm_fields(nx=nx, ny=ny, x0=box[0], y0=box[1], x1=box[2], y1=box[3],
+                      phi=_ptr(phi), mu=_ptr(mu), rho=_ptr(rho))
+        c, ha = ctypes.c_double(), ctypes.c_double()
+        self._check(self.L.tm_set_domain(self.h, ctypes.byref(f), int(n_total), ctypes.byref(c), ctypes.byref(ha)))
+        self.c, self.h_avg = c.value, ha.value
+        return self.c, self.h_avg
+
+    def tm_grid_bin(self, x, y, n_owned: Optional[int] = None, gid=None):
+        n = x.shape[0]
+        self._check(self.L.tm_grid_bin(self.h, _ptr(x), _ptr(y), n, n if n_owned is None else n_owned, _ptr(gid)))
+
+    def tm_voronoi_delaunay(self, tri, n_tri, adj=None, deg=None, d_prev=None, x_out=None, y_out=None,
+                            d_prev_out=None, status=None):
+        self._check(self.L.tm_voronoi_delaunay(self.h, _ptr(tri), tri.shape[0], _ptr(n_tri), _ptr(adj), _ptr(deg),
+                                               _ptr(d_prev), _ptr(x_out), _ptr(y_out), _ptr(d_prev_out),
+                                               _ptr(status)))
+
+    def tm_cvd_step(self, d_prev, x_hat, y_hat):
+        self._check(self.L.tm_cvd_step(self.h, _ptr(d_prev), _ptr(x_hat), _ptr(y_hat)))
+
+    def tm_distmesh_sums(self, adj, deg, sums2):
+        self._check(self.L.tm_distmesh_sums(self.h, _ptr(adj), _ptr(deg), _ptr(sums2)))
+
+    def tm_distmesh_step(self, adj, deg, sums2, fixed, d_prev, x_out, y_out, d_prev_out, status):
+        self._check(self.L.tm_distmesh_step(self.h, _ptr(adj), _ptr(deg), _ptr(sums2), _ptr(fixed), _ptr(d_prev),
+                                            _ptr(x_out), _ptr(y_out), _ptr(d_prev_out), _ptr(status)))
+
+    def tm_project_sdf(self, x_old, y_old, x_hat, y_hat, x_out, y_out, d_prev_out, status):
+        self._check(self.L.tm_project_sdf(self.h, _ptr(x_old), _ptr(y_old), _ptr(x_hat), _ptr(y_hat),
+                                          x_old.shape[0], _ptr(x_out), _ptr(y_out), _ptr(d_prev_out), _ptr(status)))
+
+    def tm_mesh_stats(self, x, y, tri, n_tri: int) -> tm_stats:
+        s = tm_stats()
+        self._check(self.L.tm_mesh_stats(self.h, _ptr(x), _ptr(y), _ptr(tri), int(n_tri), ctypes.byref(s)))
+        return s
+
+    def tm_adjacency_export(self, adj, deg, adj_out, deg_out):
+        self._check(self.L.tm_adjacency_export(self.h, _ptr(adj), _ptr(deg), _ptr(adj_out), _ptr(deg_out)))
+
+    def tm_work_counts(self) -> tm_work:
+        w = tm_work()
+        self._check(self.L.tm_work_counts(self.h, ctypes.byref(w)))
+        return w
+
+    def tm_halo_pack(self, x, y, gid, n_owned, lo, hi, width, send_lo, send_hi, cap, cnt2):
+        self._check(self.L.tm_halo_pack(self.h, _ptr(x), _ptr(y), _ptr(gid), int(n_owned), lo, hi, width,
+                                        _ptr(send_lo), _ptr(send_hi), int(cap), _ptr(cnt2)))
+
+    def tm_migrate_pack(self, x, y, gid, d_prev, n_owned, lo, hi, out_lo, out_hi, cap, cnt3):
+        self._check(self.L.tm_migrate_pack(self.h, _ptr(x), _ptr(y), _ptr(gid), _ptr(d_prev), int(n_owned), lo, hi,
+                                           _ptr(out_lo), _ptr(out_hi), int(cap), _ptr(cnt3)))
+
+
+# ------------------------------------------------------------------ driver
+@dataclass
+class IterBuffers:
+    """Device buffers for one iteration on n points (allocated once)."""
+    n: int
+    tri: torch.Tensor
+    n_tri: torch.Tensor
+    adj: torch.Tensor
+    deg: torch.Tensor
+    sums2: torch.Tensor
+    status: torch.Tensor
+
+    @classmethod
+    def alloc(cls, n: int, adj_stride: int = 16, device="cuda"):
+        return cls(n=n,
+                   tri=torch.empty((2 * n + 64, 3), dtype=torch.int32, device=device),
+                   n_tri=torch.zeros(1, dtype=torch.int64, device=device),
+                   adj=torch.empty((adj_stride, n), dtype=torch.int32, device=device),
+                   deg=torch.empty(n, dtype=torch.uint8, device=device),
+                   sums2=torch.empty(2, dtype=torch.float64, device=device),
+                   status=torch.empty(n, dtype=torch.int8, device=device))
+
+
+def iterate(ctx: Context, x, y, d_prev, mode: str, bufs: IterBuffers, x_out, y_out, d_prev_out):
+    """One TriMe++ iteration (Procedure 1 + Alg. 2 or Alg. 1 with retriangulation
+    every iteration, L5) on device tensors; all work is issued to ctx.stream.
+    Returns nothing; triangles are in bufs.tri[:bufs.n_tri]."""
+    ctx.tm_grid_bin(x, y)
+    if mode == "cvd":
+        ctx.tm_voronoi_delaunay(bufs.tri, bufs.n_tri, None, None, d_prev, x_out, y_out, d_prev_out, bufs.status)
+    elif mode == "dm":
+        ctx.tm_voronoi_delaunay(bufs.tri, bufs.n_tri, bufs.adj, bufs.deg)
+        ctx.tm_distmesh_sums(bufs.adj, bufs.deg, bufs.sums2)
+        ctx.tm_distmesh_step(bufs.adj, bufs.deg, bufs.sums2, None, d_prev, x_out, y_out, d_prev_out, bufs.status)
+    else:
+        raise ValueError(mode)

@@ -1,0 +1,646 @@
+// tm_api.cu -- context, S0 domain, S1 binning, S5 standalone treatment, S6
+// statistics, S7 halo/migration packing and host-side hooks of libtrime_gpu.so.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdlib.h>
+
+#include <new>
+
+#include "tm_internal.cuh"
+
+using namespace tmg;
+
+// ============================================================================ params / ctx
+extern "C" void tm_params_default(tm_params *p) {
+    p->n_opt = 3.3;
+    p->fac_voro_bound = 5.0;
+    p->fac_pt_mvmt = 0.4;
+    p->fac_geps = 0.01;
+    p->fac_end_mvmt = 0.001;
+    p->newton_damping = 1.0;
+    p->newton_max = 10;
+    p->quad_max_level = 10;    // L13
+    p->fscale = 1.2;
+    p->dt_k = 0.2;             // L3
+    p->keep_tol = 0.0;         // L10
+    p->adj_stride = 16;
+    p->max_cell_vertices = 32;
+    p->flags = 0;
+}
+
+extern "C" tm_status tm_create(int device, void *cuda_stream, const tm_params *p, tm_ctx **out) {
+    if (!out) return TM_E_ARG;
+    *out = nullptr;
+    tm_ctx *ctx = new (std::nothrow) tm_ctx();
+    if (!ctx) return TM_E_ARG;
+    ctx->device = device;
+    ctx->stream = (cudaStream_t)cuda_stream;
+    if (p)
+        ctx->p = *p;
+    else
+        tm_params_default(&ctx->p);
+    if (ctx->p.max_cell_vertices != 32 || ctx->p.adj_stride < 1 || ctx->p.adj_stride > 255 ||
+        ctx->p.quad_max_level < 1 || ctx->p.quad_max_level > 20 || ctx->p.newton_max < 0) {
+        delete ctx;
+        return TM_E_ARG;
+    }
+    if (cudaSetDevice(device) != cudaSuccess || cudaMalloc(&ctx->dst, sizeof(DevState)) != cudaSuccess ||
+        cudaMalloc(&ctx->stat_acc, 16 * sizeof(double)) != cudaSuccess ||
+        cudaMemsetAsync(ctx->dst, 0, sizeof(DevState), ctx->stream) != cudaSuccess) {
+        cudaGetLastError();
+        delete ctx;
+        return TM_E_CUDA;
+    }
+    *out = ctx;
+    return TM_OK;
+}
+
+static void free_points(tm_ctx *c) {
+    cudaFree(c->xs); cudaFree(c->ys); cudaFree(c->hs);
+    cudaFree(c->perm); cudaFree(c->gids); cudaFree(c->key); cudaFree(c->rank);
+    c->xs = c->ys = c->hs = nullptr;
+    c->perm = c->gids = c->key = c->rank = nullptr;
+    c->cap_points = 0;
+}
+
+extern "C" void tm_destroy(tm_ctx *ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    free_points(ctx);
+    cudaFree(ctx->bin_count); cudaFree(ctx->bin_start); cudaFree(ctx->block_sums);
+    cudaFree(ctx->phi); cudaFree(ctx->mu); cudaFree(ctx->rho);
+    cudaFree(ctx->partials); cudaFree(ctx->stat_acc); cudaFree(ctx->dst);
+    delete ctx;
+}
+
+extern "C" const char *tm_last_error(const tm_ctx *ctx) { return ctx ? ctx->err : "null context"; }
+
+tm_status tm_internal_check_launch(tm_ctx *ctx, const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) TM_FAIL(ctx, TM_E_CUDA, "%s: launch failed: %s", what, cudaGetErrorString(e));
+    return TM_OK;
+}
+
+extern "C" tm_status tm_sync(tm_ctx *ctx) {
+    if (!ctx) return TM_E_ARG;
+    TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    TM_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    DevState s;
+    TM_CUDA_TRY(ctx, cudaMemcpy(&s, ctx->dst, sizeof(s), cudaMemcpyDeviceToHost));
+    if (s.n_outside) TM_FAIL(ctx, TM_E_OUTSIDE, "%llu point(s) are NaN or outside the box B", s.n_outside);
+    if (s.n_duplicate) TM_FAIL(ctx, TM_E_DUPLICATE, "%llu bitwise-duplicate point pair(s)", s.n_duplicate);
+    if (s.n_overflow)
+        TM_FAIL(ctx, TM_E_CAPACITY, "%llu cell(s) exceeded the %d-vertex capacity", s.n_overflow,
+                ctx->p.max_cell_vertices);
+    if (s.n_tri_overflow) TM_FAIL(ctx, TM_E_CAPACITY, "triangle buffer too small (tri_cap)");
+    if (s.n_adj_overflow) TM_FAIL(ctx, TM_E_CAPACITY, "ELL row wider than adj_stride=%d", ctx->p.adj_stride);
+    return TM_OK;
+}
+
+// ============================================================================ S0
+// c and h_avg by a deterministic sequential sum in row-major cell order
+// (identical operation order to the oracle's definition, §8.0 "Local size").
+__global__ void k_domain_sums(Grid g, const double *phi, const double *mu, double *out3) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double sum_w = 0.0, sum_mu = 0.0, cnt = 0.0;
+    for (int j = 0; j < g.ny - 1; j++) {
+        const double *p0 = phi + (int64_t)j * g.nx, *p1 = p0 + g.nx;
+        for (int i = 0; i < g.nx - 1; i++) {
+            double ph = clerp(clerp(p0[i], p0[i + 1], 0.5), clerp(p1[i], p1[i + 1], 0.5), 0.5);
+            if (!(ph < 0.0)) continue;
+            double m = 1.0;
+            if (mu) {
+                const double *m0 = mu + (int64_t)j * g.nx, *m1 = m0 + g.nx;
+                m = clerp(clerp(m0[i], m0[i + 1], 0.5), clerp(m1[i], m1[i + 1], 0.5), 0.5);
+            }
+            sum_w = cadd(sum_w, cdiv(1.0, cmul(m, m)));
+            sum_mu = cadd(sum_mu, m);
+            cnt += 1.0;
+        }
+    }
+    out3[0] = sum_w;
+    out3[1] = sum_mu;
+    out3[2] = cnt;
+}
+
+extern "C" tm_status tm_set_domain(tm_ctx *ctx, const tm_fields *f, int64_t n_total, double *c_out,
+                                   double *h_avg_out) {
+    if (!ctx || !f || !f->phi) return ctx ? (snprintf(ctx->err, sizeof(ctx->err), "null argument"), TM_E_ARG) : TM_E_ARG;
+    if (f->nx < 2 || f->ny < 2 || !(f->x1 > f->x0) || !(f->y1 > f->y0) || n_total < 1)
+        TM_FAIL(ctx, TM_E_ARG, "bad domain: grid %dx%d, box [%g,%g]x[%g,%g], n_total %lld", f->nx, f->ny, f->x0,
+                f->x1, f->y0, f->y1, (long long)n_total);
+    TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    size_t nb = (size_t)f->nx * f->ny * sizeof(double);
+    if (nb != ctx->grid_bytes) {
+        cudaFree(ctx->phi); cudaFree(ctx->mu); cudaFree(ctx->rho);
+        ctx->phi = ctx->mu = ctx->rho = nullptr;
+        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->phi, nb));
+        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->mu, nb));
+        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->rho, nb));
+        ctx->grid_bytes = nb;
+    }
+    TM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->phi, f->phi, nb, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (f->mu) TM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->mu, f->mu, nb, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (f->rho) TM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->rho, f->rho, nb, cudaMemcpyDeviceToDevice, ctx->stream));
+    Grid g;
+    g.nx = f->nx; g.ny = f->ny;
+    g.x0 = f->x0; g.y0 = f->y0; g.x1 = f->x1; g.y1 = f->y1;
+    g.idx = cdiv((double)(f->nx - 1), csub(f->x1, f->x0));
+    g.idy = cdiv((double)(f->ny - 1), csub(f->y1, f->y0));
+    g.dx = cdiv(csub(f->x1, f->x0), (double)(f->nx - 1));
+    g.dy = cdiv(csub(f->y1, f->y0), (double)(f->ny - 1));
+    ctx->grid = g;
+    bool has_mu = f->mu != nullptr, has_rho = f->rho != nullptr;
+    double *d3;
+    TM_CUDA_TRY(ctx, cudaMalloc(&d3, 3 * sizeof(double)));
+    k_domain_sums<<<1, 1, 0, ctx->stream>>>(g, ctx->phi, has_mu ? ctx->mu : nullptr, d3);
+    tm_status s = tm_internal_check_launch(ctx, "k_domain_sums");
+    if (s != TM_OK) { cudaFree(d3); return s; }
+    double h3[3];
+    cudaError_t e = cudaMemcpyAsync(h3, d3, sizeof(h3), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(d3);
+    if (e != cudaSuccess) TM_FAIL(ctx, TM_E_CUDA, "set_domain: %s", cudaGetErrorString(e));
+    if (!(h3[2] > 0)) TM_FAIL(ctx, TM_E_ARG, "the SDF grid has no cell with phi < 0");
+    // c = sqrt( sum_w * (dx*dy) / N ),  h_avg = c * (sum_mu / count)   (same order as the definition)
+    ctx->c = sqrt(cdiv(cmul(h3[0], cmul(g.dx, g.dy)), (double)n_total));
+    ctx->h_avg = cmul(ctx->c, cdiv(h3[1], h3[2]));
+    if (!has_mu) { cudaFree(ctx->mu); ctx->mu = nullptr; ctx->grid_bytes = 0; }
+    if (!has_rho) { cudaFree(ctx->rho); ctx->rho = nullptr; ctx->grid_bytes = 0; }
+    ctx->n_total = n_total;
+    // level-0 bins: N_opt points per bin on average (P:343 without fac_grid; Listing P:651-654)
+    double Lx = f->x1 - f->x0, Ly = f->y1 - f->y0;
+    double lam = sqrt((double)n_total / (ctx->p.n_opt * Lx * Ly));
+    int32_t nbx = (int32_t)ceil(lam * Lx), nby = (int32_t)ceil(lam * Ly);
+    if (nbx < 1) nbx = 1;
+    if (nby < 1) nby = 1;
+    ctx->bg.nbx = nbx; ctx->bg.nby = nby;
+    ctx->bg.x0 = f->x0; ctx->bg.y0 = f->y0;
+    ctx->bg.sx = Lx / nbx; ctx->bg.sy = Ly / nby;
+    ctx->bg.isx = nbx / Lx; ctx->bg.isy = nby / Ly;
+    ctx->have_domain = true;
+    ctx->have_bins = false;
+    ctx->have_cells = false;
+    if (c_out) *c_out = ctx->c;
+    if (h_avg_out) *h_avg_out = ctx->h_avg;
+    return TM_OK;
+}
+
+// ============================================================================ S1
+__global__ void k_bin_keys(const double *__restrict__ x, const double *__restrict__ y, int64_t n, BinGeom bg,
+                           double bx0, double by0, double bx1, double by1, int32_t *__restrict__ key,
+                           int32_t *__restrict__ rank, int32_t *__restrict__ count, DevState *st) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double px = x[i], py = y[i];
+    if (!(px >= bx0 && px <= bx1 && py >= by0 && py <= by1)) {
+        atomicAdd(&st->n_outside, 1ull);
+        px = fmin(fmax(px == px ? px : bx0, bx0), bx1);
+        py = fmin(fmax(py == py ? py : by0, by0), by1);
+    }
+    int bx = (int)floor((px - bg.x0) * bg.isx), by = (int)floor((py - bg.y0) * bg.isy);
+    bx = bx < 0 ? 0 : (bx >= bg.nbx ? bg.nbx - 1 : bx);
+    by = by < 0 ? 0 : (by >= bg.nby ? bg.nby - 1 : by);
+    int32_t k = by * bg.nbx + bx;
+    key[i] = k;
+    rank[i] = atomicAdd(&count[k], 1);
+}
+
+// exclusive scan: per-block (1024 threads x 4 items)
+constexpr int SCAN_T = 1024, SCAN_ITEMS = 4, SCAN_TILE = SCAN_T * SCAN_ITEMS;
+
+__device__ __forceinline__ int32_t block_exclusive_scan(int32_t v, int32_t *smem_warp, int32_t &total) {
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) smem_warp[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        int32_t s = lane < (int)(blockDim.x >> 5) ? smem_warp[lane] : 0;
+        int32_t si = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int32_t t = __shfl_up_sync(0xffffffffu, si, o);
+            if (lane >= o) si += t;
+        }
+        smem_warp[lane] = si - s;
+        if (lane == 31) smem_warp[32] = si;
+    }
+    __syncthreads();
+    total = smem_warp[32];
+    int32_t r = smem_warp[w] + incl - v;
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(SCAN_T) k_scan_tiles(const int32_t *__restrict__ in, int32_t *__restrict__ out,
+                                                       int32_t *__restrict__ tile_sums, int64_t n) {
+    __shared__ int32_t sw[33];
+    int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+    int32_t v[SCAN_ITEMS], s = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; k++) {
+        v[k] = (base + k < n) ? in[base + k] : 0;
+        s += v[k];
+    }
+    int32_t total;
+    int32_t ex = block_exclusive_scan(s, sw, total);
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; k++) {
+        if (base + k < n) out[base + k] = ex;
+        ex += v[k];
+    }
+    if (threadIdx.x == 0) tile_sums[blockIdx.x] = total;
+}
+
+// single block: exclusive scan of tile sums in place, grand total to *total_out
+__global__ void __launch_bounds__(SCAN_T) k_scan_top(int32_t *tile_sums, int64_t ntiles, int32_t *total_out) {
+    __shared__ int32_t sw[33];
+    int32_t carry = 0;
+    for (int64_t b0 = 0; b0 < ntiles; b0 += SCAN_T) {
+        int64_t i = b0 + threadIdx.x;
+        int32_t v = i < ntiles ? tile_sums[i] : 0;
+        int32_t total;
+        int32_t ex = block_exclusive_scan(v, sw, total);
+        if (i < ntiles) tile_sums[i] = ex + carry;
+        carry += total;
+    }
+    if (threadIdx.x == 0) *total_out = carry;
+}
+
+__global__ void k_scan_add(int32_t *out, const int32_t *tile_sums, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    out[i] += tile_sums[i / SCAN_TILE];
+}
+
+__global__ void k_bin_scatter(const double *__restrict__ x, const double *__restrict__ y,
+                              const int32_t *__restrict__ gid, int64_t n, const int32_t *__restrict__ key,
+                              const int32_t *__restrict__ rank, const int32_t *__restrict__ start,
+                              double bx0, double by0, double bx1, double by1, Grid g,
+                              const double *__restrict__ mu, double c, double *__restrict__ xs,
+                              double *__restrict__ ys, double *__restrict__ hs, int32_t *__restrict__ perm,
+                              int32_t *__restrict__ gids) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int64_t s = (int64_t)start[key[i]] + rank[i];
+    double px = x[i], py = y[i];
+    px = fmin(fmax(px == px ? px : bx0, bx0), bx1);
+    py = fmin(fmax(py == py ? py : by0, by0), by1);
+    xs[s] = px;
+    ys[s] = py;
+    // h(p) = c * mu~(p)   (§8.0 "Local size")
+    hs[s] = mu ? cmul(c, bilinear(g, mu, px, py, LdgLoad())) : c;
+    perm[s] = (int32_t)i;
+    gids[s] = gid ? gid[i] : (int32_t)i;
+}
+
+static tm_status ensure_points(tm_ctx *ctx, int64_t n) {
+    if (n <= ctx->cap_points) return TM_OK;
+    free_points(ctx);
+    int64_t cap = n + n / 8 + 1024;
+    TM_CUDA_TRY(ctx, cudaMalloc(&ctx->xs, cap * sizeof(double)));
+    TM_CUDA_TRY(ctx, cudaMalloc(&ctx->ys, cap * sizeof(double)));
+    TM_CUDA_TRY(ctx, cudaMalloc(&ctx->hs, cap * sizeof(double)));
+    TM_CUDA_TRY(ctx, cudaMalloc(&ctx->perm, cap * sizeof(int32_t)));
+    TM_CUDA_TRY(ctx, cudaMalloc(&ctx->gids, cap * sizeof(int32_t)));
+    TM_CUDA_TRY(ctx, cudaMalloc(&ctx->key, cap * sizeof(int32_t)));
+    TM_CUDA_TRY(ctx, cudaMalloc(&ctx->rank, cap * sizeof(int32_t)));
+    ctx->cap_points = cap;
+    return TM_OK;
+}
+
+static tm_status ensure_bins(tm_ctx *ctx, int64_t nb) {
+    int64_t ntiles = (nb + SCAN_TILE - 1) / SCAN_TILE;
+    if (nb + 1 > ctx->cap_bins) {
+        cudaFree(ctx->bin_count); cudaFree(ctx->bin_start);
+        ctx->bin_count = ctx->bin_start = nullptr;
+        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->bin_count, (nb + 1) * sizeof(int32_t)));
+        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->bin_start, (nb + 1) * sizeof(int32_t)));
+        ctx->cap_bins = nb + 1;
+    }
+    if (ntiles > ctx->cap_block_sums) {
+        cudaFree(ctx->block_sums);
+        ctx->block_sums = nullptr;
+        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->block_sums, ntiles * sizeof(int32_t)));
+        ctx->cap_block_sums = ntiles;
+    }
+    return TM_OK;
+}
+
+// exclusive scan of n int32 values into out[0..n], out[n] = total
+static tm_status scan_counts(tm_ctx *ctx, const int32_t *in, int32_t *out, int64_t n) {
+    int64_t ntiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+    k_scan_tiles<<<(unsigned)ntiles, SCAN_T, 0, ctx->stream>>>(in, out, ctx->block_sums, n);
+    k_scan_top<<<1, SCAN_T, 0, ctx->stream>>>(ctx->block_sums, ntiles, out + n);
+    k_scan_add<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(out, ctx->block_sums, n);
+    return tm_internal_check_launch(ctx, "scan");
+}
+
+extern "C" tm_status tm_grid_bin(tm_ctx *ctx, const double *x, const double *y, int64_t n_local, int64_t n_owned,
+                                 const int32_t *gid) {
+    if (!ctx) return TM_E_ARG;
+    if (!ctx->have_domain) TM_FAIL(ctx, TM_E_STATE, "tm_grid_bin before tm_set_domain");
+    if (!x || !y) TM_FAIL(ctx, TM_E_ARG, "null x/y");
+    if (n_local < 3 || n_owned < 1 || n_owned > n_local || n_local >= (int64_t)INT32_MAX)
+        TM_FAIL(ctx, TM_E_ARG, "bad sizes n_local=%lld n_owned=%lld", (long long)n_local, (long long)n_owned);
+    TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    tm_status s = ensure_points(ctx, n_local);
+    if (s != TM_OK) return s;
+    int64_t nb = (int64_t)ctx->bg.nbx * ctx->bg.nby;
+    if ((s = ensure_bins(ctx, nb)) != TM_OK) return s;
+    TM_CUDA_TRY(ctx, cudaMemsetAsync(ctx->bin_count, 0, nb * sizeof(int32_t), ctx->stream));
+    const Grid &g = ctx->grid;
+    unsigned blocks = (unsigned)((n_local + 255) / 256);
+    k_bin_keys<<<blocks, 256, 0, ctx->stream>>>(x, y, n_local, ctx->bg, g.x0, g.y0, g.x1, g.y1, ctx->key,
+                                                ctx->rank, ctx->bin_count, ctx->dst);
+    if ((s = tm_internal_check_launch(ctx, "k_bin_keys")) != TM_OK) return s;
+    if ((s = scan_counts(ctx, ctx->bin_count, ctx->bin_start, nb)) != TM_OK) return s;
+    k_bin_scatter<<<blocks, 256, 0, ctx->stream>>>(x, y, gid, n_local, ctx->key, ctx->rank, ctx->bin_start, g.x0,
+                                                   g.y0, g.x1, g.y1, g, ctx->mu, ctx->c, ctx->xs, ctx->ys,
+                                                   ctx->hs, ctx->perm, ctx->gids);
+    if ((s = tm_internal_check_launch(ctx, "k_bin_scatter")) != TM_OK) return s;
+    ctx->n_local = n_local;
+    ctx->n_owned = n_owned;
+    ctx->have_bins = true;
+    ctx->have_cells = false;
+    return TM_OK;
+}
+
+tm_status tm_internal_fill_cell_args(tm_ctx *ctx, CellArgs *a) {
+    memset(a, 0, sizeof(*a));
+    a->xs = ctx->xs; a->ys = ctx->ys; a->hs = ctx->hs;
+    a->perm = ctx->perm; a->gids = ctx->gids; a->bin_start = ctx->bin_start;
+    a->bg = ctx->bg;
+    a->n_local = ctx->n_local; a->n_owned = ctx->n_owned;
+    a->grid = ctx->grid;
+    a->phi = ctx->phi; a->mu = ctx->mu; a->rho = ctx->rho;
+    a->c = ctx->c; a->h_avg = ctx->h_avg;
+    a->fac_voro = ctx->p.fac_voro_bound; a->fac_pt = ctx->p.fac_pt_mvmt;
+    a->fac_geps = ctx->p.fac_geps; a->fac_end = ctx->p.fac_end_mvmt;
+    a->damping = ctx->p.newton_damping; a->keep_tol = ctx->p.keep_tol;
+    a->newton_max = ctx->p.newton_max; a->quad_max = ctx->p.quad_max_level;
+    a->adj_stride = ctx->p.adj_stride;
+    a->st = ctx->dst;
+    return TM_OK;
+}
+
+// ============================================================================ S5 standalone
+__global__ void k_project(Grid g, const double *__restrict__ phi, const double *__restrict__ mu, double c,
+                          double h_avg, double fac_pt, double fac_geps, double damping, int newton_max,
+                          const double *__restrict__ xo, const double *__restrict__ yo,
+                          const double *__restrict__ xh, const double *__restrict__ yh, int64_t n,
+                          double *__restrict__ x_out, double *__restrict__ y_out, double *__restrict__ d_out,
+                          int8_t *__restrict__ status, DevState *st) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double px = xo[i], py = yo[i];
+    double h = mu ? cmul(c, bilinear(g, mu, px, py, LdgLoad())) : c;
+    double qx, qy, dp;
+    int s = treat_point(g, phi, h, h_avg, fac_pt, fac_geps, damping, newton_max, px, py, xh[i], yh[i], qx, qy, dp,
+                        LdgLoad());
+    x_out[i] = qx;
+    y_out[i] = qy;
+    d_out[i] = dp;
+    status[i] = (int8_t)s;
+    if (s & 2) atomicAdd(&st->n_fallback, 1ull);
+}
+
+extern "C" tm_status tm_project_sdf(tm_ctx *ctx, const double *x_old, const double *y_old, const double *x_hat,
+                                    const double *y_hat, int64_t n, double *x_out, double *y_out,
+                                    double *d_prev_out, int8_t *status) {
+    if (!ctx) return TM_E_ARG;
+    if (!ctx->have_domain) TM_FAIL(ctx, TM_E_STATE, "tm_project_sdf before tm_set_domain");
+    if (!x_old || !y_old || !x_hat || !y_hat || !x_out || !y_out || !d_prev_out || !status || n < 0)
+        TM_FAIL(ctx, TM_E_ARG, "null argument to tm_project_sdf");
+    if (n == 0) return TM_OK;
+    TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    k_project<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(
+        ctx->grid, ctx->phi, ctx->mu, ctx->c, ctx->h_avg, ctx->p.fac_pt_mvmt, ctx->p.fac_geps,
+        ctx->p.newton_damping, ctx->p.newton_max, x_old, y_old, x_hat, y_hat, n, x_out, y_out, d_prev_out,
+        status, ctx->dst);
+    return tm_internal_check_launch(ctx, "k_project");
+}
+
+// ============================================================================ S6
+// acc layout: 0 n, 1 sum sqrt a, 2 sum sqrt b, 3 max a, 4 max b, 5 sum a, 6 sum a2, 7 sum b, 8 sum b2,
+//             9 #a<1.2, 10 #a<2
+__device__ __forceinline__ void atomic_max_pos(double *addr, double v) {
+    // non-negative doubles order like their bit patterns
+    atomicMax((unsigned long long *)addr, (unsigned long long)__double_as_longlong(v));
+}
+
+__global__ void k_stats(const double *__restrict__ x, const double *__restrict__ y, const int32_t *__restrict__ tri,
+                        int64_t nt, double *acc) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double v[11] = {0};
+    if (t < nt) {
+        int32_t a = tri[3 * t], b = tri[3 * t + 1], c = tri[3 * t + 2];
+        double ax = x[a], ay = y[a], bx = x[b], by = y[b], cx = x[c], cy = y[c];
+        double la = sqrt((bx - cx) * (bx - cx) + (by - cy) * (by - cy));
+        double lb = sqrt((ax - cx) * (ax - cx) + (ay - cy) * (ay - cy));
+        double lc = sqrt((ax - bx) * (ax - bx) + (ay - by) * (ay - by));
+        double cr = (bx - ax) * (cy - ay) - (by - ay) * (cx - ax);
+        double s = 0.5 * (la + lb + lc);
+        double al = (la * lb * lc * s) / (2.0 * cr * cr);  // R/(2 r_in), Eq. aspect ratio
+        double be = fmax(la, fmax(lb, lc)) / fmin(la, fmin(lb, lc));
+        v[0] = 1; v[1] = sqrt(al); v[2] = sqrt(be); v[3] = al; v[4] = be;
+        v[5] = al; v[6] = al * al; v[7] = be; v[8] = be * be; v[9] = al < 1.2; v[10] = al < 2.0;
+    }
+    for (int k = 0; k < 11; k++) {
+        double w = v[k];
+        for (int o = 16; o > 0; o >>= 1) {
+            double u = __shfl_xor_sync(0xffffffffu, w, o);
+            w = (k == 3 || k == 4) ? fmax(w, u) : w + u;
+        }
+        v[k] = w;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        for (int k = 0; k < 11; k++) {
+            if (k == 3 || k == 4)
+                atomic_max_pos(&acc[k], v[k]);
+            else
+                atomicAdd(&acc[k], v[k]);
+        }
+    }
+}
+
+extern "C" tm_status tm_mesh_stats(tm_ctx *ctx, const double *x, const double *y, const int32_t *tri,
+                                   int64_t n_tri, tm_stats *out) {
+    if (!ctx) return TM_E_ARG;
+    if (!x || !y || (!tri && n_tri > 0) || !out || n_tri < 0) TM_FAIL(ctx, TM_E_ARG, "null argument to tm_mesh_stats");
+    TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    TM_CUDA_TRY(ctx, cudaMemsetAsync(ctx->stat_acc, 0, 16 * sizeof(double), ctx->stream));
+    if (n_tri > 0) {
+        k_stats<<<(unsigned)((n_tri + 255) / 256), 256, 0, ctx->stream>>>(x, y, tri, n_tri, ctx->stat_acc);
+        tm_status s = tm_internal_check_launch(ctx, "k_stats");
+        if (s != TM_OK) return s;
+    }
+    double acc[16];
+    DevState ds;
+    TM_CUDA_TRY(ctx, cudaMemcpyAsync(acc, ctx->stat_acc, sizeof(acc), cudaMemcpyDeviceToHost, ctx->stream));
+    TM_CUDA_TRY(ctx, cudaMemcpyAsync(&ds, ctx->dst, sizeof(ds), cudaMemcpyDeviceToHost, ctx->stream));
+    TM_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    memset(out, 0, sizeof(*out));
+    out->n_tri = (int64_t)acc[0];
+    out->sum_sqrt_alpha = acc[1]; out->sum_sqrt_beta = acc[2];
+    out->max_alpha = acc[3]; out->max_beta = acc[4];
+    out->sum_alpha = acc[5]; out->sum_alpha2 = acc[6]; out->sum_beta = acc[7]; out->sum_beta2 = acc[8];
+    out->n_alpha_lt_1_2 = (int64_t)acc[9]; out->n_alpha_lt_2 = (int64_t)acc[10];
+    out->n_degenerate = (int64_t)ds.n_degenerate;
+    out->n_fallback = (int64_t)ds.n_fallback;
+    out->n_overflow = (int64_t)ds.n_overflow;
+    return TM_OK;
+}
+
+extern "C" tm_status tm_work_counts(tm_ctx *ctx, tm_work *out) {
+    if (!ctx || !out) return TM_E_ARG;
+    TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    DevState ds;
+    TM_CUDA_TRY(ctx, cudaMemcpyAsync(&ds, ctx->dst, sizeof(ds), cudaMemcpyDeviceToHost, ctx->stream));
+    TM_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    int64_t *o = (int64_t *)out;
+    for (int k = 0; k < 10; k++) o[k] = (int64_t)ds.work[k];
+    return TM_OK;
+}
+
+// ============================================================================ exports
+__global__ void k_adj_export(const int32_t *__restrict__ adj, const uint8_t *__restrict__ deg,
+                             const int32_t *__restrict__ perm, const int32_t *__restrict__ gids, int64_t n_local,
+                             int64_t n_owned, int stride, int32_t *__restrict__ adj_out,
+                             uint8_t *__restrict__ deg_out) {
+    int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n_local) return;
+    int32_t o = perm[s];
+    if (o >= n_owned) return;
+    int d = deg[s];
+    deg_out[o] = (uint8_t)d;
+    for (int k = 0; k < stride; k++)
+        adj_out[(int64_t)o * stride + k] = k < d ? gids[adj[(int64_t)k * n_local + s]] : -1;
+}
+
+extern "C" tm_status tm_adjacency_export(tm_ctx *ctx, const int32_t *adj, const uint8_t *deg, int32_t *adj_out,
+                                         uint8_t *deg_out) {
+    if (!ctx) return TM_E_ARG;
+    if (!ctx->have_bins) TM_FAIL(ctx, TM_E_STATE, "tm_adjacency_export before tm_grid_bin");
+    if (!adj || !deg || !adj_out || !deg_out) TM_FAIL(ctx, TM_E_ARG, "null argument to tm_adjacency_export");
+    TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    k_adj_export<<<(unsigned)((ctx->n_local + 255) / 256), 256, 0, ctx->stream>>>(
+        adj, deg, ctx->perm, ctx->gids, ctx->n_local, ctx->n_owned, ctx->p.adj_stride, adj_out, deg_out);
+    return tm_internal_check_launch(ctx, "k_adj_export");
+}
+
+// ============================================================================ S7 packing
+__global__ void k_halo_pack(const double *__restrict__ x, const double *__restrict__ y,
+                            const int32_t *__restrict__ gid, int64_t n, double lo, double hi, double w,
+                            double *send_lo, double *send_hi, int64_t cap, unsigned long long *cnt) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double px = x[i];
+    int32_t g = gid ? gid[i] : (int32_t)i;
+    if (px < lo + w) {
+        unsigned long long k = atomicAdd(&cnt[0], 1ull);
+        if ((int64_t)k < cap) {
+            send_lo[k] = px;
+            send_lo[cap + k] = y[i];
+            ((int32_t *)(send_lo + 2 * cap))[k] = g;
+        }
+    }
+    if (px >= hi - w) {
+        unsigned long long k = atomicAdd(&cnt[1], 1ull);
+        if ((int64_t)k < cap) {
+            send_hi[k] = px;
+            send_hi[cap + k] = y[i];
+            ((int32_t *)(send_hi + 2 * cap))[k] = g;
+        }
+    }
+}
+
+extern "C" tm_status tm_halo_pack(tm_ctx *ctx, const double *x, const double *y, const int32_t *gid,
+                                  int64_t n_owned, double strip_lo, double strip_hi, double width, double *send_lo,
+                                  double *send_hi, int64_t cap, int64_t *cnt2) {
+    if (!ctx) return TM_E_ARG;
+    if (!x || !y || !send_lo || !send_hi || !cnt2 || n_owned < 0 || cap < 0)
+        TM_FAIL(ctx, TM_E_ARG, "null argument to tm_halo_pack");
+    TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    TM_CUDA_TRY(ctx, cudaMemsetAsync(cnt2, 0, 2 * sizeof(int64_t), ctx->stream));
+    if (n_owned == 0) return TM_OK;
+    k_halo_pack<<<(unsigned)((n_owned + 255) / 256), 256, 0, ctx->stream>>>(
+        x, y, gid, n_owned, strip_lo, strip_hi, width, send_lo, send_hi, cap, (unsigned long long *)cnt2);
+    return tm_internal_check_launch(ctx, "k_halo_pack");
+}
+
+__global__ void k_migrate_pack(const double *__restrict__ x, const double *__restrict__ y,
+                               const int32_t *__restrict__ gid, const double *__restrict__ dp, int64_t n, double lo,
+                               double hi, double *keep, double *out_lo, double *out_hi, int64_t cap,
+                               unsigned long long *cnt) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double px = x[i];
+    int which = px < lo ? 1 : (px >= hi ? 2 : 0);
+    double *dst = which == 0 ? keep : (which == 1 ? out_lo : out_hi);
+    int64_t c = which == 0 ? n : cap;
+    unsigned long long k = atomicAdd(&cnt[which], 1ull);
+    if ((int64_t)k < c) {
+        dst[k] = px;
+        dst[c + k] = y[i];
+        ((int32_t *)(dst + 2 * c))[k] = gid[i];
+        dst[3 * c + k] = dp ? dp[i] : 0.0;
+    }
+}
+
+__global__ void k_migrate_unpack(const double *keep, int64_t n, const unsigned long long *cnt, double *x, double *y,
+                                 int32_t *gid, double *dp) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= (int64_t)cnt[0]) return;
+    x[k] = keep[k];
+    y[k] = keep[n + k];
+    gid[k] = ((const int32_t *)(keep + 2 * n))[k];
+    if (dp) dp[k] = keep[3 * n + k];
+}
+
+extern "C" tm_status tm_migrate_pack(tm_ctx *ctx, double *x, double *y, int32_t *gid, double *d_prev,
+                                     int64_t n_owned, double strip_lo, double strip_hi, double *out_lo,
+                                     double *out_hi, int64_t cap, int64_t *cnt3) {
+    if (!ctx) return TM_E_ARG;
+    if (!x || !y || !gid || !out_lo || !out_hi || !cnt3 || n_owned < 0 || cap < 0)
+        TM_FAIL(ctx, TM_E_ARG, "null argument to tm_migrate_pack");
+    TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    TM_CUDA_TRY(ctx, cudaMemsetAsync(cnt3, 0, 3 * sizeof(int64_t), ctx->stream));
+    if (n_owned == 0) return TM_OK;
+    double *keep;
+    TM_CUDA_TRY(ctx, cudaMallocAsync(&keep, 4 * n_owned * sizeof(double), ctx->stream));
+    unsigned blocks = (unsigned)((n_owned + 255) / 256);
+    k_migrate_pack<<<blocks, 256, 0, ctx->stream>>>(x, y, gid, d_prev, n_owned, strip_lo, strip_hi, keep, out_lo,
+                                                     out_hi, cap, (unsigned long long *)cnt3);
+    k_migrate_unpack<<<blocks, 256, 0, ctx->stream>>>(keep, n_owned, (const unsigned long long *)cnt3, x, y, gid,
+                                                       d_prev);
+    TM_CUDA_TRY(ctx, cudaFreeAsync(keep, ctx->stream));
+    return tm_internal_check_launch(ctx, "k_migrate");
+}
+
+// ============================================================================ host hooks
+extern "C" int tm_host_incircle_exact(const double *a, const double *b, const double *c, const double *d) {
+    return tmg::incircle_exact(a, b, c, d);
+}
+
+extern "C" void tm_host_cramer(const double *A3, const double *B3, double *xy) {
+    Line A = {A3[0], A3[1], A3[2]}, B = {B3[0], B3[1], B3[2]};
+    cramer(A, B, xy[0], xy[1]);
+}
+
+extern "C" double tm_host_bilinear(int32_t nx, int32_t ny, double x0, double y0, double x1, double y1,
+                                   const double *F, double x, double y) {
+    Grid g;
+    g.nx = nx; g.ny = ny; g.x0 = x0; g.y0 = y0; g.x1 = x1; g.y1 = y1;
+    g.idx = cdiv((double)(nx - 1), csub(x1, x0));
+    g.idy = cdiv((double)(ny - 1), csub(y1, y0));
+    g.dx = cdiv(csub(x1, x0), (double)(nx - 1));
+    g.dy = cdiv(csub(y1, y0), (double)(ny - 1));
+    return bilinear(g, F, x, y, PlainLoad());
+}

@@ -1,0 +1,163 @@
+// tm_internal.cuh -- context layout and kernel argument blocks shared by the
+// .cu files of libtrime_gpu.so.  Not part of the public ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/trime_gpu.h"
+#include "tm_common.cuh"
+
+namespace tmg {
+
+// device-resident health counters and work counters (one per context)
+struct DevState {
+    unsigned long long n_degenerate;   // exact zeros + inconsistent clips
+    unsigned long long n_overflow;     // cells over the vertex capacity
+    unsigned long long n_duplicate;    // bitwise-equal point pairs met
+    unsigned long long n_outside;      // points outside B / NaN
+    unsigned long long n_tri_overflow; // triangles beyond tri_cap
+    unsigned long long n_adj_overflow; // ELL rows beyond adj_stride
+    unsigned long long n_fallback;     // projection fallbacks
+    unsigned long long work[10];       // tm_work fields after n_cells
+};
+
+struct BinGeom {
+    int32_t nbx, nby;
+    double x0, y0;   // bin grid origin (= box origin)
+    double sx, sy;   // bin size
+    double isx, isy; // 1/size
+};
+
+// everything a cell kernel reads or writes
+struct CellArgs {
+    const double *xs, *ys, *hs;
+    const int32_t *perm, *gids, *bin_start;
+    BinGeom bg;
+    int64_t n_local, n_owned;
+    Grid grid;
+    const double *phi, *mu, *rho;
+    double c, h_avg;
+    double fac_voro, fac_pt, fac_geps, fac_end, damping, keep_tol;
+    int32_t newton_max, quad_max;
+    // outputs
+    int32_t *tri;
+    int64_t tri_cap;
+    unsigned long long *n_tri;
+    int32_t *adj;
+    uint8_t *deg;
+    int32_t adj_stride;
+    const double *d_prev;
+    double *x_out, *y_out, *d_prev_out;
+    int8_t *status;
+    double *x_hat, *y_hat;
+    DevState *st;
+};
+
+}  // namespace tmg
+
+struct tm_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    tm_params p;
+    char err[512] = {0};
+    // domain (S0)
+    bool have_domain = false;
+    tmg::Grid grid;
+    double c = 0, h_avg = 0;
+    int64_t n_total = 0;
+    double *phi = nullptr, *mu = nullptr, *rho = nullptr;
+    size_t grid_bytes = 0;
+    tmg::BinGeom bg;
+    // sorted state (S1)
+    bool have_bins = false;
+    int64_t n_local = 0, n_owned = 0, cap_points = 0, cap_bins = 0;
+    double *xs = nullptr, *ys = nullptr, *hs = nullptr;
+    int32_t *perm = nullptr, *gids = nullptr, *key = nullptr, *rank = nullptr;
+    int32_t *bin_count = nullptr, *bin_start = nullptr, *block_sums = nullptr;
+    int64_t cap_block_sums = 0;
+    // DistMesh scratch
+    double *partials = nullptr;
+    int64_t cap_partials = 0;
+    // stats scratch
+    double *stat_acc = nullptr;
+    // device health counters
+    tmg::DevState *dst = nullptr;
+    bool have_cells = false;
+};
+
+#define TM_CUDA_TRY(ctx, call)                                                                       \
+    do {                                                                                             \
+        cudaError_t e_ = (call);                                                                     \
+        if (e_ != cudaSuccess) {                                                                     \
+            snprintf((ctx)->err, sizeof((ctx)->err), "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                     __FILE__, __LINE__);                                                            \
+            return TM_E_CUDA;                                                                        \
+        }                                                                                            \
+    } while (0)
+
+#define TM_FAIL(ctx, code, ...)                                   \
+    do {                                                          \
+        snprintf((ctx)->err, sizeof((ctx)->err), __VA_ARGS__);    \
+        return (code);                                            \
+    } while (0)
+
+// internal helpers implemented in tm_api.cu
+tm_status tm_internal_fill_cell_args(tm_ctx *ctx, tmg::CellArgs *a);
+tm_status tm_internal_check_launch(tm_ctx *ctx, const char *what);
+
+namespace tmg {
+
+// S5 treatment of one point (L20-L22); returns status
+template <typename Load>
+__device__ __forceinline__ int treat_point(const Grid &g, const double *phi, double h, double h_avg,
+                                           double fac_pt, double fac_geps, double damping, int newton_max,
+                                           double xo, double yo, double xh, double yh, double &qx_out,
+                                           double &qy_out, double &dprev, Load ld) {
+    int status = 0;
+    double T = cmul(fac_pt, h);
+    double dx = csub(xh, xo), dy = csub(yh, yo);
+    double len = sqrt(cadd(cmul(dx, dx), cmul(dy, dy)));
+    if (len > T) {
+        double sc = cdiv(T, len);
+        dx = cmul(dx, sc);
+        dy = cmul(dy, sc);
+        status |= 4;
+    }
+    double qx = fmin(fmax(cadd(xo, dx), g.x0), g.x1);
+    double qy = fmin(fmax(cadd(yo, dy), g.y0), g.y1);
+    double geps = cmul(fac_geps, h < h_avg ? h : h_avg);
+    double ph = bilinear(g, phi, qx, qy, ld);
+    if (!(ph <= geps)) {
+        bool ok = false;
+        for (int it = 0; it < newton_max; it++) {
+            double gx, gy;
+            bilinear_grad(g, phi, qx, qy, gx, gy, ld);
+            double g2 = cadd(cmul(gx, gx), cmul(gy, gy));
+            if (!(g2 > 0.0)) break;
+            double stp = cdiv(cmul(damping, ph), g2);
+            qx = fmin(fmax(csub(qx, cmul(stp, gx)), g.x0), g.x1);
+            qy = fmin(fmax(csub(qy, cmul(stp, gy)), g.y0), g.y1);
+            ph = bilinear(g, phi, qx, qy, ld);
+            if (fabs(ph) <= geps) {
+                ok = true;
+                break;
+            }
+        }
+        if (ok)
+            status |= 1;
+        else {
+            qx = xo;
+            qy = yo;
+            status = (status & 4) | 2;
+        }
+    }
+    qx_out = qx;
+    qy_out = qy;
+    double ex = csub(qx, xo), ey = csub(qy, yo);
+    dprev = sqrt(cadd(cmul(ex, ex), cmul(ey, ey)));
+    return status;
+}
+
+}  // namespace tmg

@@ -1,0 +1,241 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on
+identical inputs, element by element.
+
+Bar (BASELINE.json north_star): kept triangles bit-exact as sorted index
+triples; ELL adjacency identical (DistMesh); positions and d_prev within
+1e-12 * diam(B) after one update (reading L14); status codes identical.
+Both sides take every discrete decision with the same canonical arithmetic
+(L25) or exact predicates, so any mismatch is a bug, not rounding.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+import oracle as O
+from inputs import configs
+from tests.gpu_util import GpuRunner, compare
+
+
+def run_pair(c, x, y, mode, d_prev=None, params=None, oparams=None, runner=None):
+    r = runner or GpuRunner(c.box, c.phi, c.mu, c.rho, params=params)
+    g = r.iteration(x, y, mode, d_prev)
+    o = O.iteration(O.FieldSet.from_config(c), x, y, mode, d_prev=d_prev, params=oparams)
+    assert o.info.n_degenerate == 0
+    return g, o, r
+
+
+def test_cfg1_all_lloyd_iterations(cfg_cache):
+    """configs[0]: 10 CVD iterations, parity at every iteration from the GPU's own state."""
+    c = cfg_cache(1)
+    r = GpuRunner(c.box, c.phi)
+    x, y, dp = c.x, c.y, None
+    for it in range(10):
+        g = r.iteration(x, y, "cvd", dp)
+        o = O.iteration(O.FieldSet.from_config(c), x, y, "cvd", d_prev=dp)
+        compare(g, o, c.box, "cvd", ctx=f"cfg1 it{it}")
+        x, y, dp = g["x"], g["y"], g["d_prev"]
+
+
+def test_cfg2_distmesh(cfg_cache):
+    """configs[1]: DistMesh on the disk, iterations 0, 1 and 5 of the GPU run."""
+    c = cfg_cache(2)
+    r = GpuRunner(c.box, c.phi)
+    x, y, dp = c.x, c.y, None
+    for it in range(6):
+        g = r.iteration(x, y, "dm", dp)
+        if it in (0, 1, 5):
+            o = O.iteration(O.FieldSet.from_config(c), x, y, "dm", d_prev=dp)
+            compare(g, o, c.box, "dm", ctx=f"cfg2 it{it}")
+        x, y, dp = g["x"], g["y"], g["d_prev"]
+
+
+@pytest.mark.parametrize("k", [3, 4])
+def test_adaptive_full_size_first_dm_and_cvd(k, cfg_cache):
+    """configs[2]/[3] at full size (10^6): DistMesh iteration 0, then a CVD
+    iteration (adaptive quadrature) from the GPU state after 3 DistMesh steps."""
+    c = cfg_cache(k)
+    r = GpuRunner(c.box, c.phi, c.mu, c.rho)
+    x, y, dp = c.x, c.y, None
+    for it in range(3):
+        g = r.iteration(x, y, "dm", dp)
+        if it == 0:
+            o = O.iteration(O.FieldSet.from_config(c), x, y, "dm", d_prev=dp)
+            compare(g, o, c.box, "dm", ctx=f"cfg{k} dm it0")
+        x, y, dp = g["x"], g["y"], g["d_prev"]
+    g = r.iteration(x, y, "cvd", dp)
+    o = O.iteration(O.FieldSet.from_config(c), x, y, "cvd", d_prev=dp)
+    compare(g, o, c.box, "cvd", ctx=f"cfg{k} cvd")
+
+
+@pytest.mark.parametrize("n,seed", [(3, 1), (4, 2), (7, 3), (40, 4), (333, 5), (5000, 6)])
+def test_small_random_ragged(n, seed):
+    box = (0.0, 0.0, 1.0, 1.0)
+    phi = configs.box_phi(box, 64)
+    c = configs.Config("rand", *configs.random_points(n, seed, box), box, phi, None, None, ["cvd"])
+    for mode in ("cvd", "dm"):
+        g, o, _ = run_pair(c, c.x, c.y, mode)
+        compare(g, o, box, mode, ctx=f"rand n={n} {mode}")
+
+
+@pytest.mark.parametrize("fac", [0.6, 1.0, 2.0])
+def test_octagon_binding(fac):
+    """Small octagons (fac_voro_bound < 5) make the octagon walls bind on many
+    cells and exercise the (wall, bisector) vertices and the octagon keep tests."""
+    import paper_2309_13824_b200 as T
+    box = (0.0, 0.0, 1.0, 1.0)
+    phi = configs.box_phi(box, 64)
+    x, y = configs.random_points(4000, 17, box)
+    c = configs.Config("oct", x, y, box, phi, None, None, ["cvd"])
+    for mode in ("cvd", "dm"):
+        g, o, _ = run_pair(c, x, y, mode, params=T.default_params(fac_voro_bound=fac),
+                           oparams=O.default_params(fac_voro_bound=fac))
+        compare(g, o, box, mode, ctx=f"fac={fac} {mode}")
+
+
+def test_points_on_bin_edges_and_box_boundary():
+    """Points exactly on bin boundaries and on the box sides (L24)."""
+    box = (0.0, 0.0, 1.0, 1.0)
+    phi = configs.box_phi(box, 64)
+    n = 2000
+    rng = np.random.default_rng(8)
+    x, y = rng.random(n), rng.random(n)
+    nb = int(np.ceil(np.sqrt(n / 3.3)))
+    k = rng.integers(0, nb, 300)
+    x[:300] = k / nb  # on vertical bin edges
+    # on the box sides: at most two per side (three collinear hull points are non-generic, L12)
+    y[300:302] = 0.0
+    y[302:304] = 1.0
+    x[304:306] = 1.0
+    x[306:308] = 0.0
+    c = configs.Config("edges", x, y, box, phi, None, None, ["cvd"])
+    for mode in ("cvd", "dm"):
+        g, o, _ = run_pair(c, x, y, mode)
+        compare(g, o, box, mode, ctx=f"edges {mode}")
+
+
+def test_near_cocircular_forces_exact_path():
+    """A square lattice jittered by ~1e-13 is nearly cocircular everywhere: the
+    floating filters cannot decide and the exact expansion path must agree with
+    the oracle's big integers."""
+    import paper_2309_13824_b200 as T
+    m = 40
+    g1 = (np.arange(m) + 0.5) / m
+    X, Y = np.meshgrid(g1, g1)
+    rng = np.random.default_rng(5)
+    x = (X.ravel() + rng.uniform(-1e-13, 1e-13, m * m)).copy()
+    y = (Y.ravel() + rng.uniform(-1e-13, 1e-13, m * m)).copy()
+    box = (0.0, 0.0, 1.0, 1.0)
+    phi = configs.box_phi(box, 64)
+    c = configs.Config("lattice", x, y, box, phi, None, None, ["cvd"])
+    r = GpuRunner(box, phi, flags=T.TM_F_COUNT_WORK)
+    g, o, _ = run_pair(c, x, y, "cvd", runner=r)
+    compare(g, o, box, "cvd", ctx="lattice")
+    w = r.ctx.tm_work_counts()
+    assert w.exact_calls > 100
+
+
+def test_work_counts_match_oracle(cfg_cache):
+    """O8 work statistics: the GPU's own counters agree with the oracle's."""
+    import paper_2309_13824_b200 as T
+    c = cfg_cache(2)
+    r = GpuRunner(c.box, c.phi, flags=T.TM_F_COUNT_WORK)
+    g = r.iteration(c.x, c.y, "dm")
+    w = r.ctx.tm_work_counts()
+    o = O.iteration(O.FieldSet.from_config(c), c.x, c.y, "dm", counts=True)
+    cnt = o.counts.sum(0)
+    assert w.n_cells == c.n
+    assert w.deg == cnt[1] and w.verts == cnt[2] and w.t_own == cnt[3] and w.ell == cnt[5]
+    assert abs(w.n_cert - cnt[0]) <= 1e-4 * cnt[0]
+
+
+def test_errors_are_loud():
+    import paper_2309_13824_b200 as T
+    import torch
+    box = (0.0, 0.0, 1.0, 1.0)
+    phi = configs.box_phi(box, 16)
+    ctx = T.Context(0)
+    x = torch.rand(100, dtype=torch.float64, device="cuda")
+    y = torch.rand(100, dtype=torch.float64, device="cuda")
+    with pytest.raises(T.TmError) as e:
+        ctx.tm_grid_bin(x, y)
+    assert e.value.code == T.TM_E_STATE
+    ctx.tm_set_domain(box, torch.from_numpy(phi).cuda(), None, None, 100)
+    # duplicates
+    x2 = x.clone()
+    y2 = y.clone()
+    x2[7] = x2[3]
+    y2[7] = y2[3]
+    bufs = T.IterBuffers.alloc(100)
+    ctx.tm_grid_bin(x2, y2)
+    ctx.tm_voronoi_delaunay(bufs.tri, bufs.n_tri)
+    with pytest.raises(T.TmError) as e:
+        ctx.tm_sync()
+    assert e.value.code == T.TM_E_DUPLICATE
+    # outside the box
+    ctx2 = T.Context(0)
+    ctx2.tm_set_domain(box, torch.from_numpy(phi).cuda(), None, None, 100)
+    x3 = x.clone()
+    x3[0] = 1.5
+    ctx2.tm_grid_bin(x3, y)
+    with pytest.raises(T.TmError) as e:
+        ctx2.tm_sync()
+    assert e.value.code == T.TM_E_OUTSIDE
+    # triangle capacity
+    ctx3 = T.Context(0)
+    ctx3.tm_set_domain(box, torch.from_numpy(phi).cuda(), None, None, 100)
+    ctx3.tm_grid_bin(x, y)
+    small = torch.empty((5, 3), dtype=torch.int32, device="cuda")
+    nt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    ctx3.tm_voronoi_delaunay(small, nt)
+    with pytest.raises(T.TmError) as e:
+        ctx3.tm_sync()
+    assert e.value.code == T.TM_E_CAPACITY
+    assert int(nt.item()) > 5  # the required count is reported
+
+
+def test_standalone_project_and_cvd_step_match_fused(cfg_cache):
+    """tm_cvd_step + tm_project_sdf (unfused) == fused tm_voronoi_delaunay CVD."""
+    import torch
+    import paper_2309_13824_b200 as T
+    c = cfg_cache(1)
+    r = GpuRunner(c.box, c.phi)
+    g = r.iteration(c.x, c.y, "cvd")
+    ctx = r.ctx
+    x, y = torch.from_numpy(c.x).cuda(), torch.from_numpy(c.y).cuda()
+    ctx.tm_grid_bin(x, y)
+    xh, yh = torch.empty_like(x), torch.empty_like(y)
+    ctx.tm_cvd_step(None, xh, yh)
+    xo, yo, do = torch.empty_like(x), torch.empty_like(x), torch.empty_like(x)
+    st = torch.empty(c.n, dtype=torch.int8, device="cuda")
+    ctx.tm_project_sdf(x, y, xh, yh, xo, yo, do, st)
+    ctx.tm_sync()
+    assert np.array_equal(xo.cpu().numpy(), g["x"]) and np.array_equal(yo.cpu().numpy(), g["y"])
+    assert np.array_equal(st.cpu().numpy(), g["status"])
+
+
+def test_mesh_stats_match_oracle(cfg_cache):
+    import torch
+    c = cfg_cache(2)
+    r = GpuRunner(c.box, c.phi)
+    g = r.iteration(c.x, c.y, "dm")
+    tri = torch.from_numpy(np.ascontiguousarray(g["tri"])).cuda()
+    s = r.ctx.tm_mesh_stats(torch.from_numpy(c.x).cuda(), torch.from_numpy(c.y).cuda(), tri, len(g["tri"]))
+    o = O.stats(g["tri"], c.x, c.y)
+    assert s.n_tri == o[0] and s.n_alpha_lt_1_2 == o[9] and s.n_alpha_lt_2 == o[10]
+    assert abs(s.sum_sqrt_alpha - o[1]) < 1e-9 * o[1] and abs(s.max_alpha - o[3]) < 1e-12 * o[3]
+    assert abs(s.sum_beta2 - o[8]) < 1e-9 * o[8]
+
+
+def test_determinism(cfg_cache):
+    c = cfg_cache(2)
+    r = GpuRunner(c.box, c.phi)
+    a = r.iteration(c.x, c.y, "cvd")
+    b = r.iteration(c.x, c.y, "cvd")
+    assert np.array_equal(a["x"], b["x"]) and np.array_equal(a["y"], b["y"])
+    assert tri_set_eq(a["tri"], b["tri"])
+
+
+def tri_set_eq(a, b):
+    from tests.gpu_util import tri_set
+    return tri_set(a) == tri_set(b)
