@@ -230,7 +230,9 @@ int or_incircle_exact(const double *a, const double *b, const double *c, const d
  * path.  Pinned against exact rationals in tests/test_oracle_predicates.py. */
 static const double OR_EPS = 1.1102230246251565e-16; /* 2^-53 */
 
-int or_orient2d(const double *a, const double *b, const double *c) {
+/* counted = 0: an exact zero is legitimate (collinear points met by the
+ * point-location walk or the ghost test, which handle it explicitly) */
+static int orient2d_impl(const double *a, const double *b, const double *c, int counted) {
     double detl = (b[0] - a[0]) * (c[1] - a[1]);
     double detr = (b[1] - a[1]) * (c[0] - a[0]);
     double det = detl - detr;
@@ -239,9 +241,12 @@ int or_orient2d(const double *a, const double *b, const double *c) {
     if (det > bound) return 1;
     if (-det > bound) return -1;
     int s = or_orient2d_exact(a, b, c);
-    if (s == 0) g_degenerate++;
+    if (s == 0 && counted) g_degenerate++;
     return s;
 }
+
+int or_orient2d(const double *a, const double *b, const double *c) { return orient2d_impl(a, b, c, 1); }
+static int orient_walk(const double *a, const double *b, const double *c) { return orient2d_impl(a, b, c, 0); }
 
 int or_incircle(const double *a, const double *b, const double *c, const double *d) {
     double adx = a[0] - d[0], ady = a[1] - d[1];
@@ -344,7 +349,7 @@ static int bw_conflict(bw_state *s, int32_t id, int32_t q) {
     pt(s, q, P);
     if (t->v[2] == GHOST) {
         pt(s, t->v[0], A); pt(s, t->v[1], B);
-        int o = or_orient2d(A, B, P);
+        int o = orient_walk(A, B, P);
         if (o > 0) return 1;
         if (o < 0) return 0;
         /* collinear with the hull edge: conflict iff strictly inside the segment */
@@ -377,7 +382,7 @@ static int32_t bw_locate(bw_state *s, int32_t q) {
             int k = (start + kk) % 3;
             pt(s, t->v[(k + 1) % 3], A);
             pt(s, t->v[(k + 2) % 3], B);
-            if (or_orient2d(A, B, P) < 0) { cur = t->n[k]; moved = 1; break; }
+            if (orient_walk(A, B, P) < 0) { cur = t->n[k]; moved = 1; break; }
         }
         if (!moved) {
             if (bw_conflict(s, cur, q)) return cur;
@@ -510,11 +515,11 @@ static int bw_build(bw_state *s, int64_t n, const double *x, const double *y) {
     if (A[0] == B[0] && A[1] == B[1]) { free(ord); return -2; }
     for (int64_t k = 2; k < n; k++) {
         pt(s, ord[k].idx, C);
-        if (or_orient2d(A, B, C) != 0) { c = ord[k].idx; cpos = k; break; }
+        if (orient_walk(A, B, C) != 0) { c = ord[k].idx; cpos = k; break; }
     }
     if (c < 0) { free(ord); return -1; }
     pt(s, c, C);
-    if (or_orient2d(A, B, C) < 0) { int32_t t = a; a = b; b = t; }
+    if (orient_walk(A, B, C) < 0) { int32_t t = a; a = b; b = t; }
     int32_t T = bw_new(s, a, b, c);
     int32_t G0 = bw_new(s, c, b, GHOST), G1 = bw_new(s, a, c, GHOST), G2 = bw_new(s, b, a, GHOST);
     bw_link(s, T, b, c, G0); bw_link(s, G0, c, b, T);
