@@ -101,7 +101,7 @@ def lib():
                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                ctypes.POINTER(Info)]
         L.or_iteration.restype = ctypes.c_int
-        L.or_iteration.argtypes = [ctypes.POINTER(Fields), ctypes.POINTER(Params), ctypes.c_int64,
+        L.or_iteration.argtypes = [ctypes.POINTER(Fields), ctypes.POINTER(Params), ctypes.c_int64, ctypes.c_int64,
                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
                                    ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
@@ -246,7 +246,7 @@ class IterResult:
 
 
 def iteration(fs: FieldSet, x, y, mode: str, d_prev=None, params: Optional[Params] = None,
-              counts: bool = False) -> IterResult:
+              counts: bool = False, n_total: int = 0) -> IterResult:
     """One Delaunay + update + treatment iteration (mode 'cvd' or 'dm')."""
     params = params or default_params()
     x = np.ascontiguousarray(x, dtype=np.float64)
@@ -264,7 +264,7 @@ def iteration(fs: FieldSet, x, y, mode: str, d_prev=None, params: Optional[Param
     cnt = np.zeros((n, 6), dtype=np.int64) if counts else None
     dpi = None if d_prev is None else np.ascontiguousarray(d_prev, dtype=np.float64)
     info = Info()
-    rc = lib().or_iteration(ctypes.byref(fs.c), ctypes.byref(params), n, _p(x), _p(y), _p(dpi),
+    rc = lib().or_iteration(ctypes.byref(fs.c), ctypes.byref(params), n, n_total, _p(x), _p(y), _p(dpi),
                             0 if mode == "cvd" else 1, _p(tri), tri_cap, _p(edges), edges.shape[0],
                             _p(xh), _p(yh), _p(xo), _p(yo), _p(dp), _p(st), _p(cnt), ctypes.byref(info))
     if rc != 0:

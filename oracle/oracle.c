@@ -687,11 +687,14 @@ static line2 line_of(const cellctx *C, int32_t code) {
     return L;
 }
 
-/* Cramer intersection of two lines, relative coordinates (§8.0 canonical form) */
+/* Cramer intersection of two lines, relative coordinates, canonical form
+ * (DESIGN.md §3): inv = fl(1/det), x = fl(num_x * inv), y = fl(num_y * inv).
+ * Exactly symmetric in (A, B): det, inv and both numerators change sign. */
 static void cramer(line2 A, line2 B, double *x, double *y) {
     double det = A.nx * B.ny - A.ny * B.nx;
-    *x = (A.r * B.ny - A.ny * B.r) / det;
-    *y = (A.nx * B.r - A.r * B.nx) / det;
+    double inv = 1.0 / det;
+    *x = (A.r * B.ny - A.ny * B.r) * inv;
+    *y = (A.nx * B.r - A.r * B.nx) * inv;
 }
 
 typedef struct { int32_t la, lb; double x, y; } cvert;
@@ -1168,14 +1171,14 @@ static int64_t cgrid_count(const cgrid *g, const double *x, const double *y, dou
     return c - 1; /* exclude the point itself */
 }
 
-int or_iteration(const or_fields *f, const or_params *p, int64_t n, const double *x, const double *y,
-                 const double *d_prev, int mode, int32_t *tri_out, int64_t tri_cap, int32_t *edges_out,
+int or_iteration(const or_fields *f, const or_params *p, int64_t n, int64_t n_total, const double *x,
+                 const double *y, const double *d_prev, int mode, int32_t *tri_out, int64_t tri_cap, int32_t *edges_out,
                  int64_t edge_cap, double *x_hat, double *y_hat, double *x_out, double *y_out,
                  double *d_prev_out, int8_t *status, int64_t *counts, or_info *info) {
     int64_t deg0 = g_degenerate;
     or_info inf;
     memset(&inf, 0, sizeof(inf));
-    or_domain(f, n, &inf.c, &inf.h_avg);
+    or_domain(f, n_total > 0 ? n_total : n, &inf.c, &inf.h_avg);
     double c = inf.c;
     /* O1 */
     int64_t cap = 2 * n + 16;

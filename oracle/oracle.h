@@ -84,11 +84,12 @@ int64_t or_cells(const or_fields *f, const or_params *p, int64_t n,
 /* ---- one full iteration (O1..O6) --------------------------------------- */
 /* mode 0 = CVD (Alg. 2), 1 = DistMesh (Alg. 1 with retriangulation every
  * iteration, L5).  d_prev may be NULL (=> eps_c = fac_pt_mvmt, L13).
+ * n_total: the N of the h normalisation (0 => n; a strip of a larger set passes the global N).
  * Outputs: kept triangles K (CCW, min index first) and, for DistMesh, unique
  * kept edges (a<b); proposals x_hat/y_hat; treated x_out/y_out, d_prev_out,
  * status (0 accepted, 1 projected, 2 fallback, +4 clamped).
  * counts (nullable) = int64[n][6]: n_cert, deg, V, T_own, Q, E  (O8). */
-int or_iteration(const or_fields *f, const or_params *p, int64_t n,
+int or_iteration(const or_fields *f, const or_params *p, int64_t n, int64_t n_total,
                  const double *x, const double *y, const double *d_prev, int mode,
                  int32_t *tri, int64_t tri_cap,
                  int32_t *edges, int64_t edge_cap,

@@ -21,7 +21,7 @@ import torch
 from . import build as _build
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libtrime_gpu.so")
+LIB_PATH = os.environ.get("TRIME_LIB", os.path.join(_PKG, "libtrime_gpu.so"))
 
 TM_OK, TM_E_ARG, TM_E_CUDA, TM_E_CAPACITY, TM_E_DUPLICATE, TM_E_OUTSIDE, TM_E_STATE, TM_E_DEGENERATE = range(8)
 STATUS_NAMES = ["TM_OK", "TM_E_ARG", "TM_E_CUDA", "TM_E_CAPACITY", "TM_E_DUPLICATE", "TM_E_OUTSIDE",

@@ -4,6 +4,7 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <algorithm>
 #include <new>
 
 #include "tm_internal.cuh"
@@ -25,7 +26,7 @@ extern "C" void tm_params_default(tm_params *p) {
     p->keep_tol = 0.0;         // L10
     p->adj_stride = 16;
     p->max_cell_vertices = 32;
-    p->flags = 0;
+    p->flags = TM_F_TWO_LEVEL_BINS;
 }
 
 extern "C" tm_status tm_create(int device, void *cuda_stream, const tm_params *p, tm_ctx **out) {
@@ -68,9 +69,11 @@ extern "C" void tm_destroy(tm_ctx *ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     free_points(ctx);
-    cudaFree(ctx->bin_count); cudaFree(ctx->bin_start); cudaFree(ctx->block_sums);
+    cudaFree(ctx->bin_count); cudaFree(ctx->rlev); cudaFree(ctx->leaf_off); cudaFree(ctx->block_sums);
+    cudaFree(ctx->leaf_count); cudaFree(ctx->leaf_start);
     cudaFree(ctx->phi); cudaFree(ctx->mu); cudaFree(ctx->rho);
     cudaFree(ctx->partials); cudaFree(ctx->stat_acc); cudaFree(ctx->dst);
+    cudaFree(ctx->retry_list); cudaFree(ctx->retry_cnt);
     delete ctx;
 }
 
@@ -190,7 +193,7 @@ extern "C" tm_status tm_set_domain(tm_ctx *ctx, const tm_fields *f, int64_t n_to
 // ============================================================================ S1
 __global__ void k_bin_keys(const double *__restrict__ x, const double *__restrict__ y, int64_t n, BinGeom bg,
                            double bx0, double by0, double bx1, double by1, int32_t *__restrict__ key,
-                           int32_t *__restrict__ rank, int32_t *__restrict__ count, DevState *st) {
+                           int32_t *__restrict__ count, DevState *st) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double px = x[i], py = y[i];
@@ -204,7 +207,45 @@ __global__ void k_bin_keys(const double *__restrict__ x, const double *__restric
     by = by < 0 ? 0 : (by >= bg.nby ? bg.nby - 1 : by);
     int32_t k = by * bg.nbx + bx;
     key[i] = k;
-    rank[i] = atomicAdd(&count[k], 1);
+    atomicAdd(&count[k], 1);
+}
+
+// level of every level-0 bin: r = 0 if count <= 4*N_opt, else the smallest
+// r <= MAX_SUBLEVEL with 4^r >= count/N_opt (SURVEY §8(a) S1 two-level list)
+__global__ void k_bin_levels(const int32_t *__restrict__ count, int64_t nb, double n_opt, int two_level,
+                             uint8_t *__restrict__ rlev, int32_t *__restrict__ nleaf) {
+    int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    double c = (double)count[b];
+    int r = 0;
+    if (two_level && c > 4.0 * n_opt) {
+        r = 1;
+        while (r < MAX_SUBLEVEL && (double)(1 << (2 * r)) * n_opt < c) r++;
+    }
+    rlev[b] = (uint8_t)r;
+    nleaf[b] = 1 << (2 * r);
+}
+
+// leaf key (level-0 bin, Morton sub-index) and rank within the leaf
+__global__ void k_leaf_keys(const double *__restrict__ x, const double *__restrict__ y, int64_t n, BinGeom bg,
+                            double bx0, double by0, double bx1, double by1, int32_t *__restrict__ key,
+                            const uint8_t *__restrict__ rlev, const int32_t *__restrict__ leaf_off,
+                            int32_t *__restrict__ leaf_count, int32_t *__restrict__ rank) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double px = fmin(fmax(x[i] == x[i] ? x[i] : bx0, bx0), bx1);
+    double py = fmin(fmax(y[i] == y[i] ? y[i] : by0, by0), by1);
+    int32_t b = key[i];
+    int r = rlev[b];
+    int32_t leaf = leaf_off[b];
+    if (r > 0) {
+        int bxi = b % bg.nbx, byi = b / bg.nbx;
+        int ux = leaf_coord(px, bg.x0, bg.isx, bg.nbx, r) - (bxi << r);
+        int uy = leaf_coord(py, bg.y0, bg.isy, bg.nby, r) - (byi << r);
+        leaf += (int32_t)morton2((uint32_t)ux, (uint32_t)uy);
+    }
+    key[i] = leaf;
+    rank[i] = atomicAdd(&leaf_count[leaf], 1);
 }
 
 // exclusive scan: per-block (1024 threads x 4 items)
@@ -300,6 +341,29 @@ __global__ void k_bin_scatter(const double *__restrict__ x, const double *__rest
     gids[s] = gid ? gid[i] : (int32_t)i;
 }
 
+// Make the slot order inside every leaf deterministic (ascending caller index):
+// the atomic ranks of k_leaf_keys are not.  Leaves hold ~N_opt points.
+__global__ void k_leaf_sort(const int32_t *__restrict__ leaf_start, int64_t nleaves, double *__restrict__ xs,
+                            double *__restrict__ ys, double *__restrict__ hs, int32_t *__restrict__ perm,
+                            int32_t *__restrict__ gids) {
+    int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= nleaves) return;
+    int s = leaf_start[l], e = leaf_start[l + 1];
+    for (int a = s + 1; a < e; a++) {
+        int32_t pk = perm[a];
+        if (pk >= perm[a - 1]) continue;
+        double x = xs[a], y = ys[a], h = hs[a];
+        int32_t gk = gids[a];
+        int b = a - 1;
+        while (b >= s && perm[b] > pk) {
+            xs[b + 1] = xs[b]; ys[b + 1] = ys[b]; hs[b + 1] = hs[b];
+            perm[b + 1] = perm[b]; gids[b + 1] = gids[b];
+            b--;
+        }
+        xs[b + 1] = x; ys[b + 1] = y; hs[b + 1] = h; perm[b + 1] = pk; gids[b + 1] = gk;
+    }
+}
+
 static tm_status ensure_points(tm_ctx *ctx, int64_t n) {
     if (n <= ctx->cap_points) return TM_OK;
     free_points(ctx);
@@ -315,14 +379,22 @@ static tm_status ensure_points(tm_ctx *ctx, int64_t n) {
     return TM_OK;
 }
 
-static tm_status ensure_bins(tm_ctx *ctx, int64_t nb) {
-    int64_t ntiles = (nb + SCAN_TILE - 1) / SCAN_TILE;
+static tm_status ensure_bins(tm_ctx *ctx, int64_t nb, int64_t nleaves) {
+    int64_t ntiles = (std::max(nb, nleaves) + SCAN_TILE - 1) / SCAN_TILE;
     if (nb + 1 > ctx->cap_bins) {
-        cudaFree(ctx->bin_count); cudaFree(ctx->bin_start);
-        ctx->bin_count = ctx->bin_start = nullptr;
+        cudaFree(ctx->bin_count); cudaFree(ctx->rlev); cudaFree(ctx->leaf_off);
+        ctx->bin_count = nullptr; ctx->rlev = nullptr; ctx->leaf_off = nullptr;
         TM_CUDA_TRY(ctx, cudaMalloc(&ctx->bin_count, (nb + 1) * sizeof(int32_t)));
-        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->bin_start, (nb + 1) * sizeof(int32_t)));
+        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->rlev, (nb + 1) * sizeof(uint8_t)));
+        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->leaf_off, (nb + 1) * sizeof(int32_t)));
         ctx->cap_bins = nb + 1;
+    }
+    if (nleaves + 1 > ctx->cap_leaves) {
+        cudaFree(ctx->leaf_count); cudaFree(ctx->leaf_start);
+        ctx->leaf_count = ctx->leaf_start = nullptr;
+        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->leaf_count, (nleaves + 1) * sizeof(int32_t)));
+        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->leaf_start, (nleaves + 1) * sizeof(int32_t)));
+        ctx->cap_leaves = nleaves + 1;
     }
     if (ntiles > ctx->cap_block_sums) {
         cudaFree(ctx->block_sums);
@@ -353,18 +425,31 @@ extern "C" tm_status tm_grid_bin(tm_ctx *ctx, const double *x, const double *y, 
     tm_status s = ensure_points(ctx, n_local);
     if (s != TM_OK) return s;
     int64_t nb = (int64_t)ctx->bg.nbx * ctx->bg.nby;
-    if ((s = ensure_bins(ctx, nb)) != TM_OK) return s;
+    // leaves: 4^r per bin; for r > 0, 4^r < 4 count / N_opt, so the total is below nb + 4 N / N_opt
+    int64_t nleaves_max = nb + (int64_t)ceil(4.0 * (double)n_local / ctx->p.n_opt) + 1;
+    if ((s = ensure_bins(ctx, nb, nleaves_max)) != TM_OK) return s;
     TM_CUDA_TRY(ctx, cudaMemsetAsync(ctx->bin_count, 0, nb * sizeof(int32_t), ctx->stream));
     const Grid &g = ctx->grid;
     unsigned blocks = (unsigned)((n_local + 255) / 256);
     k_bin_keys<<<blocks, 256, 0, ctx->stream>>>(x, y, n_local, ctx->bg, g.x0, g.y0, g.x1, g.y1, ctx->key,
-                                                ctx->rank, ctx->bin_count, ctx->dst);
+                                                ctx->bin_count, ctx->dst);
     if ((s = tm_internal_check_launch(ctx, "k_bin_keys")) != TM_OK) return s;
-    if ((s = scan_counts(ctx, ctx->bin_count, ctx->bin_start, nb)) != TM_OK) return s;
-    k_bin_scatter<<<blocks, 256, 0, ctx->stream>>>(x, y, gid, n_local, ctx->key, ctx->rank, ctx->bin_start, g.x0,
+    // per-bin level and number of leaves (reuses leaf_count as scratch), scan -> leaf_off
+    k_bin_levels<<<(unsigned)((nb + 255) / 256), 256, 0, ctx->stream>>>(
+        ctx->bin_count, nb, ctx->p.n_opt, (ctx->p.flags & TM_F_TWO_LEVEL_BINS) ? 1 : 0, ctx->rlev, ctx->leaf_count);
+    if ((s = scan_counts(ctx, ctx->leaf_count, ctx->leaf_off, nb)) != TM_OK) return s;
+    TM_CUDA_TRY(ctx, cudaMemsetAsync(ctx->leaf_count, 0, nleaves_max * sizeof(int32_t), ctx->stream));
+    k_leaf_keys<<<blocks, 256, 0, ctx->stream>>>(x, y, n_local, ctx->bg, g.x0, g.y0, g.x1, g.y1, ctx->key, ctx->rlev,
+                                                 ctx->leaf_off, ctx->leaf_count, ctx->rank);
+    if ((s = tm_internal_check_launch(ctx, "k_leaf_keys")) != TM_OK) return s;
+    if ((s = scan_counts(ctx, ctx->leaf_count, ctx->leaf_start, nleaves_max)) != TM_OK) return s;
+    k_bin_scatter<<<blocks, 256, 0, ctx->stream>>>(x, y, gid, n_local, ctx->key, ctx->rank, ctx->leaf_start, g.x0,
                                                    g.y0, g.x1, g.y1, g, ctx->mu, ctx->c, ctx->xs, ctx->ys,
                                                    ctx->hs, ctx->perm, ctx->gids);
     if ((s = tm_internal_check_launch(ctx, "k_bin_scatter")) != TM_OK) return s;
+    k_leaf_sort<<<(unsigned)((nleaves_max + 255) / 256), 256, 0, ctx->stream>>>(ctx->leaf_start, nleaves_max, ctx->xs,
+                                                                              ctx->ys, ctx->hs, ctx->perm, ctx->gids);
+    if ((s = tm_internal_check_launch(ctx, "k_leaf_sort")) != TM_OK) return s;
     ctx->n_local = n_local;
     ctx->n_owned = n_owned;
     ctx->have_bins = true;
@@ -375,7 +460,8 @@ extern "C" tm_status tm_grid_bin(tm_ctx *ctx, const double *x, const double *y, 
 tm_status tm_internal_fill_cell_args(tm_ctx *ctx, CellArgs *a) {
     memset(a, 0, sizeof(*a));
     a->xs = ctx->xs; a->ys = ctx->ys; a->hs = ctx->hs;
-    a->perm = ctx->perm; a->gids = ctx->gids; a->bin_start = ctx->bin_start;
+    a->perm = ctx->perm; a->gids = ctx->gids;
+    a->rlev = ctx->rlev; a->leaf_off = ctx->leaf_off; a->leaf_start = ctx->leaf_start;
     a->bg = ctx->bg;
     a->n_local = ctx->n_local; a->n_owned = ctx->n_owned;
     a->grid = ctx->grid;

@@ -55,11 +55,15 @@ TM_HD Line bisector(double dx, double dy) {
     return L;
 }
 
-// Cramer intersection of two lines, canonical (exactly symmetric in A,B)
-TM_HD void cramer(const Line &A, const Line &B, double &x, double &y) {
+// Cramer intersection of two lines, canonical: inv = fl(1/det),
+// x = fl(num_x * inv), y = fl(num_y * inv) -- one division per vertex and
+// exactly symmetric in (A, B).  Returns inv (for error bounds).
+TM_HD double cramer(const Line &A, const Line &B, double &x, double &y) {
     double det = csub(cmul(A.nx, B.ny), cmul(A.ny, B.nx));
-    x = cdiv(csub(cmul(A.r, B.ny), cmul(A.ny, B.r)), det);
-    y = cdiv(csub(cmul(A.nx, B.r), cmul(A.r, B.nx)), det);
+    double inv = cdiv(1.0, det);
+    x = cmul(csub(cmul(A.r, B.ny), cmul(A.ny, B.r)), inv);
+    y = cmul(csub(cmul(A.nx, B.r), cmul(A.r, B.nx)), inv);
+    return inv;
 }
 
 // wall codes: octagon side k (outward normal at 45k deg) -> -1-k;

@@ -26,14 +26,40 @@ struct DevState {
 struct BinGeom {
     int32_t nbx, nby;
     double x0, y0;   // bin grid origin (= box origin)
-    double sx, sy;   // bin size
+    double sx, sy;   // level-0 bin size
     double isx, isy; // 1/size
 };
+
+// Two-level cell list: level-0 bin b (row-major) holds 4^rlev[b] leaves in
+// Morton order; leaf_start is indexed by leaf_off[b] + morton index.
+constexpr int MAX_SUBLEVEL = 5;
+
+__host__ __device__ __forceinline__ uint32_t part1by1(uint32_t v) {
+    v &= 0x0000ffffu;
+    v = (v | (v << 8)) & 0x00ff00ffu;
+    v = (v | (v << 4)) & 0x0f0f0f0fu;
+    v = (v | (v << 2)) & 0x33333333u;
+    v = (v | (v << 1)) & 0x55555555u;
+    return v;
+}
+__host__ __device__ __forceinline__ uint32_t morton2(uint32_t x, uint32_t y) { return part1by1(x) | (part1by1(y) << 1); }
+
+// leaf coordinate of x at depth r (consistent between binning and search):
+// floor((x-x0)*isx*2^r) clamped into the level-0 bin floor((x-x0)*isx)
+__device__ __forceinline__ int leaf_coord(double x, double x0, double is, int nb, int r) {
+    int b = (int)floor((x - x0) * is);
+    b = b < 0 ? 0 : (b >= nb ? nb - 1 : b);
+    int u = (int)floor((x - x0) * is * (double)(1 << r));
+    int lo = b << r, hi = ((b + 1) << r) - 1;
+    return u < lo ? lo : (u > hi ? hi : u);
+}
 
 // everything a cell kernel reads or writes
 struct CellArgs {
     const double *xs, *ys, *hs;
-    const int32_t *perm, *gids, *bin_start;
+    const int32_t *perm, *gids;
+    const uint8_t *rlev;
+    const int32_t *leaf_off, *leaf_start;
     BinGeom bg;
     int64_t n_local, n_owned;
     Grid grid;
@@ -75,13 +101,19 @@ struct tm_ctx {
     int64_t n_local = 0, n_owned = 0, cap_points = 0, cap_bins = 0;
     double *xs = nullptr, *ys = nullptr, *hs = nullptr;
     int32_t *perm = nullptr, *gids = nullptr, *key = nullptr, *rank = nullptr;
-    int32_t *bin_count = nullptr, *bin_start = nullptr, *block_sums = nullptr;
-    int64_t cap_block_sums = 0;
+    int32_t *bin_count = nullptr, *block_sums = nullptr;
+    uint8_t *rlev = nullptr;
+    int32_t *leaf_off = nullptr, *leaf_count = nullptr, *leaf_start = nullptr;
+    int64_t cap_block_sums = 0, cap_leaves = 0;
     // DistMesh scratch
     double *partials = nullptr;
     int64_t cap_partials = 0;
     // stats scratch
     double *stat_acc = nullptr;
+    // cells of the 16-lane pass that need the 32-lane retry pass
+    int32_t *retry_list = nullptr;
+    unsigned long long *retry_cnt = nullptr;
+    int64_t cap_retry = 0;
     // device health counters
     tmg::DevState *dst = nullptr;
     bool have_cells = false;

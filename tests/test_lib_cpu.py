@@ -95,8 +95,8 @@ def test_host_cramer_symmetric_and_accurate(lib):
         x = (a[2] * b[1] - a[1] * b[2]) / det
         y = (a[0] * b[2] - a[2] * b[0]) / det
         cond = (abs(A[0] * B[1]) + abs(A[1] * B[0])) / abs(float(det))
-        assert abs(xy1[0] - float(x)) <= 16 * cond * 2.2e-16 * (abs(float(x)) + abs(A[2] * B[1]) / abs(float(det)) + abs(A[1] * B[2]) / abs(float(det)))
-        assert abs(xy1[1] - float(y)) <= 16 * cond * 2.2e-16 * (abs(float(y)) + abs(A[0] * B[2]) / abs(float(det)) + abs(A[2] * B[0]) / abs(float(det)))
+        assert abs(xy1[0] - float(x)) <= 24 * cond * 2.2e-16 * (abs(float(x)) + abs(A[2] * B[1]) / abs(float(det)) + abs(A[1] * B[2]) / abs(float(det)))
+        assert abs(xy1[1] - float(y)) <= 24 * cond * 2.2e-16 * (abs(float(y)) + abs(A[0] * B[2]) / abs(float(det)) + abs(A[2] * B[0]) / abs(float(det)))
 
 
 def test_host_bilinear_exact_on_bilinear_field(lib):
