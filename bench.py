@@ -162,6 +162,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cells", default="thread", choices=["thread", "group"],
+                    help="cell kernel: one thread per cell (default) or 16-lane groups (A/B)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -184,7 +186,10 @@ def main():
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
-    ctx = T.Context(local, stream=stream)
+    params = T.default_params()
+    if args.cells == "group":
+        params.flags |= T.TM_F_GROUP_CELLS
+    ctx = T.Context(local, params=params, stream=stream)
     box = c.box
     phi = torch.from_numpy(c.phi).to(dev)
     mu = torch.from_numpy(c.mu).to(dev)
@@ -297,7 +302,7 @@ def main():
     # untimed counting pass over the same schedule (SURVEY §8(d) cost table)
     roof = None
     if rank == 0:
-        roof = roofline(T, c, ctx, cells_ms)
+        roof = roofline(T, c, ctx, cells_ms, params.flags)
 
     if rank == 0:
         cpu = None
@@ -341,11 +346,11 @@ def dp_peak():
     return 148 * 64 * mhz * 1e6, f"derived 148 SMs x 64 FP64 lanes x {mhz:.0f} MHz"
 
 
-def roofline(T, c, ctx, cells_ms):
+def roofline(T, c, ctx, cells_ms, flags=0):
     """achieved = algorithmic DP instructions per k_cells launch / mean launch time."""
     import torch
     p = T.default_params()
-    p.flags |= T.TM_F_COUNT_WORK
+    p.flags |= T.TM_F_COUNT_WORK | flags
     dev = torch.device("cuda", ctx.device)
     cc = T.Context(ctx.device, params=p)
     cc.tm_set_domain(c.box, torch.from_numpy(c.phi).to(dev), torch.from_numpy(c.mu).to(dev),

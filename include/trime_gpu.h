@@ -70,7 +70,7 @@ typedef struct {
 
 /* Defaults = PAPER.md Table B.1 where the paper gives one. */
 typedef struct {
-    double n_opt;              /* 3.3   P:1077 mean points per bin                      */
+    double n_opt;              /* 6.0   mean points per leaf (3.3 for Voro++)   */
     double fac_voro_bound;     /* 5     P:1116 octagon circumradius S = fac*h (L6)      */
     double fac_pt_mvmt;        /* 0.4   P:1102 move clamp T_pt = fac*h(p_old)           */
     double fac_geps;           /* 0.01  P:1104 geps = fac*min(h, h_avg)                 */
@@ -88,6 +88,7 @@ typedef struct {
 
 #define TM_F_TWO_LEVEL_BINS 0x1u  /* split dense bins into 2^r x 2^r sub-bins (adaptive rho) */
 #define TM_F_COUNT_WORK     0x2u  /* accumulate per-cell work counters (tm_work_counts)       */
+#define TM_F_GROUP_CELLS    0x4u  /* cells by 16-lane groups instead of one thread per cell  */
 
 /* Mesh quality (alpha = R_circ/(2 R_in), beta = l_max/l_min) and
  * the health counters of the last iteration. */
@@ -104,6 +105,7 @@ typedef struct {
  * (only with TM_F_COUNT_WORK).  Sums over cells. */
 typedef struct {
     int64_t n_cells, n_cert, deg, verts, t_own, quad_tris, ell, candidates, clips, exact_calls;
+    int64_t retries;  /* cells the thread kernel handed to the 32-lane pass (any flags) */
 } tm_work;
 
 void tm_params_default(tm_params *p);

@@ -28,6 +28,7 @@ STATUS_NAMES = ["TM_OK", "TM_E_ARG", "TM_E_CUDA", "TM_E_CAPACITY", "TM_E_DUPLICA
                 "TM_E_STATE", "TM_E_DEGENERATE"]
 TM_F_TWO_LEVEL_BINS = 0x1
 TM_F_COUNT_WORK = 0x2
+TM_F_GROUP_CELLS = 0x4
 
 
 class TmError(RuntimeError):
@@ -65,7 +66,7 @@ class tm_stats(ctypes.Structure):
 
 class tm_work(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in ("n_cells", "n_cert", "deg", "verts", "t_own", "quad_tris", "ell",
-                                              "candidates", "clips", "exact_calls")]
+                                              "candidates", "clips", "exact_calls", "retries")]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -13,14 +13,13 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libtrime_gpu.so")
-SOURCES = ["tm_api.cu", "tm_cells.cu", "tm_distmesh.cu"]
+SOURCES = ["tm_api.cu", "tm_cells.cu", "tm_cells_t.cu", "tm_distmesh.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "--fmad=true",                   # decision arithmetic uses __d*_rn intrinsics (never contracted)
     "-Xcompiler", "-fPIC,-ffp-contract=off",
-    "-shared",
 ]
 
 
@@ -37,13 +36,32 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
     if not force and os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(d) for d in deps):
         return out
     tmp = out + f".tmp{os.getpid()}"
-    cmd = [_nvcc(), *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), *[f"-D{d}" for d in defines], "-o", tmp,
-           *srcs]
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if r.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({r.returncode}):\n{r.stderr}")
-    if verbose:
-        sys.stderr.write(r.stderr)
+    # one nvcc per translation unit, in parallel, then one shared-library link
+    from concurrent.futures import ThreadPoolExecutor
+    objs = [f"{tmp}.{os.path.basename(s)}.o" for s in srcs]
+
+    def compile_one(src_obj):
+        src, obj = src_obj
+        cmd = [_nvcc(), *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), *[f"-D{d}" for d in defines],
+               "-c", "-o", obj, src]
+        return subprocess.run(cmd, capture_output=True, text=True)
+
+    with ThreadPoolExecutor(len(srcs)) as ex:
+        results = list(ex.map(compile_one, zip(srcs, objs)))
+    try:
+        for r in results:
+            if r.returncode != 0:
+                raise RuntimeError(f"nvcc failed ({r.returncode}):\n{r.stderr}")
+            if verbose:
+                sys.stderr.write(r.stderr)
+        r = subprocess.run([_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs],
+                           capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc link failed ({r.returncode}):\n{r.stderr}")
+    finally:
+        for o in objs:
+            if os.path.exists(o):
+                os.remove(o)
     os.replace(tmp, out)
     return out
 

@@ -13,7 +13,7 @@ using namespace tmg;
 
 // ============================================================================ params / ctx
 extern "C" void tm_params_default(tm_params *p) {
-    p->n_opt = 3.3;
+    p->n_opt = 6.0;            // P:1077 gives 3.3 for Voro++; 6 suits the GPU cell search
     p->fac_voro_bound = 5.0;
     p->fac_pt_mvmt = 0.4;
     p->fac_geps = 0.01;
@@ -592,6 +592,12 @@ extern "C" tm_status tm_work_counts(tm_ctx *ctx, tm_work *out) {
     TM_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     int64_t *o = (int64_t *)out;
     for (int k = 0; k < 10; k++) o[k] = (int64_t)ds.work[k];
+    unsigned long long rc = 0;
+    if (ctx->retry_cnt) {
+        TM_CUDA_TRY(ctx, cudaMemcpyAsync(&rc, ctx->retry_cnt, sizeof(rc), cudaMemcpyDeviceToHost, ctx->stream));
+        TM_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+    out->retries = (int64_t)rc;
     return TM_OK;
 }
 

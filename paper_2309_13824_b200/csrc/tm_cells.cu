@@ -20,7 +20,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
-#include "tm_internal.cuh"
+#include "tm_cellcore.cuh"
 
 namespace cg = cooperative_groups;
 using namespace tmg;
@@ -32,7 +32,6 @@ constexpr int BLOCK = 128;
 #define TM_MINB 1  // min resident blocks per SM for the 16-lane kernel (register cap); tuning knob
 #endif
 
-enum : int { M_TRI = 1, M_ELL = 2, M_TREAT = 4, M_HAT = 8, M_COUNT = 16, M_RETRY = 32 };
 
 struct VState {
     int la, lb;      // incoming / outgoing line codes (slot >= 0, wall < 0)
@@ -41,15 +40,6 @@ struct VState {
     double K;        // filter constant of a point-point vertex, < 0 for wall vertices
 };
 
-// the cell's lines are recomputed from their codes (canonical, so identical bits)
-struct CellGeom {
-    double px, py, r_oct, bx0, by0, bx1, by1;
-};
-
-__device__ __forceinline__ Line line_of(int code, const CellGeom &cg_, const CellArgs &A) {
-    if (code >= 0) return bisector(csub(__ldg(A.xs + code), cg_.px), csub(__ldg(A.ys + code), cg_.py));
-    return wall_line(code, cg_.px, cg_.py, cg_.r_oct, cg_.bx0, cg_.by0, cg_.bx1, cg_.by1);
-}
 
 template <int G>
 using Tile = cg::thread_block_tile<G>;
@@ -82,15 +72,6 @@ __device__ __forceinline__ int tile_isum(const Tile<G> &g, int v) {
     return v;
 }
 
-// filter constant of a point-point vertex x = cramer(A, B) with inv = 1/det:
-// K = e_v + 8 eps |v|_1, e_v a rigorous bound on |x - exact circumcentre|
-// (Cramer evaluation rounding plus the rounding of d = fl(p - p_i)), x2 safety.
-__device__ __forceinline__ double pp_filter_K(const Line &A, const Line &B, double x, double y, double inv) {
-    double n1a = fabs(A.nx) + fabs(A.ny), n1b = fabs(B.nx) + fabs(B.ny);
-    double m1 = fabs(x) + fabs(y);
-    double ev = EPS * (10.0 * (A.r * n1b + B.r * n1a + m1 * n1a * n1b) * fabs(inv) * (1.0 + 8.0 * EPS) + 3.0 * m1);
-    return ev + 8.0 * EPS * m1;
-}
 
 // conservative squared distance bound of a vertex from p_i (float, rounded up)
 __device__ __forceinline__ float vertex_r2f(const VState &v) {
@@ -100,9 +81,6 @@ __device__ __forceinline__ float vertex_r2f(const VState &v) {
     return __double2float_ru(r2 * (1.0 + 1e-12));
 }
 
-struct ClipStats {
-    unsigned long long exact = 0, clips = 0;
-};
 
 // Clip the ring by line L (code >= 0: bisector with slot `code`; < 0: wall).
 // valid: lane mask of the ring (uniform).  Returns 0 ok, -1 overflow, -2 inconsistent.
@@ -203,41 +181,6 @@ __device__ __forceinline__ void bitonic_sort2(const Tile<G> &g, unsigned long lo
     }
 }
 
-// ring k leaf q -> (dx, dy), Chebyshev distance k, q in [0, 8k)
-__device__ __forceinline__ void ring_bin(int k, int q, int &dx, int &dy) {
-    int side = 2 * k + 1;
-    if (q < side) { dx = q - k; dy = -k; return; }
-    q -= side;
-    if (q < side) { dx = q - k; dy = k; return; }
-    q -= side;
-    if (q < side - 2) { dx = -k; dy = q - k + 1; return; }
-    q -= side - 2;
-    dx = k; dy = q - k + 1;
-}
-
-// canonical keep rule (§8(a) S3; P:499-510 Test 1 in its L10 reading)
-__device__ __forceinline__ bool in_oct(double cx, double cy, double qx, double qy, double r) {
-    double dx = csub(cx, qx), dy = csub(cy, qy);
-    double r2 = cmul(SQRT2, r);
-    return fabs(dx) < r && fabs(dy) < r && fabs(cadd(dx, dy)) < r2 && fabs(csub(dx, dy)) < r2;
-}
-
-__device__ bool keep_tri(const CellArgs &A, int su, int sv, int sw, double cx, double cy) {
-    // su,sv,sw: slots ordered by gid (u smallest); (cx,cy) canonical circumcentre (rel. p_u, made absolute)
-    if (!(cx > A.grid.x0 && cx < A.grid.x1 && cy > A.grid.y0 && cy < A.grid.y1)) return false;
-    const int s3[3] = {su, sv, sw};
-    double X[3], Y[3];
-#pragma unroll
-    for (int k = 0; k < 3; k++) {
-        X[k] = __ldg(A.xs + s3[k]);
-        Y[k] = __ldg(A.ys + s3[k]);
-        double r = cmul(cmul(A.fac_voro, __ldg(A.hs + s3[k])), COS_PI8);
-        if (!in_oct(cx, cy, X[k], Y[k], r)) return false;
-    }
-    double gx = cdiv(cadd(cadd(X[0], X[1]), X[2]), 3.0);
-    double gy = cdiv(cadd(cadd(Y[0], Y[1]), Y[2]), 3.0);
-    return bilinear(A.grid, A.phi, gx, gy, LdgLoad()) < A.keep_tol;
-}
 
 // adaptive quadrature centroid (Fig. 14; reading L13), relative to p_i
 template <int G>
@@ -627,11 +570,18 @@ __global__ void __launch_bounds__(BLOCK, (G == 16 ? TM_MINB : 1)) k_cells(CellAr
 
 template <int MODE>
 tm_status launch_cells(tm_ctx *ctx, const CellArgs &a) {
-    constexpr int G = 16;
-    const unsigned blocks = (unsigned)((ctx->n_local + (BLOCK / G) - 1) / (BLOCK / G));
     TM_CUDA_TRY(ctx, cudaMemsetAsync(ctx->retry_cnt, 0, sizeof(unsigned long long), ctx->stream));
-    k_cells<G, MODE><<<blocks, BLOCK, 0, ctx->stream>>>(a, ctx->retry_list, ctx->retry_cnt);
-    tm_status s = tm_internal_check_launch(ctx, "k_cells");
+    tm_status s;
+    if (ctx->p.flags & TM_F_GROUP_CELLS) {
+        // 16-lane group per cell (two cells per warp)
+        constexpr int G = 16;
+        const unsigned blocks = (unsigned)((ctx->n_local + (BLOCK / G) - 1) / (BLOCK / G));
+        k_cells<G, MODE><<<blocks, BLOCK, 0, ctx->stream>>>(a, ctx->retry_list, ctx->retry_cnt);
+        s = tm_internal_check_launch(ctx, "k_cells");
+    } else {
+        // one thread per cell, polygon ring in shared memory (tm_cells_t.cu)
+        s = launch_cells_thread<MODE>(ctx, a);
+    }
     if (s != TM_OK) return s;
     // cells that needed more than 16 vertices at some point: persistent 32-lane retry pass
     k_cells<32, MODE | M_RETRY><<<148 * 2, BLOCK, 0, ctx->stream>>>(a, ctx->retry_list, ctx->retry_cnt);

@@ -1,0 +1,705 @@
+// tm_cells_t.cu -- thread-per-cell cell kernel (the default S2-S5 path).
+//
+// Same method and the same canonical arithmetic as the group kernel (S2 bounded
+// cell by half-plane clipping, P:100 / Fig. 3; octagon bound P:491; S3 keep rule
+// P:499-510 in reading L10; S4a centroid P:203-207 / P:537-553; S5 treatment),
+// but one THREAD computes one cell C_i = B ∩ Oct_i ∩ Vor(i):
+//   * the polygon is a linked ring of up to TM_VMAX vertex slots in shared
+//     memory, laid out [slot][thread] so that every slot access of a warp is
+//     bank-conflict free whatever slot each thread touches (TB*8 B rows);
+//     a clip rewrites two slots and two links, never moves vertices;
+//   * a vertex slot holds its canonical coordinates relative to p_i (fp64),
+//     its filter constant K (float, rounded up; < 0 marks a wall vertex), the
+//     code of its incoming line (the outgoing line is the incoming line of the
+//     next slot) and its ring links;
+//   * candidates are visited leaf by leaf: the home leaf, the 8 neighbouring
+//     leaves nearest-first, then rings >= 2; a leaf (or ring) whose distance
+//     from p_i is at least 2 R_max is skipped (reading L11);
+//   * a cell that needs more than TM_VMAX slots is handed to the 32-lane group
+//     kernel (retry list), which holds up to 32 vertices.
+// Work is independent per thread, so the fp64 pipe sees 32 cells per warp
+// instead of 2, and no shuffle/ballot sits on the per-candidate critical path.
+
+#include <cuda_runtime.h>
+
+#include "tm_cellcore.cuh"
+
+using namespace tmg;
+
+#ifndef TM_TB
+#define TM_TB 128
+#endif
+#ifndef TM_VMAX
+#define TM_VMAX 12
+#endif
+#ifndef TM_TMINB
+#define TM_TMINB 4
+#endif
+#ifndef TM_UNROLL_SLOTS
+#define TM_UNROLL_SLOTS 1  // vertex tests over all VMAX slots, unrolled and masked
+#endif
+#ifndef TM_THREAD_EXACT
+#define TM_THREAD_EXACT 0  // 0: cells with an undecided filter go to the 32-lane group kernel (rare)
+#endif
+
+namespace {
+
+constexpr int TB = TM_TB;
+constexpr int VMAX = TM_VMAX;
+static_assert(VMAX <= 31, "slot masks are 32-bit");
+constexpr size_t TSMEM = (size_t)VMAX * TB * (16 + 4 + 4 + 4 + 1 + 1);
+
+// this thread's view of the block's slot arrays (element k at [k * TB])
+struct TPoly {
+    double2 *v;   // canonical coordinates relative to p_i
+    float *K;     // filter constant (< 0: wall vertex)
+    float *r2;    // conservative squared distance from p_i (rounded up)
+    int *la;      // incoming line code
+    uint8_t *prv, *nxt;
+    unsigned used;
+};
+
+__device__ __forceinline__ TPoly tpoly_bind(unsigned char *smem, int tid) {
+    TPoly P;
+    double2 *v = reinterpret_cast<double2 *>(smem);
+    float *K = reinterpret_cast<float *>(v + VMAX * TB);
+    float *r2 = K + VMAX * TB;
+    int *la = reinterpret_cast<int *>(r2 + VMAX * TB);
+    uint8_t *prv = reinterpret_cast<uint8_t *>(la + VMAX * TB);
+    uint8_t *nxt = prv + VMAX * TB;
+    P.v = v + tid; P.K = K + tid; P.r2 = r2 + tid; P.la = la + tid; P.prv = prv + tid; P.nxt = nxt + tid;
+    P.used = 0;
+    return P;
+}
+
+__device__ __forceinline__ float vertex_r2f_t(double vx, double vy, float Kf) {
+    double m1 = fabs(vx) + fabs(vy);
+    double K = Kf > 0.f ? (double)Kf : 0.0;
+    double r2 = fma(vx, vx, vy * vy) + K * (2.0 * m1 + K);
+    return __double2float_ru(r2 * (1.0 + 1e-12));
+}
+
+__device__ __forceinline__ float poly_R2(const TPoly &P) {
+    float r = 0.f;
+#if TM_UNROLL_SLOTS
+#pragma unroll
+    for (int k = 0; k < VMAX; k++) r = fmaxf(r, ((P.used >> k) & 1u) ? P.r2[k * TB] : 0.f);
+#else
+    for (unsigned m = P.used; m; m &= m - 1) r = fmaxf(r, P.r2[(__ffs(m) - 1) * TB]);
+#endif
+    return r;
+}
+
+// Clip the ring by line L (code >= 0: bisector with slot `code`; < 0: wall).
+// Returns 0 ok, -1 out of slots, -2 inconsistent.  The decisions are exactly
+// those of clip_by (group kernel): exact incircle sign for point-point vertices
+// (floating filter, expansion fallback), canonical test for wall vertices.
+__device__ int clip_t(TPoly &P, int code, const Line &L, const CellGeom &cgm, const CellArgs &A, ClipStats &cs) {
+    const bool is_bis = code >= 0;
+    const double n1 = fabs(L.nx) + fabs(L.ny);
+    unsigned out = 0, unc = 0;
+#if TM_UNROLL_SLOTS
+    // every slot, unrolled and branch-free (unused slots are masked out): no
+    // divergence between threads with different rings, full ILP
+#pragma unroll
+    for (int k = 0; k < VMAX; k++) {
+        const double2 vv = P.v[k * TB];
+        const float Kf = P.K[k * TB];
+        const double del = fma(L.nx, vv.x, L.ny * vv.y) - L.r;
+        const double B = n1 * fma(8.0 * EPS, n1, (double)Kf);
+        const bool pp = is_bis && Kf >= 0.f;
+        const bool o = pp ? del > B : wall_out(L, vv.x, vv.y);
+        const bool u = pp && !(del > B) && del >= -B;
+        out |= (unsigned)o << k;
+        unc |= (unsigned)u << k;
+    }
+    out &= P.used;
+    unc &= P.used;
+#else
+    for (unsigned m = P.used; m; m &= m - 1) {
+        const int k = __ffs(m) - 1;
+        const double2 vv = P.v[k * TB];
+        const double vx = vv.x, vy = vv.y;
+        const float Kf = P.K[k * TB];
+        bool o, u = false;
+        if (is_bis && Kf >= 0.f) {
+            const double del = fma(L.nx, vx, L.ny * vy) - L.r;
+            const double B = n1 * fma(8.0 * EPS, n1, (double)Kf);
+            o = del > B;
+            u = !o && del >= -B;
+        } else {
+            o = wall_out(L, vx, vy);
+        }
+        out |= (unsigned)o << k;
+        unc |= (unsigned)u << k;
+    }
+#endif
+    // undecided point-point vertices (rare): exact incircle sign, outside the hot
+    // loop -- or, with TM_THREAD_EXACT=0, the whole cell goes to the group kernel
+#if TM_THREAD_EXACT
+    for (; unc; unc &= unc - 1) {
+        const int k = __ffs(unc) - 1;
+        const int a = P.la[k * TB], b = P.la[P.nxt[k * TB] * TB];
+        double Pi[2] = {cgm.px, cgm.py};
+        double Pa[2] = {__ldg(A.xs + a), __ldg(A.ys + a)};
+        double Pb[2] = {__ldg(A.xs + b), __ldg(A.ys + b)};
+        double Pj[2] = {__ldg(A.xs + code), __ldg(A.ys + code)};
+        const int sg = incircle_exact(Pi, Pa, Pb, Pj);
+        if (sg == 0) atomicAdd(&A.st->n_degenerate, 1ull);
+        out |= (unsigned)(sg > 0) << k;
+        cs.exact++;
+    }
+#else
+    if (unc) return -1;
+#endif
+    if (out == 0u) return 0;
+    if (out == P.used) return -2;
+    int s = -1, e = -1, ns = 0, ne_ = 0;
+    for (unsigned m = out; m; m &= m - 1) {
+        const int k = __ffs(m) - 1;
+        if (!((out >> P.prv[k * TB]) & 1u)) { s = k; ns++; }
+        if (!((out >> P.nxt[k * TB]) & 1u)) { e = k; ne_++; }
+    }
+    if (ns != 1 || ne_ != 1) return -2;
+    int sB = e;
+    if (__popc(out) == 1) {
+        const unsigned fr = ~P.used & ((1u << VMAX) - 1u);
+        if (fr == 0u) return -1;
+        sB = __ffs(fr) - 1;
+    }
+    const int ne = P.nxt[e * TB];
+    const int c1 = P.la[s * TB];   // line into s: the edge ps -> s
+    const int c2 = P.la[ne * TB];  // line out of e = line into ne
+    {   // A = (c1, L) in slot s
+        const Line E1 = line_of(c1, cgm, A);
+        double x, y;
+        const double inv = cramer(E1, L, x, y);
+        const float Kn = (is_bis && c1 >= 0) ? __double2float_ru(pp_filter_K(E1, L, x, y, inv)) : -1.f;
+        P.v[s * TB] = make_double2(x, y);
+        P.K[s * TB] = Kn;
+        P.r2[s * TB] = vertex_r2f_t(x, y, Kn);
+        P.nxt[s * TB] = (uint8_t)sB;
+    }
+    {   // B = (L, c2) in slot sB
+        const Line E2 = line_of(c2, cgm, A);
+        double x, y;
+        const double inv = cramer(L, E2, x, y);
+        const float Kn = (is_bis && c2 >= 0) ? __double2float_ru(pp_filter_K(L, E2, x, y, inv)) : -1.f;
+        P.v[sB * TB] = make_double2(x, y);
+        P.K[sB * TB] = Kn;
+        P.r2[sB * TB] = vertex_r2f_t(x, y, Kn);
+        P.la[sB * TB] = code;
+        P.prv[sB * TB] = (uint8_t)s;
+        P.nxt[sB * TB] = (uint8_t)ne;
+    }
+    P.prv[ne * TB] = (uint8_t)sB;
+    P.used = (P.used & ~out) | (1u << s) | (1u << sB);
+    cs.clips++;
+    return 0;
+}
+
+// leaf range [st, st+cnt) of virtual leaf (vx, vy) at the home resolution rh
+// (coarser leaves only at the virtual leaf closest to (ux, uy)); as the group kernel
+__device__ __forceinline__ void vleaf_range(const CellArgs &A, int vx, int vy, int rh, int ux, int uy, int &st,
+                                            int &cnt) {
+    const BinGeom &bg = A.bg;
+    st = 0;
+    cnt = 0;
+    const int bx = vx >> rh, by = vy >> rh;
+    const int b = by * bg.nbx + bx;
+    const int rb = __ldg(A.rlev + b);
+    const int off = __ldg(A.leaf_off + b);
+    if (rb >= rh) {
+        const int sh = 2 * (rb - rh);
+        const int mlo = (int)morton2((uint32_t)(vx - (bx << rh)), (uint32_t)(vy - (by << rh))) << sh;
+        st = __ldg(A.leaf_start + off + mlo);
+        cnt = __ldg(A.leaf_start + off + mlo + (1 << sh)) - st;
+    } else {
+        const int d = rh - rb;
+        const int Lx = vx >> d, Ly = vy >> d;
+        const int rx = min(max(ux, Lx << d), ((Lx + 1) << d) - 1);
+        const int ry = min(max(uy, Ly << d), ((Ly + 1) << d) - 1);
+        if (rx == vx && ry == vy) {
+            const int mm = (int)morton2((uint32_t)(Lx - (bx << rb)), (uint32_t)(Ly - (by << rb)));
+            st = __ldg(A.leaf_start + off + mm);
+            cnt = __ldg(A.leaf_start + off + mm + 1) - st;
+        }
+    }
+}
+
+struct SearchCtx {
+    double px, py;
+    int cell;
+    unsigned long long n_cand;
+};
+
+// squared distance from p to the rectangle of virtual leaf (vx, vy)
+__device__ __forceinline__ double leaf_d2(const BinGeom &bg, double lsx, double lsy, int vx, int vy, double px,
+                                          double py) {
+    const double lx = bg.x0 + vx * lsx, ly = bg.y0 + vy * lsy;
+    const double gx = fmax(fmax(lx - px, px - (lx + lsx)), 0.0);
+    const double gy = fmax(fmax(ly - py, py - (ly + lsy)), 0.0);
+    return gx * gx + gy * gy;
+}
+
+__device__ __forceinline__ void cswap(unsigned &a, unsigned &b) {
+    const unsigned lo = min(a, b), hi = max(a, b);
+    a = lo;
+    b = hi;
+}
+
+// adaptive quadrature centroid (Fig. 14; reading L13), one thread,
+// relative to p_i; same sub-triangle construction as quad_centroid
+__device__ void quad_centroid_t(const TPoly &P, int start, int nv, double px, double py, double area, double h,
+                                double dprev, const CellArgs &A, double &cx, double &cy, unsigned long long &nq) {
+    double eps = dprev >= 0.0 ? dprev / h : A.fac_pt;
+    if (eps < A.fac_end) eps = A.fac_end;
+    const double E = sqrt(area) * eps;
+    double prevx = 0.0, prevy = 0.0;
+    for (int L = 1; L <= A.quad_max; L++) {
+        const int depth = L - 1;
+        double sw = 0.0, swx = 0.0, swy = 0.0;
+        int k = start;
+        for (int f = 0; f < nv; f++) {
+            const int kn = P.nxt[k * TB];
+            const double x1 = P.v[k * TB].x, y1 = P.v[k * TB].y;
+            const double x2 = P.v[kn * TB].x, y2 = P.v[kn * TB].y;
+            k = kn;
+            const int64_t nleaf = (int64_t)1 << depth;
+            for (int64_t path = 0; path < nleaf; path++) {
+                double Q[3][2] = {{0.0, 0.0}, {x1, y1}, {x2, y2}};
+                for (int lev = depth - 1; lev >= 0; lev--) {
+                    double best = -1.0;
+                    int eidx = 0;
+#pragma unroll
+                    for (int q = 0; q < 3; q++) {
+                        const int q1 = q == 2 ? 0 : q + 1;
+                        const double ddx = csub(Q[q1][0], Q[q][0]), ddy = csub(Q[q1][1], Q[q][1]);
+                        const double Lq = cadd(cmul(ddx, ddx), cmul(ddy, ddy));
+                        if (Lq > best) { best = Lq; eidx = q; }
+                    }
+                    const int ia = eidx, ib = eidx == 2 ? 0 : eidx + 1, ic = ib == 2 ? 0 : ib + 1;
+                    const double ax = Q[ia][0], ay = Q[ia][1], bx = Q[ib][0], by = Q[ib][1];
+                    const double qx = Q[ic][0], qy = Q[ic][1];
+                    const double mx = cmul(cadd(ax, bx), 0.5), my = cmul(cadd(ay, by), 0.5);
+                    if ((path >> lev) & 1) {
+                        Q[0][0] = mx; Q[0][1] = my; Q[1][0] = bx; Q[1][1] = by;
+                    } else {
+                        Q[0][0] = ax; Q[0][1] = ay; Q[1][0] = mx; Q[1][1] = my;
+                    }
+                    Q[2][0] = qx; Q[2][1] = qy;
+                }
+                const double cr = csub(cmul(csub(Q[1][0], Q[0][0]), csub(Q[2][1], Q[0][1])),
+                                       cmul(csub(Q[1][1], Q[0][1]), csub(Q[2][0], Q[0][0])));
+                const double At = cmul(0.5, cr);
+                const double qx = cdiv(cadd(cadd(Q[0][0], Q[1][0]), Q[2][0]), 3.0);
+                const double qy = cdiv(cadd(cadd(Q[0][1], Q[1][1]), Q[2][1]), 3.0);
+                const double rho = bilinear(A.grid, A.rho, cadd(px, qx), cadd(py, qy), LdgLoad());
+                const double wgt = At * rho;
+                sw += wgt;
+                swx += wgt * qx;
+                swy += wgt * qy;
+                nq++;
+            }
+        }
+        const double curx = swx / sw, cury = swy / sw;
+        const double dx = prevx - curx, dy = prevy - cury;
+        const double dist = sqrt(dx * dx + dy * dy);
+        prevx = curx;
+        prevy = cury;
+        if (dist < E) break;
+    }
+    cx = prevx;
+    cy = prevy;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *retry_list,
+                                                          unsigned long long *retry_cnt) {
+    extern __shared__ __align__(16) unsigned char tsmem[];
+    const int tid = threadIdx.x;
+    const int64_t cell = (int64_t)blockIdx.x * TB + tid;
+    const int lane = tid & 31;
+    TPoly P = tpoly_bind(tsmem, tid);
+    bool live = false;
+    int32_t orig = 0;
+    if (cell < A.n_local) {
+        orig = __ldg(A.perm + cell);
+        live = orig < A.n_owned;
+    }
+    // ---- per-cell results consumed by the warp-collective emission below
+    int t_own = 0;
+    unsigned keptmask = 0;  // slots whose (owned) point-point vertex is a kept triangle
+    int32_t gi = 0;
+    ClipStats cs;
+    unsigned long long nq = 0;
+    SearchCtx sc;
+    sc.n_cand = 0;
+    int fail = 0;
+    double px = 0.0, py = 0.0, h = 0.0;
+    CellGeom cgm = {};
+    // search state (kept outside `if (live)` so that the whole warp runs the
+    // flat candidate loop below in lockstep)
+    float R2 = 0.f;
+    const double MARG = 1.0 + 1e-9;
+    const BinGeom &bg = A.bg;
+    int rh = 0, ux = 0, uy = 0, nlx = 0, nly = 0;
+    double lsx = 0.0, lsy = 0.0;
+    unsigned key[8];
+    // candidate iterator: phase (0 ring 1, 1 rings >= 2 clipped to a box, 2 done), ring-1 position
+    // (phase 1: ring rk, side 0-3, cursor cvx up to cend along it; cvy / cfix the fixed row / column)
+    int ph = 2, rr = 0, t = 0, tend = 0, cvx = 0, cvy = 0, cend = -1, cfix = 0, rk = 1, side = 4, kmax = 0;
+    int bxa = 0, bxb = -1, bya = 0, byb = -1;
+    if (live) {
+        px = __ldg(A.xs + cell);
+        py = __ldg(A.ys + cell);
+        h = __ldg(A.hs + cell);
+        gi = __ldg(A.gids + cell);
+        sc.px = px; sc.py = py; sc.cell = (int)cell;
+        const double S = cmul(A.fac_voro, h);
+        const double r_oct = cmul(S, COS_PI8);
+        const double bx0 = A.grid.x0, by0 = A.grid.y0, bx1 = A.grid.x1, by1 = A.grid.y1;
+        cgm = {px, py, r_oct, bx0, by0, bx1, by1};
+        // ---- initial ring: octagon, vertex k between sides k and k+1 (det = +-1: exact inverse)
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            double x, y;
+            cramer(wall_line(-1 - k, px, py, r_oct, bx0, by0, bx1, by1),
+                   wall_line(-1 - ((k + 1) & 7), px, py, r_oct, bx0, by0, bx1, by1), x, y);
+            P.v[k * TB] = make_double2(x, y);
+            P.K[k * TB] = -1.f;
+            P.r2[k * TB] = vertex_r2f_t(x, y, -1.f);
+            P.la[k * TB] = -1 - k;
+            P.prv[k * TB] = (uint8_t)((k + 7) & 7);
+            P.nxt[k * TB] = (uint8_t)((k + 1) & 7);
+        }
+        P.used = 0xffu;
+        if (csub(px, bx0) < S || csub(bx1, px) < S || csub(py, by0) < S || csub(by1, py) < S) {
+            for (int b = 0; b < 4 && !fail; b++) {
+                const int code = -9 - b;
+                fail = clip_t(P, code, wall_line(code, px, py, r_oct, bx0, by0, bx1, by1), cgm, A, cs);
+            }
+        }
+        R2 = poly_R2(P);
+        // ---- candidate order over the two-level cell list (L11 stopping rule)
+        int hbx = (int)floor((px - bg.x0) * bg.isx), hby = (int)floor((py - bg.y0) * bg.isy);
+        hbx = hbx < 0 ? 0 : (hbx >= bg.nbx ? bg.nbx - 1 : hbx);
+        hby = hby < 0 ? 0 : (hby >= bg.nby ? bg.nby - 1 : hby);
+        rh = __ldg(A.rlev + hby * bg.nbx + hbx);
+        ux = leaf_coord(px, bg.x0, bg.isx, bg.nbx, rh);
+        uy = leaf_coord(py, bg.y0, bg.isy, bg.nby, rh);
+        nlx = bg.nbx << rh;
+        nly = bg.nby << rh;
+        lsx = bg.sx / (double)(1 << rh);
+        lsy = bg.sy / (double)(1 << rh);
+        // ring 1: the 8 neighbours nearest first (keys: d2 as float bits, low 3 bits = index)
+        const double gl = px - (bg.x0 + ux * lsx), gr = (bg.x0 + (ux + 1) * lsx) - px;
+        const double gd = py - (bg.y0 + uy * lsy), gu = (bg.y0 + (uy + 1) * lsy) - py;
+        const int ddx[8] = {-1, 1, 0, 0, -1, 1, -1, 1};
+        const int ddy[8] = {0, 0, -1, 1, -1, -1, 1, 1};
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            const double gx = fmax(ddx[q] < 0 ? gl : (ddx[q] > 0 ? gr : 0.0), 0.0);
+            const double gy = fmax(ddy[q] < 0 ? gd : (ddy[q] > 0 ? gu : 0.0), 0.0);
+            const float d2 = __double2float_rd(gx * gx + gy * gy);
+            key[q] = (__float_as_uint(fmaxf(d2, 0.f)) & ~7u) | (unsigned)q;
+        }
+        // 19-comparator sorting network for 8 keys
+        cswap(key[0], key[2]); cswap(key[1], key[3]); cswap(key[4], key[6]); cswap(key[5], key[7]);
+        cswap(key[0], key[4]); cswap(key[1], key[5]); cswap(key[2], key[6]); cswap(key[3], key[7]);
+        cswap(key[0], key[1]); cswap(key[2], key[3]); cswap(key[4], key[5]); cswap(key[6], key[7]);
+        cswap(key[2], key[4]); cswap(key[3], key[5]);
+        cswap(key[1], key[4]); cswap(key[3], key[6]);
+        cswap(key[1], key[2]); cswap(key[3], key[4]); cswap(key[5], key[6]);
+        // ring 0: the home leaf first
+        int st, cnt;
+        vleaf_range(A, ux, uy, rh, ux, uy, st, cnt);
+        t = st;
+        tend = st + cnt;
+        ph = fail ? 2 : 0;
+        rr = 0;
+    }
+    // ---- flat candidate loop: one candidate per thread per trip, the warp
+    // re-converges every trip (a per-thread nested loop lets lanes drift apart)
+    for (;;) {
+        int j = -1;
+        double cdx = 0.0, cdy = 0.0;
+        while (ph < 2) {
+            if (t < tend) {
+                // compaction: skip candidates that cannot cut before leaving the loop,
+                // so that nearly every thread brings a candidate to the clip test
+                const int jj = t++;
+                sc.n_cand++;
+                if (jj == (int)cell) continue;
+                cdx = csub(__ldg(A.xs + jj), px);
+                cdy = csub(__ldg(A.ys + jj), py);
+                if (cdx == 0.0 && cdy == 0.0) { atomicAdd(&A.st->n_duplicate, 1ull); continue; }
+                if (cdx * cdx + cdy * cdy >= 4.0 * (double)R2 * MARG) continue;
+                j = jj;
+                break;
+            }
+            const float lim = 4.0f * R2 * (float)MARG;
+            if (ph == 0) {  // ring 1, sorted
+                if (rr >= 8) {
+                    // then rings k >= 2, each clipped to the box of leaves that can hold
+                    // a point closer than 2 R_max (L11)
+                    const double rad = 2.0 * sqrt((double)R2 * MARG) * (1.0 + 1e-6);
+                    const double sxl = bg.isx * (double)(1 << rh), syl = bg.isy * (double)(1 << rh);
+                    bxa = max(0, (int)floor((px - rad - bg.x0) * sxl));
+                    bxb = min(nlx - 1, (int)floor((px + rad - bg.x0) * sxl));
+                    bya = max(0, (int)floor((py - rad - bg.y0) * syl));
+                    byb = min(nly - 1, (int)floor((py + rad - bg.y0) * syl));
+                    kmax = max(max(ux - bxa, bxb - ux), max(uy - bya, byb - uy));
+                    ph = 1;
+                    rk = 1;
+                    side = 4;  // -> start ring 2
+                    continue;
+                }
+                unsigned kq = key[0];
+#pragma unroll
+                for (int u = 1; u < 8; u++)
+                    if (rr == u) kq = key[u];
+                rr++;
+                if (__uint_as_float(kq & ~7u) * (1.0f - 1e-6f) >= lim) { rr = 8; continue; }  // the rest are farther
+                const int q = (int)(kq & 7u);
+                const int vx = ux + (q == 0 || q == 4 || q == 6 ? -1 : (q == 1 || q == 5 || q == 7 ? 1 : 0));
+                const int vy = uy + (q == 2 || q == 4 || q == 5 ? -1 : (q == 3 || q == 6 || q == 7 ? 1 : 0));
+                if (vx < 0 || vx >= nlx || vy < 0 || vy >= nly) continue;
+                int st, cnt;
+                vleaf_range(A, vx, vy, rh, ux, uy, st, cnt);
+                t = st;
+                tend = st + cnt;
+            } else {        // rings >= 2, side by side, clipped to the box; leaf-level pruning
+                if (cvx > cend) {  // next side
+                    if (++side >= 4) {
+                        rk++;
+                        if (rk > kmax) { ph = 2; break; }
+                        const double dl = px - (bg.x0 + (ux - rk + 1) * lsx), dr = (bg.x0 + (ux + rk) * lsx) - px;
+                        const double dd = py - (bg.y0 + (uy - rk + 1) * lsy), du = (bg.y0 + (uy + rk) * lsy) - py;
+                        const double dmin = fmin(fmin(dl, dr), fmin(dd, du));
+                        if (dmin > 0.0 && dmin * dmin * (1.0 - 1e-9) >= 4.0 * (double)R2 * MARG) { ph = 2; break; }
+                        side = 0;
+                    }
+                    // side 0: bottom row, 1: top row, 2: left column, 3: right column
+                    if (side < 2) {
+                        cvy = side == 0 ? uy - rk : uy + rk;
+                        cvx = max(ux - rk, bxa);
+                        cend = (cvy < bya || cvy > byb) ? cvx - 1 : min(ux + rk, bxb);
+                    } else {
+                        cfix = side == 2 ? ux - rk : ux + rk;
+                        cvx = max(uy - rk + 1, bya);
+                        cend = (cfix < bxa || cfix > bxb) ? cvx - 1 : min(uy + rk - 1, byb);
+                    }
+                    continue;
+                }
+                const int vx = side < 2 ? cvx : cfix, vy = side < 2 ? cvy : cvx;
+                cvx++;
+                if (leaf_d2(bg, lsx, lsy, vx, vy, px, py) * (1.0 - 1e-9) >= 4.0 * (double)R2 * MARG) continue;
+                int st, cnt;
+                vleaf_range(A, vx, vy, rh, ux, uy, st, cnt);
+                t = st;
+                tend = st + cnt;
+            }
+        }
+        if (!__any_sync(0xffffffffu, j >= 0)) break;
+        if (j >= 0) {
+            const unsigned long long c0 = cs.clips;
+            fail = clip_t(P, j, bisector(cdx, cdy), cgm, A, cs);
+            if (fail) ph = 2;
+            else if (cs.clips != c0) R2 = poly_R2(P);
+        }
+    }
+    if (live) {
+        if (fail == -1) {
+            // more than VMAX slots (or an undecided filter without TM_THREAD_EXACT):
+            // the 32-lane group kernel redoes this cell
+            const unsigned long long k = atomicAdd(retry_cnt, 1ull);
+            retry_list[k] = (int32_t)cell;
+            live = false;
+        } else if (fail) {
+            atomicAdd(&A.st->n_degenerate, 1ull);
+            if (MODE & M_TREAT) {
+                A.x_out[orig] = px; A.y_out[orig] = py; A.d_prev_out[orig] = 0.0; A.status[orig] = 2;
+            }
+            if (MODE & M_HAT) { A.x_hat[orig] = px; A.y_hat[orig] = py; }
+            if (MODE & M_ELL) A.deg[cell] = 0;
+            live = false;
+        }
+    }
+    const int start = live ? __ffs(P.used) - 1 : 0;
+    const int nv = live ? __popc(P.used) : 0;
+    // ---- S3: Delaunay triangles at point-point vertices + keep rule; ELL rows
+    int ell = 0;
+    if (live && (MODE & (M_TRI | M_ELL))) {
+        unsigned keptall = 0;  // for the ELL: kept, owned or not
+        int k = start;
+        for (int c = 0; c < nv; c++) {
+            const int kn = P.nxt[k * TB];
+            const int a = P.la[k * TB], b = P.la[kn * TB];
+            if (a >= 0 && b >= 0) {
+                const int32_t ga = __ldg(A.gids + a), gb = __ldg(A.gids + b);
+                if (gi < ga && gi < gb) {
+                    const int sv = ga < gb ? a : b, sw = ga < gb ? b : a;
+                    if (keep_tri(A, (int)cell, sv, sw, cadd(px, P.v[k * TB].x), cadd(py, P.v[k * TB].y))) {
+                        keptmask |= 1u << k;
+                        keptall |= 1u << k;
+                    }
+                } else if (MODE & M_ELL) {
+                    int s3[3] = {(int)cell, a, b};
+                    int32_t g3[3] = {gi, ga, gb};
+                    for (int u = 0; u < 2; u++)
+                        for (int w = 0; w < 2 - u; w++)
+                            if (g3[w] > g3[w + 1]) {
+                                int32_t tg = g3[w]; g3[w] = g3[w + 1]; g3[w + 1] = tg;
+                                int ts = s3[w]; s3[w] = s3[w + 1]; s3[w + 1] = ts;
+                            }
+                    const double uxx = __ldg(A.xs + s3[0]), uyy = __ldg(A.ys + s3[0]);
+                    const Line B1 = bisector(csub(__ldg(A.xs + s3[1]), uxx), csub(__ldg(A.ys + s3[1]), uyy));
+                    const Line B2 = bisector(csub(__ldg(A.xs + s3[2]), uxx), csub(__ldg(A.ys + s3[2]), uyy));
+                    double ox, oy;
+                    cramer(B1, B2, ox, oy);
+                    if (keep_tri(A, s3[0], s3[1], s3[2], cadd(uxx, ox), cadd(uyy, oy))) keptall |= 1u << k;
+                }
+            }
+            k = kn;
+        }
+        if (!(MODE & M_TRI)) keptmask = 0;
+        t_own = __popc(keptmask);
+        if (MODE & M_ELL) {
+            // neighbour a = incoming line of slot k borders a kept triangle at k or at prev(k)
+            k = start;
+            for (int c = 0; c < nv; c++) {
+                const int a = P.la[k * TB];
+                const int kp = P.prv[k * TB];
+                if (a >= 0 && (((keptall >> k) & 1u) || ((keptall >> kp) & 1u))) {
+                    if (ell < A.adj_stride) A.adj[(int64_t)ell * A.n_local + cell] = a;
+                    ell++;
+                }
+                k = P.nxt[k * TB];
+            }
+            A.deg[cell] = (uint8_t)(ell < A.adj_stride ? ell : A.adj_stride);
+            if (ell > A.adj_stride) atomicAdd(&A.st->n_adj_overflow, 1ull);
+        }
+    }
+    if (MODE & M_TRI) {
+        // warp-aggregated allocation of the owned kept triangles
+        __syncwarp();
+        int incl = t_own;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned long long base = 0;
+        if (lane == 31 && tot > 0) base = atomicAdd(A.n_tri, (unsigned long long)tot);
+        base = __shfl_sync(0xffffffffu, base, 31) + (unsigned long long)(incl - t_own);
+        for (unsigned m = keptmask; m; m &= m - 1) {
+            const int k = __ffs(m) - 1;
+            const int a = P.la[k * TB], b = P.la[P.nxt[k * TB] * TB];
+            if ((int64_t)base < A.tri_cap) {
+                A.tri[3 * base] = gi;
+                A.tri[3 * base + 1] = __ldg(A.gids + a);
+                A.tri[3 * base + 2] = __ldg(A.gids + b);
+            } else {
+                atomicAdd(&A.st->n_tri_overflow, 1ull);
+            }
+            base++;
+        }
+    }
+    // ---- S4a centroid of C_i (relative to p_i) and S5 treatment
+    if (live && (MODE & (M_TREAT | M_HAT))) {
+        double S2 = 0.0, sx = 0.0, sy = 0.0;
+        int k = start;
+        for (int c = 0; c < nv; c++) {
+            const int kn = P.nxt[k * TB];
+            const double x0 = P.v[k * TB].x, y0 = P.v[k * TB].y, x1 = P.v[kn * TB].x, y1 = P.v[kn * TB].y;
+            const double cr = x0 * y1 - x1 * y0;
+            S2 += cr;
+            sx += cr * (x0 + x1);
+            sy += cr * (y0 + y1);
+            k = kn;
+        }
+        double cx, cy;
+        if (A.rho == nullptr) {
+            cx = sx / (3.0 * S2);
+            cy = sy / (3.0 * S2);
+            nq += nv;
+        } else {
+            const double dp = A.d_prev ? __ldg(A.d_prev + orig) : -1.0;
+            quad_centroid_t(P, start, nv, px, py, 0.5 * S2, h, dp, A, cx, cy, nq);
+        }
+        if (MODE & M_HAT) {
+            A.x_hat[orig] = px + cx;
+            A.y_hat[orig] = py + cy;
+        }
+        if (MODE & M_TREAT) {
+            double qx, qy, dpo;
+            const int s = treat_point(A.grid, A.phi, h, A.h_avg, A.fac_pt, A.fac_geps, A.damping, A.newton_max, px,
+                                      py, px + cx, py + cy, qx, qy, dpo, LdgLoad());
+            A.x_out[orig] = qx;
+            A.y_out[orig] = qy;
+            A.d_prev_out[orig] = dpo;
+            A.status[orig] = (int8_t)s;
+            if (s & 2) atomicAdd(&A.st->n_fallback, 1ull);
+        }
+    }
+    // ---- O8 work counters (TM_F_COUNT_WORK)
+    if ((MODE & M_COUNT) && live) {
+        const float R2f = poly_R2(P);
+        const double rad = 2.0 * sqrt((double)R2f);
+        const BinGeom &bg = A.bg;
+        int ncert = 0;
+        const int bxa = max(0, (int)floor((px - rad - bg.x0) * bg.isx));
+        const int bxb = min(bg.nbx - 1, (int)floor((px + rad - bg.x0) * bg.isx));
+        const int bya = max(0, (int)floor((py - rad - bg.y0) * bg.isy));
+        const int byb = min(bg.nby - 1, (int)floor((py + rad - bg.y0) * bg.isy));
+        for (int by = bya; by <= byb; by++) {
+            const int s0 = __ldg(A.leaf_start + __ldg(A.leaf_off + by * bg.nbx + bxa));
+            const int s1 = __ldg(A.leaf_start + __ldg(A.leaf_off + by * bg.nbx + bxb + 1));
+            for (int s = s0; s < s1; s++) {
+                const double dx = __ldg(A.xs + s) - px, dy = __ldg(A.ys + s) - py;
+                ncert += (s != (int)cell) && (dx * dx + dy * dy < rad * rad);
+            }
+        }
+        int degc = 0;
+        for (unsigned m = P.used; m; m &= m - 1) {
+            const int k = __ffs(m) - 1;
+            degc += P.la[P.nxt[k * TB] * TB] >= 0 ? 1 : 0;
+        }
+        atomicAdd(&A.st->work[0], 1ull);
+        atomicAdd(&A.st->work[1], (unsigned long long)ncert);
+        atomicAdd(&A.st->work[2], (unsigned long long)degc);
+        atomicAdd(&A.st->work[3], (unsigned long long)nv);
+        atomicAdd(&A.st->work[4], (unsigned long long)t_own);
+        atomicAdd(&A.st->work[5], (A.rho == nullptr) ? (unsigned long long)nv : nq);
+        atomicAdd(&A.st->work[6], (unsigned long long)ell);
+        atomicAdd(&A.st->work[7], sc.n_cand);
+        atomicAdd(&A.st->work[8], cs.clips);
+        atomicAdd(&A.st->work[9], cs.exact);
+    }
+}
+
+}  // namespace
+
+namespace tmg {
+
+template <int MODE>
+tm_status launch_cells_thread(tm_ctx *ctx, const CellArgs &a) {
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        TM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_cells_t<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TSMEM));
+        attr_set = true;
+    }
+    const unsigned blocks = (unsigned)((ctx->n_local + TB - 1) / TB);
+    k_cells_t<MODE><<<blocks, TB, TSMEM, ctx->stream>>>(a, ctx->retry_list, ctx->retry_cnt);
+    return tm_internal_check_launch(ctx, "k_cells_t");
+}
+
+#define TM_INST(M) template tm_status launch_cells_thread<M>(tm_ctx *, const CellArgs &);
+TM_INST(M_TRI) TM_INST(M_TRI | M_ELL) TM_INST(M_TRI | M_TREAT) TM_INST(M_TRI | M_ELL | M_TREAT) TM_INST(M_HAT)
+TM_INST(M_TRI | M_COUNT) TM_INST(M_TRI | M_ELL | M_COUNT) TM_INST(M_TRI | M_TREAT | M_COUNT)
+TM_INST(M_TRI | M_ELL | M_TREAT | M_COUNT) TM_INST(M_HAT | M_COUNT)
+#undef TM_INST
+
+}  // namespace tmg

@@ -100,7 +100,8 @@ def test_points_on_bin_edges_and_box_boundary():
     n = 2000
     rng = np.random.default_rng(8)
     x, y = rng.random(n), rng.random(n)
-    nb = int(np.ceil(np.sqrt(n / 3.3)))
+    import paper_2309_13824_b200 as T
+    nb = int(np.ceil(np.sqrt(n / T.default_params().n_opt)))  # level-0 bins of the unit box
     k = rng.integers(1, nb, 300)
     x[:300] = k / nb  # on interior vertical bin edges (many collinear points: generic for Delaunay)
     # on the box sides: at most two per side (three collinear hull points are non-generic, L12)
@@ -243,3 +244,85 @@ def test_determinism(cfg_cache):
 def tri_set_eq(a, b):
     from tests.gpu_util import tri_set
     return tri_set(a) == tri_set(b)
+
+
+@pytest.mark.parametrize("cells", ["thread", "group"])
+@pytest.mark.parametrize("k,mode", [(2, "dm"), (3, "dm"), (3, "cvd"), (4, "cvd")])
+def test_both_cell_kernels_match_oracle(cells, k, mode, cfg_cache):
+    """The thread-per-cell kernel (default) and the 16-lane group kernel
+    (TM_F_GROUP_CELLS) both reproduce the oracle at iteration 0 of the
+    full-size configs (the CVD case uses the adaptive quadrature on 3/4)."""
+    import paper_2309_13824_b200 as T
+    c = cfg_cache(k)
+    p = T.default_params()
+    if cells == "group":
+        p.flags |= T.TM_F_GROUP_CELLS
+    g, o, _ = run_pair(c, c.x, c.y, mode, params=p)
+    compare(g, o, c.box, mode, ctx=f"cfg{k} {mode} {cells}")
+
+
+def test_thread_kernel_overflow_retry():
+    """Cells whose ring needs more slots than the thread kernel holds go to the
+    32-lane retry pass: a point surrounded by a fine circle of 24 neighbours
+    has a 24-gon cell; the result must still equal the oracle."""
+    box = (0.0, 0.0, 1.0, 1.0)
+    phi = configs.box_phi(box, 64)
+    rng = np.random.default_rng(11)
+    n0 = 3000
+    x, y = rng.random(n0), rng.random(n0)
+    keep = np.hypot(x - 0.5, y - 0.5) > 0.08
+    x, y = x[keep], y[keep]
+    ang = 2 * np.pi * (np.arange(24) + rng.uniform(-0.05, 0.05, 24)) / 24
+    rad = 0.03 * (1 + rng.uniform(-1e-3, 1e-3, 24))
+    x = np.concatenate([x, [0.5], 0.5 + rad * np.cos(ang)])
+    y = np.concatenate([y, [0.5], 0.5 + rad * np.sin(ang)])
+    c = configs.Config("ring24", x, y, box, phi, None, None, ["cvd"])
+    import paper_2309_13824_b200 as T
+    for mode in ("cvd", "dm"):
+        g, o, _ = run_pair(c, x, y, mode, params=T.default_params(adj_stride=32))  # the 24-gon has 24 edges
+        compare(g, o, box, mode, ctx=f"ring24 {mode}")
+
+
+@pytest.mark.parametrize("n", [16_000_000, 64_000_000])
+def test_cfg5_full_size_sampled_windows(n):
+    """configs[4] at its full sizes (1.6e7 and 6.4e7 jittered-uniform points):
+    one CVD iteration on the GPU, then the oracle recomputes sampled windows
+    of the same input.  A cell, its CVD update and the triangles around it
+    depend only on points within a few h (the circumcircles of the Delaunay
+    triangles are ~h), so for points farther than a margin of 10 h from a
+    window edge (edges on the box sides need no margin) the oracle run on the
+    window's points (with the global normalisation n_total = N) must give the
+    GPU's positions, status codes and kept triangles exactly."""
+    c = configs.config5(n=n)
+    h = 1.0 / np.sqrt(n)
+    r = GpuRunner(c.box, c.phi)
+    g = r.iteration(c.x, c.y, "cvd")
+    fs = O.FieldSet.from_config(c)
+    rng = np.random.default_rng(50 + n % 7)
+    w, m = 25 * h, 10 * h
+    centers = [(w, w), (1 - w, 0.5), (0.5, 1 - w)] + [tuple(p) for p in rng.uniform(0, 1, (9, 2))]
+    gtri = g["tri"].astype(np.int64)
+    for cx, cy in centers:
+        lo_x, hi_x, lo_y, hi_y = max(cx - w, 0.0), min(cx + w, 1.0), max(cy - w, 0.0), min(cy + w, 1.0)
+        sel = np.nonzero((c.x >= lo_x) & (c.x <= hi_x) & (c.y >= lo_y) & (c.y <= hi_y))[0]
+        ix0 = lo_x + (m if lo_x > 0.0 else -1.0)
+        ix1 = hi_x - (m if hi_x < 1.0 else -1.0)
+        iy0 = lo_y + (m if lo_y > 0.0 else -1.0)
+        iy1 = hi_y - (m if hi_y < 1.0 else -1.0)
+        xs, ys = c.x[sel], c.y[sel]
+        inner = (xs > ix0) & (xs < ix1) & (ys > iy0) & (ys < iy1)
+        o = O.iteration(fs, xs, ys, "cvd", n_total=n)
+        assert o.info.n_degenerate == 0
+        gi = sel[inner]
+        diam = np.sqrt(2.0)
+        err = np.hypot(g["x"][gi] - o.x[inner], g["y"][gi] - o.y[inner])
+        assert err.max() <= 1e-12 * diam, f"window {cx:.3f},{cy:.3f}: position error {err.max():.3e}"
+        assert np.array_equal(g["status"][gi], o.status[inner])
+        # triangles with all three vertices inner, in global ids
+        inner_g = np.zeros(n, dtype=bool)
+        inner_g[gi] = True
+        gt = {tuple(t) for t in gtri[inner_g[gtri].all(1)].tolist()}
+        ot_all = sel[np.asarray(o.tri, dtype=np.int64)]
+        ot = {tuple(t) for t in ot_all[inner_g[ot_all].all(1)].tolist()}
+        assert gt == ot, f"window {cx:.3f},{cy:.3f}: {len(ot - gt)} missing, {len(gt - ot)} extra"
+        assert len(gt) > 1000
