@@ -18,8 +18,11 @@ D2H of the result (final points + triangle count) inside the timed region.
 sample of the same workload (one iteration per step, alternating DistMesh and
 CVD), printed as a JSON line with "impl": "reference".
 
-N > 1 (torchrun): every rank runs an independent replica of the workload on
-its own GPU (no data-path collective) -> "scaling": "weak".
+N > 1 (torchrun): the same mesh is split into N x-strips (x-quantiles of the
+initial points), one per GPU; every iteration exchanges a ghost halo and the
+migrating points with the neighbour strips over NCCL and all-reduces the two
+DistMesh edge sums -> "scaling": "strong" (total work fixed).
+`--strips` runs that path at N = 1 as well (smoke test of the code path).
 """
 from __future__ import annotations
 
@@ -128,7 +131,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / len(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "sample": "one oracle iteration per step (alternating DistMesh/CVD) "
                                                     "from the cfg3 initial points"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
@@ -162,6 +165,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--strips", action="store_true", help="use the x-strip path even at N=1 (smoke test)")
     ap.add_argument("--cells", default="thread", choices=["thread", "group"],
                     help="cell kernel: one thread per cell (default) or 16-lane groups (A/B)")
     args = ap.parse_args()
@@ -204,7 +208,7 @@ def main():
     flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device=dev)
     ev_cells = []  # (start, end, mode) around every tm_voronoi_delaunay in the timed region
 
-    def one_step(xin, yin, record=False):
+    def one_step_single(xin, yin, record=False):
         xc, yc, dc = xin, yin, None
         for it, mode in enumerate(schedule):
             xo, yo, do = X[it % 2], Y[it % 2], D[it % 2]
@@ -226,6 +230,28 @@ def main():
             xc, yc, dc = xo, yo, do
         return xc, yc
 
+    # N > 1 (or --strips): x-strip decomposition of the same mesh: each rank owns the
+    # points of one x-quantile strip; per iteration a ghost halo (W = 2 S_max) goes to both neighbours
+    # over NCCL, the DistMesh edge sums are all-reduced, and points that left the strip migrate.
+    strip_mode = world > 1 or args.strips
+    if strip_mode:
+        from paper_2309_13824_b200 import strips as S
+        strips = S.Strips.from_quantiles(torch.from_numpy(c.x), world, box[0], box[2])
+        st_init = S.split_initial(x0, y0, strips, rank)
+        W = S.ghost_width(ctx.c, params.fac_voro_bound, float(c.mu.max()) if c.mu is not None else 1.0)
+        comm = S.TorchP2P(rank, world, dev)
+        backend = S.GpuStripBackend(ctx, params.adj_stride, keep_tri=False)
+        n_own0 = st_init.x.shape[0]
+
+    def one_step_strips(xin, yin, record=False):
+        st = S.RankState(rank, xin, yin, st_init.gid, None)
+        for mode in schedule:
+            st = S.strip_iteration(st, strips, backend, comm.exchange, W, mode, allreduce=comm.allreduce_sum)
+        return st.x, st.y
+
+    one_step = one_step_strips if strip_mode else one_step_single
+    xs0, ys0 = (st_init.x, st_init.y) if strip_mode else (x0, y0)
+
     def barrier():
         if world > 1:
             dist.barrier()
@@ -234,7 +260,7 @@ def main():
     # warm-up
     for _ in range(args.warmup):
         flush_l2(flush)
-        one_step(x0, y0)
+        one_step(xs0, ys0)
     ctx.tm_sync()
     # timed (device, inputs resident)
     sampler = ClockSampler(local)
@@ -246,7 +272,7 @@ def main():
         s0 = torch.cuda.Event(enable_timing=True)
         s1 = torch.cuda.Event(enable_timing=True)
         s0.record(stream)
-        one_step(x0, y0, record=True)
+        one_step(xs0, ys0, record=True)
         s1.record(stream)
         s1.synchronize()
         step_ms.append(s0.elapsed_time(s1))
@@ -258,7 +284,7 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_max = float(t.item())
-    value = world * n * iters * args.steps / t_max
+    value = n * iters * args.steps / t_max  # all ranks together mesh the n points (strips at N > 1)
 
     # per-launch duration of the dominant kernel (k_cells), CUDA events on the launching stream
     cells_ms = {"dm": [], "cvd": []}
@@ -268,13 +294,14 @@ def main():
     # e2e through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        hx = torch.from_numpy(c.x).pin_memory()
-        hy = torch.from_numpy(c.y).pin_memory()
-        rx = torch.empty(n, dtype=torch.float64).pin_memory()
-        ry = torch.empty(n, dtype=torch.float64).pin_memory()
+        hx = xs0.cpu().pin_memory()  # this rank's input points (all of them at N=1)
+        hy = ys0.cpu().pin_memory()
+        n_in = hx.shape[0]
+        rx = torch.empty(2 * n_in + 1024, dtype=torch.float64).pin_memory()
+        ry = torch.empty(2 * n_in + 1024, dtype=torch.float64).pin_memory()
         rn = torch.empty(1, dtype=torch.int64).pin_memory()
-        dx = torch.empty(n, dtype=torch.float64, device=dev)
-        dy = torch.empty(n, dtype=torch.float64, device=dev)
+        dx = torch.empty(n_in, dtype=torch.float64, device=dev)
+        dy = torch.empty(n_in, dtype=torch.float64, device=dev)
         e2e_ms = []
         barrier()
         for _ in range(args.steps):
@@ -285,8 +312,8 @@ def main():
             dx.copy_(hx, non_blocking=True)
             dy.copy_(hy, non_blocking=True)
             xf, yf = one_step(dx, dy)
-            rx.copy_(xf, non_blocking=True)
-            ry.copy_(yf, non_blocking=True)
+            rx[:xf.shape[0]].copy_(xf, non_blocking=True)
+            ry[:yf.shape[0]].copy_(yf, non_blocking=True)
             rn.copy_(bufs.n_tri, non_blocking=True)
             s1.record(stream)
             s1.synchronize()
@@ -295,26 +322,30 @@ def main():
         te = torch.tensor([sum(e2e_ms) / 1e3], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * n * iters * args.steps / float(te.item()), "unit": UNIT,
+        e2e = {"value": n * iters * args.steps / float(te.item()), "unit": UNIT,
                "h2d_bytes_per_step": 2 * 8 * n, "d2h_bytes_per_step": 2 * 8 * n + 8}
 
     # algorithmic DP instructions of the dominant kernel: work counters from an
     # untimed counting pass over the same schedule (SURVEY §8(d) cost table)
     roof = None
-    if rank == 0:
+    if rank == 0 and ev_cells:
         roof = roofline(T, c, ctx, cells_ms, params.flags)
 
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline_sample()
-        launches_per_step = sum(9 if m == "dm" else 6 for m in schedule)
+        # k_bin_keys, k_bin_levels, 2 x (k_scan_tiles, k_scan_top, k_scan_add), k_leaf_keys, k_bin_scatter,
+        # k_leaf_sort = 11; cells: k_cells_t + retry pass = 2; DistMesh: k_dm_sums, k_dm_final, k_dm_step = 3
+        launches_per_step = sum(16 if m == "dm" else 13 for m in schedule) + (
+            sum(3 for _ in schedule) if strip_mode else 0)  # + k_halo_pack, k_migrate_pack, k_migrate_unpack
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD, "n_points": n, "iterations_per_step": iters,
-                       "schedule": "30 dm + 30 cvd", "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "schedule": "30 dm + 30 cvd",
+                       "parallelism": f"x-strips{world} (NCCL halo + migration)" if strip_mode else "single",
                        "l2": "flushed before every step (256 MiB write); per-iteration working set ~90 MB"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
@@ -361,6 +392,7 @@ def roofline(T, c, ctx, cells_ms, flags=0):
     xo, yo, do = torch.empty_like(xs), torch.empty_like(xs), torch.empty_like(xs)
     dc = None
     flops = {"dm": [], "cvd": []}
+    wsum = {"dm": [0] * 11, "cvd": [0] * 11}
     for mode in c.schedule:
         cc.tm_grid_bin(xs, ys)
         if mode == "cvd":
@@ -368,6 +400,8 @@ def roofline(T, c, ctx, cells_ms, flags=0):
         else:
             cc.tm_voronoi_delaunay(bufs.tri, bufs.n_tri, bufs.adj, bufs.deg)
         w = cc.tm_work_counts()
+        wsum[mode] = [a + b for a, b in zip(wsum[mode], [w.n_cells, w.n_cert, w.deg, w.verts, w.t_own, w.quad_tris,
+                                                          w.ell, w.candidates, w.clips, w.exact_calls, w.retries])]
         # 4 n_cert + 5 deg V + 50 deg + 40 T_own + [6V+15 | 30 Q] + 20 (ELL/force cost is k_dm_step)
         f = 4 * w.n_cert + 5 * w.deg * (w.verts / max(w.n_cells, 1)) + 50 * w.deg + 40 * w.t_own
         if mode == "cvd":
@@ -388,7 +422,10 @@ def roofline(T, c, ctx, cells_ms, flags=0):
     return {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "T DP-inst/s",
             "frac": achieved / peak, "traffic": None, "kernel": "k_cells (S2+S3+S4a+S5 fused)",
             "algorithmic_dp_inst_per_launch": per_launch_f, "peak_source": how,
-            "dp_inst_per_launch_by_mode": {k: (statistics.mean(v) if v else None) for k, v in flops.items()}}
+            "dp_inst_per_launch_by_mode": {k: (statistics.mean(v) if v else None) for k, v in flops.items()},
+            "work_per_cell_by_mode": {m: {k: round(v / max(1, wsum[m][0]), 3) for k, v in zip(
+                ["n_cells", "n_cert", "deg", "verts", "t_own", "quad_tris", "ell", "candidates", "clips",
+                 "exact_calls", "retries"], wsum[m])} for m in wsum}}
 
 
 if __name__ == "__main__":

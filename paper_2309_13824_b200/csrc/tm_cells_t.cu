@@ -421,23 +421,11 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
     }
     // ---- flat candidate loop: one candidate per thread per trip, the warp
     // re-converges every trip (a per-thread nested loop lets lanes drift apart)
-    for (;;) {
+    // the iterator: advance to this thread's next candidate slot (-1 when done)
+    auto next_cand = [&]() -> int {
         int j = -1;
-        double cdx = 0.0, cdy = 0.0;
         while (ph < 2) {
-            if (t < tend) {
-                // compaction: skip candidates that cannot cut before leaving the loop,
-                // so that nearly every thread brings a candidate to the clip test
-                const int jj = t++;
-                sc.n_cand++;
-                if (jj == (int)cell) continue;
-                cdx = csub(__ldg(A.xs + jj), px);
-                cdy = csub(__ldg(A.ys + jj), py);
-                if (cdx == 0.0 && cdy == 0.0) { atomicAdd(&A.st->n_duplicate, 1ull); continue; }
-                if (cdx * cdx + cdy * cdy >= 4.0 * (double)R2 * MARG) continue;
-                j = jj;
-                break;
-            }
+            if (t < tend) { j = t++; break; }
             const float lim = 4.0f * R2 * (float)MARG;
             if (ph == 0) {  // ring 1, sorted
                 if (rr >= 8) {
@@ -501,12 +489,33 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
                 tend = st + cnt;
             }
         }
+        return j;
+    };
+    int j = next_cand();
+    double xj = 0.0, yj = 0.0;
+    if (j >= 0) { xj = __ldg(A.xs + j); yj = __ldg(A.ys + j); }
+    for (;;) {
         if (!__any_sync(0xffffffffu, j >= 0)) break;
-        if (j >= 0) {
-            const unsigned long long c0 = cs.clips;
-            fail = clip_t(P, j, bisector(cdx, cdy), cgm, A, cs);
-            if (fail) ph = 2;
-            else if (cs.clips != c0) R2 = poly_R2(P);
+        // one candidate per thread per trip (skipping far candidates inside the iterator,
+        // or testing several per step, lets single lanes run alone: measured slower);
+        // the next candidate is fetched before this one is clipped (its load overlaps the
+        // clip; leaf pruning then uses the R_max before the clip, which is conservative)
+        const int cj = j;
+        const double cxj = xj, cyj = yj;
+        j = next_cand();
+        if (j >= 0) { xj = __ldg(A.xs + j); yj = __ldg(A.ys + j); }
+        if (cj >= 0) {
+            sc.n_cand++;
+            const double dx = csub(cxj, px), dy = csub(cyj, py);
+            if (cj == (int)cell) {
+            } else if (dx == 0.0 && dy == 0.0) {
+                atomicAdd(&A.st->n_duplicate, 1ull);
+            } else if (dx * dx + dy * dy < 4.0 * (double)R2 * MARG) {
+                const unsigned long long c0 = cs.clips;
+                fail = clip_t(P, cj, bisector(dx, dy), cgm, A, cs);
+                if (fail) { ph = 2; j = -1; }
+                else if (cs.clips != c0) R2 = poly_R2(P);
+            }
         }
     }
     if (live) {

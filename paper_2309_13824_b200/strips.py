@@ -29,18 +29,35 @@ import torch
 
 @dataclass
 class Strips:
+    """P x-strips of [x0, x1): equal widths, or explicit interior cuts
+    (e.g. x-quantiles of the points, for adaptive densities)."""
     x0: float
     x1: float
     P: int
+    cuts: Optional[List[float]] = None  # P-1 increasing interior boundaries
+
+    @classmethod
+    def from_quantiles(cls, x: torch.Tensor, P: int, x0: float, x1: float) -> "Strips":
+        if P == 1:
+            return cls(x0, x1, 1)
+        q = torch.quantile(x.double().cpu()[:: max(1, x.shape[0] // 1_000_000)],
+                           torch.linspace(0, 1, P + 1, dtype=torch.float64)[1:-1])
+        return cls(x0, x1, P, [float(v) for v in q])
+
+    def _cut(self, k: int) -> float:
+        if self.cuts is not None:
+            return self.cuts[k - 1]
+        return self.x0 + k * (self.x1 - self.x0) / self.P
 
     def bounds(self, r: int):
-        w = (self.x1 - self.x0) / self.P
-        lo = self.x0 + r * w
-        hi = self.x0 + (r + 1) * w if r < self.P - 1 else float("inf")
-        lo = lo if r > 0 else float("-inf")
+        lo = self._cut(r) if r > 0 else float("-inf")
+        hi = self._cut(r + 1) if r < self.P - 1 else float("inf")
         return lo, hi
 
     def owner(self, x: torch.Tensor) -> torch.Tensor:
+        if self.cuts is not None:
+            c = torch.tensor(self.cuts, dtype=x.dtype, device=x.device)
+            return torch.bucketize(x, c, right=True).to(torch.int64)
         w = (self.x1 - self.x0) / self.P
         return torch.clamp(((x - self.x0) / w).floor().to(torch.int64), 0, self.P - 1)
 
@@ -109,7 +126,8 @@ class TorchP2P:
 
     def allreduce_sum(self, t: torch.Tensor):
         import torch.distributed as dist
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return t
 
 
@@ -145,9 +163,10 @@ class _LoopbackView:
 class GpuStripBackend:
     """The per-rank arithmetic through the C ABI (no CPU work)."""
 
-    def __init__(self, ctx, adj_stride=16):
+    def __init__(self, ctx, adj_stride=16, keep_tri=True):
         self.ctx = ctx
         self.adj_stride = adj_stride
+        self.keep_tri = keep_tri  # False: leave the triangles in the device buffers (no count readback)
 
     def halo(self, st: RankState, lo, hi, W):
         dev = st.x.device
@@ -196,6 +215,8 @@ class GpuStripBackend:
                 bufs.sums2.copy_(sums2)
             self.ctx.tm_distmesh_step(bufs.adj, bufs.deg, bufs.sums2, None, st.d_prev, h["xo"], h["yo"], h["do"],
                                       h["status"])
+        if not self.keep_tri:
+            return None, h["xo"], h["yo"], h["do"], h["status"]
         nt = int(bufs.n_tri.item())
         return bufs.tri[:nt].clone(), h["xo"], h["yo"], h["do"], h["status"]
 
