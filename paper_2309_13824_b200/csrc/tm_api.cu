@@ -74,6 +74,7 @@ extern "C" void tm_destroy(tm_ctx *ctx) {
     cudaFree(ctx->phi); cudaFree(ctx->mu); cudaFree(ctx->rho);
     cudaFree(ctx->partials); cudaFree(ctx->stat_acc); cudaFree(ctx->dst);
     cudaFree(ctx->retry_list); cudaFree(ctx->retry_cnt);
+    cudaFree(ctx->mig_keep); cudaFree(ctx->mig_cnt); cudaFree(ctx->mig_off);
     delete ctx;
 }
 
@@ -405,6 +406,17 @@ static tm_status ensure_bins(tm_ctx *ctx, int64_t nb, int64_t nleaves) {
     return TM_OK;
 }
 
+static tm_status ensure_scan_scratch(tm_ctx *ctx, int64_t n) {
+    const int64_t ntiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+    if (ntiles > ctx->cap_block_sums) {
+        cudaFree(ctx->block_sums);
+        ctx->block_sums = nullptr;
+        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->block_sums, ntiles * sizeof(int32_t)));
+        ctx->cap_block_sums = ntiles;
+    }
+    return TM_OK;
+}
+
 // exclusive scan of n int32 values into out[0..n], out[n] = total
 static tm_status scan_counts(tm_ctx *ctx, const int32_t *in, int32_t *out, int64_t n) {
     int64_t ntiles = (n + SCAN_TILE - 1) / SCAN_TILE;
@@ -631,24 +643,28 @@ extern "C" tm_status tm_adjacency_export(tm_ctx *ctx, const int32_t *adj, const 
 __global__ void k_halo_pack(const double *__restrict__ x, const double *__restrict__ y,
                             const int32_t *__restrict__ gid, int64_t n, double lo, double hi, double w,
                             double *send_lo, double *send_hi, int64_t cap, unsigned long long *cnt) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    double px = x[i];
-    int32_t g = gid ? gid[i] : (int32_t)i;
-    if (px < lo + w) {
-        unsigned long long k = atomicAdd(&cnt[0], 1ull);
-        if ((int64_t)k < cap) {
-            send_lo[k] = px;
-            send_lo[cap + k] = y[i];
-            ((int32_t *)(send_lo + 2 * cap))[k] = g;
-        }
-    }
-    if (px >= hi - w) {
-        unsigned long long k = atomicAdd(&cnt[1], 1ull);
-        if ((int64_t)k < cap) {
-            send_hi[k] = px;
-            send_hi[cap + k] = y[i];
-            ((int32_t *)(send_hi + 2 * cap))[k] = g;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const double px = i < n ? x[i] : 0.0;
+    const bool in_n = i < n;
+    // two bands (a point can be in both when the strip is narrower than 2w);
+    // one atomic per warp and band
+#pragma unroll
+    for (int side = 0; side < 2; side++) {
+        const bool sel = in_n && (side == 0 ? px < lo + w : px >= hi - w);
+        const unsigned m = __ballot_sync(0xffffffffu, sel);
+        if (!m) continue;
+        unsigned long long base = 0;
+        if (lane == __ffs(m) - 1) base = atomicAdd(&cnt[side], (unsigned long long)__popc(m));
+        base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+        if (sel) {
+            const unsigned long long k = base + __popc(m & ((1u << lane) - 1u));
+            double *dst = side == 0 ? send_lo : send_hi;
+            if ((int64_t)k < cap) {
+                dst[k] = px;
+                dst[cap + k] = y[i];
+                ((int32_t *)(dst + 2 * cap))[k] = gid ? gid[i] : (int32_t)i;
+            }
         }
     }
 }
@@ -667,23 +683,64 @@ extern "C" tm_status tm_halo_pack(tm_ctx *ctx, const double *x, const double *y,
     return tm_internal_check_launch(ctx, "k_halo_pack");
 }
 
-__global__ void k_migrate_pack(const double *__restrict__ x, const double *__restrict__ y,
-                               const int32_t *__restrict__ gid, const double *__restrict__ dp, int64_t n, double lo,
-                               double hi, double *keep, double *out_lo, double *out_hi, int64_t cap,
-                               unsigned long long *cnt) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    double px = x[i];
-    int which = px < lo ? 1 : (px >= hi ? 2 : 0);
-    double *dst = which == 0 ? keep : (which == 1 ? out_lo : out_hi);
-    int64_t c = which == 0 ? n : cap;
-    unsigned long long k = atomicAdd(&cnt[which], 1ull);
-    if ((int64_t)k < c) {
-        dst[k] = px;
-        dst[c + k] = y[i];
-        ((int32_t *)(dst + 2 * c))[k] = gid[i];
-        dst[3 * c + k] = dp ? dp[i] : 0.0;
+// Stable 3-way partition of the owned points after an update (SURVEY §8(e)
+// step 4): category 0 stays, 1 leaves to the lower strip, 2 to the upper one.
+// Per-block counts -> exclusive scan -> per-block ranks by warp ballots: the
+// order inside every category is the input order (deterministic, no atomics).
+constexpr int MIG_T = 256;
+
+__device__ __forceinline__ int mig_cat(double px, double lo, double hi) {
+    return px < lo ? 1 : (px >= hi ? 2 : 0);
+}
+
+__global__ void __launch_bounds__(MIG_T) k_migrate_count(const double *__restrict__ x, int64_t n, double lo,
+                                                         double hi, int32_t *__restrict__ bc, int64_t nblk) {
+    __shared__ int sc[3];
+    if (threadIdx.x < 3) sc[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t i = (int64_t)blockIdx.x * MIG_T + threadIdx.x;
+    const int c = i < n ? mig_cat(x[i], lo, hi) : -1;
+#pragma unroll
+    for (int cc = 0; cc < 3; cc++) {
+        const unsigned m = __ballot_sync(0xffffffffu, c == cc);
+        if ((threadIdx.x & 31) == 0 && m) atomicAdd(&sc[cc], __popc(m));
     }
+    __syncthreads();
+    if (threadIdx.x < 3) bc[threadIdx.x * nblk + blockIdx.x] = sc[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(MIG_T) k_migrate_scatter(const double *__restrict__ x, const double *__restrict__ y,
+                                                           const int32_t *__restrict__ gid,
+                                                           const double *__restrict__ dp, int64_t n, double lo,
+                                                           double hi, const int32_t *__restrict__ off, int64_t nblk,
+                                                           double *keep, double *out_lo, double *out_hi, int64_t cap,
+                                                           unsigned long long *cnt) {
+    __shared__ int wc[3][MIG_T / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t i = (int64_t)blockIdx.x * MIG_T + threadIdx.x;
+    const int c = i < n ? mig_cat(x[i], lo, hi) : -1;
+    int rank = 0;
+#pragma unroll
+    for (int cc = 0; cc < 3; cc++) {
+        const unsigned m = __ballot_sync(0xffffffffu, c == cc);
+        if (c == cc) rank = __popc(m & ((1u << lane) - 1u));
+        if (lane == 0) wc[cc][w] = __popc(m);
+    }
+    __syncthreads();
+    if (c >= 0) {
+        for (int ww = 0; ww < w; ww++) rank += wc[c][ww];
+        const int64_t pos = (int64_t)(off[c * nblk + blockIdx.x] - off[c * nblk]) + rank;
+        double *dst = c == 0 ? keep : (c == 1 ? out_lo : out_hi);
+        const int64_t cc_cap = c == 0 ? n : cap;
+        if (pos < cc_cap) {
+            dst[pos] = x[i];
+            dst[cc_cap + pos] = y[i];
+            ((int32_t *)(dst + 2 * cc_cap))[pos] = gid[i];
+            dst[3 * cc_cap + pos] = dp ? dp[i] : 0.0;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 3)
+        cnt[threadIdx.x] = (unsigned long long)(off[(threadIdx.x + 1) * nblk] - off[threadIdx.x * nblk]);
 }
 
 __global__ void k_migrate_unpack(const double *keep, int64_t n, const unsigned long long *cnt, double *x, double *y,
@@ -705,18 +762,36 @@ extern "C" tm_status tm_migrate_pack(tm_ctx *ctx, double *x, double *y, int32_t 
     TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
     TM_CUDA_TRY(ctx, cudaMemsetAsync(cnt3, 0, 3 * sizeof(int64_t), ctx->stream));
     if (n_owned == 0) return TM_OK;
-    double *keep;
-    TM_CUDA_TRY(ctx, cudaMallocAsync(&keep, 4 * n_owned * sizeof(double), ctx->stream));
-    unsigned blocks = (unsigned)((n_owned + 255) / 256);
-    k_migrate_pack<<<blocks, 256, 0, ctx->stream>>>(x, y, gid, d_prev, n_owned, strip_lo, strip_hi, keep, out_lo,
-                                                     out_hi, cap, (unsigned long long *)cnt3);
-    k_migrate_unpack<<<blocks, 256, 0, ctx->stream>>>(keep, n_owned, (const unsigned long long *)cnt3, x, y, gid,
-                                                       d_prev);
-    TM_CUDA_TRY(ctx, cudaFreeAsync(keep, ctx->stream));
+    const int64_t nblk = (n_owned + MIG_T - 1) / MIG_T;
+    if (n_owned > ctx->cap_mig) {
+        cudaFree(ctx->mig_keep);
+        ctx->mig_keep = nullptr;
+        const int64_t c = n_owned + n_owned / 8 + 1024;
+        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->mig_keep, 4 * c * sizeof(double)));
+        ctx->cap_mig = c;
+    }
+    if (3 * nblk + 1 > ctx->cap_mig_blk) {
+        cudaFree(ctx->mig_cnt);
+        cudaFree(ctx->mig_off);
+        ctx->mig_cnt = ctx->mig_off = nullptr;
+        const int64_t c = 3 * nblk + 1 + 1024;
+        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->mig_cnt, c * sizeof(int32_t)));
+        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->mig_off, c * sizeof(int32_t)));
+        ctx->cap_mig_blk = c;
+    }
+    tm_status s = ensure_scan_scratch(ctx, 3 * nblk);
+    if (s != TM_OK) return s;
+    // keep is n_owned-strided: the scatter writes [x | y | gid | d_prev] segments of stride n_owned
+    k_migrate_count<<<(unsigned)nblk, MIG_T, 0, ctx->stream>>>(x, n_owned, strip_lo, strip_hi, ctx->mig_cnt, nblk);
+    if ((s = scan_counts(ctx, ctx->mig_cnt, ctx->mig_off, 3 * nblk)) != TM_OK) return s;
+    k_migrate_scatter<<<(unsigned)nblk, MIG_T, 0, ctx->stream>>>(x, y, gid, d_prev, n_owned, strip_lo, strip_hi,
+                                                                 ctx->mig_off, nblk, ctx->mig_keep, out_lo, out_hi,
+                                                                 cap, (unsigned long long *)cnt3);
+    k_migrate_unpack<<<(unsigned)nblk, MIG_T, 0, ctx->stream>>>(ctx->mig_keep, n_owned,
+                                                                (const unsigned long long *)cnt3, x, y, gid, d_prev);
     return tm_internal_check_launch(ctx, "k_migrate");
 }
 
-// ============================================================================ host hooks
 extern "C" int tm_host_incircle_exact(const double *a, const double *b, const double *c, const double *d) {
     return tmg::incircle_exact(a, b, c, d);
 }

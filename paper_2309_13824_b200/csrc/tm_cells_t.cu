@@ -35,8 +35,17 @@ using namespace tmg;
 #ifndef TM_TMINB
 #define TM_TMINB 4
 #endif
-#ifndef TM_UNROLL_SLOTS
-#define TM_UNROLL_SLOTS 1  // vertex tests over all VMAX slots, unrolled and masked
+#ifndef TM_PREFETCH
+#define TM_PREFETCH 1  // fetch the next candidate before clipping with the current one
+#endif
+#ifndef TM_WALL_FAST
+#define TM_WALL_FAST 0  // 1: separate point-point-only test loop for rings without walls (measured slower)
+#endif
+#ifndef TM_K_DOUBLE
+#define TM_K_DOUBLE 0  // filter constants as float (rounded up): less shared memory, more L1
+#endif
+#ifndef TM_R2_CACHE
+#define TM_R2_CACHE 1  // cache each vertex's r^2 bound in shared memory
 #endif
 #ifndef TM_THREAD_EXACT
 #define TM_THREAD_EXACT 0  // 0: cells with an undecided filter go to the 32-lane group kernel (rare)
@@ -47,93 +56,110 @@ namespace {
 constexpr int TB = TM_TB;
 constexpr int VMAX = TM_VMAX;
 static_assert(VMAX <= 31, "slot masks are 32-bit");
-constexpr size_t TSMEM = (size_t)VMAX * TB * (16 + 4 + 4 + 4 + 1 + 1);
+#if TM_K_DOUBLE
+typedef double KT;  // filter constant storage
+#else
+typedef float KT;   // rounded up: still a valid bound
+#endif
+constexpr size_t TSMEM = (size_t)VMAX * TB * (16 + sizeof(KT) + (TM_R2_CACHE ? 4 : 0) + 4 + 1 + 1);
 
 // this thread's view of the block's slot arrays (element k at [k * TB])
 struct TPoly {
-    double2 *v;   // canonical coordinates relative to p_i
-    float *K;     // filter constant (< 0: wall vertex)
-    float *r2;    // conservative squared distance from p_i (rounded up)
-    int *la;      // incoming line code
+    double2 *v;     // canonical coordinates relative to p_i
+    KT *K;          // filter constant of a point-point vertex (< 0: wall vertex)
+    float *r2;      // conservative squared distance from p_i (rounded up), if TM_R2_CACHE
+    int *la;        // incoming line code
     uint8_t *prv, *nxt;
-    unsigned used;
+    unsigned used;  // occupied slots
+    unsigned wall;  // slots holding a wall vertex (an octagon or box side among its lines)
 };
 
 __device__ __forceinline__ TPoly tpoly_bind(unsigned char *smem, int tid) {
     TPoly P;
     double2 *v = reinterpret_cast<double2 *>(smem);
-    float *K = reinterpret_cast<float *>(v + VMAX * TB);
-    float *r2 = K + VMAX * TB;
-    int *la = reinterpret_cast<int *>(r2 + VMAX * TB);
+    KT *K = reinterpret_cast<KT *>(v + VMAX * TB);
+    float *r2 = reinterpret_cast<float *>(K + VMAX * TB);
+    int *la = reinterpret_cast<int *>(r2 + (TM_R2_CACHE ? VMAX * TB : 0));
     uint8_t *prv = reinterpret_cast<uint8_t *>(la + VMAX * TB);
     uint8_t *nxt = prv + VMAX * TB;
     P.v = v + tid; P.K = K + tid; P.r2 = r2 + tid; P.la = la + tid; P.prv = prv + tid; P.nxt = nxt + tid;
     P.used = 0;
+    P.wall = 0;
     return P;
 }
 
-__device__ __forceinline__ float vertex_r2f_t(double vx, double vy, float Kf) {
+__device__ __forceinline__ float vertex_r2f_t(double vx, double vy, double K) {
     double m1 = fabs(vx) + fabs(vy);
-    double K = Kf > 0.f ? (double)Kf : 0.0;
+    K = K > 0.0 ? K : 0.0;
     double r2 = fma(vx, vx, vy * vy) + K * (2.0 * m1 + K);
     return __double2float_ru(r2 * (1.0 + 1e-12));
 }
 
 __device__ __forceinline__ float poly_R2(const TPoly &P) {
     float r = 0.f;
-#if TM_UNROLL_SLOTS
 #pragma unroll
-    for (int k = 0; k < VMAX; k++) r = fmaxf(r, ((P.used >> k) & 1u) ? P.r2[k * TB] : 0.f);
+    for (int k = 0; k < VMAX; k++) {
+#if TM_R2_CACHE
+        const float rk = P.r2[k * TB];
 #else
-    for (unsigned m = P.used; m; m &= m - 1) r = fmaxf(r, P.r2[(__ffs(m) - 1) * TB]);
+        const double2 vv = P.v[k * TB];
+        const float rk = vertex_r2f_t(vv.x, vv.y, (double)P.K[k * TB]);
 #endif
+        r = fmaxf(r, ((P.used >> k) & 1u) ? rk : 0.f);
+    }
     return r;
 }
 
+__device__ __forceinline__ void set_r2(TPoly &P, int k, double x, double y, double K) {
+#if TM_R2_CACHE
+    P.r2[k * TB] = vertex_r2f_t(x, y, K);
+#endif
+}
+
+__device__ __forceinline__ KT store_K(double K) {
+#if TM_K_DOUBLE
+    return K;
+#else
+    return K < 0.0 ? -1.f : __double2float_ru(K);
+#endif
+}
+
 // Clip the ring by line L (code >= 0: bisector with slot `code`; < 0: wall).
-// Returns 0 ok, -1 out of slots, -2 inconsistent.  The decisions are exactly
-// those of clip_by (group kernel): exact incircle sign for point-point vertices
-// (floating filter, expansion fallback), canonical test for wall vertices.
+// Returns 0 ok, -1 out of slots (or undecided filter, see TM_THREAD_EXACT),
+// -2 inconsistent.  The decisions are exactly those of clip_by (group kernel):
+// exact incircle sign for point-point vertices (floating filter, expansion
+// fallback), canonical test for wall vertices.  All VMAX slots are tested,
+// unrolled and branch-free (unused slots are masked out): no divergence between
+// threads with rings of different sizes, full ILP.
 __device__ int clip_t(TPoly &P, int code, const Line &L, const CellGeom &cgm, const CellArgs &A, ClipStats &cs) {
     const bool is_bis = code >= 0;
     const double n1 = fabs(L.nx) + fabs(L.ny);
+    const double c8 = 8.0 * EPS * n1 * n1;  // filter bound |d|_1 (K + 8 eps |d|_1) = n1 K + c8
     unsigned out = 0, unc = 0;
-#if TM_UNROLL_SLOTS
-    // every slot, unrolled and branch-free (unused slots are masked out): no
-    // divergence between threads with different rings, full ILP
+    if (TM_WALL_FAST && is_bis && !(P.used & P.wall)) {
+        // interior ring: point-point vertices only
 #pragma unroll
-    for (int k = 0; k < VMAX; k++) {
-        const double2 vv = P.v[k * TB];
-        const float Kf = P.K[k * TB];
-        const double del = fma(L.nx, vv.x, L.ny * vv.y) - L.r;
-        const double B = n1 * fma(8.0 * EPS, n1, (double)Kf);
-        const bool pp = is_bis && Kf >= 0.f;
-        const bool o = pp ? del > B : wall_out(L, vv.x, vv.y);
-        const bool u = pp && !(del > B) && del >= -B;
-        out |= (unsigned)o << k;
-        unc |= (unsigned)u << k;
+        for (int k = 0; k < VMAX; k++) {
+            const double2 vv = P.v[k * TB];
+            const double del = fma(L.nx, vv.x, L.ny * vv.y) - L.r;
+            const double B = fma(n1, (double)P.K[k * TB], c8);
+            out |= (unsigned)(del > B) << k;
+            unc |= (unsigned)(del <= B && del >= -B) << k;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < VMAX; k++) {
+            const double2 vv = P.v[k * TB];
+            const double del = fma(L.nx, vv.x, L.ny * vv.y) - L.r;
+            const double B = fma(n1, (double)P.K[k * TB], c8);
+            const bool pp = is_bis && !((P.wall >> k) & 1u);
+            const bool o = pp ? del > B : wall_out(L, vv.x, vv.y);
+            out |= (unsigned)o << k;
+            unc |= (unsigned)(pp && del <= B && del >= -B) << k;
+        }
     }
     out &= P.used;
     unc &= P.used;
-#else
-    for (unsigned m = P.used; m; m &= m - 1) {
-        const int k = __ffs(m) - 1;
-        const double2 vv = P.v[k * TB];
-        const double vx = vv.x, vy = vv.y;
-        const float Kf = P.K[k * TB];
-        bool o, u = false;
-        if (is_bis && Kf >= 0.f) {
-            const double del = fma(L.nx, vx, L.ny * vy) - L.r;
-            const double B = n1 * fma(8.0 * EPS, n1, (double)Kf);
-            o = del > B;
-            u = !o && del >= -B;
-        } else {
-            o = wall_out(L, vx, vy);
-        }
-        out |= (unsigned)o << k;
-        unc |= (unsigned)u << k;
-    }
-#endif
     // undecided point-point vertices (rare): exact incircle sign, outside the hot
     // loop -- or, with TM_THREAD_EXACT=0, the whole cell goes to the group kernel
 #if TM_THREAD_EXACT
@@ -174,20 +200,24 @@ __device__ int clip_t(TPoly &P, int code, const Line &L, const CellGeom &cgm, co
         const Line E1 = line_of(c1, cgm, A);
         double x, y;
         const double inv = cramer(E1, L, x, y);
-        const float Kn = (is_bis && c1 >= 0) ? __double2float_ru(pp_filter_K(E1, L, x, y, inv)) : -1.f;
+        const bool ppv = is_bis && c1 >= 0;
+        const double Kn = ppv ? pp_filter_K(E1, L, x, y, inv) : -1.0;
         P.v[s * TB] = make_double2(x, y);
-        P.K[s * TB] = Kn;
-        P.r2[s * TB] = vertex_r2f_t(x, y, Kn);
+        P.K[s * TB] = store_K(Kn);
+        set_r2(P, s, x, y, Kn);
+        P.wall = ppv ? (P.wall & ~(1u << s)) : (P.wall | (1u << s));
         P.nxt[s * TB] = (uint8_t)sB;
     }
     {   // B = (L, c2) in slot sB
         const Line E2 = line_of(c2, cgm, A);
         double x, y;
         const double inv = cramer(L, E2, x, y);
-        const float Kn = (is_bis && c2 >= 0) ? __double2float_ru(pp_filter_K(L, E2, x, y, inv)) : -1.f;
+        const bool ppv = is_bis && c2 >= 0;
+        const double Kn = ppv ? pp_filter_K(L, E2, x, y, inv) : -1.0;
         P.v[sB * TB] = make_double2(x, y);
-        P.K[sB * TB] = Kn;
-        P.r2[sB * TB] = vertex_r2f_t(x, y, Kn);
+        P.K[sB * TB] = store_K(Kn);
+        set_r2(P, sB, x, y, Kn);
+        P.wall = ppv ? (P.wall & ~(1u << sB)) : (P.wall | (1u << sB));
         P.la[sB * TB] = code;
         P.prv[sB * TB] = (uint8_t)s;
         P.nxt[sB * TB] = (uint8_t)ne;
@@ -367,13 +397,14 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
             cramer(wall_line(-1 - k, px, py, r_oct, bx0, by0, bx1, by1),
                    wall_line(-1 - ((k + 1) & 7), px, py, r_oct, bx0, by0, bx1, by1), x, y);
             P.v[k * TB] = make_double2(x, y);
-            P.K[k * TB] = -1.f;
-            P.r2[k * TB] = vertex_r2f_t(x, y, -1.f);
+            P.K[k * TB] = store_K(-1.0);
+            set_r2(P, k, x, y, -1.0);
             P.la[k * TB] = -1 - k;
             P.prv[k * TB] = (uint8_t)((k + 7) & 7);
             P.nxt[k * TB] = (uint8_t)((k + 1) & 7);
         }
         P.used = 0xffu;
+        P.wall = 0xffu;
         if (csub(px, bx0) < S || csub(bx1, px) < S || csub(py, by0) < S || csub(by1, py) < S) {
             for (int b = 0; b < 4 && !fail; b++) {
                 const int code = -9 - b;
@@ -502,8 +533,10 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
         // clip; leaf pruning then uses the R_max before the clip, which is conservative)
         const int cj = j;
         const double cxj = xj, cyj = yj;
+#if TM_PREFETCH
         j = next_cand();
         if (j >= 0) { xj = __ldg(A.xs + j); yj = __ldg(A.ys + j); }
+#endif
         if (cj >= 0) {
             sc.n_cand++;
             const double dx = csub(cxj, px), dy = csub(cyj, py);
@@ -517,6 +550,10 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
                 else if (cs.clips != c0) R2 = poly_R2(P);
             }
         }
+#if !TM_PREFETCH
+        j = next_cand();
+        if (j >= 0) { xj = __ldg(A.xs + j); yj = __ldg(A.ys + j); }
+#endif
     }
     if (live) {
         if (fail == -1) {

@@ -72,11 +72,11 @@ TM_HD Line wall_line(int code, double px, double py, double r_oct, double bx0, d
                      double by1) {
     Line L;
     if (code >= -8) {
-        int k = -1 - code;
-        const double ax[8] = {1, 1, 0, -1, -1, -1, 0, 1};
-        const double ay[8] = {0, 1, 1, 1, 0, -1, -1, -1};
-        L.nx = ax[k];
-        L.ny = ay[k];
+        // octagon side k: outward normal at 45k degrees, unnormalised (no table:
+        // a dynamically indexed local array would live in local memory)
+        const int k = -1 - code;
+        L.nx = (k == 0 || k == 1 || k == 7) ? 1.0 : ((k >= 3 && k <= 5) ? -1.0 : 0.0);
+        L.ny = (k >= 1 && k <= 3) ? 1.0 : ((k >= 5) ? -1.0 : 0.0);
         L.r = (k & 1) ? cmul(SQRT2, r_oct) : r_oct;
         return L;
     }

@@ -114,6 +114,10 @@ struct tm_ctx {
     int32_t *retry_list = nullptr;
     unsigned long long *retry_cnt = nullptr;
     int64_t cap_retry = 0;
+    // strip migration scratch (stable partition)
+    double *mig_keep = nullptr;
+    int32_t *mig_cnt = nullptr, *mig_off = nullptr;
+    int64_t cap_mig = 0, cap_mig_blk = 0;
     // device health counters
     tmg::DevState *dst = nullptr;
     bool have_cells = false;

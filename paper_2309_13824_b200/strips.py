@@ -167,14 +167,23 @@ class GpuStripBackend:
         self.ctx = ctx
         self.adj_stride = adj_stride
         self.keep_tri = keep_tri  # False: leave the triangles in the device buffers (no count readback)
+        self.bufs = {}
+
+    def _buf(self, name, numel, dtype, dev):
+        """Persistent scratch (grown on demand): no per-iteration allocation."""
+        b = self.bufs.get(name)
+        if b is None or b.numel() < numel or b.device != dev:
+            b = torch.empty(int(numel * 1.125) + 1024, dtype=dtype, device=dev)
+            self.bufs[name] = b
+        return b
 
     def halo(self, st: RankState, lo, hi, W):
         dev = st.x.device
         n = st.x.shape[0]
         cap = n
-        send_lo = torch.empty(3 * cap + 1, dtype=torch.float64, device=dev)
-        send_hi = torch.empty(3 * cap + 1, dtype=torch.float64, device=dev)
-        cnt = torch.zeros(2, dtype=torch.int64, device=dev)
+        send_lo = self._buf("send_lo", 3 * cap + 1, torch.float64, dev)
+        send_hi = self._buf("send_hi", 3 * cap + 1, torch.float64, dev)
+        cnt = self._buf("hcnt", 2, torch.int64, dev)[:2]
         self.ctx.tm_halo_pack(st.x, st.y, st.gid, n, lo if lo > -1e300 else -1e300, hi if hi < 1e300 else 1e300,
                               W, send_lo, send_hi, cap, cnt)
         c = cnt.tolist()
@@ -221,13 +230,16 @@ class GpuStripBackend:
         return bufs.tri[:nt].clone(), h["xo"], h["yo"], h["do"], h["status"]
 
     def migrate(self, st: RankState, lo, hi):
+        """Partition the updated owned points (stable, in place in st's arrays,
+        which this iteration produced): kept ones stay at the front, leavers are
+        packed for the neighbours."""
         dev = st.x.device
         n = st.x.shape[0]
-        out_lo = torch.empty(4 * n + 1, dtype=torch.float64, device=dev)
-        out_hi = torch.empty(4 * n + 1, dtype=torch.float64, device=dev)
-        cnt = torch.zeros(3, dtype=torch.int64, device=dev)
+        out_lo = self._buf("out_lo", 4 * n + 1, torch.float64, dev)
+        out_hi = self._buf("out_hi", 4 * n + 1, torch.float64, dev)
+        cnt = self._buf("mcnt", 3, torch.int64, dev)[:3]
         dp = st.d_prev if st.d_prev is not None else torch.zeros(n, dtype=torch.float64, device=dev)
-        x, y, g = st.x.clone(), st.y.clone(), st.gid.clone()
+        x, y, g = st.x, st.y, st.gid.clone()  # gid is shared with the previous state
         self.ctx.tm_migrate_pack(x, y, g, dp, n, lo if lo > -1e300 else -1e300, hi if hi < 1e300 else 1e300,
                                  out_lo, out_hi, n, cnt)
         k, a, b = cnt.tolist()
@@ -235,7 +247,7 @@ class GpuStripBackend:
         def seg(buf, m):
             return [buf[:m].clone(), buf[n:n + m].clone(),
                     buf[2 * n:2 * n + (m + 1) // 2 + 1].view(torch.int32)[:m].clone(), buf[3 * n:3 * n + m].clone()]
-        keep = [x[:k].clone(), y[:k].clone(), g[:k].clone(), dp[:k].clone()]
+        keep = [x[:k], y[:k], g[:k], dp[:k]]
         return keep, seg(out_lo, a), seg(out_hi, b)
 
 

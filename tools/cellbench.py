@@ -20,8 +20,19 @@ import paper_2309_13824_b200 as T  # noqa: E402
 from inputs import configs  # noqa: E402
 
 
+def load_cfg(cfg):
+    """3 (default) / 1..5: BASELINE configs; 'iid': 10^6 i.i.d. uniform points in the unit square
+    (box SDF 1024^2, uniform density) -- isolates the point distribution from the adaptive grids."""
+    if cfg == "iid":
+        import numpy as np
+        box = (0.0, 0.0, 1.0, 1.0)
+        x, y = configs.random_points(1_000_000, 7, box)
+        return configs.Config("iid1e6", x, y, box, configs.box_phi(box, 1024), None, None, ["dm", "cvd"])
+    return configs.load(int(cfg))
+
+
 def main(cfg=3, warm=3, reps=10, group=False, n_opt=None):
-    c = configs.load(cfg)
+    c = load_cfg(cfg)
     dev = torch.device("cuda", 0)
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
@@ -43,7 +54,8 @@ def main(cfg=3, warm=3, reps=10, group=False, n_opt=None):
         x, y, dp = xo, yo, do
     ctx.tm_grid_bin(x, y)
     xo, yo, do = torch.empty_like(x), torch.empty_like(x), torch.empty_like(x)
-    out = {"lib": os.path.basename(T.LIB_PATH), "cells": "group" if group else "thread", "n_opt": p.n_opt}
+    out = {"lib": os.path.basename(T.LIB_PATH), "cells": "group" if group else "thread", "n_opt": p.n_opt,
+           "config": c.name, "n": c.n}
     for mode in ("dm", "cvd"):
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps + 1)]
         for r in range(reps + 1):
@@ -68,5 +80,9 @@ if __name__ == "__main__":
     for a in sys.argv[1:]:
         if a.startswith("--n-opt="):
             nopts = [float(v) for v in a.split("=", 1)[1].split(",")]
+    cfg = "3"
+    for a in sys.argv[1:]:
+        if a.startswith("--cfg="):
+            cfg = a.split("=", 1)[1]
     for v in nopts:
-        main(group="--group" in sys.argv, n_opt=v)
+        main(cfg=cfg, group="--group" in sys.argv, n_opt=v)
