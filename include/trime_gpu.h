@@ -105,7 +105,8 @@ typedef struct {
  * (only with TM_F_COUNT_WORK).  Sums over cells. */
 typedef struct {
     int64_t n_cells, n_cert, deg, verts, t_own, quad_tris, ell, candidates, clips, exact_calls;
-    int64_t retries;  /* cells the thread kernel handed to the 32-lane pass (any flags) */
+    int64_t retries;    /* cells the thread kernel handed to the 32-lane pass (any flags)           */
+    int64_t warp_trips; /* thread kernel: candidate-loop trips summed over warps (x32 = lane slots) */
 } tm_work;
 
 void tm_params_default(tm_params *p);

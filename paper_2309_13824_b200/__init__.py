@@ -66,7 +66,7 @@ class tm_stats(ctypes.Structure):
 
 class tm_work(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in ("n_cells", "n_cert", "deg", "verts", "t_own", "quad_tris", "ell",
-                                              "candidates", "clips", "exact_calls", "retries")]
+                                              "candidates", "clips", "exact_calls", "retries", "warp_trips")]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -58,7 +58,8 @@ extern "C" tm_status tm_create(int device, void *cuda_stream, const tm_params *p
 
 static void free_points(tm_ctx *c) {
     cudaFree(c->xs); cudaFree(c->ys); cudaFree(c->hs);
-    cudaFree(c->perm); cudaFree(c->gids); cudaFree(c->key); cudaFree(c->rank);
+    cudaFree(c->perm); cudaFree(c->gids); cudaFree(c->key); cudaFree(c->rank); cudaFree(c->inv_perm);
+    c->inv_perm = nullptr;
     c->xs = c->ys = c->hs = nullptr;
     c->perm = c->gids = c->key = c->rank = nullptr;
     c->cap_points = 0;
@@ -75,6 +76,7 @@ extern "C" void tm_destroy(tm_ctx *ctx) {
     cudaFree(ctx->partials); cudaFree(ctx->stat_acc); cudaFree(ctx->dst);
     cudaFree(ctx->retry_list); cudaFree(ctx->retry_cnt);
     cudaFree(ctx->mig_keep); cudaFree(ctx->mig_cnt); cudaFree(ctx->mig_off);
+    cudaFree(ctx->nbr); cudaFree(ctx->nbr_cnt);
     delete ctx;
 }
 
@@ -184,6 +186,7 @@ extern "C" tm_status tm_set_domain(tm_ctx *ctx, const tm_fields *f, int64_t n_to
     ctx->bg.sx = Lx / nbx; ctx->bg.sy = Ly / nby;
     ctx->bg.isx = nbx / Lx; ctx->bg.isy = nby / Ly;
     ctx->have_domain = true;
+    ctx->nbr_n = -1;
     ctx->have_bins = false;
     ctx->have_cells = false;
     if (c_out) *c_out = ctx->c;
@@ -346,7 +349,7 @@ __global__ void k_bin_scatter(const double *__restrict__ x, const double *__rest
 // the atomic ranks of k_leaf_keys are not.  Leaves hold ~N_opt points.
 __global__ void k_leaf_sort(const int32_t *__restrict__ leaf_start, int64_t nleaves, double *__restrict__ xs,
                             double *__restrict__ ys, double *__restrict__ hs, int32_t *__restrict__ perm,
-                            int32_t *__restrict__ gids) {
+                            int32_t *__restrict__ gids, int32_t *__restrict__ inv_perm) {
     int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (l >= nleaves) return;
     int s = leaf_start[l], e = leaf_start[l + 1];
@@ -363,6 +366,7 @@ __global__ void k_leaf_sort(const int32_t *__restrict__ leaf_start, int64_t nlea
         }
         xs[b + 1] = x; ys[b + 1] = y; hs[b + 1] = h; perm[b + 1] = pk; gids[b + 1] = gk;
     }
+    for (int a = s; a < e; a++) inv_perm[perm[a]] = a;  // caller index -> slot
 }
 
 static tm_status ensure_points(tm_ctx *ctx, int64_t n) {
@@ -376,6 +380,7 @@ static tm_status ensure_points(tm_ctx *ctx, int64_t n) {
     TM_CUDA_TRY(ctx, cudaMalloc(&ctx->gids, cap * sizeof(int32_t)));
     TM_CUDA_TRY(ctx, cudaMalloc(&ctx->key, cap * sizeof(int32_t)));
     TM_CUDA_TRY(ctx, cudaMalloc(&ctx->rank, cap * sizeof(int32_t)));
+    TM_CUDA_TRY(ctx, cudaMalloc(&ctx->inv_perm, cap * sizeof(int32_t)));
     ctx->cap_points = cap;
     return TM_OK;
 }
@@ -459,9 +464,22 @@ extern "C" tm_status tm_grid_bin(tm_ctx *ctx, const double *x, const double *y, 
                                                    g.y0, g.x1, g.y1, g, ctx->mu, ctx->c, ctx->xs, ctx->ys,
                                                    ctx->hs, ctx->perm, ctx->gids);
     if ((s = tm_internal_check_launch(ctx, "k_bin_scatter")) != TM_OK) return s;
-    k_leaf_sort<<<(unsigned)((nleaves_max + 255) / 256), 256, 0, ctx->stream>>>(ctx->leaf_start, nleaves_max, ctx->xs,
-                                                                              ctx->ys, ctx->hs, ctx->perm, ctx->gids);
+    k_leaf_sort<<<(unsigned)((nleaves_max + 255) / 256), 256, 0, ctx->stream>>>(
+        ctx->leaf_start, nleaves_max, ctx->xs, ctx->ys, ctx->hs, ctx->perm, ctx->gids, ctx->inv_perm);
     if ((s = tm_internal_check_launch(ctx, "k_leaf_sort")) != TM_OK) return s;
+    if (n_local != ctx->nbr_n || (gid != nullptr) != ctx->have_gid) ctx->nbr_n = -1;  // warm start invalid
+    if (!gid && n_local > ctx->cap_nbr) {
+        cudaFree(ctx->nbr);
+        cudaFree(ctx->nbr_cnt);
+        ctx->nbr = nullptr;
+        ctx->nbr_cnt = nullptr;
+        const int64_t c = n_local + n_local / 8 + 1024;
+        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->nbr, c * TM_NBR * sizeof(int32_t)));
+        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->nbr_cnt, c * sizeof(uint8_t)));
+        ctx->cap_nbr = c;
+        ctx->nbr_n = -1;
+    }
+    ctx->have_gid = gid != nullptr;
     ctx->n_local = n_local;
     ctx->n_owned = n_owned;
     ctx->have_bins = true;
@@ -472,7 +490,10 @@ extern "C" tm_status tm_grid_bin(tm_ctx *ctx, const double *x, const double *y, 
 tm_status tm_internal_fill_cell_args(tm_ctx *ctx, CellArgs *a) {
     memset(a, 0, sizeof(*a));
     a->xs = ctx->xs; a->ys = ctx->ys; a->hs = ctx->hs;
-    a->perm = ctx->perm; a->gids = ctx->gids;
+    a->perm = ctx->perm; a->gids = ctx->gids; a->inv_perm = ctx->inv_perm;
+    a->nbr = ctx->have_gid ? nullptr : ctx->nbr;  // single domain only (caller ids are stable)
+    a->nbr_cnt = ctx->have_gid ? nullptr : ctx->nbr_cnt;
+    a->warm = (a->nbr && ctx->nbr_n == ctx->n_local) ? 1 : 0;
     a->rlev = ctx->rlev; a->leaf_off = ctx->leaf_off; a->leaf_start = ctx->leaf_start;
     a->bg = ctx->bg;
     a->n_local = ctx->n_local; a->n_owned = ctx->n_owned;
@@ -610,6 +631,7 @@ extern "C" tm_status tm_work_counts(tm_ctx *ctx, tm_work *out) {
         TM_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     }
     out->retries = (int64_t)rc;
+    out->warp_trips = (int64_t)ds.work[10];
     return TM_OK;
 }
 

@@ -631,7 +631,11 @@ extern "C" tm_status tm_voronoi_delaunay(tm_ctx *ctx, int32_t *tri, int64_t tri_
     else if (treat) s = dispatch_count<M_TRI | M_TREAT>(ctx, a);
     else if (adj) s = dispatch_count<M_TRI | M_ELL>(ctx, a);
     else s = dispatch_count<M_TRI>(ctx, a);
-    if (s == TM_OK) ctx->have_cells = true;
+    if (s == TM_OK) {
+        ctx->have_cells = true;
+        // neighbour lists written (thread kernel only): warm start for the next launch
+        ctx->nbr_n = (a.nbr && !(ctx->p.flags & TM_F_GROUP_CELLS)) ? ctx->n_local : -1;
+    }
     return s;
 }
 
@@ -647,5 +651,7 @@ extern "C" tm_status tm_cvd_step(tm_ctx *ctx, const double *d_prev, double *x_ha
     a.d_prev = d_prev; a.x_hat = x_hat; a.y_hat = y_hat;
     if (ctx->p.flags & TM_F_COUNT_WORK)
         TM_CUDA_TRY(ctx, cudaMemsetAsync(ctx->dst->work, 0, sizeof(ctx->dst->work), ctx->stream));
-    return dispatch_count<M_HAT>(ctx, a);
+    s = dispatch_count<M_HAT>(ctx, a);
+    if (s == TM_OK) ctx->nbr_n = (a.nbr && !(ctx->p.flags & TM_F_GROUP_CELLS)) ? ctx->n_local : -1;
+    return s;
 }

@@ -21,6 +21,7 @@
 // instead of 2, and no shuffle/ballot sits on the per-candidate critical path.
 
 #include <cuda_runtime.h>
+#include <climits>
 
 #include "tm_cellcore.cuh"
 
@@ -136,6 +137,7 @@ __device__ int clip_t(TPoly &P, int code, const Line &L, const CellGeom &cgm, co
     const double n1 = fabs(L.nx) + fabs(L.ny);
     const double c8 = 8.0 * EPS * n1 * n1;  // filter bound |d|_1 (K + 8 eps |d|_1) = n1 K + c8
     unsigned out = 0, unc = 0;
+    unsigned dup = 0;  // L already bounds the ring (a warm-start neighbour met again): no cut
     if (TM_WALL_FAST && is_bis && !(P.used & P.wall)) {
         // interior ring: point-point vertices only
 #pragma unroll
@@ -145,7 +147,9 @@ __device__ int clip_t(TPoly &P, int code, const Line &L, const CellGeom &cgm, co
             const double B = fma(n1, (double)P.K[k * TB], c8);
             out |= (unsigned)(del > B) << k;
             unc |= (unsigned)(del <= B && del >= -B) << k;
+            dup |= (unsigned)(P.la[k * TB] == code) << k;
         }
+        if (dup & P.used) return 0;
     } else {
 #pragma unroll
         for (int k = 0; k < VMAX; k++) {
@@ -156,7 +160,9 @@ __device__ int clip_t(TPoly &P, int code, const Line &L, const CellGeom &cgm, co
             const bool o = pp ? del > B : wall_out(L, vv.x, vv.y);
             out |= (unsigned)o << k;
             unc |= (unsigned)(pp && del <= B && del >= -B) << k;
+            dup |= (unsigned)(P.la[k * TB] == code) << k;
         }
+        if (dup & P.used) return 0;
     }
     out &= P.used;
     unc &= P.used;
@@ -378,6 +384,7 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
     unsigned key[8];
     // candidate iterator: phase (0 ring 1, 1 rings >= 2 clipped to a box, 2 done), ring-1 position
     // (phase 1: ring rk, side 0-3, cursor cvx up to cend along it; cvy / cfix the fixed row / column)
+    int wi = 0, wn = 0;  // warm-start cursor (phase -1)
     int ph = 2, rr = 0, t = 0, tend = 0, cvx = 0, cvy = 0, cend = -1, cfix = 0, rk = 1, side = 4, kmax = 0;
     int bxa = 0, bxb = -1, bya = 0, byb = -1;
     if (live) {
@@ -393,9 +400,12 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
         // ---- initial ring: octagon, vertex k between sides k and k+1 (det = +-1: exact inverse)
 #pragma unroll
         for (int k = 0; k < 8; k++) {
-            double x, y;
-            cramer(wall_line(-1 - k, px, py, r_oct, bx0, by0, bx1, by1),
-                   wall_line(-1 - ((k + 1) & 7), px, py, r_oct, bx0, by0, bx1, by1), x, y);
+            // consecutive octagon sides have det = 1 exactly, so the canonical Cramer
+            // vertex is the numerators themselves (x * fl(1/1) = x): no division
+            const Line La = wall_line(-1 - k, px, py, r_oct, bx0, by0, bx1, by1);
+            const Line Lb = wall_line(-1 - ((k + 1) & 7), px, py, r_oct, bx0, by0, bx1, by1);
+            const double x = csub(cmul(La.r, Lb.ny), cmul(La.ny, Lb.r));
+            const double y = csub(cmul(La.nx, Lb.r), cmul(La.r, Lb.nx));
             P.v[k * TB] = make_double2(x, y);
             P.K[k * TB] = store_K(-1.0);
             set_r2(P, k, x, y, -1.0);
@@ -447,7 +457,12 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
         vleaf_range(A, ux, uy, rh, ux, uy, st, cnt);
         t = st;
         tend = st + cnt;
-        ph = fail ? 2 : 0;
+        // warm start: the cell's neighbours of the previous launch on the same point set
+        // (caller ids) are clipped first -- the ring is then nearly final and R_max small
+        // before the search; the search still certifies the cell (L11), so the result
+        // does not depend on them
+        wn = (A.warm && A.nbr_cnt) ? min((int)A.nbr_cnt[orig], TM_NBR) : 0;
+        ph = fail ? 2 : (wn > 0 ? -1 : 0);
         rr = 0;
     }
     // ---- flat candidate loop: one candidate per thread per trip, the warp
@@ -456,6 +471,13 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
     auto next_cand = [&]() -> int {
         int j = -1;
         while (ph < 2) {
+            if (ph < 0) {
+                if (wi >= wn) { ph = 0; continue; }
+                const int id = A.nbr[(int64_t)orig * TM_NBR + wi++];
+                if (id < 0 || (int64_t)id >= A.n_local) continue;
+                j = A.inv_perm[id];
+                break;
+            }
             if (t < tend) { j = t++; break; }
             const float lim = 4.0f * R2 * (float)MARG;
             if (ph == 0) {  // ring 1, sorted
@@ -525,8 +547,10 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
     int j = next_cand();
     double xj = 0.0, yj = 0.0;
     if (j >= 0) { xj = __ldg(A.xs + j); yj = __ldg(A.ys + j); }
+    unsigned trips = 0;
     for (;;) {
         if (!__any_sync(0xffffffffu, j >= 0)) break;
+        trips++;
         // one candidate per thread per trip (skipping far candidates inside the iterator,
         // or testing several per step, lets single lanes run alone: measured slower);
         // the next candidate is fetched before this one is clipped (its load overlaps the
@@ -561,8 +585,10 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
             // the 32-lane group kernel redoes this cell
             const unsigned long long k = atomicAdd(retry_cnt, 1ull);
             retry_list[k] = (int32_t)cell;
+            if (A.nbr_cnt) A.nbr_cnt[orig] = 0;
             live = false;
         } else if (fail) {
+            if (A.nbr_cnt) A.nbr_cnt[orig] = 0;
             atomicAdd(&A.st->n_degenerate, 1ull);
             if (MODE & M_TREAT) {
                 A.x_out[orig] = px; A.y_out[orig] = py; A.d_prev_out[orig] = 0.0; A.status[orig] = 2;
@@ -572,8 +598,29 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
             live = false;
         }
     }
-    const int start = live ? __ffs(P.used) - 1 : 0;
+    // canonical start vertex (smallest (incoming, outgoing) line pair): every ring
+    // traversal below -- neighbour lists, ELL rows, centroid sums -- is then
+    // independent of the order in which the cell was clipped
+    int start = 0;
+    if (live) {
+        long long best = LLONG_MAX;
+        for (unsigned m = P.used; m; m &= m - 1) {  // used slots only: a free slot's link is garbage
+            const int k = __ffs(m) - 1;
+            const long long key = ((long long)P.la[k * TB] << 32) | (unsigned)P.la[P.nxt[k * TB] * TB];
+            if (key < best) { best = key; start = k; }
+        }
+    }
     const int nv = live ? __popc(P.used) : 0;
+    // neighbour list for the next launch's warm start (caller ids, ring order)
+    if (live && A.nbr) {
+        int k = start, c = 0;
+        for (int q = 0; q < nv; q++) {
+            const int a = P.la[k * TB];
+            if (a >= 0) A.nbr[(int64_t)orig * TM_NBR + c++] = __ldg(A.perm + a);
+            k = P.nxt[k * TB];
+        }
+        A.nbr_cnt[orig] = (uint8_t)c;
+    }
     // ---- S3: Delaunay triangles at point-point vertices + keep rule; ELL rows
     int ell = 0;
     if (live && (MODE & (M_TRI | M_ELL))) {
@@ -691,6 +738,7 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
         }
     }
     // ---- O8 work counters (TM_F_COUNT_WORK)
+    if ((MODE & M_COUNT) && lane == 0) atomicAdd(&A.st->work[10], (unsigned long long)trips);
     if ((MODE & M_COUNT) && live) {
         const float R2f = poly_R2(P);
         const double rad = 2.0 * sqrt((double)R2f);

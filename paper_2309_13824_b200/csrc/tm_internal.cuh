@@ -11,6 +11,8 @@
 
 namespace tmg {
 
+constexpr int TM_NBR = 12;  // warm-start neighbours kept per point (= thread-kernel slot capacity)
+
 // device-resident health counters and work counters (one per context)
 struct DevState {
     unsigned long long n_degenerate;   // exact zeros + inconsistent clips
@@ -20,7 +22,7 @@ struct DevState {
     unsigned long long n_tri_overflow; // triangles beyond tri_cap
     unsigned long long n_adj_overflow; // ELL rows beyond adj_stride
     unsigned long long n_fallback;     // projection fallbacks
-    unsigned long long work[10];       // tm_work fields after n_cells
+    unsigned long long work[11];       // tm_work fields n_cells .. exact_calls, then warp_trips
 };
 
 struct BinGeom {
@@ -58,6 +60,10 @@ __device__ __forceinline__ int leaf_coord(double x, double x0, double is, int nb
 struct CellArgs {
     const double *xs, *ys, *hs;
     const int32_t *perm, *gids;
+    const int32_t *inv_perm;   // caller index -> sorted slot (this binning)
+    int32_t *nbr;              // warm start: per caller index, the cell's neighbours (caller ids) of the
+    uint8_t *nbr_cnt;          //   last cell launch on the same point set; nbr_cnt[i] entries (<= TM_NBR)
+    int32_t warm;              // 1: read nbr/nbr_cnt before the search (they are written back either way)
     const uint8_t *rlev;
     const int32_t *leaf_off, *leaf_start;
     BinGeom bg;
@@ -100,7 +106,12 @@ struct tm_ctx {
     bool have_bins = false;
     int64_t n_local = 0, n_owned = 0, cap_points = 0, cap_bins = 0;
     double *xs = nullptr, *ys = nullptr, *hs = nullptr;
-    int32_t *perm = nullptr, *gids = nullptr, *key = nullptr, *rank = nullptr;
+    int32_t *perm = nullptr, *gids = nullptr, *key = nullptr, *rank = nullptr, *inv_perm = nullptr;
+    // warm start of the cell search (previous iteration's neighbours, caller ids; single domain only)
+    int32_t *nbr = nullptr;
+    uint8_t *nbr_cnt = nullptr;
+    int64_t cap_nbr = 0, nbr_n = -1;
+    bool have_gid = false;
     int32_t *bin_count = nullptr, *block_sums = nullptr;
     uint8_t *rlev = nullptr;
     int32_t *leaf_off = nullptr, *leaf_count = nullptr, *leaf_start = nullptr;

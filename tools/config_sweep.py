@@ -98,7 +98,8 @@ def run(k, warm=3, timed=5):
                     "work_per_cell": {kk: round(getattr(w, kk) / max(w.n_cells, 1), 3) for kk in
                                       ("n_cert", "deg", "verts", "t_own", "quad_tris", "candidates", "clips",
                                        "exact_calls")},
-                    "retries": int(w.retries)})
+                    "retries": int(w.retries),
+                    "lane_utilisation_search": w.candidates / max(1, 32 * w.warp_trips)})
         print(json.dumps(out[-1]), flush=True)
     ctx.close()
     cctx.close()
