@@ -166,6 +166,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--strips", action="store_true", help="use the x-strip path even at N=1 (smoke test)")
+    ap.add_argument("--n-opt", type=float, default=None, help="override tm_params.n_opt (tuning)")
     ap.add_argument("--cells", default="thread", choices=["thread", "group"],
                     help="cell kernel: one thread per cell (default) or 16-lane groups (A/B)")
     args = ap.parse_args()
@@ -193,6 +194,8 @@ def main():
     params = T.default_params()
     if args.cells == "group":
         params.flags |= T.TM_F_GROUP_CELLS
+    if args.n_opt:
+        params.n_opt = args.n_opt
     ctx = T.Context(local, params=params, stream=stream)
     box = c.box
     phi = torch.from_numpy(c.phi).to(dev)
@@ -329,7 +332,7 @@ def main():
     # untimed counting pass over the same schedule (SURVEY §8(d) cost table)
     roof = None
     if rank == 0 and ev_cells:
-        roof = roofline(T, c, ctx, cells_ms, params.flags)
+        roof = roofline(T, c, ctx, cells_ms, params.flags, params.n_opt)
 
     if rank == 0:
         cpu = None
@@ -377,11 +380,13 @@ def dp_peak():
     return 148 * 64 * mhz * 1e6, f"derived 148 SMs x 64 FP64 lanes x {mhz:.0f} MHz"
 
 
-def roofline(T, c, ctx, cells_ms, flags=0):
+def roofline(T, c, ctx, cells_ms, flags=0, n_opt=None):
     """achieved = algorithmic DP instructions per k_cells launch / mean launch time."""
     import torch
     p = T.default_params()
     p.flags |= T.TM_F_COUNT_WORK | flags
+    if n_opt:
+        p.n_opt = n_opt
     dev = torch.device("cuda", ctx.device)
     cc = T.Context(ctx.device, params=p)
     cc.tm_set_domain(c.box, torch.from_numpy(c.phi).to(dev), torch.from_numpy(c.mu).to(dev),

@@ -73,6 +73,7 @@ struct TPoly {
     uint8_t *prv, *nxt;
     unsigned used;  // occupied slots
     unsigned wall;  // slots holding a wall vertex (an octagon or box side among its lines)
+    unsigned long long lmask;  // bit (code & 63) for every bisector line of the ring (a filter)
 };
 
 __device__ __forceinline__ TPoly tpoly_bind(unsigned char *smem, int tid) {
@@ -86,6 +87,7 @@ __device__ __forceinline__ TPoly tpoly_bind(unsigned char *smem, int tid) {
     P.v = v + tid; P.K = K + tid; P.r2 = r2 + tid; P.la = la + tid; P.prv = prv + tid; P.nxt = nxt + tid;
     P.used = 0;
     P.wall = 0;
+    P.lmask = 0;
     return P;
 }
 
@@ -137,7 +139,14 @@ __device__ int clip_t(TPoly &P, int code, const Line &L, const CellGeom &cgm, co
     const double n1 = fabs(L.nx) + fabs(L.ny);
     const double c8 = 8.0 * EPS * n1 * n1;  // filter bound |d|_1 (K + 8 eps |d|_1) = n1 K + c8
     unsigned out = 0, unc = 0;
-    unsigned dup = 0;  // L already bounds the ring (a warm-start neighbour met again): no cut
+    // L already bounds the ring (a warm-start neighbour met again): no cut.  lmask filters;
+    // the full check over the ring's lines runs on a filter hit only
+    if (is_bis && ((P.lmask >> (code & 63)) & 1ull)) {
+        unsigned dup = 0;
+#pragma unroll
+        for (int k = 0; k < VMAX; k++) dup |= (unsigned)(P.la[k * TB] == code) << k;
+        if (dup & P.used) return 0;
+    }
     if (TM_WALL_FAST && is_bis && !(P.used & P.wall)) {
         // interior ring: point-point vertices only
 #pragma unroll
@@ -147,9 +156,7 @@ __device__ int clip_t(TPoly &P, int code, const Line &L, const CellGeom &cgm, co
             const double B = fma(n1, (double)P.K[k * TB], c8);
             out |= (unsigned)(del > B) << k;
             unc |= (unsigned)(del <= B && del >= -B) << k;
-            dup |= (unsigned)(P.la[k * TB] == code) << k;
         }
-        if (dup & P.used) return 0;
     } else {
 #pragma unroll
         for (int k = 0; k < VMAX; k++) {
@@ -160,9 +167,7 @@ __device__ int clip_t(TPoly &P, int code, const Line &L, const CellGeom &cgm, co
             const bool o = pp ? del > B : wall_out(L, vv.x, vv.y);
             out |= (unsigned)o << k;
             unc |= (unsigned)(pp && del <= B && del >= -B) << k;
-            dup |= (unsigned)(P.la[k * TB] == code) << k;
         }
-        if (dup & P.used) return 0;
     }
     out &= P.used;
     unc &= P.used;
@@ -230,6 +235,12 @@ __device__ int clip_t(TPoly &P, int code, const Line &L, const CellGeom &cgm, co
     }
     P.prv[ne * TB] = (uint8_t)sB;
     P.used = (P.used & ~out) | (1u << s) | (1u << sB);
+    unsigned long long lm = 0;
+    for (unsigned m = P.used; m; m &= m - 1) {
+        const int la = P.la[(__ffs(m) - 1) * TB];
+        if (la >= 0) lm |= 1ull << (la & 63);
+    }
+    P.lmask = lm;
     cs.clips++;
     return 0;
 }

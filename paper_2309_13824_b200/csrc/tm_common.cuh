@@ -27,12 +27,14 @@ TM_HD double cadd(double a, double b) { return __dadd_rn(a, b); }
 TM_HD double csub(double a, double b) { return __dsub_rn(a, b); }
 TM_HD double cdiv(double a, double b) { return __ddiv_rn(a, b); }
 TM_HD double cfma(double a, double b, double c) { return __fma_rn(a, b, c); }
+TM_HD double crcp(double a) { return __drcp_rn(a); }  // IEEE RN 1/a: the same bits as __ddiv_rn(1.0, a)
 #else
 TM_HD double cmul(double a, double b) { volatile double r = a * b; return r; }
 TM_HD double cadd(double a, double b) { volatile double r = a + b; return r; }
 TM_HD double csub(double a, double b) { volatile double r = a - b; return r; }
 TM_HD double cdiv(double a, double b) { volatile double r = a / b; return r; }
 TM_HD double cfma(double a, double b, double c) { return fma(a, b, c); }
+TM_HD double crcp(double a) { volatile double r = 1.0 / a; return r; }
 #endif
 
 // fl(cos(pi/8)) and fl(sqrt(2)): octagon geometry literals
@@ -60,7 +62,7 @@ TM_HD Line bisector(double dx, double dy) {
 // exactly symmetric in (A, B).  Returns inv (for error bounds).
 TM_HD double cramer(const Line &A, const Line &B, double &x, double &y) {
     double det = csub(cmul(A.nx, B.ny), cmul(A.ny, B.nx));
-    double inv = cdiv(1.0, det);
+    double inv = crcp(det);
     x = cmul(csub(cmul(A.r, B.ny), cmul(A.ny, B.r)), inv);
     y = cmul(csub(cmul(A.nx, B.r), cmul(A.r, B.nx)), inv);
     return inv;
