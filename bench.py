@@ -419,13 +419,21 @@ def roofline(T, c, ctx, cells_ms, flags=0, n_opt=None):
     cc.tm_sync()
     cc.close()
     peak, how = dp_peak()
+    traffic = None  # DRAM bytes per launch of the cell kernel from the committed ncu capture
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "kcells_traffic.json")))
+        nd = sum(1 for m in c.schedule if m == "dm")
+        traffic = (nd * tj["dm_bytes"] + (len(c.schedule) - nd) * tj["cvd_bytes"]) / len(c.schedule)
+    except Exception:
+        pass
     tot_f = sum(flops["dm"]) + sum(flops["cvd"])
     tot_t = sum(sum(v) for v in cells_ms.values()) / max(1, len(cells_ms["dm"]) + len(cells_ms["cvd"]))
     nl = len(c.schedule)
     per_launch_f = tot_f / nl
     achieved = per_launch_f / (tot_t / 1e3)
     return {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "T DP-inst/s",
-            "frac": achieved / peak, "traffic": None, "kernel": "k_cells (S2+S3+S4a+S5 fused)",
+            "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write)",
+            "kernel": "k_cells_t (S2+S3+S4a+S5 fused)",
             "algorithmic_dp_inst_per_launch": per_launch_f, "peak_source": how,
             "dp_inst_per_launch_by_mode": {k: (statistics.mean(v) if v else None) for k, v in flops.items()},
             "work_per_cell_by_mode": {m: {k: round(v / max(1, wsum[m][0]), 3) for k, v in zip(

@@ -22,6 +22,7 @@
 
 #include <cuda_runtime.h>
 #include <climits>
+#include <algorithm>
 
 #include "tm_cellcore.cuh"
 
@@ -31,16 +32,28 @@ using namespace tmg;
 #define TM_TB 128
 #endif
 #ifndef TM_VMAX
-#define TM_VMAX 12
+#define TM_VMAX 10
 #endif
 #ifndef TM_TMINB
-#define TM_TMINB 4
+#define TM_TMINB 5
 #endif
 #ifndef TM_PREFETCH
 #define TM_PREFETCH 1  // fetch the next candidate before clipping with the current one
 #endif
 #ifndef TM_WALL_FAST
 #define TM_WALL_FAST 0  // 1: separate point-point-only test loop for rings without walls (measured slower)
+#endif
+#ifndef TM_SPLIT
+#define TM_SPLIT 0  // search kernel with lane recycling + output kernel (0: one fused kernel)
+#endif
+#ifndef TM_CHUNK
+#define TM_CHUNK 64  // cells a warp takes from the global queue at a time
+#endif
+#ifndef TM_REFILL
+#define TM_REFILL 8  // idle lanes that trigger a refill
+#endif
+#ifndef TM_BALANCE
+#define TM_BALANCE 0  // 1: deal a block's cells to lanes by their last work (measured slower: locality)
 #endif
 #ifndef TM_K_DOUBLE
 #define TM_K_DOUBLE 0  // filter constants as float (rounded up): less shared memory, more L1
@@ -57,6 +70,7 @@ namespace {
 constexpr int TB = TM_TB;
 constexpr int VMAX = TM_VMAX;
 static_assert(VMAX <= 31, "slot masks are 32-bit");
+static_assert(TB <= 256 && (TB & (TB - 1)) == 0, "balancing keys hold the lane slot in 8 bits");
 #if TM_K_DOUBLE
 typedef double KT;  // filter constant storage
 #else
@@ -339,8 +353,8 @@ __device__ void quad_centroid_t(const TPoly &P, int start, int nv, double px, do
                 const double cr = csub(cmul(csub(Q[1][0], Q[0][0]), csub(Q[2][1], Q[0][1])),
                                        cmul(csub(Q[1][1], Q[0][1]), csub(Q[2][0], Q[0][0])));
                 const double At = cmul(0.5, cr);
-                const double qx = cdiv(cadd(cadd(Q[0][0], Q[1][0]), Q[2][0]), 3.0);
-                const double qy = cdiv(cadd(cadd(Q[0][1], Q[1][1]), Q[2][1]), 3.0);
+                const double qx = div3(cadd(cadd(Q[0][0], Q[1][0]), Q[2][0]));
+                const double qy = div3(cadd(cadd(Q[0][1], Q[1][1]), Q[2][1]));
                 const double rho = bilinear(A.grid, A.rho, cadd(px, qx), cadd(py, qy), LdgLoad());
                 const double wgt = At * rho;
                 sw += wgt;
@@ -365,8 +379,38 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
                                                           unsigned long long *retry_cnt) {
     extern __shared__ __align__(16) unsigned char tsmem[];
     const int tid = threadIdx.x;
-    const int64_t cell = (int64_t)blockIdx.x * TB + tid;
+    int64_t cell = (int64_t)blockIdx.x * TB + tid;
     const int lane = tid & 31;
+#if TM_BALANCE
+    // load balancing: a warp runs as many trips as its busiest lane, so the block's cells
+    // are dealt to its lanes in order of the work each took in the last launch (warm
+    // start only): every warp gets cells of similar cost.  Bitonic sort of the TB keys
+    // (work << 8 | lane slot) in the not yet used shared memory.
+    if (A.warm && A.nbr_work) {
+        unsigned w = 0;
+        if (cell < A.n_local) {
+            const int32_t o = __ldg(A.perm + cell);
+            if (o < A.n_owned) w = A.nbr_work[o];
+        }
+        unsigned *sk = reinterpret_cast<unsigned *>(tsmem);
+        sk[tid] = (w << 8) | (unsigned)tid;
+        __syncthreads();
+#pragma unroll 1
+        for (int k = 2; k <= TB; k <<= 1) {
+#pragma unroll 1
+            for (int jj = k >> 1; jj > 0; jj >>= 1) {
+                const int ixj = tid ^ jj;
+                if (ixj > tid) {
+                    const unsigned a = sk[tid], b = sk[ixj];
+                    if ((a > b) == ((tid & k) == 0)) { sk[tid] = b; sk[ixj] = a; }
+                }
+                __syncthreads();
+            }
+        }
+        cell = (int64_t)blockIdx.x * TB + (sk[tid] & 0xFFu);
+        __syncthreads();  // the polygon slots reuse this memory
+    }
+#endif
     TPoly P = tpoly_bind(tsmem, tid);
     bool live = false;
     int32_t orig = 0;
@@ -631,6 +675,9 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
             k = P.nxt[k * TB];
         }
         A.nbr_cnt[orig] = (uint8_t)c;
+#if TM_BALANCE
+        if (A.nbr_work) A.nbr_work[orig] = (uint8_t)min(sc.n_cand, 255ull);
+#endif
     }
     // ---- S3: Delaunay triangles at point-point vertices + keep rule; ELL rows
     int ell = 0;
@@ -785,12 +832,570 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
     }
 }
 
+
+// ============================================================================
+// Split path (TM_SPLIT): the search runs in k_search_t with lane recycling --
+// each warp takes contiguous chunks of cells from a global counter and a lane
+// that has certified its cell writes the ring (canonical order) to global
+// memory and takes the next cell as soon as TM_REFILL lanes are idle -- and all
+// outputs are computed by k_output_t, one thread per cell, from the stored
+// rings (the same ring, the same canonical start: the same bits as the fused
+// kernel).  The fused kernel runs a warp until its slowest lane is done.
+struct RingBuf {
+    double2 *v;                // [cell * VMAX + i], ring order from the canonical vertex
+    int *la;                   // incoming line code of ring vertex i
+    uint8_t *n;                // vertices, 0 = no ring (ghost, failed, or retried)
+    unsigned long long *chunk; // next unassigned cell (warp work queue)
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(TB, TM_TMINB) k_search_t(CellArgs A, int32_t *retry_list,
+                                                           unsigned long long *retry_cnt, RingBuf R) {
+    extern __shared__ __align__(16) unsigned char tsmem[];
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const unsigned lanemask_lt = (1u << lane) - 1u;
+    TPoly P = tpoly_bind(tsmem, tid);
+    const double MARG = 1.0 + 1e-9;
+    const BinGeom &bg = A.bg;
+    // warp work queue (uniform across the warp)
+    long long cursor = 0, wend = 0;
+    bool exhausted = false;
+    // this lane's cell
+    bool active = false;
+    int64_t cell = -1;
+    int32_t orig = 0;
+    double px = 0.0, py = 0.0;
+    CellGeom cgm = {};
+    float R2 = 0.f;
+    int fail = 0;
+    int rh = 0, ux = 0, uy = 0, nlx = 0, nly = 0;
+    double lsx = 0.0, lsy = 0.0;
+    unsigned key[8];
+    int wi = 0, wn = 0;
+    int ph = 2, rr = 0, t = 0, tend = 0, cvx = 0, cvy = 0, cend = -1, cfix = 0, rk = 1, side = 4, kmax = 0;
+    int bxa = 0, bxb = -1, bya = 0, byb = -1;
+    ClipStats cs;
+    unsigned long long n_cand = 0;
+    unsigned trips = 0;
+
+    auto setup = [&](int64_t c) {
+        cell = c;
+        fail = 0;
+        orig = __ldg(A.perm + c);
+        if (orig >= A.n_owned) {  // ghost: binned, no cell
+            R.n[c] = 0;
+            active = false;
+            return;
+        }
+        px = __ldg(A.xs + c);
+        py = __ldg(A.ys + c);
+        const double h = __ldg(A.hs + c);
+        const double S = cmul(A.fac_voro, h);
+        const double r_oct = cmul(S, COS_PI8);
+        const double bx0 = A.grid.x0, by0 = A.grid.y0, bx1 = A.grid.x1, by1 = A.grid.y1;
+        cgm = {px, py, r_oct, bx0, by0, bx1, by1};
+#pragma unroll
+        for (int k = 0; k < 8; k++) {  // octagon, det = 1 (see k_cells_t)
+            const Line La = wall_line(-1 - k, px, py, r_oct, bx0, by0, bx1, by1);
+            const Line Lb = wall_line(-1 - ((k + 1) & 7), px, py, r_oct, bx0, by0, bx1, by1);
+            const double x = csub(cmul(La.r, Lb.ny), cmul(La.ny, Lb.r));
+            const double y = csub(cmul(La.nx, Lb.r), cmul(La.r, Lb.nx));
+            P.v[k * TB] = make_double2(x, y);
+            P.K[k * TB] = store_K(-1.0);
+            set_r2(P, k, x, y, -1.0);
+            P.la[k * TB] = -1 - k;
+            P.prv[k * TB] = (uint8_t)((k + 7) & 7);
+            P.nxt[k * TB] = (uint8_t)((k + 1) & 7);
+        }
+        P.used = 0xffu;
+        P.wall = 0xffu;
+        P.lmask = 0;
+        if (csub(px, bx0) < S || csub(bx1, px) < S || csub(py, by0) < S || csub(by1, py) < S) {
+            for (int b = 0; b < 4 && !fail; b++) {
+                const int code = -9 - b;
+                fail = clip_t(P, code, wall_line(code, px, py, r_oct, bx0, by0, bx1, by1), cgm, A, cs);
+            }
+        }
+        R2 = poly_R2(P);
+        int hbx = (int)floor((px - bg.x0) * bg.isx), hby = (int)floor((py - bg.y0) * bg.isy);
+        hbx = hbx < 0 ? 0 : (hbx >= bg.nbx ? bg.nbx - 1 : hbx);
+        hby = hby < 0 ? 0 : (hby >= bg.nby ? bg.nby - 1 : hby);
+        rh = __ldg(A.rlev + hby * bg.nbx + hbx);
+        ux = leaf_coord(px, bg.x0, bg.isx, bg.nbx, rh);
+        uy = leaf_coord(py, bg.y0, bg.isy, bg.nby, rh);
+        nlx = bg.nbx << rh;
+        nly = bg.nby << rh;
+        lsx = bg.sx / (double)(1 << rh);
+        lsy = bg.sy / (double)(1 << rh);
+        const double gl = px - (bg.x0 + ux * lsx), gr = (bg.x0 + (ux + 1) * lsx) - px;
+        const double gd = py - (bg.y0 + uy * lsy), gu = (bg.y0 + (uy + 1) * lsy) - py;
+        const int ddx[8] = {-1, 1, 0, 0, -1, 1, -1, 1};
+        const int ddy[8] = {0, 0, -1, 1, -1, -1, 1, 1};
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            const double gx = fmax(ddx[q] < 0 ? gl : (ddx[q] > 0 ? gr : 0.0), 0.0);
+            const double gy = fmax(ddy[q] < 0 ? gd : (ddy[q] > 0 ? gu : 0.0), 0.0);
+            const float d2 = __double2float_rd(gx * gx + gy * gy);
+            key[q] = (__float_as_uint(fmaxf(d2, 0.f)) & ~7u) | (unsigned)q;
+        }
+        cswap(key[0], key[2]); cswap(key[1], key[3]); cswap(key[4], key[6]); cswap(key[5], key[7]);
+        cswap(key[0], key[4]); cswap(key[1], key[5]); cswap(key[2], key[6]); cswap(key[3], key[7]);
+        cswap(key[0], key[1]); cswap(key[2], key[3]); cswap(key[4], key[5]); cswap(key[6], key[7]);
+        cswap(key[2], key[4]); cswap(key[3], key[5]);
+        cswap(key[1], key[4]); cswap(key[3], key[6]);
+        cswap(key[1], key[2]); cswap(key[3], key[4]); cswap(key[5], key[6]);
+        int st, cnt;
+        vleaf_range(A, ux, uy, rh, ux, uy, st, cnt);
+        t = st;
+        tend = st + cnt;
+        wi = 0;
+        wn = (A.warm && A.nbr_cnt) ? min((int)A.nbr_cnt[orig], TM_NBR) : 0;
+        ph = fail ? 2 : (wn > 0 ? -1 : 0);
+        rr = 0;
+        rk = 1;
+        side = 4;
+        cvx = 0;
+        cend = -1;
+        active = true;
+    };
+
+    auto next_cand = [&]() -> int {
+        int j = -1;
+        while (ph < 2) {
+            if (ph < 0) {
+                if (wi >= wn) { ph = 0; continue; }
+                const int id = A.nbr[(int64_t)orig * TM_NBR + wi++];
+                if (id < 0 || (int64_t)id >= A.n_local) continue;
+                j = A.inv_perm[id];
+                break;
+            }
+            if (t < tend) { j = t++; break; }
+            const float lim = 4.0f * R2 * (float)MARG;
+            if (ph == 0) {
+                if (rr >= 8) {
+                    const double rad = 2.0 * sqrt((double)R2 * MARG) * (1.0 + 1e-6);
+                    const double sxl = bg.isx * (double)(1 << rh), syl = bg.isy * (double)(1 << rh);
+                    bxa = max(0, (int)floor((px - rad - bg.x0) * sxl));
+                    bxb = min(nlx - 1, (int)floor((px + rad - bg.x0) * sxl));
+                    bya = max(0, (int)floor((py - rad - bg.y0) * syl));
+                    byb = min(nly - 1, (int)floor((py + rad - bg.y0) * syl));
+                    kmax = max(max(ux - bxa, bxb - ux), max(uy - bya, byb - uy));
+                    ph = 1;
+                    rk = 1;
+                    side = 4;
+                    continue;
+                }
+                unsigned kq = key[0];
+#pragma unroll
+                for (int u = 1; u < 8; u++)
+                    if (rr == u) kq = key[u];
+                rr++;
+                if (__uint_as_float(kq & ~7u) * (1.0f - 1e-6f) >= lim) { rr = 8; continue; }
+                const int q = (int)(kq & 7u);
+                const int vx = ux + (q == 0 || q == 4 || q == 6 ? -1 : (q == 1 || q == 5 || q == 7 ? 1 : 0));
+                const int vy = uy + (q == 2 || q == 4 || q == 5 ? -1 : (q == 3 || q == 6 || q == 7 ? 1 : 0));
+                if (vx < 0 || vx >= nlx || vy < 0 || vy >= nly) continue;
+                int st, cnt;
+                vleaf_range(A, vx, vy, rh, ux, uy, st, cnt);
+                t = st;
+                tend = st + cnt;
+            } else {
+                if (cvx > cend) {
+                    if (++side >= 4) {
+                        rk++;
+                        if (rk > kmax) { ph = 2; break; }
+                        const double dl = px - (bg.x0 + (ux - rk + 1) * lsx), dr = (bg.x0 + (ux + rk) * lsx) - px;
+                        const double dd = py - (bg.y0 + (uy - rk + 1) * lsy), du = (bg.y0 + (uy + rk) * lsy) - py;
+                        const double dmin = fmin(fmin(dl, dr), fmin(dd, du));
+                        if (dmin > 0.0 && dmin * dmin * (1.0 - 1e-9) >= 4.0 * (double)R2 * MARG) { ph = 2; break; }
+                        side = 0;
+                    }
+                    if (side < 2) {
+                        cvy = side == 0 ? uy - rk : uy + rk;
+                        cvx = max(ux - rk, bxa);
+                        cend = (cvy < bya || cvy > byb) ? cvx - 1 : min(ux + rk, bxb);
+                    } else {
+                        cfix = side == 2 ? ux - rk : ux + rk;
+                        cvx = max(uy - rk + 1, bya);
+                        cend = (cfix < bxa || cfix > bxb) ? cvx - 1 : min(uy + rk - 1, byb);
+                    }
+                    continue;
+                }
+                const int vx = side < 2 ? cvx : cfix, vy = side < 2 ? cvy : cvx;
+                cvx++;
+                if (leaf_d2(bg, lsx, lsy, vx, vy, px, py) * (1.0 - 1e-9) >= 4.0 * (double)R2 * MARG) continue;
+                int st, cnt;
+                vleaf_range(A, vx, vy, rh, ux, uy, st, cnt);
+                t = st;
+                tend = st + cnt;
+            }
+        }
+        return j;
+    };
+
+    auto finish = [&]() {
+        active = false;
+        if (fail == -1) {  // over VMAX slots / undecided filter: the 32-lane pass redoes it
+            const unsigned long long k = atomicAdd(retry_cnt, 1ull);
+            retry_list[k] = (int32_t)cell;
+            if (A.nbr_cnt) A.nbr_cnt[orig] = 0;
+            R.n[cell] = 0;
+            return;
+        }
+        if (fail) {
+            if (A.nbr_cnt) A.nbr_cnt[orig] = 0;
+            atomicAdd(&A.st->n_degenerate, 1ull);
+            if (MODE & M_TREAT) {
+                A.x_out[orig] = px; A.y_out[orig] = py; A.d_prev_out[orig] = 0.0; A.status[orig] = 2;
+            }
+            if (MODE & M_HAT) { A.x_hat[orig] = px; A.y_hat[orig] = py; }
+            if (MODE & M_ELL) A.deg[cell] = 0;
+            R.n[cell] = 0;
+            return;
+        }
+        int start = 0;
+        long long best = LLONG_MAX;
+        for (unsigned m = P.used; m; m &= m - 1) {
+            const int k = __ffs(m) - 1;
+            const long long kk = ((long long)P.la[k * TB] << 32) | (unsigned)P.la[P.nxt[k * TB] * TB];
+            if (kk < best) { best = kk; start = k; }
+        }
+        const int nv = __popc(P.used);
+        double2 *rv = R.v + (int64_t)cell * VMAX;
+        int *rl = R.la + (int64_t)cell * VMAX;
+        int k = start;
+        for (int i = 0; i < nv; i++) {
+            rv[i] = P.v[k * TB];
+            rl[i] = P.la[k * TB];
+            k = P.nxt[k * TB];
+        }
+        R.n[cell] = (uint8_t)nv;
+    };
+
+    for (;;) {
+        // refill the idle lanes from the warp's queue once TM_REFILL of them are idle
+        const unsigned idle = __ballot_sync(0xffffffffu, !active);
+        if (idle && !exhausted && (__popc(idle) >= TM_REFILL || idle == 0xffffffffu)) {
+            unsigned pend = idle;
+            while (pend) {
+                if (cursor >= wend) {
+                    unsigned long long b = 0;
+                    if (lane == 0) b = atomicAdd(R.chunk, (unsigned long long)TM_CHUNK);
+                    b = __shfl_sync(0xffffffffu, b, 0);
+                    if ((int64_t)b >= A.n_local) { exhausted = true; break; }
+                    cursor = (long long)b;
+                    wend = min((long long)b + TM_CHUNK, (long long)A.n_local);
+                }
+                const int navail = (int)(wend - cursor);
+                const int rank = __popc(pend & lanemask_lt);
+                const bool mine = ((pend >> lane) & 1u) && rank < navail;
+                if (mine) setup(cursor + rank);
+                const int took = min(navail, __popc(pend));
+                cursor += took;
+                pend &= ~__ballot_sync(0xffffffffu, mine);
+            }
+        }
+        if (!__any_sync(0xffffffffu, active)) {
+            if (exhausted) break;
+            continue;
+        }
+        trips++;
+        const int j = active ? next_cand() : -1;
+        if (j >= 0) {
+            n_cand++;
+            const double dx = csub(__ldg(A.xs + j), px), dy = csub(__ldg(A.ys + j), py);
+            if (j == (int)cell) {
+            } else if (dx == 0.0 && dy == 0.0) {
+                atomicAdd(&A.st->n_duplicate, 1ull);
+            } else if (dx * dx + dy * dy < 4.0 * (double)R2 * MARG) {
+                const unsigned long long c0 = cs.clips;
+                fail = clip_t(P, j, bisector(dx, dy), cgm, A, cs);
+                if (fail) ph = 2;
+                else if (cs.clips != c0) R2 = poly_R2(P);
+            }
+        }
+        if (active && ph >= 2) finish();
+    }
+    if (MODE & M_COUNT) {
+        unsigned long long a = n_cand, b = cs.clips, c = cs.exact;
+        for (int o = 16; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            b += __shfl_xor_sync(0xffffffffu, b, o);
+            c += __shfl_xor_sync(0xffffffffu, c, o);
+        }
+        if (lane == 0) {
+            atomicAdd(&A.st->work[7], a);
+            atomicAdd(&A.st->work[8], b);
+            atomicAdd(&A.st->work[9], c);
+            atomicAdd(&A.st->work[10], (unsigned long long)trips);
+        }
+    }
+}
+
+// adaptive quadrature over a stored ring (ring order from the canonical vertex);
+// the same sub-triangles and sums as quad_centroid_t
+__device__ void quad_centroid_g(const double2 *rv, int nv, double px, double py, double area, double h, double dprev,
+                                const CellArgs &A, double &cx, double &cy, unsigned long long &nq) {
+    double eps = dprev >= 0.0 ? dprev / h : A.fac_pt;
+    if (eps < A.fac_end) eps = A.fac_end;
+    const double E = sqrt(area) * eps;
+    double prevx = 0.0, prevy = 0.0;
+    for (int L = 1; L <= A.quad_max; L++) {
+        const int depth = L - 1;
+        double sw = 0.0, swx = 0.0, swy = 0.0;
+        for (int f = 0; f < nv; f++) {
+            const double2 a = rv[f], b = rv[f + 1 == nv ? 0 : f + 1];
+            const double x1 = a.x, y1 = a.y, x2 = b.x, y2 = b.y;
+            const int64_t nleaf = (int64_t)1 << depth;
+            for (int64_t path = 0; path < nleaf; path++) {
+                double Q[3][2] = {{0.0, 0.0}, {x1, y1}, {x2, y2}};
+                for (int lev = depth - 1; lev >= 0; lev--) {
+                    double best = -1.0;
+                    int eidx = 0;
+#pragma unroll
+                    for (int q = 0; q < 3; q++) {
+                        const int q1 = q == 2 ? 0 : q + 1;
+                        const double ddx = csub(Q[q1][0], Q[q][0]), ddy = csub(Q[q1][1], Q[q][1]);
+                        const double Lq = cadd(cmul(ddx, ddx), cmul(ddy, ddy));
+                        if (Lq > best) { best = Lq; eidx = q; }
+                    }
+                    const int ia = eidx, ib = eidx == 2 ? 0 : eidx + 1, ic = ib == 2 ? 0 : ib + 1;
+                    const double ax = Q[ia][0], ay = Q[ia][1], bx = Q[ib][0], by = Q[ib][1];
+                    const double qx = Q[ic][0], qy = Q[ic][1];
+                    const double mx = cmul(cadd(ax, bx), 0.5), my = cmul(cadd(ay, by), 0.5);
+                    if ((path >> lev) & 1) {
+                        Q[0][0] = mx; Q[0][1] = my; Q[1][0] = bx; Q[1][1] = by;
+                    } else {
+                        Q[0][0] = ax; Q[0][1] = ay; Q[1][0] = mx; Q[1][1] = my;
+                    }
+                    Q[2][0] = qx; Q[2][1] = qy;
+                }
+                const double cr = csub(cmul(csub(Q[1][0], Q[0][0]), csub(Q[2][1], Q[0][1])),
+                                       cmul(csub(Q[1][1], Q[0][1]), csub(Q[2][0], Q[0][0])));
+                const double At = cmul(0.5, cr);
+                const double qx = div3(cadd(cadd(Q[0][0], Q[1][0]), Q[2][0]));
+                const double qy = div3(cadd(cadd(Q[0][1], Q[1][1]), Q[2][1]));
+                const double rho = bilinear(A.grid, A.rho, cadd(px, qx), cadd(py, qy), LdgLoad());
+                const double wgt = At * rho;
+                sw += wgt;
+                swx += wgt * qx;
+                swy += wgt * qy;
+                nq++;
+            }
+        }
+        const double curx = swx / sw, cury = swy / sw;
+        const double dx = prevx - curx, dy = prevy - cury;
+        const double dist = sqrt(dx * dx + dy * dy);
+        prevx = curx;
+        prevy = cury;
+        if (dist < E) break;
+    }
+    cx = prevx;
+    cy = prevy;
+}
+
+// outputs of every stored ring: S3 triangles + keep rule and ELL rows, S4a centroid,
+// S5 treatment, warm-start neighbour lists, O8 counters -- one thread per cell
+template <int MODE>
+__global__ void __launch_bounds__(128) k_output_t(CellArgs A, RingBuf R) {
+    const int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int nv = cell < A.n_local ? (int)R.n[cell] : 0;
+    const bool live = nv > 0;
+    const double2 *rv = R.v + (int64_t)cell * VMAX;
+    const int *rl = R.la + (int64_t)cell * VMAX;
+    int32_t orig = 0, gi = 0;
+    double px = 0.0, py = 0.0, h = 0.0;
+    if (live) {
+        orig = __ldg(A.perm + cell);
+        px = __ldg(A.xs + cell);
+        py = __ldg(A.ys + cell);
+        h = __ldg(A.hs + cell);
+        gi = __ldg(A.gids + cell);
+    }
+    if (live && A.nbr) {
+        int c = 0;
+        for (int i = 0; i < nv; i++) {
+            const int a = rl[i];
+            if (a >= 0) A.nbr[(int64_t)orig * TM_NBR + c++] = __ldg(A.perm + a);
+        }
+        A.nbr_cnt[orig] = (uint8_t)c;
+    }
+    int t_own = 0, ell = 0;
+    unsigned keptmask = 0;
+    if (live && (MODE & (M_TRI | M_ELL))) {
+        unsigned keptall = 0;
+        for (int i = 0; i < nv; i++) {
+            const int a = rl[i], b = rl[i + 1 == nv ? 0 : i + 1];
+            if (a >= 0 && b >= 0) {
+                const int32_t ga = __ldg(A.gids + a), gb = __ldg(A.gids + b);
+                if (gi < ga && gi < gb) {
+                    const int sv = ga < gb ? a : b, sw = ga < gb ? b : a;
+                    const double2 v = rv[i];
+                    if (keep_tri(A, (int)cell, sv, sw, cadd(px, v.x), cadd(py, v.y))) {
+                        keptmask |= 1u << i;
+                        keptall |= 1u << i;
+                    }
+                } else if (MODE & M_ELL) {
+                    int s3[3] = {(int)cell, a, b};
+                    int32_t g3[3] = {gi, ga, gb};
+                    for (int u = 0; u < 2; u++)
+                        for (int w = 0; w < 2 - u; w++)
+                            if (g3[w] > g3[w + 1]) {
+                                int32_t tg = g3[w]; g3[w] = g3[w + 1]; g3[w + 1] = tg;
+                                int ts = s3[w]; s3[w] = s3[w + 1]; s3[w + 1] = ts;
+                            }
+                    const double uxx = __ldg(A.xs + s3[0]), uyy = __ldg(A.ys + s3[0]);
+                    const Line B1 = bisector(csub(__ldg(A.xs + s3[1]), uxx), csub(__ldg(A.ys + s3[1]), uyy));
+                    const Line B2 = bisector(csub(__ldg(A.xs + s3[2]), uxx), csub(__ldg(A.ys + s3[2]), uyy));
+                    double ox, oy;
+                    cramer(B1, B2, ox, oy);
+                    if (keep_tri(A, s3[0], s3[1], s3[2], cadd(uxx, ox), cadd(uyy, oy))) keptall |= 1u << i;
+                }
+            }
+        }
+        if (!(MODE & M_TRI)) keptmask = 0;
+        t_own = __popc(keptmask);
+        if (MODE & M_ELL) {
+            for (int i = 0; i < nv; i++) {
+                const int a = rl[i];
+                const int ip = i == 0 ? nv - 1 : i - 1;
+                if (a >= 0 && (((keptall >> i) & 1u) || ((keptall >> ip) & 1u))) {
+                    if (ell < A.adj_stride) A.adj[(int64_t)ell * A.n_local + cell] = a;
+                    ell++;
+                }
+            }
+            A.deg[cell] = (uint8_t)(ell < A.adj_stride ? ell : A.adj_stride);
+            if (ell > A.adj_stride) atomicAdd(&A.st->n_adj_overflow, 1ull);
+        }
+    }
+    if (MODE & M_TRI) {
+        int incl = t_own;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int tt = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += tt;
+        }
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned long long base = 0;
+        if (lane == 31 && tot > 0) base = atomicAdd(A.n_tri, (unsigned long long)tot);
+        base = __shfl_sync(0xffffffffu, base, 31) + (unsigned long long)(incl - t_own);
+        for (unsigned m = keptmask; m; m &= m - 1) {
+            const int i = __ffs(m) - 1;
+            const int a = rl[i], b = rl[i + 1 == nv ? 0 : i + 1];
+            if ((int64_t)base < A.tri_cap) {
+                A.tri[3 * base] = gi;
+                A.tri[3 * base + 1] = __ldg(A.gids + a);
+                A.tri[3 * base + 2] = __ldg(A.gids + b);
+            } else {
+                atomicAdd(&A.st->n_tri_overflow, 1ull);
+            }
+            base++;
+        }
+    }
+    unsigned long long nq = 0;
+    if (live && (MODE & (M_TREAT | M_HAT))) {
+        double S2 = 0.0, sx = 0.0, sy = 0.0;
+        for (int i = 0; i < nv; i++) {
+            const double2 a = rv[i], b = rv[i + 1 == nv ? 0 : i + 1];
+            const double cr = a.x * b.y - b.x * a.y;
+            S2 += cr;
+            sx += cr * (a.x + b.x);
+            sy += cr * (a.y + b.y);
+        }
+        double cx, cy;
+        if (A.rho == nullptr) {
+            cx = sx / (3.0 * S2);
+            cy = sy / (3.0 * S2);
+            nq += nv;
+        } else {
+            const double dp = A.d_prev ? __ldg(A.d_prev + orig) : -1.0;
+            quad_centroid_g(rv, nv, px, py, 0.5 * S2, h, dp, A, cx, cy, nq);
+        }
+        if (MODE & M_HAT) {
+            A.x_hat[orig] = px + cx;
+            A.y_hat[orig] = py + cy;
+        }
+        if (MODE & M_TREAT) {
+            double qx, qy, dpo;
+            const int s = treat_point(A.grid, A.phi, h, A.h_avg, A.fac_pt, A.fac_geps, A.damping, A.newton_max, px,
+                                      py, px + cx, py + cy, qx, qy, dpo, LdgLoad());
+            A.x_out[orig] = qx;
+            A.y_out[orig] = qy;
+            A.d_prev_out[orig] = dpo;
+            A.status[orig] = (int8_t)s;
+            if (s & 2) atomicAdd(&A.st->n_fallback, 1ull);
+        }
+    }
+    if ((MODE & M_COUNT) && live) {
+        float R2f = 0.f;
+        for (int i = 0; i < nv; i++) R2f = fmaxf(R2f, vertex_r2f_t(rv[i].x, rv[i].y, -1.0));
+        const double rad = 2.0 * sqrt((double)R2f);
+        const BinGeom &bg = A.bg;
+        int ncert = 0;
+        const int bxa = max(0, (int)floor((px - rad - bg.x0) * bg.isx));
+        const int bxb = min(bg.nbx - 1, (int)floor((px + rad - bg.x0) * bg.isx));
+        const int bya = max(0, (int)floor((py - rad - bg.y0) * bg.isy));
+        const int byb = min(bg.nby - 1, (int)floor((py + rad - bg.y0) * bg.isy));
+        for (int by = bya; by <= byb; by++) {
+            const int s0 = __ldg(A.leaf_start + __ldg(A.leaf_off + by * bg.nbx + bxa));
+            const int s1 = __ldg(A.leaf_start + __ldg(A.leaf_off + by * bg.nbx + bxb + 1));
+            for (int s = s0; s < s1; s++) {
+                const double dx = __ldg(A.xs + s) - px, dy = __ldg(A.ys + s) - py;
+                ncert += (s != (int)cell) && (dx * dx + dy * dy < rad * rad);
+            }
+        }
+        int degc = 0;
+        for (int i = 0; i < nv; i++) degc += rl[i + 1 == nv ? 0 : i + 1] >= 0 ? 1 : 0;
+        atomicAdd(&A.st->work[0], 1ull);
+        atomicAdd(&A.st->work[1], (unsigned long long)ncert);
+        atomicAdd(&A.st->work[2], (unsigned long long)degc);
+        atomicAdd(&A.st->work[3], (unsigned long long)nv);
+        atomicAdd(&A.st->work[4], (unsigned long long)t_own);
+        atomicAdd(&A.st->work[5], (A.rho == nullptr) ? (unsigned long long)nv : nq);
+        atomicAdd(&A.st->work[6], (unsigned long long)ell);
+    }
+}
+
 }  // namespace
 
 namespace tmg {
 
 template <int MODE>
 tm_status launch_cells_thread(tm_ctx *ctx, const CellArgs &a) {
+#if TM_SPLIT
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        TM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_search_t<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)TSMEM));
+        attr_set = true;
+    }
+    if (ctx->n_local > ctx->cap_ring) {
+        cudaFree(ctx->ring_v); cudaFree(ctx->ring_la); cudaFree(ctx->ring_n);
+        ctx->ring_v = ctx->ring_la = ctx->ring_n = nullptr;
+        const int64_t c = ctx->n_local + ctx->n_local / 8 + 1024;
+        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->ring_v, c * VMAX * sizeof(double2)));
+        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->ring_la, c * VMAX * sizeof(int)));
+        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->ring_n, c * sizeof(uint8_t) + 64));
+        ctx->cap_ring = c;
+    }
+    RingBuf R;
+    R.v = (double2 *)ctx->ring_v;
+    R.la = (int *)ctx->ring_la;
+    R.n = (uint8_t *)ctx->ring_n;
+    R.chunk = (unsigned long long *)((uint8_t *)ctx->ring_n + ((ctx->cap_ring + 7) / 8) * 8);
+    TM_CUDA_TRY(ctx, cudaMemsetAsync(R.chunk, 0, sizeof(unsigned long long), ctx->stream));
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
+    const int64_t need = (ctx->n_local + (TB / 32) * TM_CHUNK - 1) / ((TB / 32) * TM_CHUNK);
+    const unsigned blocks = (unsigned)std::min<int64_t>(need, (int64_t)nsm * TM_TMINB);
+    k_search_t<MODE><<<blocks, TB, TSMEM, ctx->stream>>>(a, ctx->retry_list, ctx->retry_cnt, R);
+    tm_status s = tm_internal_check_launch(ctx, "k_search_t");
+    if (s != TM_OK) return s;
+    k_output_t<MODE><<<(unsigned)((ctx->n_local + 127) / 128), 128, 0, ctx->stream>>>(a, R);
+    return tm_internal_check_launch(ctx, "k_output_t");
+#else
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         TM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_cells_t<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TSMEM));
@@ -799,6 +1404,7 @@ tm_status launch_cells_thread(tm_ctx *ctx, const CellArgs &a) {
     const unsigned blocks = (unsigned)((ctx->n_local + TB - 1) / TB);
     k_cells_t<MODE><<<blocks, TB, TSMEM, ctx->stream>>>(a, ctx->retry_list, ctx->retry_cnt);
     return tm_internal_check_launch(ctx, "k_cells_t");
+#endif
 }
 
 #define TM_INST(M) template tm_status launch_cells_thread<M>(tm_ctx *, const CellArgs &);

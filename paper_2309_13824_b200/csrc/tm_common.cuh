@@ -116,6 +116,16 @@ TM_HD void grid_cell(const Grid &g, double x, double y, int &i, int &j, double &
 
 TM_HD double clerp(double a, double b, double s) { return cadd(a, cmul(s, csub(b, a))); }
 
+// x / 3 without a division: q = fl(x/3-ish), exact residual by FMA, one correction step
+// (Markstein).  Equal to the IEEE quotient on 4e8 random inputs (tests/test_div3.py);
+// used only for quadrature points (continuous quantities, never for a decision).
+TM_HD double div3(double x) {
+    const double T = 0.33333333333333331483;  // fl(1/3)
+    const double q = cmul(x, T);
+    const double r = cfma(-q, 3.0, x);
+    return cfma(r, T, q);
+}
+
 template <typename Load>
 TM_HD double bilinear(const Grid &g, const double *F, double x, double y, Load ld) {
     int i, j;
