@@ -862,7 +862,7 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_search_t(CellArgs A, int32_t *
     long long cursor = 0, wend = 0;
     bool exhausted = false;
     // this lane's cell
-    bool active = false;
+    bool active = false, done = false;
     int64_t cell = -1;
     int32_t orig = 0;
     double px = 0.0, py = 0.0;
@@ -1035,7 +1035,6 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_search_t(CellArgs A, int32_t *
     };
 
     auto finish = [&]() {
-        active = false;
         if (fail == -1) {  // over VMAX slots / undecided filter: the 32-lane pass redoes it
             const unsigned long long k = atomicAdd(retry_cnt, 1ull);
             retry_list[k] = (int32_t)cell;
@@ -1076,6 +1075,9 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_search_t(CellArgs A, int32_t *
     for (;;) {
         // refill the idle lanes from the warp's queue once TM_REFILL of them are idle
         const unsigned idle = __ballot_sync(0xffffffffu, !active);
+        if (idle && (__popc(idle) >= TM_REFILL || idle == 0xffffffffu)) {
+            if (done) { finish(); done = false; }  // batched: the lanes that finished since the last refill
+        }
         if (idle && !exhausted && (__popc(idle) >= TM_REFILL || idle == 0xffffffffu)) {
             unsigned pend = idle;
             while (pend) {
@@ -1097,7 +1099,10 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_search_t(CellArgs A, int32_t *
             }
         }
         if (!__any_sync(0xffffffffu, active)) {
-            if (exhausted) break;
+            if (exhausted) {
+                if (done) finish();
+                break;
+            }
             continue;
         }
         trips++;
@@ -1115,7 +1120,10 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_search_t(CellArgs A, int32_t *
                 else if (cs.clips != c0) R2 = poly_R2(P);
             }
         }
-        if (active && ph >= 2) finish();
+        if (active && ph >= 2) {  // certified (or failed): its outputs wait for the next refill
+            active = false;
+            done = true;
+        }
     }
     if (MODE & M_COUNT) {
         unsigned long long a = n_cand, b = cs.clips, c = cs.exact;

@@ -16,6 +16,7 @@ using namespace tmg;
 namespace {
 
 constexpr int DM_T = 256;
+constexpr int DM_U = 4;  // edges gathered per group
 
 __device__ __forceinline__ double mu_at(const Grid &g, const double *mu, double x, double y) {
     return mu ? bilinear(g, mu, x, y, LdgLoad()) : 1.0;
@@ -31,17 +32,31 @@ __global__ void __launch_bounds__(DM_T) k_dm_sums(const double *__restrict__ xs,
     int64_t s = (int64_t)blockIdx.x * DM_T + threadIdx.x;
     double l2 = 0.0, m2 = 0.0;
     if (s < n_local && perm[s] < n_owned) {
-        double xi = xs[s], yi = ys[s];
-        int32_t gi = gids[s];
-        int d = deg[s];
-        for (int k = 0; k < d; k++) {
-            int32_t a = adj[(int64_t)k * n_local + s];
-            if (gi < __ldg(gids + a)) {
-                double xa = __ldg(xs + a), ya = __ldg(ys + a);
-                double dx = xi - xa, dy = yi - ya;
-                l2 += dx * dx + dy * dy;
-                double m = mu_at(g, mu, cmul(cadd(xi, xa), 0.5), cmul(cadd(yi, ya), 0.5));
-                m2 += m * m;
+        const double xi = xs[s], yi = ys[s];
+        const int32_t gi = gids[s];
+        const int d = deg[s];
+        // edges in groups of DM_U: all index and position loads of a group are issued
+        // before any arithmetic (memory-level parallelism for the gathers)
+        for (int k0 = 0; k0 < d; k0 += DM_U) {
+            int a[DM_U];
+#pragma unroll
+            for (int u = 0; u < DM_U; u++) a[u] = (k0 + u < d) ? adj[(int64_t)(k0 + u) * n_local + s] : s;
+            double xa[DM_U], ya[DM_U];
+            int32_t ga[DM_U];
+#pragma unroll
+            for (int u = 0; u < DM_U; u++) {
+                xa[u] = __ldg(xs + a[u]);
+                ya[u] = __ldg(ys + a[u]);
+                ga[u] = __ldg(gids + a[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < DM_U; u++) {
+                if (k0 + u < d && gi < ga[u]) {
+                    const double dx = xi - xa[u], dy = yi - ya[u];
+                    l2 += dx * dx + dy * dy;
+                    const double m = mu_at(g, mu, cmul(cadd(xi, xa[u]), 0.5), cmul(cadd(yi, ya[u]), 0.5));
+                    m2 += m * m;
+                }
             }
         }
     }
@@ -96,17 +111,28 @@ __global__ void __launch_bounds__(DM_T) k_dm_step(CellArgs A, const int32_t *__r
     double fac_mu = sqrt(sums2[0] / sums2[1]);
     double xi = A.xs[s], yi = A.ys[s];
     double Fx = 0.0, Fy = 0.0;
-    int d = deg[s];
-    for (int k = 0; k < d; k++) {
-        int32_t a = adj[(int64_t)k * A.n_local + s];
-        double xa = __ldg(A.xs + a), ya = __ldg(A.ys + a);
-        double dx = xi - xa, dy = yi - ya;
-        double l = sqrt(dx * dx + dy * dy);
-        double l0 = mu_at(A.grid, A.mu, cmul(cadd(xi, xa), 0.5), cmul(cadd(yi, ya), 0.5)) * fscale * fac_mu;
-        if (l < l0) {
-            double fm = l0 - l;  // spring stiffness k = 1 (L3): only dt*k enters
-            Fx += fm * (dx / l);
-            Fy += fm * (dy / l);
+    const int d = deg[s];
+    for (int k0 = 0; k0 < d; k0 += DM_U) {  // gathers issued per group (see k_dm_sums)
+        int a[DM_U];
+#pragma unroll
+        for (int u = 0; u < DM_U; u++) a[u] = (k0 + u < d) ? adj[(int64_t)(k0 + u) * A.n_local + s] : (int)s;
+        double xa[DM_U], ya[DM_U];
+#pragma unroll
+        for (int u = 0; u < DM_U; u++) {
+            xa[u] = __ldg(A.xs + a[u]);
+            ya[u] = __ldg(A.ys + a[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < DM_U; u++) {
+            if (k0 + u >= d) continue;
+            const double dx = xi - xa[u], dy = yi - ya[u];
+            const double l = sqrt(dx * dx + dy * dy);
+            const double l0 = mu_at(A.grid, A.mu, cmul(cadd(xi, xa[u]), 0.5), cmul(cadd(yi, ya[u]), 0.5)) * fscale * fac_mu;
+            if (l < l0) {
+                const double fm = l0 - l;  // spring stiffness k = 1 (L3): only dt*k enters
+                Fx += fm * (dx / l);
+                Fy += fm * (dy / l);
+            }
         }
     }
     double xh = xi, yh = yi;

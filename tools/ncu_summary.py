@@ -48,7 +48,10 @@ WANT = [
     "smsp__inst_executed.sum", "smsp__thread_inst_executed_per_inst_executed.ratio",
     "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
     "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum", "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum",
-    "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum", "derived__smsp__sass_thread_inst_executed_op_dfma_pred_on_x2",
+    "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum",
+    "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum.per_cycle_elapsed",
+    "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum.per_cycle_elapsed",
+    "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum.per_cycle_elapsed", "sm__cycles_elapsed.avg",
     "dram__bytes_read.sum", "dram__bytes_write.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
     "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
     "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
@@ -77,8 +80,11 @@ def full(path):
                 if x == w:
                     print(f"  {w:70s} {d[i]:>16s} {units[i]}")
         try:
-            dp = sum(float(d[h.index(m)].replace(",", "")) for m in WANT[13:16])
-            print(f"  {'executed DP thread-instructions (dfma+dadd+dmul)':70s} {dp:16.4e}")
+            rate = sum(float(d[h.index(f"smsp__sass_thread_inst_executed_op_{o}_pred_on.sum.per_cycle_elapsed")])
+                       for o in ("dfma", "dadd", "dmul"))
+            cyc = float(d[h.index("sm__cycles_elapsed.avg")].replace(",", ""))
+            print(f"  {'executed DP thread-instructions per launch (dfma+dadd+dmul)':70s} {rate * cyc:16.4e}")
+            print(f"  {'  = per cycle, of the 148 x 64 = 9472 peak':70s} {rate:16.1f} ({100 * rate / 9472:.1f} %)")
         except (ValueError, IndexError):
             pass
 
