@@ -108,23 +108,55 @@ extern "C" tm_status tm_sync(tm_ctx *ctx) {
 // ============================================================================ S0
 // c and h_avg by a deterministic sequential sum in row-major cell order
 // (identical operation order to the oracle's definition, §8.0 "Local size").
-__global__ void k_domain_sums(Grid g, const double *phi, const double *mu, double *out3) {
+// S0 sums (reading L7): the per-cell terms are evaluated in parallel, then summed by
+// one thread in row-major order, so that c and h_avg keep the bits of the sequential
+// definition (the oracle's order) -- the sums are sequential, the bilinear work is not.
+__global__ void k_domain_terms(Grid g, const double *phi, const double *mu, double *w, double *m) {
+    const int64_t ncx = g.nx - 1, ncy = g.ny - 1;
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= ncx * ncy) return;
+    const int64_t j = k / ncx, i = k % ncx;
+    const double *p0 = phi + j * g.nx, *p1 = p0 + g.nx;
+    const double ph = clerp(clerp(p0[i], p0[i + 1], 0.5), clerp(p1[i], p1[i + 1], 0.5), 0.5);
+    if (!(ph < 0.0)) {
+        w[k] = -1.0;  // outside: skipped by the sum
+        return;
+    }
+    double mm = 1.0;
+    if (mu) {
+        const double *m0 = mu + j * g.nx, *m1 = m0 + g.nx;
+        mm = clerp(clerp(m0[i], m0[i + 1], 0.5), clerp(m1[i], m1[i + 1], 0.5), 0.5);
+    }
+    w[k] = cdiv(1.0, cmul(mm, mm));
+    m[k] = mm;
+}
+
+__global__ void k_domain_sums(int64_t n, const double *__restrict__ w, const double *__restrict__ m, double *out3) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     double sum_w = 0.0, sum_mu = 0.0, cnt = 0.0;
-    for (int j = 0; j < g.ny - 1; j++) {
-        const double *p0 = phi + (int64_t)j * g.nx, *p1 = p0 + g.nx;
-        for (int i = 0; i < g.nx - 1; i++) {
-            double ph = clerp(clerp(p0[i], p0[i + 1], 0.5), clerp(p1[i], p1[i + 1], 0.5), 0.5);
-            if (!(ph < 0.0)) continue;
-            double m = 1.0;
-            if (mu) {
-                const double *m0 = mu + (int64_t)j * g.nx, *m1 = m0 + g.nx;
-                m = clerp(clerp(m0[i], m0[i + 1], 0.5), clerp(m1[i], m1[i + 1], 0.5), 0.5);
-            }
-            sum_w = cadd(sum_w, cdiv(1.0, cmul(m, m)));
-            sum_mu = cadd(sum_mu, m);
+    constexpr int U = 16;  // loads of a group issued together; the adds stay in order
+    int64_t k = 0;
+    for (; k + U <= n; k += U) {
+        double wk[U], mk[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            wk[u] = __ldg(w + k + u);
+            mk[u] = __ldg(m + k + u);
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            if (wk[u] < 0.0) continue;
+            sum_w = cadd(sum_w, wk[u]);
+            sum_mu = cadd(sum_mu, mk[u]);
             cnt += 1.0;
         }
+    }
+    for (; k < n; k++) {
+        const double wk = w[k];
+        if (wk < 0.0) continue;
+        sum_w = cadd(sum_w, wk);
+        sum_mu = cadd(sum_mu, m[k]);
+        cnt += 1.0;
     }
     out3[0] = sum_w;
     out3[1] = sum_mu;
@@ -159,15 +191,20 @@ extern "C" tm_status tm_set_domain(tm_ctx *ctx, const tm_fields *f, int64_t n_to
     g.dy = cdiv(csub(f->y1, f->y0), (double)(f->ny - 1));
     ctx->grid = g;
     bool has_mu = f->mu != nullptr, has_rho = f->rho != nullptr;
-    double *d3;
+    double *d3, *terms;
+    const int64_t ncell = (int64_t)(g.nx - 1) * (g.ny - 1);
     TM_CUDA_TRY(ctx, cudaMalloc(&d3, 3 * sizeof(double)));
-    k_domain_sums<<<1, 1, 0, ctx->stream>>>(g, ctx->phi, has_mu ? ctx->mu : nullptr, d3);
+    TM_CUDA_TRY(ctx, cudaMalloc(&terms, 2 * ncell * sizeof(double)));
+    k_domain_terms<<<(unsigned)((ncell + 255) / 256), 256, 0, ctx->stream>>>(g, ctx->phi, has_mu ? ctx->mu : nullptr,
+                                                                             terms, terms + ncell);
+    k_domain_sums<<<1, 1, 0, ctx->stream>>>(ncell, terms, terms + ncell, d3);
     tm_status s = tm_internal_check_launch(ctx, "k_domain_sums");
-    if (s != TM_OK) { cudaFree(d3); return s; }
+    if (s != TM_OK) { cudaFree(d3); cudaFree(terms); return s; }
     double h3[3];
     cudaError_t e = cudaMemcpyAsync(h3, d3, sizeof(h3), cudaMemcpyDeviceToHost, ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     cudaFree(d3);
+    cudaFree(terms);
     if (e != cudaSuccess) TM_FAIL(ctx, TM_E_CUDA, "set_domain: %s", cudaGetErrorString(e));
     if (!(h3[2] > 0)) TM_FAIL(ctx, TM_E_ARG, "the SDF grid has no cell with phi < 0");
     // c = sqrt( sum_w * (dx*dy) / N ),  h_avg = c * (sum_mu / count)   (same order as the definition)

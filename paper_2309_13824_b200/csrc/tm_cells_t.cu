@@ -43,6 +43,9 @@ using namespace tmg;
 #ifndef TM_WALL_FAST
 #define TM_WALL_FAST 0  // 1: separate point-point-only test loop for rings without walls (measured slower)
 #endif
+#ifndef TM_COLD_NOINLINE
+#define TM_COLD_NOINLINE 0  // 1: once-per-cell code out of line (ABI calls; see DESIGN)
+#endif
 #ifndef TM_SPLIT
 #define TM_SPLIT 0  // search kernel with lane recycling + output kernel (0: one fused kernel)
 #endif
@@ -148,7 +151,8 @@ __device__ __forceinline__ KT store_K(double K) {
 // fallback), canonical test for wall vertices.  All VMAX slots are tested,
 // unrolled and branch-free (unused slots are masked out): no divergence between
 // threads with rings of different sizes, full ILP.
-__device__ int clip_t(TPoly &P, int code, const Line &L, const CellGeom &cgm, const CellArgs &A, ClipStats &cs) {
+__device__ __forceinline__ int clip_t(TPoly &P, int code, const Line &L, const CellGeom &cgm, const CellArgs &A,
+                                      ClipStats &cs) {
     const bool is_bis = code >= 0;
     const double n1 = fabs(L.nx) + fabs(L.ny);
     const double c8 = 8.0 * EPS * n1 * n1;  // filter bound |d|_1 (K + 8 eps |d|_1) = n1 K + c8
@@ -288,6 +292,26 @@ __device__ __forceinline__ void vleaf_range(const CellArgs &A, int vx, int vy, i
     }
 }
 
+// Code that runs once per cell (or rarely) is kept out of line (TM_COLD_NOINLINE):
+// the kernel is ~5-6k SASS instructions, and instruction-cache misses showed up as
+// "no instruction" stalls in the CVD variant.
+#if TM_COLD_NOINLINE
+#define TM_COLD __device__ __noinline__
+#else
+#define TM_COLD __device__ __forceinline__
+#endif
+TM_COLD int clip_t_cold(TPoly &P, int code, const Line &L, const CellGeom &cgm, const CellArgs &A, ClipStats &cs) {
+    return clip_t(P, code, L, cgm, A, cs);
+}
+TM_COLD bool keep_tri_cold(const CellArgs &A, int su, int sv, int sw, double cx, double cy) {
+    return keep_tri(A, su, sv, sw, cx, cy);
+}
+TM_COLD int treat_point_cold(const CellArgs &A, double h, double px, double py, double hx, double hy, double &qx,
+                             double &qy, double &dpo) {
+    return treat_point(A.grid, A.phi, h, A.h_avg, A.fac_pt, A.fac_geps, A.damping, A.newton_max, px, py, hx, hy, qx,
+                       qy, dpo, LdgLoad());
+}
+
 struct SearchCtx {
     double px, py;
     int cell;
@@ -311,7 +335,7 @@ __device__ __forceinline__ void cswap(unsigned &a, unsigned &b) {
 
 // adaptive quadrature centroid (Fig. 14; reading L13), one thread,
 // relative to p_i; same sub-triangle construction as quad_centroid
-__device__ void quad_centroid_t(const TPoly &P, int start, int nv, double px, double py, double area, double h,
+TM_COLD void quad_centroid_t(const TPoly &P, int start, int nv, double px, double py, double area, double h,
                                 double dprev, const CellArgs &A, double &cx, double &cy, unsigned long long &nq) {
     double eps = dprev >= 0.0 ? dprev / h : A.fac_pt;
     if (eps < A.fac_end) eps = A.fac_end;
@@ -473,7 +497,7 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
         if (csub(px, bx0) < S || csub(bx1, px) < S || csub(py, by0) < S || csub(by1, py) < S) {
             for (int b = 0; b < 4 && !fail; b++) {
                 const int code = -9 - b;
-                fail = clip_t(P, code, wall_line(code, px, py, r_oct, bx0, by0, bx1, by1), cgm, A, cs);
+                fail = clip_t_cold(P, code, wall_line(code, px, py, r_oct, bx0, by0, bx1, by1), cgm, A, cs);
             }
         }
         R2 = poly_R2(P);
@@ -691,7 +715,7 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
                 const int32_t ga = __ldg(A.gids + a), gb = __ldg(A.gids + b);
                 if (gi < ga && gi < gb) {
                     const int sv = ga < gb ? a : b, sw = ga < gb ? b : a;
-                    if (keep_tri(A, (int)cell, sv, sw, cadd(px, P.v[k * TB].x), cadd(py, P.v[k * TB].y))) {
+                    if (keep_tri_cold(A, (int)cell, sv, sw, cadd(px, P.v[k * TB].x), cadd(py, P.v[k * TB].y))) {
                         keptmask |= 1u << k;
                         keptall |= 1u << k;
                     }
@@ -709,7 +733,7 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
                     const Line B2 = bisector(csub(__ldg(A.xs + s3[2]), uxx), csub(__ldg(A.ys + s3[2]), uyy));
                     double ox, oy;
                     cramer(B1, B2, ox, oy);
-                    if (keep_tri(A, s3[0], s3[1], s3[2], cadd(uxx, ox), cadd(uyy, oy))) keptall |= 1u << k;
+                    if (keep_tri_cold(A, s3[0], s3[1], s3[2], cadd(uxx, ox), cadd(uyy, oy))) keptall |= 1u << k;
                 }
             }
             k = kn;
@@ -786,8 +810,7 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
         }
         if (MODE & M_TREAT) {
             double qx, qy, dpo;
-            const int s = treat_point(A.grid, A.phi, h, A.h_avg, A.fac_pt, A.fac_geps, A.damping, A.newton_max, px,
-                                      py, px + cx, py + cy, qx, qy, dpo, LdgLoad());
+            const int s = treat_point_cold(A, h, px, py, px + cx, py + cy, qx, qy, dpo);
             A.x_out[orig] = qx;
             A.y_out[orig] = qy;
             A.d_prev_out[orig] = dpo;
