@@ -104,24 +104,33 @@ class TorchP2P:
         return recv
 
     def exchange(self, to_lo: List[torch.Tensor], to_hi: List[torch.Tensor]):
-        """to_lo/to_hi: lists of 1-D tensors (same dtypes on both sides).
-        Returns (from_lo, from_hi) lists (None where there is no neighbour)."""
+        """to_lo/to_hi: lists of 1-D tensors of equal length (same dtypes on both sides).
+        Returns (from_lo, from_hi) lists (None where there is no neighbour).  Two rounds:
+        the element counts, then every array of a side packed into one byte buffer."""
         dev = self.device
         n = [torch.tensor([to_lo[0].shape[0]], dtype=torch.int64, device=dev),
              torch.tensor([to_hi[0].shape[0]], dtype=torch.int64, device=dev)]
         cnt = self._pair(n, lambda s: torch.empty(1, dtype=torch.int64, device=dev))
+        dts = [t.dtype for t in to_lo]
+        esz = [torch.empty(0, dtype=d).element_size() for d in dts]
+        order = sorted(range(len(dts)), key=lambda i: -esz[i])  # widest first: every view stays aligned
+
+        def pack(lst):
+            if not lst[0].numel():
+                return torch.empty(0, dtype=torch.uint8, device=dev)
+            return torch.cat([lst[i].contiguous().view(torch.uint8) for i in order])
+        k = [None if c is None else int(c.item()) for c in cnt]
+        got = self._pair([pack(to_lo), pack(to_hi)],
+                         lambda s: torch.empty(k[s] * sum(esz), dtype=torch.uint8, device=dev))
         out = [None, None]
-        for side, src in ((0, to_lo), (1, to_hi)):
-            if cnt[side] is None:
+        for side in (0, 1):
+            if got[side] is None:
                 continue
-            out[side] = []
-        for k in range(len(to_lo)):
-            dt = to_lo[k].dtype
-            got = self._pair([to_lo[k].contiguous(), to_hi[k].contiguous()],
-                             lambda s: torch.empty(int(cnt[s].item()), dtype=dt, device=dev))
-            for side in (0, 1):
-                if out[side] is not None:
-                    out[side].append(got[side])
+            parts, off = [None] * len(dts), 0
+            for i in order:
+                parts[i] = got[side][off:off + k[side] * esz[i]].view(dts[i])
+                off += k[side] * esz[i]
+            out[side] = parts
         return out[0], out[1]
 
     def allreduce_sum(self, t: torch.Tensor):
