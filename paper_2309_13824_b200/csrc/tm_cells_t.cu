@@ -43,6 +43,9 @@ using namespace tmg;
 #ifndef TM_WALL_FAST
 #define TM_WALL_FAST 0  // 1: separate point-point-only test loop for rings without walls (measured slower)
 #endif
+#ifndef TM_LCAP
+#define TM_LCAP 0  // >0: collect-then-clip queue per warm-started cell (measured slower, see DESIGN)
+#endif
 #ifndef TM_COLD_NOINLINE
 #define TM_COLD_NOINLINE 0  // 1: once-per-cell code out of line (ABI calls; see DESIGN)
 #endif
@@ -79,6 +82,7 @@ typedef double KT;  // filter constant storage
 #else
 typedef float KT;   // rounded up: still a valid bound
 #endif
+constexpr int LCAP = TM_LCAP;  // near-candidate queue per thread (warm-started cells), 0 = off
 constexpr size_t TSMEM = (size_t)VMAX * TB * (16 + sizeof(KT) + (TM_R2_CACHE ? 4 : 0) + 4 + 1 + 1);
 
 // this thread's view of the block's slot arrays (element k at [k * TB])
@@ -623,10 +627,89 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
         }
         return j;
     };
+    unsigned trips = 0;
+#if TM_LCAP > 0
+    // ---- warm-started cells: the flat loop below would pay a clip test (and often a ring
+    // update) in every trip in which any one lane has a near candidate.  Instead:
+    // (W) clip with the warm neighbours, flat; (A) collect, flat and cheap (iterator, load,
+    // distance test), every candidate closer than 2 R_max -- now nearly final -- that is
+    // not already a line of the ring into a per-thread queue; (B) clip from the queues,
+    // flat, so that nearly every lane of a trip has a useful clip test.  A full queue stops
+    // (A) for that thread; the flat loop (C) then continues its search.
+    if (__any_sync(0xffffffffu, ph == -1)) {
+        for (;;) {  // (W)
+            int cj = -1;
+            if (ph == -1) {
+                while (wi < wn) {
+                    const int id = A.nbr[(int64_t)orig * TM_NBR + wi++];
+                    if (id >= 0 && (int64_t)id < A.n_local) { cj = A.inv_perm[id]; break; }
+                }
+                if (cj < 0) ph = -2;  // warm list done: collect next
+            }
+            if (!__any_sync(0xffffffffu, cj >= 0)) break;
+            trips++;
+            if (cj >= 0) {
+                sc.n_cand++;
+                const double dx = csub(__ldg(A.xs + cj), px), dy = csub(__ldg(A.ys + cj), py);
+                if (cj != (int)cell && !(dx == 0.0 && dy == 0.0) && dx * dx + dy * dy < 4.0 * (double)R2 * MARG) {
+                    const unsigned long long c0 = cs.clips;
+                    fail = clip_t(P, cj, bisector(dx, dy), cgm, A, cs);
+                    if (fail) ph = 2;
+                    else if (cs.clips != c0) R2 = poly_R2(P);
+                }
+            }
+        }
+        int queue[LCAP > 0 ? LCAP : 1];  // thread-local (L1-resident local memory, not shared)
+        int nq_ = 0;
+        bool collecting = ph == -2;
+        if (collecting) ph = 0;
+        for (;;) {  // (A)
+            int cj = -1;
+            if (collecting) {
+                if (nq_ == LCAP) collecting = false;  // queue full: (C) continues this search
+                else {
+                    cj = next_cand();
+                    if (cj < 0) collecting = false;  // search space exhausted (ph == 2)
+                }
+            }
+            if (!__any_sync(0xffffffffu, cj >= 0)) break;
+            trips++;
+            if (cj >= 0) {
+                sc.n_cand++;
+                const double dx = csub(__ldg(A.xs + cj), px), dy = csub(__ldg(A.ys + cj), py);
+                if (cj == (int)cell) {
+                } else if (dx == 0.0 && dy == 0.0) {
+                    atomicAdd(&A.st->n_duplicate, 1ull);
+                } else if (dx * dx + dy * dy < 4.0 * (double)R2 * MARG) {
+                    bool line = false;  // already bounds the ring (a warm neighbour)
+                    if ((P.lmask >> (cj & 63)) & 1ull) {
+#pragma unroll
+                        for (int k = 0; k < VMAX; k++) line |= ((P.used >> k) & 1u) && P.la[k * TB] == cj;
+                    }
+                    if (!line) queue[nq_++] = cj;
+                }
+            }
+        }
+        for (int qi = 0;;) {  // (B)
+            const int cj = (qi < nq_ && !fail) ? queue[qi++] : -1;
+            if (!__any_sync(0xffffffffu, cj >= 0)) break;
+            trips++;
+            if (cj >= 0) {
+                const double dx = csub(__ldg(A.xs + cj), px), dy = csub(__ldg(A.ys + cj), py);
+                if (dx * dx + dy * dy < 4.0 * (double)R2 * MARG) {
+                    const unsigned long long c0 = cs.clips;
+                    fail = clip_t(P, cj, bisector(dx, dy), cgm, A, cs);
+                    if (fail) ph = 2;
+                    else if (cs.clips != c0) R2 = poly_R2(P);
+                }
+            }
+        }
+    }
+#endif
+    // ---- (C) flat candidate loop
     int j = next_cand();
     double xj = 0.0, yj = 0.0;
     if (j >= 0) { xj = __ldg(A.xs + j); yj = __ldg(A.ys + j); }
-    unsigned trips = 0;
     for (;;) {
         if (!__any_sync(0xffffffffu, j >= 0)) break;
         trips++;
