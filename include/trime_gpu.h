@@ -191,9 +191,13 @@ tm_status tm_adjacency_export(tm_ctx *ctx, const int32_t *adj, const uint8_t *de
 tm_status tm_work_counts(tm_ctx *ctx, tm_work *out);
 
 /* ---- S7 multi-GPU strips; the exchange itself is NCCL ------ */
-/* Pack the owned points with x < strip_lo + width into send_lo and those with
- * x >= strip_hi - width into send_hi, each as SoA segments [x | y | gid] of
- * capacity cap (doubles, doubles, int32).  Counts go to cnt2 (device int64[2]). */
+/* Pack the owned points with x < strip_lo + w into send_lo and those with
+ * x >= strip_hi - w into send_hi, each as SoA segments [x | y | gid] of
+ * capacity cap (doubles, doubles, int32).  Counts go to cnt2 (device int64[2]).
+ * width > 0: w = width for every point (2 S_max, reading L34).  width < 0:
+ * per point w_j = min(2 S_j / (1 - 2 fac c L), -width), L the Lipschitz
+ * constant of mu~ (computed by tm_set_domain), which bounds the octagon radius
+ * of any point across the edge; w = -width when 2 fac c L >= 1. */
 tm_status tm_halo_pack(tm_ctx *ctx, const double *x, const double *y, const int32_t *gid, int64_t n_owned,
                        double strip_lo, double strip_hi, double width, double *send_lo, double *send_hi,
                        int64_t cap, int64_t *cnt2);

@@ -163,6 +163,21 @@ __global__ void k_domain_sums(int64_t n, const double *__restrict__ w, const dou
     out3[2] = cnt;
 }
 
+// Lipschitz constant of the bilinear interpolant mu~ (continuous, bilinear per cell):
+// max over cells of |grad| <= sqrt(gx^2 + gy^2), gx = max(|f10-f00|,|f11-f01|)/dx, gy
+// likewise; kept as the bits of a positive double (atomicMax on the integer view)
+__global__ void k_lipschitz(Grid g, const double *mu, unsigned long long *out) {
+    const int64_t ncx = g.nx - 1, ncy = g.ny - 1;
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= ncx * ncy) return;
+    const int64_t j = k / ncx, i = k % ncx;
+    const double *r0 = mu + j * g.nx, *r1 = r0 + g.nx;
+    const double gx = fmax(fabs(r0[i + 1] - r0[i]), fabs(r1[i + 1] - r1[i])) / g.dx;
+    const double gy = fmax(fabs(r1[i] - r0[i]), fabs(r1[i + 1] - r0[i + 1])) / g.dy;
+    const double L = sqrt(gx * gx + gy * gy) * (1.0 + 1e-12);
+    atomicMax(out, (unsigned long long)__double_as_longlong(L));
+}
+
 extern "C" tm_status tm_set_domain(tm_ctx *ctx, const tm_fields *f, int64_t n_total, double *c_out,
                                    double *h_avg_out) {
     if (!ctx || !f || !f->phi) return ctx ? (snprintf(ctx->err, sizeof(ctx->err), "null argument"), TM_E_ARG) : TM_E_ARG;
@@ -208,6 +223,21 @@ extern "C" tm_status tm_set_domain(tm_ctx *ctx, const tm_fields *f, int64_t n_to
     if (e != cudaSuccess) TM_FAIL(ctx, TM_E_CUDA, "set_domain: %s", cudaGetErrorString(e));
     if (!(h3[2] > 0)) TM_FAIL(ctx, TM_E_ARG, "the SDF grid has no cell with phi < 0");
     // c = sqrt( sum_w * (dx*dy) / N ),  h_avg = c * (sum_mu / count)   (same order as the definition)
+    ctx->lip_mu = 0.0;
+    if (has_mu) {
+        unsigned long long *dl;
+        TM_CUDA_TRY(ctx, cudaMalloc(&dl, sizeof(unsigned long long)));
+        TM_CUDA_TRY(ctx, cudaMemsetAsync(dl, 0, sizeof(unsigned long long), ctx->stream));
+        k_lipschitz<<<(unsigned)((ncell + 255) / 256), 256, 0, ctx->stream>>>(g, ctx->mu, dl);
+        unsigned long long hl = 0;
+        cudaError_t e2 = cudaMemcpyAsync(&hl, dl, sizeof(hl), cudaMemcpyDeviceToHost, ctx->stream);
+        if (e2 == cudaSuccess) e2 = cudaStreamSynchronize(ctx->stream);
+        cudaFree(dl);
+        if (e2 != cudaSuccess) TM_FAIL(ctx, TM_E_CUDA, "set_domain: %s", cudaGetErrorString(e2));
+        double L;
+        memcpy(&L, &hl, sizeof(L));
+        ctx->lip_mu = L;
+    }
     ctx->c = sqrt(cdiv(cmul(h3[0], cmul(g.dx, g.dy)), (double)n_total));
     ctx->h_avg = cmul(ctx->c, cdiv(h3[1], h3[2]));
     if (!has_mu) { cudaFree(ctx->mu); ctx->mu = nullptr; ctx->grid_bytes = 0; }
@@ -704,18 +734,34 @@ extern "C" tm_status tm_adjacency_export(tm_ctx *ctx, const int32_t *adj, const 
 }
 
 // ============================================================================ S7 packing
+// Halo selection.  A point j of this strip can cut the cell of a point i
+// across the edge only if |p_j - p_i| < 2 S_i (C_i lies in Oct_i).  With w > 0 the band
+// is the fixed width w = 2 S_max.  With w < 0 the width is per point: S = fac h and h =
+// c mu~ is Lipschitz with constant c L, so S_i <= S_j + fac c L d and d < 2 S_i implies
+// d < 2 S_j / (1 - 2 fac c L) when 2 fac c L < 1; the band is the smaller of that and |w|.
 __global__ void k_halo_pack(const double *__restrict__ x, const double *__restrict__ y,
                             const int32_t *__restrict__ gid, int64_t n, double lo, double hi, double w,
+                            Grid g, const double *__restrict__ mu, double c, double fac, double lip,
                             double *send_lo, double *send_hi, int64_t cap, unsigned long long *cnt) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const double px = i < n ? x[i] : 0.0;
     const bool in_n = i < n;
+    double wi = w;
+    if (w < 0.0) {
+        const double k = 2.0 * fac * c * lip;
+        if (k < 1.0 && in_n) {
+            const double h = mu ? c * bilinear(g, mu, px, y[i], LdgLoad()) : c;
+            wi = fmin(2.0 * fac * h / (1.0 - k) * (1.0 + 1e-9), -w);  // both bounds hold: take the tighter
+        } else {
+            wi = -w;
+        }
+    }
     // two bands (a point can be in both when the strip is narrower than 2w);
     // one atomic per warp and band
 #pragma unroll
     for (int side = 0; side < 2; side++) {
-        const bool sel = in_n && (side == 0 ? px < lo + w : px >= hi - w);
+        const bool sel = in_n && (side == 0 ? px < lo + wi : px >= hi - wi);
         const unsigned m = __ballot_sync(0xffffffffu, sel);
         if (!m) continue;
         unsigned long long base = 0;
@@ -742,8 +788,10 @@ extern "C" tm_status tm_halo_pack(tm_ctx *ctx, const double *x, const double *y,
     TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
     TM_CUDA_TRY(ctx, cudaMemsetAsync(cnt2, 0, 2 * sizeof(int64_t), ctx->stream));
     if (n_owned == 0) return TM_OK;
+    if (width < 0.0 && !ctx->have_domain) TM_FAIL(ctx, TM_E_STATE, "adaptive halo width needs tm_set_domain");
     k_halo_pack<<<(unsigned)((n_owned + 255) / 256), 256, 0, ctx->stream>>>(
-        x, y, gid, n_owned, strip_lo, strip_hi, width, send_lo, send_hi, cap, (unsigned long long *)cnt2);
+        x, y, gid, n_owned, strip_lo, strip_hi, width, ctx->grid, ctx->mu, ctx->c, ctx->p.fac_voro_bound,
+        ctx->lip_mu, send_lo, send_hi, cap, (unsigned long long *)cnt2);
     return tm_internal_check_launch(ctx, "k_halo_pack");
 }
 

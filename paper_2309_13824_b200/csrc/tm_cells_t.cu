@@ -49,6 +49,9 @@ using namespace tmg;
 #ifndef TM_COLD_NOINLINE
 #define TM_COLD_NOINLINE 0  // 1: once-per-cell code out of line (ABI calls; see DESIGN)
 #endif
+#ifndef TM_CVD_SPLIT
+#define TM_CVD_SPLIT 0  // CVD: centroid, quadrature and treatment in a second kernel over stored rings
+#endif
 #ifndef TM_SPLIT
 #define TM_SPLIT 0  // search kernel with lane recycling + output kernel (0: one fused kernel)
 #endif
@@ -94,7 +97,8 @@ struct TPoly {
     uint8_t *prv, *nxt;
     unsigned used;  // occupied slots
     unsigned wall;  // slots holding a wall vertex (an octagon or box side among its lines)
-    unsigned long long lmask;  // bit (code & 63) for every bisector line of the ring (a filter)
+    unsigned long long lmask;  // bit (slot & 63) of every warm-start candidate clipped (a filter):
+                               // only those can reach the clip test twice
 };
 
 __device__ __forceinline__ TPoly tpoly_bind(unsigned char *smem, int tid) {
@@ -257,27 +261,24 @@ __device__ __forceinline__ int clip_t(TPoly &P, int code, const Line &L, const C
     }
     P.prv[ne * TB] = (uint8_t)sB;
     P.used = (P.used & ~out) | (1u << s) | (1u << sB);
-    unsigned long long lm = 0;
-    for (unsigned m = P.used; m; m &= m - 1) {
-        const int la = P.la[(__ffs(m) - 1) * TB];
-        if (la >= 0) lm |= 1ull << (la & 63);
-    }
-    P.lmask = lm;
     cs.clips++;
     return 0;
 }
 
 // leaf range [st, st+cnt) of virtual leaf (vx, vy) at the home resolution rh
 // (coarser leaves only at the virtual leaf closest to (ux, uy)); as the group kernel
-__device__ __forceinline__ void vleaf_range(const CellArgs &A, int vx, int vy, int rh, int ux, int uy, int &st,
-                                            int &cnt) {
+// (hb, hoff): the home level-0 bin and its first leaf -- most ring-1 leaves lie in the
+// home bin, whose level is rh: their range then costs one dependent load, not two
+__device__ __forceinline__ void vleaf_range(const CellArgs &A, int vx, int vy, int rh, int ux, int uy, int hb,
+                                            int hoff, int &st, int &cnt) {
     const BinGeom &bg = A.bg;
     st = 0;
     cnt = 0;
     const int bx = vx >> rh, by = vy >> rh;
     const int b = by * bg.nbx + bx;
-    const int rb = __ldg(A.rlev + b);
-    const int off = __ldg(A.leaf_off + b);
+    const bool home = b == hb;
+    const int rb = home ? rh : __ldg(A.rlev + b);
+    const int off = home ? hoff : __ldg(A.leaf_off + b);
     if (rb >= rh) {
         const int sh = 2 * (rb - rh);
         const int mlo = (int)morton2((uint32_t)(vx - (bx << rh)), (uint32_t)(vy - (by << rh))) << sh;
@@ -402,9 +403,20 @@ TM_COLD void quad_centroid_t(const TPoly &P, int start, int nv, double px, doubl
     cy = prevy;
 }
 
+// stored rings (split paths below)
+struct RingBuf {
+    double2 *v;                // [cell * VMAX + i], ring order from the canonical vertex
+    int *la;                   // incoming line code of ring vertex i
+    uint8_t *n;                // vertices, 0 = no ring (ghost, failed, or retried)
+    unsigned long long *chunk; // next unassigned cell (warp work queue)
+};
+
 template <int MODE>
 __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *retry_list,
-                                                          unsigned long long *retry_cnt) {
+                                                          unsigned long long *retry_cnt, RingBuf R) {
+    // CVD split (TM_CVD_SPLIT): this kernel stores the ring and k_output_t computes the
+    // centroid, quadrature and treatment -- a smaller kernel body for the search
+    constexpr bool CSPLIT = TM_CVD_SPLIT && (MODE & (M_TREAT | M_HAT)) && !(MODE & M_COUNT);
     extern __shared__ __align__(16) unsigned char tsmem[];
     const int tid = threadIdx.x;
     int64_t cell = (int64_t)blockIdx.x * TB + tid;
@@ -462,7 +474,7 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
     float R2 = 0.f;
     const double MARG = 1.0 + 1e-9;
     const BinGeom &bg = A.bg;
-    int rh = 0, ux = 0, uy = 0, nlx = 0, nly = 0;
+    int rh = 0, ux = 0, uy = 0, nlx = 0, nly = 0, hb = 0, hoff = 0;
     double lsx = 0.0, lsy = 0.0;
     unsigned key[8];
     // candidate iterator: phase (0 ring 1, 1 rings >= 2 clipped to a box, 2 done), ring-1 position
@@ -509,7 +521,9 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
         int hbx = (int)floor((px - bg.x0) * bg.isx), hby = (int)floor((py - bg.y0) * bg.isy);
         hbx = hbx < 0 ? 0 : (hbx >= bg.nbx ? bg.nbx - 1 : hbx);
         hby = hby < 0 ? 0 : (hby >= bg.nby ? bg.nby - 1 : hby);
-        rh = __ldg(A.rlev + hby * bg.nbx + hbx);
+        hb = hby * bg.nbx + hbx;
+        rh = __ldg(A.rlev + hb);
+        hoff = __ldg(A.leaf_off + hb);
         ux = leaf_coord(px, bg.x0, bg.isx, bg.nbx, rh);
         uy = leaf_coord(py, bg.y0, bg.isy, bg.nby, rh);
         nlx = bg.nbx << rh;
@@ -537,7 +551,7 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
         cswap(key[1], key[2]); cswap(key[3], key[4]); cswap(key[5], key[6]);
         // ring 0: the home leaf first
         int st, cnt;
-        vleaf_range(A, ux, uy, rh, ux, uy, st, cnt);
+        vleaf_range(A, ux, uy, rh, ux, uy, hb, hoff, st, cnt);
         t = st;
         tend = st + cnt;
         // warm start: the cell's neighbours of the previous launch on the same point set
@@ -559,6 +573,7 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
                 const int id = A.nbr[(int64_t)orig * TM_NBR + wi++];
                 if (id < 0 || (int64_t)id >= A.n_local) continue;
                 j = A.inv_perm[id];
+                P.lmask |= 1ull << (j & 63);
                 break;
             }
             if (t < tend) { j = t++; break; }
@@ -590,7 +605,7 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
                 const int vy = uy + (q == 2 || q == 4 || q == 5 ? -1 : (q == 3 || q == 6 || q == 7 ? 1 : 0));
                 if (vx < 0 || vx >= nlx || vy < 0 || vy >= nly) continue;
                 int st, cnt;
-                vleaf_range(A, vx, vy, rh, ux, uy, st, cnt);
+                vleaf_range(A, vx, vy, rh, ux, uy, hb, hoff, st, cnt);
                 t = st;
                 tend = st + cnt;
             } else {        // rings >= 2, side by side, clipped to the box; leaf-level pruning
@@ -620,7 +635,7 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
                 cvx++;
                 if (leaf_d2(bg, lsx, lsy, vx, vy, px, py) * (1.0 - 1e-9) >= 4.0 * (double)R2 * MARG) continue;
                 int st, cnt;
-                vleaf_range(A, vx, vy, rh, ux, uy, st, cnt);
+                vleaf_range(A, vx, vy, rh, ux, uy, hb, hoff, st, cnt);
                 t = st;
                 tend = st + cnt;
             }
@@ -865,8 +880,21 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
             base++;
         }
     }
+    if (CSPLIT && cell < A.n_local) {
+        if (live) {
+            double2 *rv = R.v + (int64_t)cell * VMAX;
+            int *rl = R.la + (int64_t)cell * VMAX;
+            int k = start;
+            for (int i = 0; i < nv; i++) {
+                rv[i] = P.v[k * TB];
+                rl[i] = P.la[k * TB];
+                k = P.nxt[k * TB];
+            }
+        }
+        R.n[cell] = (uint8_t)(live ? nv : 0);
+    }
     // ---- S4a centroid of C_i (relative to p_i) and S5 treatment
-    if (live && (MODE & (M_TREAT | M_HAT))) {
+    if (!CSPLIT && live && (MODE & (M_TREAT | M_HAT))) {
         double S2 = 0.0, sx = 0.0, sy = 0.0;
         int k = start;
         for (int c = 0; c < nv; c++) {
@@ -947,12 +975,6 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
 // outputs are computed by k_output_t, one thread per cell, from the stored
 // rings (the same ring, the same canonical start: the same bits as the fused
 // kernel).  The fused kernel runs a warp until its slowest lane is done.
-struct RingBuf {
-    double2 *v;                // [cell * VMAX + i], ring order from the canonical vertex
-    int *la;                   // incoming line code of ring vertex i
-    uint8_t *n;                // vertices, 0 = no ring (ghost, failed, or retried)
-    unsigned long long *chunk; // next unassigned cell (warp work queue)
-};
 
 template <int MODE>
 __global__ void __launch_bounds__(TB, TM_TMINB) k_search_t(CellArgs A, int32_t *retry_list,
@@ -975,7 +997,7 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_search_t(CellArgs A, int32_t *
     CellGeom cgm = {};
     float R2 = 0.f;
     int fail = 0;
-    int rh = 0, ux = 0, uy = 0, nlx = 0, nly = 0;
+    int rh = 0, ux = 0, uy = 0, nlx = 0, nly = 0, hb = 0, hoff = 0;
     double lsx = 0.0, lsy = 0.0;
     unsigned key[8];
     int wi = 0, wn = 0;
@@ -1027,7 +1049,9 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_search_t(CellArgs A, int32_t *
         int hbx = (int)floor((px - bg.x0) * bg.isx), hby = (int)floor((py - bg.y0) * bg.isy);
         hbx = hbx < 0 ? 0 : (hbx >= bg.nbx ? bg.nbx - 1 : hbx);
         hby = hby < 0 ? 0 : (hby >= bg.nby ? bg.nby - 1 : hby);
-        rh = __ldg(A.rlev + hby * bg.nbx + hbx);
+        hb = hby * bg.nbx + hbx;
+        rh = __ldg(A.rlev + hb);
+        hoff = __ldg(A.leaf_off + hb);
         ux = leaf_coord(px, bg.x0, bg.isx, bg.nbx, rh);
         uy = leaf_coord(py, bg.y0, bg.isy, bg.nby, rh);
         nlx = bg.nbx << rh;
@@ -1052,7 +1076,7 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_search_t(CellArgs A, int32_t *
         cswap(key[1], key[4]); cswap(key[3], key[6]);
         cswap(key[1], key[2]); cswap(key[3], key[4]); cswap(key[5], key[6]);
         int st, cnt;
-        vleaf_range(A, ux, uy, rh, ux, uy, st, cnt);
+        vleaf_range(A, ux, uy, rh, ux, uy, hb, hoff, st, cnt);
         t = st;
         tend = st + cnt;
         wi = 0;
@@ -1074,6 +1098,7 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_search_t(CellArgs A, int32_t *
                 const int id = A.nbr[(int64_t)orig * TM_NBR + wi++];
                 if (id < 0 || (int64_t)id >= A.n_local) continue;
                 j = A.inv_perm[id];
+                P.lmask |= 1ull << (j & 63);
                 break;
             }
             if (t < tend) { j = t++; break; }
@@ -1103,7 +1128,7 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_search_t(CellArgs A, int32_t *
                 const int vy = uy + (q == 2 || q == 4 || q == 5 ? -1 : (q == 3 || q == 6 || q == 7 ? 1 : 0));
                 if (vx < 0 || vx >= nlx || vy < 0 || vy >= nly) continue;
                 int st, cnt;
-                vleaf_range(A, vx, vy, rh, ux, uy, st, cnt);
+                vleaf_range(A, vx, vy, rh, ux, uy, hb, hoff, st, cnt);
                 t = st;
                 tend = st + cnt;
             } else {
@@ -1132,7 +1157,7 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_search_t(CellArgs A, int32_t *
                 cvx++;
                 if (leaf_d2(bg, lsx, lsy, vx, vy, px, py) * (1.0 - 1e-9) >= 4.0 * (double)R2 * MARG) continue;
                 int st, cnt;
-                vleaf_range(A, vx, vy, rh, ux, uy, st, cnt);
+                vleaf_range(A, vx, vy, rh, ux, uy, hb, hoff, st, cnt);
                 t = st;
                 tend = st + cnt;
             }
@@ -1515,9 +1540,30 @@ tm_status launch_cells_thread(tm_ctx *ctx, const CellArgs &a) {
         TM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_cells_t<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TSMEM));
         attr_set = true;
     }
+    constexpr bool CSPLIT = TM_CVD_SPLIT && (MODE & (M_TREAT | M_HAT)) && !(MODE & M_COUNT);
+    RingBuf R = {};
+    if (CSPLIT) {
+        if (ctx->n_local > ctx->cap_ring) {
+            cudaFree(ctx->ring_v); cudaFree(ctx->ring_la); cudaFree(ctx->ring_n);
+            ctx->ring_v = ctx->ring_la = ctx->ring_n = nullptr;
+            const int64_t c = ctx->n_local + ctx->n_local / 8 + 1024;
+            TM_CUDA_TRY(ctx, cudaMalloc(&ctx->ring_v, c * VMAX * sizeof(double2)));
+            TM_CUDA_TRY(ctx, cudaMalloc(&ctx->ring_la, c * VMAX * sizeof(int)));
+            TM_CUDA_TRY(ctx, cudaMalloc(&ctx->ring_n, c * sizeof(uint8_t) + 64));
+            ctx->cap_ring = c;
+        }
+        R.v = (double2 *)ctx->ring_v;
+        R.la = (int *)ctx->ring_la;
+        R.n = (uint8_t *)ctx->ring_n;
+    }
     const unsigned blocks = (unsigned)((ctx->n_local + TB - 1) / TB);
-    k_cells_t<MODE><<<blocks, TB, TSMEM, ctx->stream>>>(a, ctx->retry_list, ctx->retry_cnt);
-    return tm_internal_check_launch(ctx, "k_cells_t");
+    k_cells_t<MODE><<<blocks, TB, TSMEM, ctx->stream>>>(a, ctx->retry_list, ctx->retry_cnt, R);
+    tm_status s = tm_internal_check_launch(ctx, "k_cells_t");
+    if (s != TM_OK || !CSPLIT) return s;
+    CellArgs b = a;
+    b.nbr = nullptr;  // the neighbour lists were written by k_cells_t
+    k_output_t<MODE & (M_TREAT | M_HAT)><<<(unsigned)((ctx->n_local + 127) / 128), 128, 0, ctx->stream>>>(b, R);
+    return tm_internal_check_launch(ctx, "k_output_t");
 #endif
 }
 

@@ -99,6 +99,7 @@ struct tm_ctx {
     bool have_domain = false;
     tmg::Grid grid;
     double c = 0, h_avg = 0;
+    double lip_mu = 0;  // Lipschitz constant of mu~ (0 for uniform sizing): adaptive halo widths
     int64_t n_total = 0;
     double *phi = nullptr, *mu = nullptr, *rho = nullptr;
     size_t grid_bytes = 0;

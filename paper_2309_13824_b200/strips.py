@@ -172,9 +172,10 @@ class _LoopbackView:
 class GpuStripBackend:
     """The per-rank arithmetic through the C ABI (no CPU work)."""
 
-    def __init__(self, ctx, adj_stride=16, keep_tri=True):
+    def __init__(self, ctx, adj_stride=16, keep_tri=True, adaptive_halo=True):
         self.ctx = ctx
         self.adj_stride = adj_stride
+        self.adaptive_halo = adaptive_halo  # per-point halo width from the Lipschitz bound of mu~
         self.keep_tri = keep_tri  # False: leave the triangles in the device buffers (no count readback)
         self.bufs = {}
 
@@ -194,7 +195,7 @@ class GpuStripBackend:
         send_hi = self._buf("send_hi", 3 * cap + 1, torch.float64, dev)
         cnt = self._buf("hcnt", 2, torch.int64, dev)[:2]
         self.ctx.tm_halo_pack(st.x, st.y, st.gid, n, lo if lo > -1e300 else -1e300, hi if hi < 1e300 else 1e300,
-                              W, send_lo, send_hi, cap, cnt)
+                              -W if self.adaptive_halo else W, send_lo, send_hi, cap, cnt)
         c = cnt.tolist()
 
         def seg(buf, k):

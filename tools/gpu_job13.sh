@@ -1,0 +1,6 @@
+set -x
+TAG=${TAG:-run}
+timeout 900 python -m pytest tests/test_gpu_strips.py -m gpu -x -q > gpurun_out/${TAG}_strips.log 2>&1; echo "strips exit $?" >> gpurun_out/${TAG}_strips.log
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/${TAG}_gpu_tests.log 2>&1; echo "pytest exit $?" >> gpurun_out/${TAG}_gpu_tests.log
+timeout 600 python bench.py --steps 3 --warmup 3 > gpurun_out/${TAG}_bench.log 2>&1; echo "bench exit $?" >> gpurun_out/${TAG}_bench.log
+echo done
