@@ -50,7 +50,8 @@ using namespace tmg;
 #define TM_COLD_NOINLINE 0  // 1: once-per-cell code out of line (ABI calls; see DESIGN)
 #endif
 #ifndef TM_CVD_SPLIT
-#define TM_CVD_SPLIT 0  // CVD: centroid, quadrature and treatment in a second kernel over stored rings
+#define TM_CVD_SPLIT 1  // 1: CVD centroid, quadrature, treatment in a second kernel over stored rings;
+                        // 2: triangles and ELL rows there too (all modes)
 #endif
 #ifndef TM_SPLIT
 #define TM_SPLIT 0  // search kernel with lane recycling + output kernel (0: one fused kernel)
@@ -416,7 +417,9 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
                                                           unsigned long long *retry_cnt, RingBuf R) {
     // CVD split (TM_CVD_SPLIT): this kernel stores the ring and k_output_t computes the
     // centroid, quadrature and treatment -- a smaller kernel body for the search
-    constexpr bool CSPLIT = TM_CVD_SPLIT && (MODE & (M_TREAT | M_HAT)) && !(MODE & M_COUNT);
+    constexpr bool CSPLIT = !(MODE & M_COUNT) && ((TM_CVD_SPLIT >= 1 && (MODE & (M_TREAT | M_HAT))) ||
+                                                  (TM_CVD_SPLIT >= 2 && (MODE & M_ELL)));
+    constexpr bool TSPLIT = CSPLIT && TM_CVD_SPLIT >= 2;  // triangles / ELL rows in k_output_t too
     extern __shared__ __align__(16) unsigned char tsmem[];
     const int tid = threadIdx.x;
     int64_t cell = (int64_t)blockIdx.x * TB + tid;
@@ -803,7 +806,7 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
     }
     // ---- S3: Delaunay triangles at point-point vertices + keep rule; ELL rows
     int ell = 0;
-    if (live && (MODE & (M_TRI | M_ELL))) {
+    if (!TSPLIT && live && (MODE & (M_TRI | M_ELL))) {
         unsigned keptall = 0;  // for the ELL: kept, owned or not
         int k = start;
         for (int c = 0; c < nv; c++) {
@@ -854,7 +857,7 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
             if (ell > A.adj_stride) atomicAdd(&A.st->n_adj_overflow, 1ull);
         }
     }
-    if (MODE & M_TRI) {
+    if (!TSPLIT && (MODE & M_TRI)) {
         // warp-aggregated allocation of the owned kept triangles
         __syncwarp();
         int incl = t_own;
@@ -1540,7 +1543,9 @@ tm_status launch_cells_thread(tm_ctx *ctx, const CellArgs &a) {
         TM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_cells_t<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TSMEM));
         attr_set = true;
     }
-    constexpr bool CSPLIT = TM_CVD_SPLIT && (MODE & (M_TREAT | M_HAT)) && !(MODE & M_COUNT);
+    constexpr bool CSPLIT = !(MODE & M_COUNT) && ((TM_CVD_SPLIT >= 1 && (MODE & (M_TREAT | M_HAT))) ||
+                                                  (TM_CVD_SPLIT >= 2 && (MODE & M_ELL)));
+    constexpr int OMODE = TM_CVD_SPLIT >= 2 ? (MODE & (M_TRI | M_ELL | M_TREAT | M_HAT)) : (MODE & (M_TREAT | M_HAT));
     RingBuf R = {};
     if (CSPLIT) {
         if (ctx->n_local > ctx->cap_ring) {
@@ -1562,7 +1567,7 @@ tm_status launch_cells_thread(tm_ctx *ctx, const CellArgs &a) {
     if (s != TM_OK || !CSPLIT) return s;
     CellArgs b = a;
     b.nbr = nullptr;  // the neighbour lists were written by k_cells_t
-    k_output_t<MODE & (M_TREAT | M_HAT)><<<(unsigned)((ctx->n_local + 127) / 128), 128, 0, ctx->stream>>>(b, R);
+    k_output_t<OMODE><<<(unsigned)((ctx->n_local + 127) / 128), 128, 0, ctx->stream>>>(b, R);
     return tm_internal_check_launch(ctx, "k_output_t");
 #endif
 }
