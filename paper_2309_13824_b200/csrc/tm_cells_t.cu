@@ -885,12 +885,12 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
     }
     if (CSPLIT && cell < A.n_local) {
         if (live) {
-            double2 *rv = R.v + (int64_t)cell * VMAX;
-            int *rl = R.la + (int64_t)cell * VMAX;
+            double2 *rv = R.v + cell;
+            int *rl = R.la + cell;
             int k = start;
             for (int i = 0; i < nv; i++) {
-                rv[i] = P.v[k * TB];
-                rl[i] = P.la[k * TB];
+                rv[(int64_t)i * A.n_local] = P.v[k * TB];  // slot-major: a warp's stores coalesce
+                rl[(int64_t)i * A.n_local] = P.la[k * TB];
                 k = P.nxt[k * TB];
             }
         }
@@ -1195,12 +1195,12 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_search_t(CellArgs A, int32_t *
             if (kk < best) { best = kk; start = k; }
         }
         const int nv = __popc(P.used);
-        double2 *rv = R.v + (int64_t)cell * VMAX;
-        int *rl = R.la + (int64_t)cell * VMAX;
+        double2 *rv = R.v + cell;
+        int *rl = R.la + cell;
         int k = start;
         for (int i = 0; i < nv; i++) {
-            rv[i] = P.v[k * TB];
-            rl[i] = P.la[k * TB];
+            rv[(int64_t)i * A.n_local] = P.v[k * TB];
+            rl[(int64_t)i * A.n_local] = P.la[k * TB];
             k = P.nxt[k * TB];
         }
         R.n[cell] = (uint8_t)nv;
@@ -1276,53 +1276,80 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_search_t(CellArgs A, int32_t *
 }
 
 // adaptive quadrature over a stored ring (ring order from the canonical vertex);
-// the same sub-triangles and sums as quad_centroid_t
-__device__ void quad_centroid_g(const double2 *rv, int nv, double px, double py, double area, double h, double dprev,
-                                const CellArgs &A, double &cx, double &cy, unsigned long long &nq) {
+// the same sub-triangles and sums, in the same order, as quad_centroid_t.  Sub-triangles
+// are taken QB at a time: their geometry and the four density corners of each are loaded
+// first, then summed in order -- the kernel is bound by the latency of those loads.
+__device__ __forceinline__ void quad_sub(const double2 a, const double2 b, int depth, int64_t path, double &At,
+                                         double &qx, double &qy) {
+    double Q[3][2] = {{0.0, 0.0}, {a.x, a.y}, {b.x, b.y}};
+    for (int lev = depth - 1; lev >= 0; lev--) {
+        double best = -1.0;
+        int eidx = 0;
+#pragma unroll
+        for (int q = 0; q < 3; q++) {
+            const int q1 = q == 2 ? 0 : q + 1;
+            const double ddx = csub(Q[q1][0], Q[q][0]), ddy = csub(Q[q1][1], Q[q][1]);
+            const double Lq = cadd(cmul(ddx, ddx), cmul(ddy, ddy));
+            if (Lq > best) { best = Lq; eidx = q; }
+        }
+        const int ia = eidx, ib = eidx == 2 ? 0 : eidx + 1, ic = ib == 2 ? 0 : ib + 1;
+        const double ax = Q[ia][0], ay = Q[ia][1], bx = Q[ib][0], by = Q[ib][1];
+        const double cx = Q[ic][0], cy = Q[ic][1];
+        const double mx = cmul(cadd(ax, bx), 0.5), my = cmul(cadd(ay, by), 0.5);
+        if ((path >> lev) & 1) {
+            Q[0][0] = mx; Q[0][1] = my; Q[1][0] = bx; Q[1][1] = by;
+        } else {
+            Q[0][0] = ax; Q[0][1] = ay; Q[1][0] = mx; Q[1][1] = my;
+        }
+        Q[2][0] = cx; Q[2][1] = cy;
+    }
+    const double cr = csub(cmul(csub(Q[1][0], Q[0][0]), csub(Q[2][1], Q[0][1])),
+                           cmul(csub(Q[1][1], Q[0][1]), csub(Q[2][0], Q[0][0])));
+    At = cmul(0.5, cr);
+    qx = div3(cadd(cadd(Q[0][0], Q[1][0]), Q[2][0]));
+    qy = div3(cadd(cadd(Q[0][1], Q[1][1]), Q[2][1]));
+}
+
+#ifndef TM_QB
+#define TM_QB 2  // sub-triangles whose density loads are in flight together
+#endif
+
+__device__ void quad_centroid_g(const double2 *rv, int64_t ns, int nv, double px, double py, double area, double h,
+                                double dprev, const CellArgs &A, double &cx, double &cy, unsigned long long &nq) {
     double eps = dprev >= 0.0 ? dprev / h : A.fac_pt;
     if (eps < A.fac_end) eps = A.fac_end;
     const double E = sqrt(area) * eps;
+    const Grid &g = A.grid;
     double prevx = 0.0, prevy = 0.0;
     for (int L = 1; L <= A.quad_max; L++) {
         const int depth = L - 1;
+        const int64_t ntot = (int64_t)nv << depth;
         double sw = 0.0, swx = 0.0, swy = 0.0;
-        for (int f = 0; f < nv; f++) {
-            const double2 a = rv[f], b = rv[f + 1 == nv ? 0 : f + 1];
-            const double x1 = a.x, y1 = a.y, x2 = b.x, y2 = b.y;
-            const int64_t nleaf = (int64_t)1 << depth;
-            for (int64_t path = 0; path < nleaf; path++) {
-                double Q[3][2] = {{0.0, 0.0}, {x1, y1}, {x2, y2}};
-                for (int lev = depth - 1; lev >= 0; lev--) {
-                    double best = -1.0;
-                    int eidx = 0;
+        for (int64_t t0 = 0; t0 < ntot; t0 += TM_QB) {
+            double At[TM_QB], qx[TM_QB], qy[TM_QB], ss[TM_QB], tt[TM_QB];
+            double f00[TM_QB], f10[TM_QB], f01[TM_QB], f11[TM_QB];
 #pragma unroll
-                    for (int q = 0; q < 3; q++) {
-                        const int q1 = q == 2 ? 0 : q + 1;
-                        const double ddx = csub(Q[q1][0], Q[q][0]), ddy = csub(Q[q1][1], Q[q][1]);
-                        const double Lq = cadd(cmul(ddx, ddx), cmul(ddy, ddy));
-                        if (Lq > best) { best = Lq; eidx = q; }
-                    }
-                    const int ia = eidx, ib = eidx == 2 ? 0 : eidx + 1, ic = ib == 2 ? 0 : ib + 1;
-                    const double ax = Q[ia][0], ay = Q[ia][1], bx = Q[ib][0], by = Q[ib][1];
-                    const double qx = Q[ic][0], qy = Q[ic][1];
-                    const double mx = cmul(cadd(ax, bx), 0.5), my = cmul(cadd(ay, by), 0.5);
-                    if ((path >> lev) & 1) {
-                        Q[0][0] = mx; Q[0][1] = my; Q[1][0] = bx; Q[1][1] = by;
-                    } else {
-                        Q[0][0] = ax; Q[0][1] = ay; Q[1][0] = mx; Q[1][1] = my;
-                    }
-                    Q[2][0] = qx; Q[2][1] = qy;
-                }
-                const double cr = csub(cmul(csub(Q[1][0], Q[0][0]), csub(Q[2][1], Q[0][1])),
-                                       cmul(csub(Q[1][1], Q[0][1]), csub(Q[2][0], Q[0][0])));
-                const double At = cmul(0.5, cr);
-                const double qx = div3(cadd(cadd(Q[0][0], Q[1][0]), Q[2][0]));
-                const double qy = div3(cadd(cadd(Q[0][1], Q[1][1]), Q[2][1]));
-                const double rho = bilinear(A.grid, A.rho, cadd(px, qx), cadd(py, qy), LdgLoad());
-                const double wgt = At * rho;
+            for (int u = 0; u < TM_QB; u++) {
+                const int64_t t = t0 + u < ntot ? t0 + u : ntot - 1;  // tail: recompute the last one
+                const int f = (int)(t >> depth);
+                quad_sub(rv[(int64_t)f * ns], rv[(int64_t)(f + 1 == nv ? 0 : f + 1) * ns], depth, t & (((int64_t)1 << depth) - 1), At[u], qx[u],
+                         qy[u]);
+                int gi, gj;
+                grid_cell(g, cadd(px, qx[u]), cadd(py, qy[u]), gi, gj, ss[u], tt[u]);
+                const double *r0 = A.rho + (int64_t)gj * g.nx + gi, *r1 = r0 + g.nx;
+                f00[u] = __ldg(r0);
+                f10[u] = __ldg(r0 + 1);
+                f01[u] = __ldg(r1);
+                f11[u] = __ldg(r1 + 1);
+            }
+#pragma unroll
+            for (int u = 0; u < TM_QB; u++) {
+                if (t0 + u >= ntot) break;
+                const double rho = clerp(clerp(f00[u], f10[u], ss[u]), clerp(f01[u], f11[u], ss[u]), tt[u]);
+                const double wgt = At[u] * rho;
                 sw += wgt;
-                swx += wgt * qx;
-                swy += wgt * qy;
+                swx += wgt * qx[u];
+                swy += wgt * qy[u];
                 nq++;
             }
         }
@@ -1345,8 +1372,12 @@ __global__ void __launch_bounds__(128) k_output_t(CellArgs A, RingBuf R) {
     const int lane = threadIdx.x & 31;
     const int nv = cell < A.n_local ? (int)R.n[cell] : 0;
     const bool live = nv > 0;
-    const double2 *rv = R.v + (int64_t)cell * VMAX;
-    const int *rl = R.la + (int64_t)cell * VMAX;
+    // rings are slot-major ([i][cell]): the loads of a warp for the same i coalesce
+    const double2 *rv0 = R.v + cell;
+    const int *rl0 = R.la + cell;
+    const int64_t ns = A.n_local;
+    auto RV = [&](int i) { return rv0[(int64_t)i * ns]; };
+    auto RL = [&](int i) { return rl0[(int64_t)i * ns]; };
     int32_t orig = 0, gi = 0;
     double px = 0.0, py = 0.0, h = 0.0;
     if (live) {
@@ -1359,7 +1390,7 @@ __global__ void __launch_bounds__(128) k_output_t(CellArgs A, RingBuf R) {
     if (live && A.nbr) {
         int c = 0;
         for (int i = 0; i < nv; i++) {
-            const int a = rl[i];
+            const int a = RL(i);
             if (a >= 0) A.nbr[(int64_t)orig * TM_NBR + c++] = __ldg(A.perm + a);
         }
         A.nbr_cnt[orig] = (uint8_t)c;
@@ -1369,12 +1400,12 @@ __global__ void __launch_bounds__(128) k_output_t(CellArgs A, RingBuf R) {
     if (live && (MODE & (M_TRI | M_ELL))) {
         unsigned keptall = 0;
         for (int i = 0; i < nv; i++) {
-            const int a = rl[i], b = rl[i + 1 == nv ? 0 : i + 1];
+            const int a = RL(i), b = RL(i + 1 == nv ? 0 : i + 1);
             if (a >= 0 && b >= 0) {
                 const int32_t ga = __ldg(A.gids + a), gb = __ldg(A.gids + b);
                 if (gi < ga && gi < gb) {
                     const int sv = ga < gb ? a : b, sw = ga < gb ? b : a;
-                    const double2 v = rv[i];
+                    const double2 v = RV(i);
                     if (keep_tri(A, (int)cell, sv, sw, cadd(px, v.x), cadd(py, v.y))) {
                         keptmask |= 1u << i;
                         keptall |= 1u << i;
@@ -1401,7 +1432,7 @@ __global__ void __launch_bounds__(128) k_output_t(CellArgs A, RingBuf R) {
         t_own = __popc(keptmask);
         if (MODE & M_ELL) {
             for (int i = 0; i < nv; i++) {
-                const int a = rl[i];
+                const int a = RL(i);
                 const int ip = i == 0 ? nv - 1 : i - 1;
                 if (a >= 0 && (((keptall >> i) & 1u) || ((keptall >> ip) & 1u))) {
                     if (ell < A.adj_stride) A.adj[(int64_t)ell * A.n_local + cell] = a;
@@ -1425,7 +1456,7 @@ __global__ void __launch_bounds__(128) k_output_t(CellArgs A, RingBuf R) {
         base = __shfl_sync(0xffffffffu, base, 31) + (unsigned long long)(incl - t_own);
         for (unsigned m = keptmask; m; m &= m - 1) {
             const int i = __ffs(m) - 1;
-            const int a = rl[i], b = rl[i + 1 == nv ? 0 : i + 1];
+            const int a = RL(i), b = RL(i + 1 == nv ? 0 : i + 1);
             if ((int64_t)base < A.tri_cap) {
                 A.tri[3 * base] = gi;
                 A.tri[3 * base + 1] = __ldg(A.gids + a);
@@ -1440,7 +1471,7 @@ __global__ void __launch_bounds__(128) k_output_t(CellArgs A, RingBuf R) {
     if (live && (MODE & (M_TREAT | M_HAT))) {
         double S2 = 0.0, sx = 0.0, sy = 0.0;
         for (int i = 0; i < nv; i++) {
-            const double2 a = rv[i], b = rv[i + 1 == nv ? 0 : i + 1];
+            const double2 a = RV(i), b = RV(i + 1 == nv ? 0 : i + 1);
             const double cr = a.x * b.y - b.x * a.y;
             S2 += cr;
             sx += cr * (a.x + b.x);
@@ -1453,7 +1484,7 @@ __global__ void __launch_bounds__(128) k_output_t(CellArgs A, RingBuf R) {
             nq += nv;
         } else {
             const double dp = A.d_prev ? __ldg(A.d_prev + orig) : -1.0;
-            quad_centroid_g(rv, nv, px, py, 0.5 * S2, h, dp, A, cx, cy, nq);
+            quad_centroid_g(rv0, ns, nv, px, py, 0.5 * S2, h, dp, A, cx, cy, nq);
         }
         if (MODE & M_HAT) {
             A.x_hat[orig] = px + cx;
@@ -1472,7 +1503,7 @@ __global__ void __launch_bounds__(128) k_output_t(CellArgs A, RingBuf R) {
     }
     if ((MODE & M_COUNT) && live) {
         float R2f = 0.f;
-        for (int i = 0; i < nv; i++) R2f = fmaxf(R2f, vertex_r2f_t(rv[i].x, rv[i].y, -1.0));
+        for (int i = 0; i < nv; i++) R2f = fmaxf(R2f, vertex_r2f_t(RV(i).x, RV(i).y, -1.0));
         const double rad = 2.0 * sqrt((double)R2f);
         const BinGeom &bg = A.bg;
         int ncert = 0;
@@ -1489,7 +1520,7 @@ __global__ void __launch_bounds__(128) k_output_t(CellArgs A, RingBuf R) {
             }
         }
         int degc = 0;
-        for (int i = 0; i < nv; i++) degc += rl[i + 1 == nv ? 0 : i + 1] >= 0 ? 1 : 0;
+        for (int i = 0; i < nv; i++) degc += RL(i + 1 == nv ? 0 : i + 1) >= 0 ? 1 : 0;
         atomicAdd(&A.st->work[0], 1ull);
         atomicAdd(&A.st->work[1], (unsigned long long)ncert);
         atomicAdd(&A.st->work[2], (unsigned long long)degc);
