@@ -37,35 +37,40 @@ def test_cfg1_all_lloyd_iterations(cfg_cache):
         x, y, dp = g["x"], g["y"], g["d_prev"]
 
 
-def test_cfg2_distmesh(cfg_cache):
-    """configs[1]: DistMesh on the disk, iterations 0, 1 and 5 of the GPU run."""
-    c = cfg_cache(2)
-    r = GpuRunner(c.box, c.phi)
+def _protocol(c, check):
+    """SURVEY §8(c) parity protocol: run the GPU through the config's whole schedule from
+    its own state; at the iterations in `check` the oracle performs the same iteration
+    from the identical input bits and the outputs are compared (triangles exact, ELL
+    edges exact, positions within 1e-12 diam, status codes)."""
+    r = GpuRunner(c.box, c.phi, c.mu, c.rho)
+    fs = O.FieldSet.from_config(c)
     x, y, dp = c.x, c.y, None
-    for it in range(6):
-        g = r.iteration(x, y, "dm", dp)
-        if it in (0, 1, 5):
-            o = O.iteration(O.FieldSet.from_config(c), x, y, "dm", d_prev=dp)
-            compare(g, o, c.box, "dm", ctx=f"cfg2 it{it}")
+    for it, mode in enumerate(c.schedule):
+        g = r.iteration(x, y, mode, dp)
+        if it in check:
+            o = O.iteration(fs, x, y, mode, d_prev=dp)
+            assert o.info.n_degenerate == 0
+            compare(g, o, c.box, mode, ctx=f"{c.name} it{it} {mode}")
         x, y, dp = g["x"], g["y"], g["d_prev"]
+
+
+def test_cfg2_distmesh(cfg_cache):
+    """configs[1]: 50 DistMesh iterations on the disk; parity at {0, 1, 25, 49}."""
+    c = cfg_cache(2)
+    n = len(c.schedule)
+    _protocol(c, {0, 1, n // 2, n - 1})
 
 
 @pytest.mark.parametrize("k", [3, 4])
-def test_adaptive_full_size_first_dm_and_cvd(k, cfg_cache):
-    """configs[2]/[3] at full size (10^6): DistMesh iteration 0, then a CVD
-    iteration (adaptive quadrature) from the GPU state after 3 DistMesh steps."""
+def test_adaptive_full_size_protocol(k, cfg_cache):
+    """configs[2]/[3] at full size (10^6, adaptive): the whole hybrid schedule (30+30 /
+    20+20 iterations, warm-started from the second iteration on); parity at the first two
+    iterations, the last DistMesh and first CVD iteration (adaptive quadrature), and the
+    last iteration."""
     c = cfg_cache(k)
-    r = GpuRunner(c.box, c.phi, c.mu, c.rho)
-    x, y, dp = c.x, c.y, None
-    for it in range(3):
-        g = r.iteration(x, y, "dm", dp)
-        if it == 0:
-            o = O.iteration(O.FieldSet.from_config(c), x, y, "dm", d_prev=dp)
-            compare(g, o, c.box, "dm", ctx=f"cfg{k} dm it0")
-        x, y, dp = g["x"], g["y"], g["d_prev"]
-    g = r.iteration(x, y, "cvd", dp)
-    o = O.iteration(O.FieldSet.from_config(c), x, y, "cvd", d_prev=dp)
-    compare(g, o, c.box, "cvd", ctx=f"cfg{k} cvd")
+    n = len(c.schedule)
+    ndm = sum(1 for m in c.schedule if m == "dm")
+    _protocol(c, {0, 1, ndm - 1, ndm, n - 1})
 
 
 @pytest.mark.parametrize("n,seed", [(3, 1), (4, 2), (7, 3), (40, 4), (333, 5), (5000, 6)])
