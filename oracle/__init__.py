@@ -58,7 +58,7 @@ class Info(ctypes.Structure):
                 ("sum_l2", ctypes.c_double), ("sum_mu2", ctypes.c_double),
                 ("n_delaunay", ctypes.c_int64), ("n_kept", ctypes.c_int64),
                 ("n_edges", ctypes.c_int64), ("n_degenerate", ctypes.c_int64),
-                ("n_hull", ctypes.c_int64)]
+                ("n_hull", ctypes.c_int64), ("n_near_ties", ctypes.c_int64)]
 
 
 def default_params(**kw) -> Params:

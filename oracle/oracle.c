@@ -28,6 +28,14 @@
 #define ORACLE_DIE(...) do { fprintf(stderr, "oracle: " __VA_ARGS__); fputc('\n', stderr); abort(); } while (0)
 
 static int64_t g_degenerate = 0; /* exact zeros met by predicates / invariant faults */
+/* decision-margin report (SURVEY §8(c) parity protocol): floating decisions -- keep-rule
+ * box/octagon/phi tests, quadrature stop, treatment accept and Newton stop -- whose two
+ * sides differ by at most 1e-13 of the decision's own scale.  Reporting only: no result
+ * depends on it. */
+static int64_t g_near = 0;
+static void near_tie(double a, double b, double scale) {
+    if (fabs(a - b) <= 1e-13 * fabs(scale)) g_near++;
+}
 
 /* ========================================================================== */
 /* Big integers: sign-magnitude, 32-bit limbs, little endian.                  */
@@ -896,12 +904,21 @@ static int keep_triangle(const or_fields *f, const or_params *p, double c, const
     double ox, oy;
     cramer(A, B, &ox, &oy);
     double cx = x[u] + ox, cy = y[u] + oy;
+    const double Lb = (f->x1 - f->x0) + (f->y1 - f->y0);
+    near_tie(cx, f->x0, Lb); near_tie(cx, f->x1, Lb); near_tie(cy, f->y0, Lb); near_tie(cy, f->y1, Lb);
     if (!(cx > f->x0 && cx < f->x1 && cy > f->y0 && cy < f->y1)) return 0;
     int32_t q[3] = {u, v, w};
-    for (int k = 0; k < 3; k++)
-        if (!in_octagon(cx, cy, x[q[k]], y[q[k]], r_oct_of(f, p, c, x[q[k]], y[q[k]]))) return 0;
+    for (int k = 0; k < 3; k++) {
+        const double r = r_oct_of(f, p, c, x[q[k]], y[q[k]]);
+        const double dx = cx - x[q[k]], dy = cy - y[q[k]];
+        near_tie(fabs(dx), r, r); near_tie(fabs(dy), r, r);
+        near_tie(fabs(dx + dy), OR_SQRT2 * r, r); near_tie(fabs(dx - dy), OR_SQRT2 * r, r);
+        if (!in_octagon(cx, cy, x[q[k]], y[q[k]], r)) return 0;
+    }
     double gx = ((x[u] + x[v]) + x[w]) / 3.0, gy = ((y[u] + y[v]) + y[w]) / 3.0;
-    return or_field_value(f, f->phi, gx, gy) < p->keep_tol;
+    const double ph = or_field_value(f, f->phi, gx, gy);
+    near_tie(ph, p->keep_tol, sqrt(ox * ox + oy * oy));
+    return ph < p->keep_tol;
 }
 
 /* ========================================================================== */
@@ -980,6 +997,7 @@ static void cvd_rel(const or_fields *f, const or_params *p, int nv, const double
         double dx = prevx - curx, dy = prevy - cury;
         double dist = sqrt(dx * dx + dy * dy);
         prevx = curx; prevy = cury;
+        near_tie(dist, E, E);
         if (dist < E) break;        /* |c^_{L-1} - c^_L| < E  -> return c^_L */
     }
     if (L > p->quad_max_level) L = p->quad_max_level;
@@ -1057,6 +1075,7 @@ int or_treat(const or_fields *f, const or_params *p, double c, double h_avg,
     double qx = clampd(xo + dx, f->x0, f->x1), qy = clampd(yo + dy, f->y0, f->y1);
     double geps = p->fac_geps * (h < h_avg ? h : h_avg);
     double ph = or_field_value(f, f->phi, qx, qy);
+    near_tie(ph, geps, geps);
     if (!(ph <= geps)) {
         int ok = 0;
         for (int it = 0; it < p->newton_max; it++) {
@@ -1068,6 +1087,7 @@ int or_treat(const or_fields *f, const or_params *p, double c, double h_avg,
             qx = clampd(qx - st * gx, f->x0, f->x1);
             qy = clampd(qy - st * gy, f->y0, f->y1);
             ph = or_field_value(f, f->phi, qx, qy);
+            near_tie(fabs(ph), geps, geps);
             if (fabs(ph) <= geps) { ok = 1; break; }
         }
         if (ok) status |= 1;
@@ -1175,7 +1195,7 @@ int or_iteration(const or_fields *f, const or_params *p, int64_t n, int64_t n_to
                  const double *y, const double *d_prev, int mode, int32_t *tri_out, int64_t tri_cap, int32_t *edges_out,
                  int64_t edge_cap, double *x_hat, double *y_hat, double *x_out, double *y_out,
                  double *d_prev_out, int8_t *status, int64_t *counts, or_info *info) {
-    int64_t deg0 = g_degenerate;
+    int64_t deg0 = g_degenerate, near0 = g_near;
     or_info inf;
     memset(&inf, 0, sizeof(inf));
     or_domain(f, n_total > 0 ? n_total : n, &inf.c, &inf.h_avg);
@@ -1273,6 +1293,7 @@ int or_iteration(const or_fields *f, const or_params *p, int64_t n, int64_t n_to
         status[i] = (int8_t)or_treat(f, p, c, inf.h_avg, x[i], y[i], x_hat[i], y_hat[i], &x_out[i], &y_out[i],
                                      &d_prev_out[i]);
     inf.n_degenerate = g_degenerate - deg0;
+    inf.n_near_ties = g_near - near0;
     if (info) *info = inf;
     free(D); free(own); free(E); free(erow); free(g.start); free(g.nb);
     if (counts) { free(cg.start); free(cg.idx); }

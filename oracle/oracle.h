@@ -50,6 +50,7 @@ typedef struct {
     int64_t n_edges;       /* unique kept edges                        */
     int64_t n_degenerate;  /* exact predicate zeros / invariant faults */
     int64_t n_hull;        /* convex hull vertices of the input        */
+    int64_t n_near_ties;   /* floating decisions within 1e-13 of their threshold (report) */
 } or_info;
 
 /* ---- exact predicates (sign only: -1, 0, +1) ---------------------------- */

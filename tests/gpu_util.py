@@ -78,8 +78,9 @@ def compare(gpu, orc, box, mode, pos_tol=1e-12, ctx=""):
     ot = tri_set(orc.tri)
     assert len(gt) == len(gpu["tri"]), f"{ctx}: duplicate GPU triangles"
     missing, extra = ot - gt, gt - ot
+    nt = getattr(orc.info, "n_near_ties", 0)
     assert not missing and not extra, f"{ctx}: triangle sets differ: {len(missing)} missing, {len(extra)} extra " \
-                                      f"(e.g. {list(missing)[:3]} / {list(extra)[:3]})"
+                                      f"(e.g. {list(missing)[:3]} / {list(extra)[:3]}); oracle near ties: {nt}"
     diam = float(np.hypot(box[2] - box[0], box[3] - box[1]))
     err = np.hypot(gpu["x"] - orc.x, gpu["y"] - orc.y)
     k = int(np.argmax(err))

@@ -233,3 +233,21 @@ def test_quality_worked_examples():
     # 1/2-mean (Eq. 1/2 mean): ((1 + sqrt(1.25))/2)^2, and M_1/2 <= arithmetic mean
     assert abs(s[11] - ((1 + math.sqrt(1.25)) / 2) ** 2) < 1e-14
     assert s[11] <= s[5] / s[0]
+
+
+def test_decision_margins_generic_inputs():
+    """SURVEY §8(c) parity protocol: the oracle reports the floating decisions that fall
+    within 1e-13 of their threshold (keep-rule box/octagon/phi tests, quadrature stop,
+    treatment accept, Newton stop).  For the generic seeded inputs the report is empty
+    (a non-empty one would explain, not excuse, a GPU/oracle mismatch)."""
+    import oracle as O
+    from inputs import configs
+    c = configs.load(1)
+    fs = O.FieldSet.from_config(c)
+    x, y, dp = c.x, c.y, None
+    for it in range(3):
+        o = O.iteration(fs, x, y, "cvd", d_prev=dp)
+        assert o.info.n_near_ties == 0 and o.info.n_degenerate == 0
+        x, y, dp = o.x, o.y, o.d_prev
+    o = O.iteration(fs, x, y, "dm", d_prev=dp)
+    assert o.info.n_near_ties == 0
