@@ -262,6 +262,10 @@ extern "C" tm_status tm_set_domain(tm_ctx *ctx, const tm_fields *f, int64_t n_to
     return TM_OK;
 }
 
+#ifndef TM_BIN_GATHER
+#define TM_BIN_GATHER 1  // sort caller indices per leaf, then gather the point data in slot order
+#endif
+
 // ============================================================================ S1
 __global__ void k_bin_keys(const double *__restrict__ x, const double *__restrict__ y, int64_t n, BinGeom bg,
                            double bx0, double by0, double bx1, double by1, int32_t *__restrict__ key,
@@ -437,6 +441,51 @@ __global__ void k_leaf_sort(const int32_t *__restrict__ leaf_start, int64_t nlea
     for (int a = s; a < e; a++) inv_perm[perm[a]] = a;  // caller index -> slot
 }
 
+// S1 tail: the slot of every point is its leaf's start plus its rank in the leaf; the
+// ranks come from atomics (arbitrary order), so each leaf's caller indices are then
+// sorted (4-byte keys only) and the point data gathered once into slot order with
+// coalesced stores: the in-leaf order is the caller order, deterministic.
+__global__ void k_perm_scatter(int64_t n, const int32_t *__restrict__ key, const int32_t *__restrict__ rank,
+                               const int32_t *__restrict__ start, int32_t *__restrict__ perm) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    perm[(int64_t)start[key[i]] + rank[i]] = (int32_t)i;
+}
+
+__global__ void k_leaf_sort_perm(const int32_t *__restrict__ leaf_start, int64_t nleaves, int32_t *__restrict__ perm,
+                                 int32_t *__restrict__ inv_perm) {
+    const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= nleaves) return;
+    const int s = leaf_start[l], e = leaf_start[l + 1];
+    for (int a = s + 1; a < e; a++) {
+        const int32_t pk = perm[a];
+        int b = a - 1;
+        while (b >= s && perm[b] > pk) {
+            perm[b + 1] = perm[b];
+            b--;
+        }
+        perm[b + 1] = pk;
+    }
+    for (int a = s; a < e; a++) inv_perm[perm[a]] = a;  // caller index -> slot
+}
+
+__global__ void k_gather_sorted(const double *__restrict__ x, const double *__restrict__ y,
+                                const int32_t *__restrict__ gid, int64_t n, const int32_t *__restrict__ perm,
+                                double bx0, double by0, double bx1, double by1, Grid g, const double *__restrict__ mu,
+                                double c, double *__restrict__ xs, double *__restrict__ ys, double *__restrict__ hs,
+                                int32_t *__restrict__ gids) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    const int32_t i = perm[s];
+    double px = x[i], py = y[i];
+    px = fmin(fmax(px == px ? px : bx0, bx0), bx1);
+    py = fmin(fmax(py == py ? py : by0, by0), by1);
+    xs[s] = px;
+    ys[s] = py;
+    hs[s] = mu ? cmul(c, bilinear(g, mu, px, py, LdgLoad())) : c;  // h(p) = c mu~(p) (§8.0 "Local size")
+    gids[s] = gid ? gid[i] : i;
+}
+
 static tm_status ensure_points(tm_ctx *ctx, int64_t n) {
     if (n <= ctx->cap_points) return TM_OK;
     free_points(ctx);
@@ -528,6 +577,14 @@ extern "C" tm_status tm_grid_bin(tm_ctx *ctx, const double *x, const double *y, 
                                                  ctx->leaf_off, ctx->leaf_count, ctx->rank);
     if ((s = tm_internal_check_launch(ctx, "k_leaf_keys")) != TM_OK) return s;
     if ((s = scan_counts(ctx, ctx->leaf_count, ctx->leaf_start, nleaves_max)) != TM_OK) return s;
+#if TM_BIN_GATHER
+    k_perm_scatter<<<blocks, 256, 0, ctx->stream>>>(n_local, ctx->key, ctx->rank, ctx->leaf_start, ctx->perm);
+    k_leaf_sort_perm<<<(unsigned)((nleaves_max + 255) / 256), 256, 0, ctx->stream>>>(ctx->leaf_start, nleaves_max,
+                                                                                   ctx->perm, ctx->inv_perm);
+    k_gather_sorted<<<blocks, 256, 0, ctx->stream>>>(x, y, gid, n_local, ctx->perm, g.x0, g.y0, g.x1, g.y1, g, ctx->mu,
+                                                     ctx->c, ctx->xs, ctx->ys, ctx->hs, ctx->gids);
+    if ((s = tm_internal_check_launch(ctx, "k_gather_sorted")) != TM_OK) return s;
+#else
     k_bin_scatter<<<blocks, 256, 0, ctx->stream>>>(x, y, gid, n_local, ctx->key, ctx->rank, ctx->leaf_start, g.x0,
                                                    g.y0, g.x1, g.y1, g, ctx->mu, ctx->c, ctx->xs, ctx->ys,
                                                    ctx->hs, ctx->perm, ctx->gids);
@@ -535,6 +592,7 @@ extern "C" tm_status tm_grid_bin(tm_ctx *ctx, const double *x, const double *y, 
     k_leaf_sort<<<(unsigned)((nleaves_max + 255) / 256), 256, 0, ctx->stream>>>(
         ctx->leaf_start, nleaves_max, ctx->xs, ctx->ys, ctx->hs, ctx->perm, ctx->gids, ctx->inv_perm);
     if ((s = tm_internal_check_launch(ctx, "k_leaf_sort")) != TM_OK) return s;
+#endif
     if (n_local != ctx->nbr_n || (gid != nullptr) != ctx->have_gid) ctx->nbr_n = -1;  // warm start invalid
     if (!gid && n_local > ctx->cap_nbr) {
         cudaFree(ctx->nbr);
