@@ -338,10 +338,11 @@ def main():
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline_sample()
-        # k_bin_keys, k_bin_levels, 2 x (k_scan_tiles, k_scan_top, k_scan_add), k_leaf_keys, k_bin_scatter,
-        # k_leaf_sort = 11; cells: k_cells_t + retry pass = 2; DistMesh: k_dm_sums, k_dm_final, k_dm_step = 3
-        launches_per_step = sum(16 if m == "dm" else 13 for m in schedule) + (
-            sum(3 for _ in schedule) if strip_mode else 0)  # + k_halo_pack, k_migrate_pack, k_migrate_unpack
+        # binning: k_bin_keys, k_bin_levels, 2 x (k_scan_tiles, k_scan_top, k_scan_add), k_leaf_keys,
+        # k_perm_scatter, k_leaf_sort_perm, k_gather_sorted = 12; cells: k_cells_t + the retry pass = 2,
+        # + k_output_t in CVD mode; DistMesh: k_dm_sums, k_dm_final, k_dm_step = 3
+        launches_per_step = sum(17 if m == "dm" else 15 for m in schedule) + (
+            7 * len(schedule) if strip_mode else 0)  # k_halo_pack; k_migrate_count, 3 scan kernels, scatter, unpack
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,

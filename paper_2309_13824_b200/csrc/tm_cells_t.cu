@@ -49,6 +49,9 @@ using namespace tmg;
 #ifndef TM_COLD_NOINLINE
 #define TM_COLD_NOINLINE 0  // 1: once-per-cell code out of line (ABI calls; see DESIGN)
 #endif
+#ifndef TM_OUT_MINB
+#define TM_OUT_MINB 1  // min resident 128-thread blocks per SM for k_output_t (register cap)
+#endif
 #ifndef TM_CVD_SPLIT
 #define TM_CVD_SPLIT 1  // 1: CVD centroid, quadrature, treatment in a second kernel over stored rings;
                         // 2: triangles and ELL rows there too (all modes)
@@ -1367,7 +1370,7 @@ __device__ void quad_centroid_g(const double2 *rv, int64_t ns, int nv, double px
 // outputs of every stored ring: S3 triangles + keep rule and ELL rows, S4a centroid,
 // S5 treatment, warm-start neighbour lists, O8 counters -- one thread per cell
 template <int MODE>
-__global__ void __launch_bounds__(128) k_output_t(CellArgs A, RingBuf R) {
+__global__ void __launch_bounds__(128, TM_OUT_MINB) k_output_t(CellArgs A, RingBuf R) {
     const int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const int nv = cell < A.n_local ? (int)R.n[cell] : 0;
