@@ -9,7 +9,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def dram(rep):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    h, u, d = rows[0], rows[1], rows[2]
+    h, u = rows[0], rows[1]
+    kn = h.index("Kernel Name")
+    d = next(r for r in rows[2:] if "k_cells_t" in r[kn])  # the cell kernel's launch
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     tot = 0.0
     for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
