@@ -76,7 +76,7 @@ extern "C" void tm_destroy(tm_ctx *ctx) {
     cudaFree(ctx->partials); cudaFree(ctx->stat_acc); cudaFree(ctx->dst);
     cudaFree(ctx->retry_list); cudaFree(ctx->retry_cnt);
     cudaFree(ctx->mig_keep); cudaFree(ctx->mig_cnt); cudaFree(ctx->mig_off);
-    cudaFree(ctx->nbr); cudaFree(ctx->nbr_cnt); cudaFree(ctx->nbr_work);
+    cudaFree(ctx->nbr); cudaFree(ctx->nbr_cnt);
     cudaFree(ctx->ring_v); cudaFree(ctx->ring_la); cudaFree(ctx->ring_n);
     delete ctx;
 }
@@ -597,14 +597,11 @@ extern "C" tm_status tm_grid_bin(tm_ctx *ctx, const double *x, const double *y, 
     if (!gid && n_local > ctx->cap_nbr) {
         cudaFree(ctx->nbr);
         cudaFree(ctx->nbr_cnt);
-        cudaFree(ctx->nbr_work);
         ctx->nbr = nullptr;
         ctx->nbr_cnt = nullptr;
-        ctx->nbr_work = nullptr;
         const int64_t c = n_local + n_local / 8 + 1024;
         TM_CUDA_TRY(ctx, cudaMalloc(&ctx->nbr, c * TM_NBR * sizeof(int32_t)));
         TM_CUDA_TRY(ctx, cudaMalloc(&ctx->nbr_cnt, c * sizeof(uint8_t)));
-        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->nbr_work, c * sizeof(uint8_t)));
         ctx->cap_nbr = c;
         ctx->nbr_n = -1;
     }
@@ -622,7 +619,6 @@ tm_status tm_internal_fill_cell_args(tm_ctx *ctx, CellArgs *a) {
     a->perm = ctx->perm; a->gids = ctx->gids; a->inv_perm = ctx->inv_perm;
     a->nbr = ctx->have_gid ? nullptr : ctx->nbr;  // single domain only (caller ids are stable)
     a->nbr_cnt = ctx->have_gid ? nullptr : ctx->nbr_cnt;
-    a->nbr_work = ctx->have_gid ? nullptr : ctx->nbr_work;
     a->warm = (a->nbr && ctx->nbr_n == ctx->n_local) ? 1 : 0;
     a->rlev = ctx->rlev; a->leaf_off = ctx->leaf_off; a->leaf_start = ctx->leaf_start;
     a->bg = ctx->bg;

@@ -37,36 +37,12 @@ using namespace tmg;
 #ifndef TM_TMINB
 #define TM_TMINB 5
 #endif
-#ifndef TM_PREFETCH
-#define TM_PREFETCH 1  // fetch the next candidate before clipping with the current one
-#endif
-#ifndef TM_WALL_FAST
-#define TM_WALL_FAST 0  // 1: separate point-point-only test loop for rings without walls (measured slower)
-#endif
-#ifndef TM_LCAP
-#define TM_LCAP 0  // >0: collect-then-clip queue per warm-started cell (measured slower, see DESIGN)
-#endif
-#ifndef TM_COLD_NOINLINE
-#define TM_COLD_NOINLINE 0  // 1: once-per-cell code out of line (ABI calls; see DESIGN)
-#endif
 #ifndef TM_OUT_MINB
 #define TM_OUT_MINB 1  // min resident 128-thread blocks per SM for k_output_t (register cap)
 #endif
 #ifndef TM_CVD_SPLIT
 #define TM_CVD_SPLIT 1  // 1: CVD centroid, quadrature, treatment in a second kernel over stored rings;
                         // 2: triangles and ELL rows there too (all modes)
-#endif
-#ifndef TM_SPLIT
-#define TM_SPLIT 0  // search kernel with lane recycling + output kernel (0: one fused kernel)
-#endif
-#ifndef TM_CHUNK
-#define TM_CHUNK 64  // cells a warp takes from the global queue at a time
-#endif
-#ifndef TM_REFILL
-#define TM_REFILL 8  // idle lanes that trigger a refill
-#endif
-#ifndef TM_BALANCE
-#define TM_BALANCE 0  // 1: deal a block's cells to lanes by their last work (measured slower: locality)
 #endif
 #ifndef TM_K_DOUBLE
 #define TM_K_DOUBLE 0  // filter constants as float (rounded up): less shared memory, more L1
@@ -89,7 +65,6 @@ typedef double KT;  // filter constant storage
 #else
 typedef float KT;   // rounded up: still a valid bound
 #endif
-constexpr int LCAP = TM_LCAP;  // near-candidate queue per thread (warm-started cells), 0 = off
 constexpr size_t TSMEM = (size_t)VMAX * TB * (16 + sizeof(KT) + (TM_R2_CACHE ? 4 : 0) + 4 + 1 + 1);
 
 // this thread's view of the block's slot arrays (element k at [k * TB])
@@ -177,27 +152,15 @@ __device__ __forceinline__ int clip_t(TPoly &P, int code, const Line &L, const C
         for (int k = 0; k < VMAX; k++) dup |= (unsigned)(P.la[k * TB] == code) << k;
         if (dup & P.used) return 0;
     }
-    if (TM_WALL_FAST && is_bis && !(P.used & P.wall)) {
-        // interior ring: point-point vertices only
 #pragma unroll
-        for (int k = 0; k < VMAX; k++) {
-            const double2 vv = P.v[k * TB];
-            const double del = fma(L.nx, vv.x, L.ny * vv.y) - L.r;
-            const double B = fma(n1, (double)P.K[k * TB], c8);
-            out |= (unsigned)(del > B) << k;
-            unc |= (unsigned)(del <= B && del >= -B) << k;
-        }
-    } else {
-#pragma unroll
-        for (int k = 0; k < VMAX; k++) {
-            const double2 vv = P.v[k * TB];
-            const double del = fma(L.nx, vv.x, L.ny * vv.y) - L.r;
-            const double B = fma(n1, (double)P.K[k * TB], c8);
-            const bool pp = is_bis && !((P.wall >> k) & 1u);
-            const bool o = pp ? del > B : wall_out(L, vv.x, vv.y);
-            out |= (unsigned)o << k;
-            unc |= (unsigned)(pp && del <= B && del >= -B) << k;
-        }
+    for (int k = 0; k < VMAX; k++) {
+        const double2 vv = P.v[k * TB];
+        const double del = fma(L.nx, vv.x, L.ny * vv.y) - L.r;
+        const double B = fma(n1, (double)P.K[k * TB], c8);
+        const bool pp = is_bis && !((P.wall >> k) & 1u);
+        const bool o = pp ? del > B : wall_out(L, vv.x, vv.y);
+        out |= (unsigned)o << k;
+        unc |= (unsigned)(pp && del <= B && del >= -B) << k;
     }
     out &= P.used;
     unc &= P.used;
@@ -301,26 +264,6 @@ __device__ __forceinline__ void vleaf_range(const CellArgs &A, int vx, int vy, i
     }
 }
 
-// Code that runs once per cell (or rarely) is kept out of line (TM_COLD_NOINLINE):
-// the kernel is ~5-6k SASS instructions, and instruction-cache misses showed up as
-// "no instruction" stalls in the CVD variant.
-#if TM_COLD_NOINLINE
-#define TM_COLD __device__ __noinline__
-#else
-#define TM_COLD __device__ __forceinline__
-#endif
-TM_COLD int clip_t_cold(TPoly &P, int code, const Line &L, const CellGeom &cgm, const CellArgs &A, ClipStats &cs) {
-    return clip_t(P, code, L, cgm, A, cs);
-}
-TM_COLD bool keep_tri_cold(const CellArgs &A, int su, int sv, int sw, double cx, double cy) {
-    return keep_tri(A, su, sv, sw, cx, cy);
-}
-TM_COLD int treat_point_cold(const CellArgs &A, double h, double px, double py, double hx, double hy, double &qx,
-                             double &qy, double &dpo) {
-    return treat_point(A.grid, A.phi, h, A.h_avg, A.fac_pt, A.fac_geps, A.damping, A.newton_max, px, py, hx, hy, qx,
-                       qy, dpo, LdgLoad());
-}
-
 struct SearchCtx {
     double px, py;
     int cell;
@@ -344,7 +287,7 @@ __device__ __forceinline__ void cswap(unsigned &a, unsigned &b) {
 
 // adaptive quadrature centroid (Fig. 14; reading L13), one thread,
 // relative to p_i; same sub-triangle construction as quad_centroid
-TM_COLD void quad_centroid_t(const TPoly &P, int start, int nv, double px, double py, double area, double h,
+__device__ void quad_centroid_t(const TPoly &P, int start, int nv, double px, double py, double area, double h,
                                 double dprev, const CellArgs &A, double &cx, double &cy, unsigned long long &nq) {
     double eps = dprev >= 0.0 ? dprev / h : A.fac_pt;
     if (eps < A.fac_end) eps = A.fac_end;
@@ -407,12 +350,11 @@ TM_COLD void quad_centroid_t(const TPoly &P, int start, int nv, double px, doubl
     cy = prevy;
 }
 
-// stored rings (split paths below)
+// stored rings: k_cells_t writes them in CVD mode, k_output_t reads them
 struct RingBuf {
-    double2 *v;                // [cell * VMAX + i], ring order from the canonical vertex
+    double2 *v;                // [i * n_local + cell] (slot-major), ring order from the canonical vertex
     int *la;                   // incoming line code of ring vertex i
     uint8_t *n;                // vertices, 0 = no ring (ghost, failed, or retried)
-    unsigned long long *chunk; // next unassigned cell (warp work queue)
 };
 
 template <int MODE>
@@ -425,38 +367,8 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
     constexpr bool TSPLIT = CSPLIT && TM_CVD_SPLIT >= 2;  // triangles / ELL rows in k_output_t too
     extern __shared__ __align__(16) unsigned char tsmem[];
     const int tid = threadIdx.x;
-    int64_t cell = (int64_t)blockIdx.x * TB + tid;
+    const int64_t cell = (int64_t)blockIdx.x * TB + tid;
     const int lane = tid & 31;
-#if TM_BALANCE
-    // load balancing: a warp runs as many trips as its busiest lane, so the block's cells
-    // are dealt to its lanes in order of the work each took in the last launch (warm
-    // start only): every warp gets cells of similar cost.  Bitonic sort of the TB keys
-    // (work << 8 | lane slot) in the not yet used shared memory.
-    if (A.warm && A.nbr_work) {
-        unsigned w = 0;
-        if (cell < A.n_local) {
-            const int32_t o = __ldg(A.perm + cell);
-            if (o < A.n_owned) w = A.nbr_work[o];
-        }
-        unsigned *sk = reinterpret_cast<unsigned *>(tsmem);
-        sk[tid] = (w << 8) | (unsigned)tid;
-        __syncthreads();
-#pragma unroll 1
-        for (int k = 2; k <= TB; k <<= 1) {
-#pragma unroll 1
-            for (int jj = k >> 1; jj > 0; jj >>= 1) {
-                const int ixj = tid ^ jj;
-                if (ixj > tid) {
-                    const unsigned a = sk[tid], b = sk[ixj];
-                    if ((a > b) == ((tid & k) == 0)) { sk[tid] = b; sk[ixj] = a; }
-                }
-                __syncthreads();
-            }
-        }
-        cell = (int64_t)blockIdx.x * TB + (sk[tid] & 0xFFu);
-        __syncthreads();  // the polygon slots reuse this memory
-    }
-#endif
     TPoly P = tpoly_bind(tsmem, tid);
     bool live = false;
     int32_t orig = 0;
@@ -519,7 +431,7 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
         if (csub(px, bx0) < S || csub(bx1, px) < S || csub(py, by0) < S || csub(by1, py) < S) {
             for (int b = 0; b < 4 && !fail; b++) {
                 const int code = -9 - b;
-                fail = clip_t_cold(P, code, wall_line(code, px, py, r_oct, bx0, by0, bx1, by1), cgm, A, cs);
+                fail = clip_t(P, code, wall_line(code, px, py, r_oct, bx0, by0, bx1, by1), cgm, A, cs);
             }
         }
         R2 = poly_R2(P);
@@ -649,84 +561,6 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
         return j;
     };
     unsigned trips = 0;
-#if TM_LCAP > 0
-    // ---- warm-started cells: the flat loop below would pay a clip test (and often a ring
-    // update) in every trip in which any one lane has a near candidate.  Instead:
-    // (W) clip with the warm neighbours, flat; (A) collect, flat and cheap (iterator, load,
-    // distance test), every candidate closer than 2 R_max -- now nearly final -- that is
-    // not already a line of the ring into a per-thread queue; (B) clip from the queues,
-    // flat, so that nearly every lane of a trip has a useful clip test.  A full queue stops
-    // (A) for that thread; the flat loop (C) then continues its search.
-    if (__any_sync(0xffffffffu, ph == -1)) {
-        for (;;) {  // (W)
-            int cj = -1;
-            if (ph == -1) {
-                while (wi < wn) {
-                    const int id = A.nbr[(int64_t)orig * TM_NBR + wi++];
-                    if (id >= 0 && (int64_t)id < A.n_local) { cj = A.inv_perm[id]; break; }
-                }
-                if (cj < 0) ph = -2;  // warm list done: collect next
-            }
-            if (!__any_sync(0xffffffffu, cj >= 0)) break;
-            trips++;
-            if (cj >= 0) {
-                sc.n_cand++;
-                const double dx = csub(__ldg(A.xs + cj), px), dy = csub(__ldg(A.ys + cj), py);
-                if (cj != (int)cell && !(dx == 0.0 && dy == 0.0) && dx * dx + dy * dy < 4.0 * (double)R2 * MARG) {
-                    const unsigned long long c0 = cs.clips;
-                    fail = clip_t(P, cj, bisector(dx, dy), cgm, A, cs);
-                    if (fail) ph = 2;
-                    else if (cs.clips != c0) R2 = poly_R2(P);
-                }
-            }
-        }
-        int queue[LCAP > 0 ? LCAP : 1];  // thread-local (L1-resident local memory, not shared)
-        int nq_ = 0;
-        bool collecting = ph == -2;
-        if (collecting) ph = 0;
-        for (;;) {  // (A)
-            int cj = -1;
-            if (collecting) {
-                if (nq_ == LCAP) collecting = false;  // queue full: (C) continues this search
-                else {
-                    cj = next_cand();
-                    if (cj < 0) collecting = false;  // search space exhausted (ph == 2)
-                }
-            }
-            if (!__any_sync(0xffffffffu, cj >= 0)) break;
-            trips++;
-            if (cj >= 0) {
-                sc.n_cand++;
-                const double dx = csub(__ldg(A.xs + cj), px), dy = csub(__ldg(A.ys + cj), py);
-                if (cj == (int)cell) {
-                } else if (dx == 0.0 && dy == 0.0) {
-                    atomicAdd(&A.st->n_duplicate, 1ull);
-                } else if (dx * dx + dy * dy < 4.0 * (double)R2 * MARG) {
-                    bool line = false;  // already bounds the ring (a warm neighbour)
-                    if ((P.lmask >> (cj & 63)) & 1ull) {
-#pragma unroll
-                        for (int k = 0; k < VMAX; k++) line |= ((P.used >> k) & 1u) && P.la[k * TB] == cj;
-                    }
-                    if (!line) queue[nq_++] = cj;
-                }
-            }
-        }
-        for (int qi = 0;;) {  // (B)
-            const int cj = (qi < nq_ && !fail) ? queue[qi++] : -1;
-            if (!__any_sync(0xffffffffu, cj >= 0)) break;
-            trips++;
-            if (cj >= 0) {
-                const double dx = csub(__ldg(A.xs + cj), px), dy = csub(__ldg(A.ys + cj), py);
-                if (dx * dx + dy * dy < 4.0 * (double)R2 * MARG) {
-                    const unsigned long long c0 = cs.clips;
-                    fail = clip_t(P, cj, bisector(dx, dy), cgm, A, cs);
-                    if (fail) ph = 2;
-                    else if (cs.clips != c0) R2 = poly_R2(P);
-                }
-            }
-        }
-    }
-#endif
     // ---- (C) flat candidate loop
     int j = next_cand();
     double xj = 0.0, yj = 0.0;
@@ -740,10 +574,8 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
         // clip; leaf pruning then uses the R_max before the clip, which is conservative)
         const int cj = j;
         const double cxj = xj, cyj = yj;
-#if TM_PREFETCH
         j = next_cand();
         if (j >= 0) { xj = __ldg(A.xs + j); yj = __ldg(A.ys + j); }
-#endif
         if (cj >= 0) {
             sc.n_cand++;
             const double dx = csub(cxj, px), dy = csub(cyj, py);
@@ -757,10 +589,6 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
                 else if (cs.clips != c0) R2 = poly_R2(P);
             }
         }
-#if !TM_PREFETCH
-        j = next_cand();
-        if (j >= 0) { xj = __ldg(A.xs + j); yj = __ldg(A.ys + j); }
-#endif
     }
     if (live) {
         if (fail == -1) {
@@ -803,9 +631,6 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
             k = P.nxt[k * TB];
         }
         A.nbr_cnt[orig] = (uint8_t)c;
-#if TM_BALANCE
-        if (A.nbr_work) A.nbr_work[orig] = (uint8_t)min(sc.n_cand, 255ull);
-#endif
     }
     // ---- S3: Delaunay triangles at point-point vertices + keep rule; ELL rows
     int ell = 0;
@@ -819,7 +644,7 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
                 const int32_t ga = __ldg(A.gids + a), gb = __ldg(A.gids + b);
                 if (gi < ga && gi < gb) {
                     const int sv = ga < gb ? a : b, sw = ga < gb ? b : a;
-                    if (keep_tri_cold(A, (int)cell, sv, sw, cadd(px, P.v[k * TB].x), cadd(py, P.v[k * TB].y))) {
+                    if (keep_tri(A, (int)cell, sv, sw, cadd(px, P.v[k * TB].x), cadd(py, P.v[k * TB].y))) {
                         keptmask |= 1u << k;
                         keptall |= 1u << k;
                     }
@@ -837,7 +662,7 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
                     const Line B2 = bisector(csub(__ldg(A.xs + s3[2]), uxx), csub(__ldg(A.ys + s3[2]), uyy));
                     double ox, oy;
                     cramer(B1, B2, ox, oy);
-                    if (keep_tri_cold(A, s3[0], s3[1], s3[2], cadd(uxx, ox), cadd(uyy, oy))) keptall |= 1u << k;
+                    if (keep_tri(A, s3[0], s3[1], s3[2], cadd(uxx, ox), cadd(uyy, oy))) keptall |= 1u << k;
                 }
             }
             k = kn;
@@ -927,7 +752,8 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
         }
         if (MODE & M_TREAT) {
             double qx, qy, dpo;
-            const int s = treat_point_cold(A, h, px, py, px + cx, py + cy, qx, qy, dpo);
+            const int s = treat_point(A.grid, A.phi, h, A.h_avg, A.fac_pt, A.fac_geps, A.damping, A.newton_max, px,
+                                      py, px + cx, py + cy, qx, qy, dpo, LdgLoad());
             A.x_out[orig] = qx;
             A.y_out[orig] = qy;
             A.d_prev_out[orig] = dpo;
@@ -972,311 +798,6 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
     }
 }
 
-
-// ============================================================================
-// Split path (TM_SPLIT): the search runs in k_search_t with lane recycling --
-// each warp takes contiguous chunks of cells from a global counter and a lane
-// that has certified its cell writes the ring (canonical order) to global
-// memory and takes the next cell as soon as TM_REFILL lanes are idle -- and all
-// outputs are computed by k_output_t, one thread per cell, from the stored
-// rings (the same ring, the same canonical start: the same bits as the fused
-// kernel).  The fused kernel runs a warp until its slowest lane is done.
-
-template <int MODE>
-__global__ void __launch_bounds__(TB, TM_TMINB) k_search_t(CellArgs A, int32_t *retry_list,
-                                                           unsigned long long *retry_cnt, RingBuf R) {
-    extern __shared__ __align__(16) unsigned char tsmem[];
-    const int tid = threadIdx.x;
-    const int lane = tid & 31;
-    const unsigned lanemask_lt = (1u << lane) - 1u;
-    TPoly P = tpoly_bind(tsmem, tid);
-    const double MARG = 1.0 + 1e-9;
-    const BinGeom &bg = A.bg;
-    // warp work queue (uniform across the warp)
-    long long cursor = 0, wend = 0;
-    bool exhausted = false;
-    // this lane's cell
-    bool active = false, done = false;
-    int64_t cell = -1;
-    int32_t orig = 0;
-    double px = 0.0, py = 0.0;
-    CellGeom cgm = {};
-    float R2 = 0.f;
-    int fail = 0;
-    int rh = 0, ux = 0, uy = 0, nlx = 0, nly = 0, hb = 0, hoff = 0;
-    double lsx = 0.0, lsy = 0.0;
-    unsigned key[8];
-    int wi = 0, wn = 0;
-    int ph = 2, rr = 0, t = 0, tend = 0, cvx = 0, cvy = 0, cend = -1, cfix = 0, rk = 1, side = 4, kmax = 0;
-    int bxa = 0, bxb = -1, bya = 0, byb = -1;
-    ClipStats cs;
-    unsigned long long n_cand = 0;
-    unsigned trips = 0;
-
-    auto setup = [&](int64_t c) {
-        cell = c;
-        fail = 0;
-        orig = __ldg(A.perm + c);
-        if (orig >= A.n_owned) {  // ghost: binned, no cell
-            R.n[c] = 0;
-            active = false;
-            return;
-        }
-        px = __ldg(A.xs + c);
-        py = __ldg(A.ys + c);
-        const double h = __ldg(A.hs + c);
-        const double S = cmul(A.fac_voro, h);
-        const double r_oct = cmul(S, COS_PI8);
-        const double bx0 = A.grid.x0, by0 = A.grid.y0, bx1 = A.grid.x1, by1 = A.grid.y1;
-        cgm = {px, py, r_oct, bx0, by0, bx1, by1};
-#pragma unroll
-        for (int k = 0; k < 8; k++) {  // octagon, det = 1 (see k_cells_t)
-            const Line La = wall_line(-1 - k, px, py, r_oct, bx0, by0, bx1, by1);
-            const Line Lb = wall_line(-1 - ((k + 1) & 7), px, py, r_oct, bx0, by0, bx1, by1);
-            const double x = csub(cmul(La.r, Lb.ny), cmul(La.ny, Lb.r));
-            const double y = csub(cmul(La.nx, Lb.r), cmul(La.r, Lb.nx));
-            P.v[k * TB] = make_double2(x, y);
-            P.K[k * TB] = store_K(-1.0);
-            set_r2(P, k, x, y, -1.0);
-            P.la[k * TB] = -1 - k;
-            P.prv[k * TB] = (uint8_t)((k + 7) & 7);
-            P.nxt[k * TB] = (uint8_t)((k + 1) & 7);
-        }
-        P.used = 0xffu;
-        P.wall = 0xffu;
-        P.lmask = 0;
-        if (csub(px, bx0) < S || csub(bx1, px) < S || csub(py, by0) < S || csub(by1, py) < S) {
-            for (int b = 0; b < 4 && !fail; b++) {
-                const int code = -9 - b;
-                fail = clip_t(P, code, wall_line(code, px, py, r_oct, bx0, by0, bx1, by1), cgm, A, cs);
-            }
-        }
-        R2 = poly_R2(P);
-        int hbx = (int)floor((px - bg.x0) * bg.isx), hby = (int)floor((py - bg.y0) * bg.isy);
-        hbx = hbx < 0 ? 0 : (hbx >= bg.nbx ? bg.nbx - 1 : hbx);
-        hby = hby < 0 ? 0 : (hby >= bg.nby ? bg.nby - 1 : hby);
-        hb = hby * bg.nbx + hbx;
-        rh = __ldg(A.rlev + hb);
-        hoff = __ldg(A.leaf_off + hb);
-        ux = leaf_coord(px, bg.x0, bg.isx, bg.nbx, rh);
-        uy = leaf_coord(py, bg.y0, bg.isy, bg.nby, rh);
-        nlx = bg.nbx << rh;
-        nly = bg.nby << rh;
-        lsx = bg.sx / (double)(1 << rh);
-        lsy = bg.sy / (double)(1 << rh);
-        const double gl = px - (bg.x0 + ux * lsx), gr = (bg.x0 + (ux + 1) * lsx) - px;
-        const double gd = py - (bg.y0 + uy * lsy), gu = (bg.y0 + (uy + 1) * lsy) - py;
-        const int ddx[8] = {-1, 1, 0, 0, -1, 1, -1, 1};
-        const int ddy[8] = {0, 0, -1, 1, -1, -1, 1, 1};
-#pragma unroll
-        for (int q = 0; q < 8; q++) {
-            const double gx = fmax(ddx[q] < 0 ? gl : (ddx[q] > 0 ? gr : 0.0), 0.0);
-            const double gy = fmax(ddy[q] < 0 ? gd : (ddy[q] > 0 ? gu : 0.0), 0.0);
-            const float d2 = __double2float_rd(gx * gx + gy * gy);
-            key[q] = (__float_as_uint(fmaxf(d2, 0.f)) & ~7u) | (unsigned)q;
-        }
-        cswap(key[0], key[2]); cswap(key[1], key[3]); cswap(key[4], key[6]); cswap(key[5], key[7]);
-        cswap(key[0], key[4]); cswap(key[1], key[5]); cswap(key[2], key[6]); cswap(key[3], key[7]);
-        cswap(key[0], key[1]); cswap(key[2], key[3]); cswap(key[4], key[5]); cswap(key[6], key[7]);
-        cswap(key[2], key[4]); cswap(key[3], key[5]);
-        cswap(key[1], key[4]); cswap(key[3], key[6]);
-        cswap(key[1], key[2]); cswap(key[3], key[4]); cswap(key[5], key[6]);
-        int st, cnt;
-        vleaf_range(A, ux, uy, rh, ux, uy, hb, hoff, st, cnt);
-        t = st;
-        tend = st + cnt;
-        wi = 0;
-        wn = (A.warm && A.nbr_cnt) ? min((int)A.nbr_cnt[orig], TM_NBR) : 0;
-        ph = fail ? 2 : (wn > 0 ? -1 : 0);
-        rr = 0;
-        rk = 1;
-        side = 4;
-        cvx = 0;
-        cend = -1;
-        active = true;
-    };
-
-    auto next_cand = [&]() -> int {
-        int j = -1;
-        while (ph < 2) {
-            if (ph < 0) {
-                if (wi >= wn) { ph = 0; continue; }
-                const int id = A.nbr[(int64_t)orig * TM_NBR + wi++];
-                if (id < 0 || (int64_t)id >= A.n_local) continue;
-                j = A.inv_perm[id];
-                P.lmask |= 1ull << (j & 63);
-                break;
-            }
-            if (t < tend) { j = t++; break; }
-            const float lim = 4.0f * R2 * (float)MARG;
-            if (ph == 0) {
-                if (rr >= 8) {
-                    const double rad = 2.0 * sqrt((double)R2 * MARG) * (1.0 + 1e-6);
-                    const double sxl = bg.isx * (double)(1 << rh), syl = bg.isy * (double)(1 << rh);
-                    bxa = max(0, (int)floor((px - rad - bg.x0) * sxl));
-                    bxb = min(nlx - 1, (int)floor((px + rad - bg.x0) * sxl));
-                    bya = max(0, (int)floor((py - rad - bg.y0) * syl));
-                    byb = min(nly - 1, (int)floor((py + rad - bg.y0) * syl));
-                    kmax = max(max(ux - bxa, bxb - ux), max(uy - bya, byb - uy));
-                    ph = 1;
-                    rk = 1;
-                    side = 4;
-                    continue;
-                }
-                unsigned kq = key[0];
-#pragma unroll
-                for (int u = 1; u < 8; u++)
-                    if (rr == u) kq = key[u];
-                rr++;
-                if (__uint_as_float(kq & ~7u) * (1.0f - 1e-6f) >= lim) { rr = 8; continue; }
-                const int q = (int)(kq & 7u);
-                const int vx = ux + (q == 0 || q == 4 || q == 6 ? -1 : (q == 1 || q == 5 || q == 7 ? 1 : 0));
-                const int vy = uy + (q == 2 || q == 4 || q == 5 ? -1 : (q == 3 || q == 6 || q == 7 ? 1 : 0));
-                if (vx < 0 || vx >= nlx || vy < 0 || vy >= nly) continue;
-                int st, cnt;
-                vleaf_range(A, vx, vy, rh, ux, uy, hb, hoff, st, cnt);
-                t = st;
-                tend = st + cnt;
-            } else {
-                if (cvx > cend) {
-                    if (++side >= 4) {
-                        rk++;
-                        if (rk > kmax) { ph = 2; break; }
-                        const double dl = px - (bg.x0 + (ux - rk + 1) * lsx), dr = (bg.x0 + (ux + rk) * lsx) - px;
-                        const double dd = py - (bg.y0 + (uy - rk + 1) * lsy), du = (bg.y0 + (uy + rk) * lsy) - py;
-                        const double dmin = fmin(fmin(dl, dr), fmin(dd, du));
-                        if (dmin > 0.0 && dmin * dmin * (1.0 - 1e-9) >= 4.0 * (double)R2 * MARG) { ph = 2; break; }
-                        side = 0;
-                    }
-                    if (side < 2) {
-                        cvy = side == 0 ? uy - rk : uy + rk;
-                        cvx = max(ux - rk, bxa);
-                        cend = (cvy < bya || cvy > byb) ? cvx - 1 : min(ux + rk, bxb);
-                    } else {
-                        cfix = side == 2 ? ux - rk : ux + rk;
-                        cvx = max(uy - rk + 1, bya);
-                        cend = (cfix < bxa || cfix > bxb) ? cvx - 1 : min(uy + rk - 1, byb);
-                    }
-                    continue;
-                }
-                const int vx = side < 2 ? cvx : cfix, vy = side < 2 ? cvy : cvx;
-                cvx++;
-                if (leaf_d2(bg, lsx, lsy, vx, vy, px, py) * (1.0 - 1e-9) >= 4.0 * (double)R2 * MARG) continue;
-                int st, cnt;
-                vleaf_range(A, vx, vy, rh, ux, uy, hb, hoff, st, cnt);
-                t = st;
-                tend = st + cnt;
-            }
-        }
-        return j;
-    };
-
-    auto finish = [&]() {
-        if (fail == -1) {  // over VMAX slots / undecided filter: the 32-lane pass redoes it
-            const unsigned long long k = atomicAdd(retry_cnt, 1ull);
-            retry_list[k] = (int32_t)cell;
-            if (A.nbr_cnt) A.nbr_cnt[orig] = 0;
-            R.n[cell] = 0;
-            return;
-        }
-        if (fail) {
-            if (A.nbr_cnt) A.nbr_cnt[orig] = 0;
-            atomicAdd(&A.st->n_degenerate, 1ull);
-            if (MODE & M_TREAT) {
-                A.x_out[orig] = px; A.y_out[orig] = py; A.d_prev_out[orig] = 0.0; A.status[orig] = 2;
-            }
-            if (MODE & M_HAT) { A.x_hat[orig] = px; A.y_hat[orig] = py; }
-            if (MODE & M_ELL) A.deg[cell] = 0;
-            R.n[cell] = 0;
-            return;
-        }
-        int start = 0;
-        long long best = LLONG_MAX;
-        for (unsigned m = P.used; m; m &= m - 1) {
-            const int k = __ffs(m) - 1;
-            const long long kk = ((long long)P.la[k * TB] << 32) | (unsigned)P.la[P.nxt[k * TB] * TB];
-            if (kk < best) { best = kk; start = k; }
-        }
-        const int nv = __popc(P.used);
-        double2 *rv = R.v + cell;
-        int *rl = R.la + cell;
-        int k = start;
-        for (int i = 0; i < nv; i++) {
-            rv[(int64_t)i * A.n_local] = P.v[k * TB];
-            rl[(int64_t)i * A.n_local] = P.la[k * TB];
-            k = P.nxt[k * TB];
-        }
-        R.n[cell] = (uint8_t)nv;
-    };
-
-    for (;;) {
-        // refill the idle lanes from the warp's queue once TM_REFILL of them are idle
-        const unsigned idle = __ballot_sync(0xffffffffu, !active);
-        if (idle && (__popc(idle) >= TM_REFILL || idle == 0xffffffffu)) {
-            if (done) { finish(); done = false; }  // batched: the lanes that finished since the last refill
-        }
-        if (idle && !exhausted && (__popc(idle) >= TM_REFILL || idle == 0xffffffffu)) {
-            unsigned pend = idle;
-            while (pend) {
-                if (cursor >= wend) {
-                    unsigned long long b = 0;
-                    if (lane == 0) b = atomicAdd(R.chunk, (unsigned long long)TM_CHUNK);
-                    b = __shfl_sync(0xffffffffu, b, 0);
-                    if ((int64_t)b >= A.n_local) { exhausted = true; break; }
-                    cursor = (long long)b;
-                    wend = min((long long)b + TM_CHUNK, (long long)A.n_local);
-                }
-                const int navail = (int)(wend - cursor);
-                const int rank = __popc(pend & lanemask_lt);
-                const bool mine = ((pend >> lane) & 1u) && rank < navail;
-                if (mine) setup(cursor + rank);
-                const int took = min(navail, __popc(pend));
-                cursor += took;
-                pend &= ~__ballot_sync(0xffffffffu, mine);
-            }
-        }
-        if (!__any_sync(0xffffffffu, active)) {
-            if (exhausted) {
-                if (done) finish();
-                break;
-            }
-            continue;
-        }
-        trips++;
-        const int j = active ? next_cand() : -1;
-        if (j >= 0) {
-            n_cand++;
-            const double dx = csub(__ldg(A.xs + j), px), dy = csub(__ldg(A.ys + j), py);
-            if (j == (int)cell) {
-            } else if (dx == 0.0 && dy == 0.0) {
-                atomicAdd(&A.st->n_duplicate, 1ull);
-            } else if (dx * dx + dy * dy < 4.0 * (double)R2 * MARG) {
-                const unsigned long long c0 = cs.clips;
-                fail = clip_t(P, j, bisector(dx, dy), cgm, A, cs);
-                if (fail) ph = 2;
-                else if (cs.clips != c0) R2 = poly_R2(P);
-            }
-        }
-        if (active && ph >= 2) {  // certified (or failed): its outputs wait for the next refill
-            active = false;
-            done = true;
-        }
-    }
-    if (MODE & M_COUNT) {
-        unsigned long long a = n_cand, b = cs.clips, c = cs.exact;
-        for (int o = 16; o > 0; o >>= 1) {
-            a += __shfl_xor_sync(0xffffffffu, a, o);
-            b += __shfl_xor_sync(0xffffffffu, b, o);
-            c += __shfl_xor_sync(0xffffffffu, c, o);
-        }
-        if (lane == 0) {
-            atomicAdd(&A.st->work[7], a);
-            atomicAdd(&A.st->work[8], b);
-            atomicAdd(&A.st->work[9], c);
-            atomicAdd(&A.st->work[10], (unsigned long long)trips);
-        }
-    }
-}
 
 // adaptive quadrature over a stored ring (ring order from the canonical vertex);
 // the same sub-triangles and sums, in the same order, as quad_centroid_t.  Sub-triangles
@@ -1540,38 +1061,6 @@ namespace tmg {
 
 template <int MODE>
 tm_status launch_cells_thread(tm_ctx *ctx, const CellArgs &a) {
-#if TM_SPLIT
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-        TM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_search_t<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)TSMEM));
-        attr_set = true;
-    }
-    if (ctx->n_local > ctx->cap_ring) {
-        cudaFree(ctx->ring_v); cudaFree(ctx->ring_la); cudaFree(ctx->ring_n);
-        ctx->ring_v = ctx->ring_la = ctx->ring_n = nullptr;
-        const int64_t c = ctx->n_local + ctx->n_local / 8 + 1024;
-        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->ring_v, c * VMAX * sizeof(double2)));
-        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->ring_la, c * VMAX * sizeof(int)));
-        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->ring_n, c * sizeof(uint8_t) + 64));
-        ctx->cap_ring = c;
-    }
-    RingBuf R;
-    R.v = (double2 *)ctx->ring_v;
-    R.la = (int *)ctx->ring_la;
-    R.n = (uint8_t *)ctx->ring_n;
-    R.chunk = (unsigned long long *)((uint8_t *)ctx->ring_n + ((ctx->cap_ring + 7) / 8) * 8);
-    TM_CUDA_TRY(ctx, cudaMemsetAsync(R.chunk, 0, sizeof(unsigned long long), ctx->stream));
-    int nsm = 148;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
-    const int64_t need = (ctx->n_local + (TB / 32) * TM_CHUNK - 1) / ((TB / 32) * TM_CHUNK);
-    const unsigned blocks = (unsigned)std::min<int64_t>(need, (int64_t)nsm * TM_TMINB);
-    k_search_t<MODE><<<blocks, TB, TSMEM, ctx->stream>>>(a, ctx->retry_list, ctx->retry_cnt, R);
-    tm_status s = tm_internal_check_launch(ctx, "k_search_t");
-    if (s != TM_OK) return s;
-    k_output_t<MODE><<<(unsigned)((ctx->n_local + 127) / 128), 128, 0, ctx->stream>>>(a, R);
-    return tm_internal_check_launch(ctx, "k_output_t");
-#else
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         TM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_cells_t<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TSMEM));
@@ -1603,7 +1092,6 @@ tm_status launch_cells_thread(tm_ctx *ctx, const CellArgs &a) {
     b.nbr = nullptr;  // the neighbour lists were written by k_cells_t
     k_output_t<OMODE><<<(unsigned)((ctx->n_local + 127) / 128), 128, 0, ctx->stream>>>(b, R);
     return tm_internal_check_launch(ctx, "k_output_t");
-#endif
 }
 
 #define TM_INST(M) template tm_status launch_cells_thread<M>(tm_ctx *, const CellArgs &);

@@ -63,7 +63,6 @@ struct CellArgs {
     const int32_t *inv_perm;   // caller index -> sorted slot (this binning)
     int32_t *nbr;              // warm start: per caller index, the cell's neighbours (caller ids) of the
     uint8_t *nbr_cnt;          //   last cell launch on the same point set; nbr_cnt[i] entries (<= TM_NBR)
-    uint8_t *nbr_work;         //   and the number of candidates that cell examined (load balancing)
     int32_t warm;              // 1: read nbr/nbr_cnt before the search (they are written back either way)
     const uint8_t *rlev;
     const int32_t *leaf_off, *leaf_start;
@@ -111,7 +110,7 @@ struct tm_ctx {
     int32_t *perm = nullptr, *gids = nullptr, *key = nullptr, *rank = nullptr, *inv_perm = nullptr;
     // warm start of the cell search (previous iteration's neighbours, caller ids; single domain only)
     int32_t *nbr = nullptr;
-    uint8_t *nbr_cnt = nullptr, *nbr_work = nullptr;
+    uint8_t *nbr_cnt = nullptr;
     int64_t cap_nbr = 0, nbr_n = -1;
     bool have_gid = false;
     int32_t *bin_count = nullptr, *block_sums = nullptr;
@@ -127,7 +126,7 @@ struct tm_ctx {
     int32_t *retry_list = nullptr;
     unsigned long long *retry_cnt = nullptr;
     int64_t cap_retry = 0;
-    // split cell path: stored rings (thread-kernel layout, see tm_cells_t.cu) and the work queue
+    // CVD split: stored rings (slot-major, see tm_cells_t.cu RingBuf)
     void *ring_v = nullptr, *ring_la = nullptr, *ring_n = nullptr;
     int64_t cap_ring = 0;
     // strip migration scratch (stable partition)
