@@ -58,8 +58,7 @@ extern "C" tm_status tm_create(int device, void *cuda_stream, const tm_params *p
 
 static void free_points(tm_ctx *c) {
     cudaFree(c->xs); cudaFree(c->ys); cudaFree(c->hs);
-    cudaFree(c->perm); cudaFree(c->gids); cudaFree(c->key); cudaFree(c->rank); cudaFree(c->inv_perm);
-    c->inv_perm = nullptr;
+    cudaFree(c->perm); cudaFree(c->gids); cudaFree(c->key); cudaFree(c->rank);
     c->xs = c->ys = c->hs = nullptr;
     c->perm = c->gids = c->key = c->rank = nullptr;
     c->cap_points = 0;
@@ -76,7 +75,7 @@ extern "C" void tm_destroy(tm_ctx *ctx) {
     cudaFree(ctx->partials); cudaFree(ctx->stat_acc); cudaFree(ctx->dst);
     cudaFree(ctx->retry_list); cudaFree(ctx->retry_cnt);
     cudaFree(ctx->mig_keep); cudaFree(ctx->mig_cnt); cudaFree(ctx->mig_off);
-    cudaFree(ctx->nbr); cudaFree(ctx->nbr_cnt);
+    cudaFree(ctx->nbr); cudaFree(ctx->nbr_cnt); cudaFree(ctx->inv_id);
     cudaFree(ctx->ring_v); cudaFree(ctx->ring_la); cudaFree(ctx->ring_n);
     delete ctx;
 }
@@ -262,10 +261,6 @@ extern "C" tm_status tm_set_domain(tm_ctx *ctx, const tm_fields *f, int64_t n_to
     return TM_OK;
 }
 
-#ifndef TM_BIN_GATHER
-#define TM_BIN_GATHER 1  // sort caller indices per leaf, then gather the point data in slot order
-#endif
-
 // ============================================================================ S1
 __global__ void k_bin_keys(const double *__restrict__ x, const double *__restrict__ y, int64_t n, BinGeom bg,
                            double bx0, double by0, double bx1, double by1, int32_t *__restrict__ key,
@@ -396,51 +391,6 @@ __global__ void k_scan_add(int32_t *out, const int32_t *tile_sums, int64_t n) {
     out[i] += tile_sums[i / SCAN_TILE];
 }
 
-__global__ void k_bin_scatter(const double *__restrict__ x, const double *__restrict__ y,
-                              const int32_t *__restrict__ gid, int64_t n, const int32_t *__restrict__ key,
-                              const int32_t *__restrict__ rank, const int32_t *__restrict__ start,
-                              double bx0, double by0, double bx1, double by1, Grid g,
-                              const double *__restrict__ mu, double c, double *__restrict__ xs,
-                              double *__restrict__ ys, double *__restrict__ hs, int32_t *__restrict__ perm,
-                              int32_t *__restrict__ gids) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    int64_t s = (int64_t)start[key[i]] + rank[i];
-    double px = x[i], py = y[i];
-    px = fmin(fmax(px == px ? px : bx0, bx0), bx1);
-    py = fmin(fmax(py == py ? py : by0, by0), by1);
-    xs[s] = px;
-    ys[s] = py;
-    // h(p) = c * mu~(p)   (§8.0 "Local size")
-    hs[s] = mu ? cmul(c, bilinear(g, mu, px, py, LdgLoad())) : c;
-    perm[s] = (int32_t)i;
-    gids[s] = gid ? gid[i] : (int32_t)i;
-}
-
-// Make the slot order inside every leaf deterministic (ascending caller index):
-// the atomic ranks of k_leaf_keys are not.  Leaves hold ~N_opt points.
-__global__ void k_leaf_sort(const int32_t *__restrict__ leaf_start, int64_t nleaves, double *__restrict__ xs,
-                            double *__restrict__ ys, double *__restrict__ hs, int32_t *__restrict__ perm,
-                            int32_t *__restrict__ gids, int32_t *__restrict__ inv_perm) {
-    int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (l >= nleaves) return;
-    int s = leaf_start[l], e = leaf_start[l + 1];
-    for (int a = s + 1; a < e; a++) {
-        int32_t pk = perm[a];
-        if (pk >= perm[a - 1]) continue;
-        double x = xs[a], y = ys[a], h = hs[a];
-        int32_t gk = gids[a];
-        int b = a - 1;
-        while (b >= s && perm[b] > pk) {
-            xs[b + 1] = xs[b]; ys[b + 1] = ys[b]; hs[b + 1] = hs[b];
-            perm[b + 1] = perm[b]; gids[b + 1] = gids[b];
-            b--;
-        }
-        xs[b + 1] = x; ys[b + 1] = y; hs[b + 1] = h; perm[b + 1] = pk; gids[b + 1] = gk;
-    }
-    for (int a = s; a < e; a++) inv_perm[perm[a]] = a;  // caller index -> slot
-}
-
 // S1 tail: the slot of every point is its leaf's start plus its rank in the leaf; the
 // ranks come from atomics (arbitrary order), so each leaf's caller indices are then
 // sorted (4-byte keys only) and the point data gathered once into slot order with
@@ -453,7 +403,7 @@ __global__ void k_perm_scatter(int64_t n, const int32_t *__restrict__ key, const
 }
 
 __global__ void k_leaf_sort_perm(const int32_t *__restrict__ leaf_start, int64_t nleaves, int32_t *__restrict__ perm,
-                                 int32_t *__restrict__ inv_perm) {
+                                 const int32_t *__restrict__ gid, int64_t nkey, int32_t *__restrict__ inv_id) {
     const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (l >= nleaves) return;
     const int s = leaf_start[l], e = leaf_start[l + 1];
@@ -466,7 +416,11 @@ __global__ void k_leaf_sort_perm(const int32_t *__restrict__ leaf_start, int64_t
         }
         perm[b + 1] = pk;
     }
-    for (int a = s; a < e; a++) inv_perm[perm[a]] = a;  // caller index -> slot
+    // point id (gid if given, else caller index) -> slot, for the warm start
+    for (int a = s; a < e; a++) {
+        const int32_t id = gid ? gid[perm[a]] : perm[a];
+        if (id >= 0 && (int64_t)id < nkey) inv_id[id] = a;  // gids outside [0, n_total): no warm start
+    }
 }
 
 __global__ void k_gather_sorted(const double *__restrict__ x, const double *__restrict__ y,
@@ -497,7 +451,6 @@ static tm_status ensure_points(tm_ctx *ctx, int64_t n) {
     TM_CUDA_TRY(ctx, cudaMalloc(&ctx->gids, cap * sizeof(int32_t)));
     TM_CUDA_TRY(ctx, cudaMalloc(&ctx->key, cap * sizeof(int32_t)));
     TM_CUDA_TRY(ctx, cudaMalloc(&ctx->rank, cap * sizeof(int32_t)));
-    TM_CUDA_TRY(ctx, cudaMalloc(&ctx->inv_perm, cap * sizeof(int32_t)));
     ctx->cap_points = cap;
     return TM_OK;
 }
@@ -562,6 +515,26 @@ extern "C" tm_status tm_grid_bin(tm_ctx *ctx, const double *x, const double *y, 
     // leaves: 4^r per bin; for r > 0, 4^r < 4 count / N_opt, so the total is below nb + 4 N / N_opt
     int64_t nleaves_max = nb + (int64_t)ceil(4.0 * (double)n_local / ctx->p.n_opt) + 1;
     if ((s = ensure_bins(ctx, nb, nleaves_max)) != TM_OK) return s;
+    // warm start (tm_cells_t.cu): neighbour lists and the id -> slot map are keyed by point id,
+    // the gid when given (strips: ids are global and stable while local positions change),
+    // else the caller index; the key space is n_total resp. n_local
+    const int64_t nkey = gid ? ctx->n_total : n_local;
+    if (nkey != ctx->nbr_n || (gid != nullptr) != ctx->have_gid) ctx->nbr_n = -1;  // warm start invalid
+    if (nkey > ctx->cap_nbr) {
+        cudaFree(ctx->nbr);
+        cudaFree(ctx->nbr_cnt);
+        cudaFree(ctx->inv_id);
+        ctx->nbr = nullptr;
+        ctx->nbr_cnt = nullptr;
+        ctx->inv_id = nullptr;
+        const int64_t c = nkey + nkey / 8 + 1024;
+        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->nbr, c * TM_NBR * sizeof(int32_t)));
+        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->nbr_cnt, c * sizeof(uint8_t)));
+        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->inv_id, c * sizeof(int32_t)));
+        TM_CUDA_TRY(ctx, cudaMemsetAsync(ctx->nbr_cnt, 0, c * sizeof(uint8_t), ctx->stream));
+        ctx->cap_nbr = c;
+        ctx->nbr_n = -1;
+    }
     TM_CUDA_TRY(ctx, cudaMemsetAsync(ctx->bin_count, 0, nb * sizeof(int32_t), ctx->stream));
     const Grid &g = ctx->grid;
     unsigned blocks = (unsigned)((n_local + 255) / 256);
@@ -577,34 +550,12 @@ extern "C" tm_status tm_grid_bin(tm_ctx *ctx, const double *x, const double *y, 
                                                  ctx->leaf_off, ctx->leaf_count, ctx->rank);
     if ((s = tm_internal_check_launch(ctx, "k_leaf_keys")) != TM_OK) return s;
     if ((s = scan_counts(ctx, ctx->leaf_count, ctx->leaf_start, nleaves_max)) != TM_OK) return s;
-#if TM_BIN_GATHER
     k_perm_scatter<<<blocks, 256, 0, ctx->stream>>>(n_local, ctx->key, ctx->rank, ctx->leaf_start, ctx->perm);
     k_leaf_sort_perm<<<(unsigned)((nleaves_max + 255) / 256), 256, 0, ctx->stream>>>(ctx->leaf_start, nleaves_max,
-                                                                                   ctx->perm, ctx->inv_perm);
+                                                                                   ctx->perm, gid, nkey, ctx->inv_id);
     k_gather_sorted<<<blocks, 256, 0, ctx->stream>>>(x, y, gid, n_local, ctx->perm, g.x0, g.y0, g.x1, g.y1, g, ctx->mu,
                                                      ctx->c, ctx->xs, ctx->ys, ctx->hs, ctx->gids);
     if ((s = tm_internal_check_launch(ctx, "k_gather_sorted")) != TM_OK) return s;
-#else
-    k_bin_scatter<<<blocks, 256, 0, ctx->stream>>>(x, y, gid, n_local, ctx->key, ctx->rank, ctx->leaf_start, g.x0,
-                                                   g.y0, g.x1, g.y1, g, ctx->mu, ctx->c, ctx->xs, ctx->ys,
-                                                   ctx->hs, ctx->perm, ctx->gids);
-    if ((s = tm_internal_check_launch(ctx, "k_bin_scatter")) != TM_OK) return s;
-    k_leaf_sort<<<(unsigned)((nleaves_max + 255) / 256), 256, 0, ctx->stream>>>(
-        ctx->leaf_start, nleaves_max, ctx->xs, ctx->ys, ctx->hs, ctx->perm, ctx->gids, ctx->inv_perm);
-    if ((s = tm_internal_check_launch(ctx, "k_leaf_sort")) != TM_OK) return s;
-#endif
-    if (n_local != ctx->nbr_n || (gid != nullptr) != ctx->have_gid) ctx->nbr_n = -1;  // warm start invalid
-    if (!gid && n_local > ctx->cap_nbr) {
-        cudaFree(ctx->nbr);
-        cudaFree(ctx->nbr_cnt);
-        ctx->nbr = nullptr;
-        ctx->nbr_cnt = nullptr;
-        const int64_t c = n_local + n_local / 8 + 1024;
-        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->nbr, c * TM_NBR * sizeof(int32_t)));
-        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->nbr_cnt, c * sizeof(uint8_t)));
-        ctx->cap_nbr = c;
-        ctx->nbr_n = -1;
-    }
     ctx->have_gid = gid != nullptr;
     ctx->n_local = n_local;
     ctx->n_owned = n_owned;
@@ -616,10 +567,12 @@ extern "C" tm_status tm_grid_bin(tm_ctx *ctx, const double *x, const double *y, 
 tm_status tm_internal_fill_cell_args(tm_ctx *ctx, CellArgs *a) {
     memset(a, 0, sizeof(*a));
     a->xs = ctx->xs; a->ys = ctx->ys; a->hs = ctx->hs;
-    a->perm = ctx->perm; a->gids = ctx->gids; a->inv_perm = ctx->inv_perm;
-    a->nbr = ctx->have_gid ? nullptr : ctx->nbr;  // single domain only (caller ids are stable)
-    a->nbr_cnt = ctx->have_gid ? nullptr : ctx->nbr_cnt;
-    a->warm = (a->nbr && ctx->nbr_n == ctx->n_local) ? 1 : 0;
+    a->perm = ctx->perm; a->gids = ctx->gids; a->inv_perm = ctx->inv_id;
+    a->nbr = ctx->nbr;
+    a->nbr_cnt = ctx->nbr_cnt;
+    a->nbr_by_gid = ctx->have_gid ? 1 : 0;
+    a->nbr_keys = ctx->have_gid ? ctx->n_total : ctx->n_local;
+    a->warm = (a->nbr && ctx->nbr_n == a->nbr_keys) ? 1 : 0;
     a->rlev = ctx->rlev; a->leaf_off = ctx->leaf_off; a->leaf_start = ctx->leaf_start;
     a->bg = ctx->bg;
     a->n_local = ctx->n_local; a->n_owned = ctx->n_owned;

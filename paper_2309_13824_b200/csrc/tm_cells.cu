@@ -634,7 +634,7 @@ extern "C" tm_status tm_voronoi_delaunay(tm_ctx *ctx, int32_t *tri, int64_t tri_
     if (s == TM_OK) {
         ctx->have_cells = true;
         // neighbour lists written (thread kernel only): warm start for the next launch
-        ctx->nbr_n = (a.nbr && !(ctx->p.flags & TM_F_GROUP_CELLS)) ? ctx->n_local : -1;
+        ctx->nbr_n = (a.nbr && !(ctx->p.flags & TM_F_GROUP_CELLS)) ? a.nbr_keys : -1;
     }
     return s;
 }
@@ -652,6 +652,6 @@ extern "C" tm_status tm_cvd_step(tm_ctx *ctx, const double *d_prev, double *x_ha
     if (ctx->p.flags & TM_F_COUNT_WORK)
         TM_CUDA_TRY(ctx, cudaMemsetAsync(ctx->dst->work, 0, sizeof(ctx->dst->work), ctx->stream));
     s = dispatch_count<M_HAT>(ctx, a);
-    if (s == TM_OK) ctx->nbr_n = (a.nbr && !(ctx->p.flags & TM_F_GROUP_CELLS)) ? ctx->n_local : -1;
+    if (s == TM_OK) ctx->nbr_n = (a.nbr && !(ctx->p.flags & TM_F_GROUP_CELLS)) ? a.nbr_keys : -1;
     return s;
 }

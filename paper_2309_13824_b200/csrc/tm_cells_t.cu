@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
     // ---- per-cell results consumed by the warp-collective emission below
     int t_own = 0;
     unsigned keptmask = 0;  // slots whose (owned) point-point vertex is a kept triangle
-    int32_t gi = 0;
+    int32_t gi = 0, nid = 0;
     ClipStats cs;
     unsigned long long nq = 0;
     SearchCtx sc;
@@ -405,6 +405,8 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
         py = __ldg(A.ys + cell);
         h = __ldg(A.hs + cell);
         gi = __ldg(A.gids + cell);
+        nid = A.nbr_by_gid ? gi : orig;  // warm-start key (gid on strips, else caller index)
+        if (nid < 0 || (int64_t)nid >= A.nbr_keys) nid = -1;  // outside the key space: no warm start
         sc.px = px; sc.py = py; sc.cell = (int)cell;
         const double S = cmul(A.fac_voro, h);
         const double r_oct = cmul(S, COS_PI8);
@@ -476,7 +478,7 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
         // (caller ids) are clipped first -- the ring is then nearly final and R_max small
         // before the search; the search still certifies the cell (L11), so the result
         // does not depend on them
-        wn = (A.warm && A.nbr_cnt) ? min((int)A.nbr_cnt[orig], TM_NBR) : 0;
+        wn = (A.warm && A.nbr_cnt && nid >= 0) ? min((int)A.nbr_cnt[nid], TM_NBR) : 0;
         ph = fail ? 2 : (wn > 0 ? -1 : 0);
         rr = 0;
     }
@@ -488,9 +490,11 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
         while (ph < 2) {
             if (ph < 0) {
                 if (wi >= wn) { ph = 0; continue; }
-                const int id = A.nbr[(int64_t)orig * TM_NBR + wi++];
-                if (id < 0 || (int64_t)id >= A.n_local) continue;
-                j = A.inv_perm[id];
+                const int id = A.nbr[(int64_t)nid * TM_NBR + wi++];
+                if (id < 0 || (int64_t)id >= A.nbr_keys) continue;
+                const int js = A.inv_perm[id];  // stale for a gid not binned here: checked
+                if (js < 0 || (int64_t)js >= A.n_local || (A.nbr_by_gid && __ldg(A.gids + js) != id)) continue;
+                j = js;
                 P.lmask |= 1ull << (j & 63);
                 break;
             }
@@ -596,10 +600,10 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
             // the 32-lane group kernel redoes this cell
             const unsigned long long k = atomicAdd(retry_cnt, 1ull);
             retry_list[k] = (int32_t)cell;
-            if (A.nbr_cnt) A.nbr_cnt[orig] = 0;
+            if (A.nbr_cnt && nid >= 0) A.nbr_cnt[nid] = 0;
             live = false;
         } else if (fail) {
-            if (A.nbr_cnt) A.nbr_cnt[orig] = 0;
+            if (A.nbr_cnt && nid >= 0) A.nbr_cnt[nid] = 0;
             atomicAdd(&A.st->n_degenerate, 1ull);
             if (MODE & M_TREAT) {
                 A.x_out[orig] = px; A.y_out[orig] = py; A.d_prev_out[orig] = 0.0; A.status[orig] = 2;
@@ -622,15 +626,15 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
         }
     }
     const int nv = live ? __popc(P.used) : 0;
-    // neighbour list for the next launch's warm start (caller ids, ring order)
-    if (live && A.nbr) {
+    // neighbour list for the next launch's warm start (point ids, ring order)
+    if (live && A.nbr && nid >= 0) {
         int k = start, c = 0;
         for (int q = 0; q < nv; q++) {
             const int a = P.la[k * TB];
-            if (a >= 0) A.nbr[(int64_t)orig * TM_NBR + c++] = __ldg(A.perm + a);
+            if (a >= 0) A.nbr[(int64_t)nid * TM_NBR + c++] = A.nbr_by_gid ? __ldg(A.gids + a) : __ldg(A.perm + a);
             k = P.nxt[k * TB];
         }
-        A.nbr_cnt[orig] = (uint8_t)c;
+        A.nbr_cnt[nid] = (uint8_t)c;
     }
     // ---- S3: Delaunay triangles at point-point vertices + keep rule; ELL rows
     int ell = 0;
@@ -902,7 +906,7 @@ __global__ void __launch_bounds__(128, TM_OUT_MINB) k_output_t(CellArgs A, RingB
     const int64_t ns = A.n_local;
     auto RV = [&](int i) { return rv0[(int64_t)i * ns]; };
     auto RL = [&](int i) { return rl0[(int64_t)i * ns]; };
-    int32_t orig = 0, gi = 0;
+    int32_t orig = 0, gi = 0, nid = 0;
     double px = 0.0, py = 0.0, h = 0.0;
     if (live) {
         orig = __ldg(A.perm + cell);
@@ -910,14 +914,16 @@ __global__ void __launch_bounds__(128, TM_OUT_MINB) k_output_t(CellArgs A, RingB
         py = __ldg(A.ys + cell);
         h = __ldg(A.hs + cell);
         gi = __ldg(A.gids + cell);
+        nid = A.nbr_by_gid ? gi : orig;
+        if (nid < 0 || (int64_t)nid >= A.nbr_keys) nid = -1;
     }
-    if (live && A.nbr) {
+    if (live && A.nbr && nid >= 0) {
         int c = 0;
         for (int i = 0; i < nv; i++) {
             const int a = RL(i);
-            if (a >= 0) A.nbr[(int64_t)orig * TM_NBR + c++] = __ldg(A.perm + a);
+            if (a >= 0) A.nbr[(int64_t)nid * TM_NBR + c++] = A.nbr_by_gid ? __ldg(A.gids + a) : __ldg(A.perm + a);
         }
-        A.nbr_cnt[orig] = (uint8_t)c;
+        A.nbr_cnt[nid] = (uint8_t)c;
     }
     int t_own = 0, ell = 0;
     unsigned keptmask = 0;

@@ -60,10 +60,12 @@ __device__ __forceinline__ int leaf_coord(double x, double x0, double is, int nb
 struct CellArgs {
     const double *xs, *ys, *hs;
     const int32_t *perm, *gids;
-    const int32_t *inv_perm;   // caller index -> sorted slot (this binning)
+    const int32_t *inv_perm;   // point id -> sorted slot (this binning; stale for absent gids)
     int32_t *nbr;              // warm start: per caller index, the cell's neighbours (caller ids) of the
     uint8_t *nbr_cnt;          //   last cell launch on the same point set; nbr_cnt[i] entries (<= TM_NBR)
     int32_t warm;              // 1: read nbr/nbr_cnt before the search (they are written back either way)
+    int32_t nbr_by_gid;        // ids are gids (strips), else caller indices
+    int64_t nbr_keys;          // size of the id space (n_total with gids, else n_local)
     const uint8_t *rlev;
     const int32_t *leaf_off, *leaf_start;
     BinGeom bg;
@@ -107,10 +109,11 @@ struct tm_ctx {
     bool have_bins = false;
     int64_t n_local = 0, n_owned = 0, cap_points = 0, cap_bins = 0;
     double *xs = nullptr, *ys = nullptr, *hs = nullptr;
-    int32_t *perm = nullptr, *gids = nullptr, *key = nullptr, *rank = nullptr, *inv_perm = nullptr;
+    int32_t *perm = nullptr, *gids = nullptr, *key = nullptr, *rank = nullptr;
     // warm start of the cell search (previous iteration's neighbours, caller ids; single domain only)
     int32_t *nbr = nullptr;
     uint8_t *nbr_cnt = nullptr;
+    int32_t *inv_id = nullptr;  // point id -> slot of the last binning
     int64_t cap_nbr = 0, nbr_n = -1;
     bool have_gid = false;
     int32_t *bin_count = nullptr, *block_sums = nullptr;

@@ -1,0 +1,7 @@
+set -x
+TAG=${TAG:-run}
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; echo "smoke exit $?" >> gpurun_out/${TAG}_smoke.log
+timeout 2400 python -m pytest tests -m gpu -x -q > gpurun_out/${TAG}_gpu_tests.log 2>&1; echo "pytest exit $?" >> gpurun_out/${TAG}_gpu_tests.log
+timeout 600 python bench.py --steps 3 --warmup 3 > gpurun_out/${TAG}_bench.log 2>&1; echo "bench exit $?" >> gpurun_out/${TAG}_bench.log
+timeout 600 python bench.py --steps 2 --warmup 2 --strips --no-cpu-baseline > gpurun_out/${TAG}_bench_strips1.log 2>&1; echo "exit $?" >> gpurun_out/${TAG}_bench_strips1.log
+echo done
