@@ -331,3 +331,49 @@ def test_cfg5_full_size_sampled_windows(n):
         ot = {tuple(t) for t in ot_all[inner_g[ot_all].all(1)].tolist()}
         assert gt == ot, f"window {cx:.3f},{cy:.3f}: {len(ot - gt)} missing, {len(gt - ot)} extra"
         assert len(gt) > 1000
+
+
+def test_cell_vertex_capacity_error_is_loud():
+    """A cell with more vertices than the 32-lane retry pass can hold (a point ringed by 40
+    near-cocircular neighbours) must latch TM_E_CAPACITY (reported by tm_sync), not
+    return a wrong mesh silently (SURVEY §8(b) errors)."""
+    import torch
+    import paper_2309_13824_b200 as T
+    box = (0.0, 0.0, 1.0, 1.0)
+    rng = np.random.default_rng(12)
+    x, y = rng.random(2000), rng.random(2000)
+    keep = np.hypot(x - 0.5, y - 0.5) > 0.1
+    x, y = x[keep], y[keep]
+    m = 40
+    ang = 2 * np.pi * (np.arange(m) + rng.uniform(-0.05, 0.05, m)) / m
+    rad = 0.03 * (1 + rng.uniform(-1e-3, 1e-3, m))
+    x = np.concatenate([x, [0.5], 0.5 + rad * np.cos(ang)])
+    y = np.concatenate([y, [0.5], 0.5 + rad * np.sin(ang)])
+    ctx = T.Context(0)
+    ctx.tm_set_domain(box, torch.from_numpy(configs.box_phi(box, 64)).cuda(), None, None, len(x))
+    xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    bufs = T.IterBuffers.alloc(len(x))
+    ctx.tm_grid_bin(xd, yd)
+    ctx.tm_voronoi_delaunay(bufs.tri, bufs.n_tri)
+    with pytest.raises(T.TmError) as e:
+        ctx.tm_sync()
+    assert e.value.code == T.TM_E_CAPACITY
+
+
+def test_cocircular_input_is_reported_degenerate():
+    """Four exactly cocircular points (a square): the Delaunay triangulation is not unique
+    (P:43 assumes general position, reading L12).  The exact predicates meet a zero and the
+    library counts it in n_degenerate (tm_mesh_stats) -- parity is only promised when 0."""
+    import torch
+    import paper_2309_13824_b200 as T
+    box = (0.0, 0.0, 1.0, 1.0)
+    x = np.array([0.25, 0.75, 0.75, 0.25])
+    y = np.array([0.25, 0.25, 0.75, 0.75])
+    ctx = T.Context(0)
+    ctx.tm_set_domain(box, torch.from_numpy(configs.box_phi(box, 64)).cuda(), None, None, 4)
+    xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    bufs = T.IterBuffers.alloc(4)
+    ctx.tm_grid_bin(xd, yd)
+    ctx.tm_voronoi_delaunay(bufs.tri, bufs.n_tri)
+    st = ctx.tm_mesh_stats(xd, yd, bufs.tri, int(bufs.n_tri.item()))
+    assert st.n_degenerate > 0
