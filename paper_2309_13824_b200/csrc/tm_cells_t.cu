@@ -803,77 +803,106 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
 }
 
 
-// adaptive quadrature over a stored ring (ring order from the canonical vertex);
-// the same sub-triangles and sums, in the same order, as quad_centroid_t.  Sub-triangles
-// are taken QB at a time: their geometry and the four density corners of each are loaded
-// first, then summed in order -- the kernel is bound by the latency of those loads.
-__device__ __forceinline__ void quad_sub(const double2 a, const double2 b, int depth, int64_t path, double &At,
-                                         double &qx, double &qy) {
-    double Q[3][2] = {{0.0, 0.0}, {a.x, a.y}, {b.x, b.y}};
-    for (int lev = depth - 1; lev >= 0; lev--) {
-        double best = -1.0;
-        int eidx = 0;
+// one longest-edge bisection of sub-triangle Q (Fig. 14): child `bit`
+// (0: (a, m, c), 1: (m, b, c) with ab the longest edge, m its midpoint)
+__device__ __forceinline__ void quad_split(const double Q[3][2], int bit, double C[3][2]) {
+    double best = -1.0;
+    int eidx = 0;
 #pragma unroll
-        for (int q = 0; q < 3; q++) {
-            const int q1 = q == 2 ? 0 : q + 1;
-            const double ddx = csub(Q[q1][0], Q[q][0]), ddy = csub(Q[q1][1], Q[q][1]);
-            const double Lq = cadd(cmul(ddx, ddx), cmul(ddy, ddy));
-            if (Lq > best) { best = Lq; eidx = q; }
-        }
-        const int ia = eidx, ib = eidx == 2 ? 0 : eidx + 1, ic = ib == 2 ? 0 : ib + 1;
-        const double ax = Q[ia][0], ay = Q[ia][1], bx = Q[ib][0], by = Q[ib][1];
-        const double cx = Q[ic][0], cy = Q[ic][1];
-        const double mx = cmul(cadd(ax, bx), 0.5), my = cmul(cadd(ay, by), 0.5);
-        if ((path >> lev) & 1) {
-            Q[0][0] = mx; Q[0][1] = my; Q[1][0] = bx; Q[1][1] = by;
-        } else {
-            Q[0][0] = ax; Q[0][1] = ay; Q[1][0] = mx; Q[1][1] = my;
-        }
-        Q[2][0] = cx; Q[2][1] = cy;
+    for (int q = 0; q < 3; q++) {
+        const int q1 = q == 2 ? 0 : q + 1;
+        const double ddx = csub(Q[q1][0], Q[q][0]), ddy = csub(Q[q1][1], Q[q][1]);
+        const double Lq = cadd(cmul(ddx, ddx), cmul(ddy, ddy));
+        if (Lq > best) { best = Lq; eidx = q; }
     }
+    // edge (a, b) = (Q[e], Q[e+1]), c the third vertex; selects, not indexing (registers)
+    const double ax = eidx == 0 ? Q[0][0] : (eidx == 1 ? Q[1][0] : Q[2][0]);
+    const double ay = eidx == 0 ? Q[0][1] : (eidx == 1 ? Q[1][1] : Q[2][1]);
+    const double bx = eidx == 0 ? Q[1][0] : (eidx == 1 ? Q[2][0] : Q[0][0]);
+    const double by = eidx == 0 ? Q[1][1] : (eidx == 1 ? Q[2][1] : Q[0][1]);
+    const double cx = eidx == 0 ? Q[2][0] : (eidx == 1 ? Q[0][0] : Q[1][0]);
+    const double cy = eidx == 0 ? Q[2][1] : (eidx == 1 ? Q[0][1] : Q[1][1]);
+    const double mx = cmul(cadd(ax, bx), 0.5), my = cmul(cadd(ay, by), 0.5);
+    if (bit) {
+        C[0][0] = mx; C[0][1] = my; C[1][0] = bx; C[1][1] = by;
+    } else {
+        C[0][0] = ax; C[0][1] = ay; C[1][0] = mx; C[1][1] = my;
+    }
+    C[2][0] = cx; C[2][1] = cy;
+}
+
+// sub-triangle of fan triangle (0, a, b) reached by `levels` bisections along `path`
+// (bit lev taken at level lev, from the top)
+__device__ __forceinline__ void quad_descend(const double2 a, const double2 b, int levels, int64_t path,
+                                             double Q[3][2]) {
+    Q[0][0] = 0.0; Q[0][1] = 0.0; Q[1][0] = a.x; Q[1][1] = a.y; Q[2][0] = b.x; Q[2][1] = b.y;
+    for (int lev = levels - 1; lev >= 0; lev--) {
+        double C[3][2];
+        quad_split(Q, (int)((path >> lev) & 1), C);
+#pragma unroll
+        for (int q = 0; q < 3; q++) { Q[q][0] = C[q][0]; Q[q][1] = C[q][1]; }
+    }
+}
+
+// area and centroid of a sub-triangle, and its density corners
+__device__ __forceinline__ void quad_leaf(const double Q[3][2], const CellArgs &A, double px, double py, double &At,
+                                          double &qx, double &qy, double &ss, double &tt, double f[4]) {
     const double cr = csub(cmul(csub(Q[1][0], Q[0][0]), csub(Q[2][1], Q[0][1])),
                            cmul(csub(Q[1][1], Q[0][1]), csub(Q[2][0], Q[0][0])));
     At = cmul(0.5, cr);
     qx = div3(cadd(cadd(Q[0][0], Q[1][0]), Q[2][0]));
     qy = div3(cadd(cadd(Q[0][1], Q[1][1]), Q[2][1]));
+    int gi, gj;
+    grid_cell(A.grid, cadd(px, qx), cadd(py, qy), gi, gj, ss, tt);
+    const double *r0 = A.rho + (int64_t)gj * A.grid.nx + gi, *r1 = r0 + A.grid.nx;
+    f[0] = __ldg(r0);
+    f[1] = __ldg(r0 + 1);
+    f[2] = __ldg(r1);
+    f[3] = __ldg(r1 + 1);
 }
 
-#ifndef TM_QB
-#define TM_QB 2  // sub-triangles whose density loads are in flight together
-#endif
-
+// adaptive quadrature over a stored ring (ring order from the canonical vertex); the
+// same sub-triangles and sums, in the same order, as quad_centroid_t.  Sub-triangles
+// are taken two at a time with their density loads in flight together (the kernel is
+// bound by the latency of those loads); below level 1 the two are siblings, so the
+// descent to their parent is shared.
 __device__ void quad_centroid_g(const double2 *rv, int64_t ns, int nv, double px, double py, double area, double h,
                                 double dprev, const CellArgs &A, double &cx, double &cy, unsigned long long &nq) {
     double eps = dprev >= 0.0 ? dprev / h : A.fac_pt;
     if (eps < A.fac_end) eps = A.fac_end;
     const double E = sqrt(area) * eps;
-    const Grid &g = A.grid;
     double prevx = 0.0, prevy = 0.0;
     for (int L = 1; L <= A.quad_max; L++) {
         const int depth = L - 1;
         const int64_t ntot = (int64_t)nv << depth;
         double sw = 0.0, swx = 0.0, swy = 0.0;
-        for (int64_t t0 = 0; t0 < ntot; t0 += TM_QB) {
-            double At[TM_QB], qx[TM_QB], qy[TM_QB], ss[TM_QB], tt[TM_QB];
-            double f00[TM_QB], f10[TM_QB], f01[TM_QB], f11[TM_QB];
+        for (int64_t t0 = 0; t0 < ntot; t0 += 2) {
+            double At[2], qx[2], qy[2], ss[2], tt[2], f[2][4];
+            if (depth == 0) {  // fan triangles t0, t0 + 1 (the last one again for odd nv)
 #pragma unroll
-            for (int u = 0; u < TM_QB; u++) {
-                const int64_t t = t0 + u < ntot ? t0 + u : ntot - 1;  // tail: recompute the last one
-                const int f = (int)(t >> depth);
-                quad_sub(rv[(int64_t)f * ns], rv[(int64_t)(f + 1 == nv ? 0 : f + 1) * ns], depth, t & (((int64_t)1 << depth) - 1), At[u], qx[u],
-                         qy[u]);
-                int gi, gj;
-                grid_cell(g, cadd(px, qx[u]), cadd(py, qy[u]), gi, gj, ss[u], tt[u]);
-                const double *r0 = A.rho + (int64_t)gj * g.nx + gi, *r1 = r0 + g.nx;
-                f00[u] = __ldg(r0);
-                f10[u] = __ldg(r0 + 1);
-                f01[u] = __ldg(r1);
-                f11[u] = __ldg(r1 + 1);
+                for (int u = 0; u < 2; u++) {
+                    const int fi = (int)(t0 + u < ntot ? t0 + u : ntot - 1);
+                    double Q[3][2];
+                    quad_descend(rv[(int64_t)fi * ns], rv[(int64_t)(fi + 1 == nv ? 0 : fi + 1) * ns], 0, 0, Q);
+                    quad_leaf(Q, A, px, py, At[u], qx[u], qy[u], ss[u], tt[u], f[u]);
+                }
+            } else {           // siblings t0, t0 + 1 of parent t0 / 2
+                const int64_t par = t0 >> 1;
+                const int fi = (int)(par >> (depth - 1));
+                double Q[3][2];
+                quad_descend(rv[(int64_t)fi * ns], rv[(int64_t)(fi + 1 == nv ? 0 : fi + 1) * ns], depth - 1,
+                             par & (((int64_t)1 << (depth - 1)) - 1), Q);
+#pragma unroll
+                for (int u = 0; u < 2; u++) {
+                    double C[3][2];
+                    quad_split(Q, u, C);
+                    quad_leaf(C, A, px, py, At[u], qx[u], qy[u], ss[u], tt[u], f[u]);
+                }
             }
 #pragma unroll
-            for (int u = 0; u < TM_QB; u++) {
+            for (int u = 0; u < 2; u++) {
                 if (t0 + u >= ntot) break;
-                const double rho = clerp(clerp(f00[u], f10[u], ss[u]), clerp(f01[u], f11[u], ss[u]), tt[u]);
+                const double rho = clerp(clerp(f[u][0], f[u][1], ss[u]), clerp(f[u][2], f[u][3], ss[u]), tt[u]);
                 const double wgt = At[u] * rho;
                 sw += wgt;
                 swx += wgt * qx[u];
