@@ -481,15 +481,18 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
         wn = (A.warm && A.nbr_cnt && nid >= 0) ? min((int)A.nbr_cnt[nid], TM_NBR) : 0;
         ph = fail ? 2 : (wn > 0 ? -1 : 0);
         rr = 0;
+        if (ph == -1) { cvx = t; cend = tend; t = tend = 0; }  // home range parked until the warm list ends
+        if (ph == 2) t = tend;
     }
     // ---- flat candidate loop: one candidate per thread per trip, the warp
     // re-converges every trip (a per-thread nested loop lets lanes drift apart)
     // the iterator: advance to this thread's next candidate slot (-1 when done)
     auto next_cand = [&]() -> int {
         int j = -1;
+        if (t < tend) return t++;  // common case first: the next point of the current leaf
         while (ph < 2) {
             if (ph < 0) {
-                if (wi >= wn) { ph = 0; continue; }
+                if (wi >= wn) { ph = 0; t = cvx; tend = cend; cvx = 0; cend = -1; continue; }
                 const int id = A.nbr[(int64_t)nid * TM_NBR + wi++];
                 if (id < 0 || (int64_t)id >= A.nbr_keys) continue;
                 const int js = A.inv_perm[id];  // stale for a gid not binned here: checked
@@ -565,6 +568,7 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
         return j;
     };
     unsigned trips = 0;
+    double lim2 = 4.0 * (double)R2 * MARG;  // (2 R_max)^2 with margin, updated with R_max
     // ---- (C) flat candidate loop
     int j = next_cand();
     double xj = 0.0, yj = 0.0;
@@ -583,14 +587,16 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
         if (cj >= 0) {
             sc.n_cand++;
             const double dx = csub(cxj, px), dy = csub(cyj, py);
-            if (cj == (int)cell) {
-            } else if (dx == 0.0 && dy == 0.0) {
-                atomicAdd(&A.st->n_duplicate, 1ull);
-            } else if (dx * dx + dy * dy < 4.0 * (double)R2 * MARG) {
-                const unsigned long long c0 = cs.clips;
-                fail = clip_t(P, cj, bisector(dx, dy), cgm, A, cs);
-                if (fail) { ph = 2; j = -1; }
-                else if (cs.clips != c0) R2 = poly_R2(P);
+            const double d2 = dx * dx + dy * dy;
+            if (d2 < lim2 && cj != (int)cell) {
+                if (dx == 0.0 && dy == 0.0) {
+                    atomicAdd(&A.st->n_duplicate, 1ull);
+                } else {
+                    const unsigned long long c0 = cs.clips;
+                    fail = clip_t(P, cj, bisector(dx, dy), cgm, A, cs);
+                    if (fail) { ph = 2; j = -1; t = tend; }
+                    else if (cs.clips != c0) { R2 = poly_R2(P); lim2 = 4.0 * (double)R2 * MARG; }
+                }
             }
         }
     }
