@@ -130,36 +130,46 @@ __global__ void k_domain_terms(Grid g, const double *phi, const double *mu, doub
     m[k] = mm;
 }
 
-__global__ void k_domain_sums(int64_t n, const double *__restrict__ w, const double *__restrict__ m, double *out3) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// S0 sums in row-major order, one adder (the oracle's order, so the same bits): the block's
+// other warps stage the next tile of terms in shared memory while thread 0 adds the current
+// one -- the adds then wait on shared-memory loads, not on DRAM round trips
+constexpr int DS_TILE = 1024;
+__global__ void __launch_bounds__(256) k_domain_sums(int64_t n, const double *__restrict__ w,
+                                                     const double *__restrict__ m, double *out3) {
+    __shared__ double tw[2][DS_TILE], tm[2][DS_TILE];
+    const int tid = threadIdx.x;
+    auto stage = [&](int buf, int64_t base, int t0, int stride) {
+        for (int i = t0; i < DS_TILE; i += stride) {
+            const int64_t k = base + i;
+            tw[buf][i] = k < n ? w[k] : -1.0;  // padding: w < 0 is skipped like an outside cell
+            tm[buf][i] = k < n ? m[k] : 0.0;
+        }
+    };
+    stage(0, 0, tid, blockDim.x);
+    __syncthreads();
     double sum_w = 0.0, sum_mu = 0.0, cnt = 0.0;
-    constexpr int U = 16;  // loads of a group issued together; the adds stay in order
-    int64_t k = 0;
-    for (; k + U <= n; k += U) {
-        double wk[U], mk[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            wk[u] = __ldg(w + k + u);
-            mk[u] = __ldg(m + k + u);
+    const int64_t ntiles = (n + DS_TILE - 1) / DS_TILE;
+    for (int64_t t = 0; t < ntiles; t++) {
+        const int b = (int)(t & 1);
+        if (tid >= 32) {
+            if (t + 1 < ntiles) stage(b ^ 1, (t + 1) * DS_TILE, tid - 32, blockDim.x - 32);
+        } else if (tid == 0) {
+#pragma unroll 16
+            for (int i = 0; i < DS_TILE; i++) {
+                const double wk = tw[b][i];
+                if (wk < 0.0) continue;
+                sum_w = cadd(sum_w, wk);
+                sum_mu = cadd(sum_mu, tm[b][i]);
+                cnt += 1.0;
+            }
         }
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            if (wk[u] < 0.0) continue;
-            sum_w = cadd(sum_w, wk[u]);
-            sum_mu = cadd(sum_mu, mk[u]);
-            cnt += 1.0;
-        }
+        __syncthreads();
     }
-    for (; k < n; k++) {
-        const double wk = w[k];
-        if (wk < 0.0) continue;
-        sum_w = cadd(sum_w, wk);
-        sum_mu = cadd(sum_mu, m[k]);
-        cnt += 1.0;
+    if (tid == 0) {
+        out3[0] = sum_w;
+        out3[1] = sum_mu;
+        out3[2] = cnt;
     }
-    out3[0] = sum_w;
-    out3[1] = sum_mu;
-    out3[2] = cnt;
 }
 
 // Lipschitz constant of the bilinear interpolant mu~ (continuous, bilinear per cell):
@@ -211,7 +221,7 @@ extern "C" tm_status tm_set_domain(tm_ctx *ctx, const tm_fields *f, int64_t n_to
     TM_CUDA_TRY(ctx, cudaMalloc(&terms, 2 * ncell * sizeof(double)));
     k_domain_terms<<<(unsigned)((ncell + 255) / 256), 256, 0, ctx->stream>>>(g, ctx->phi, has_mu ? ctx->mu : nullptr,
                                                                              terms, terms + ncell);
-    k_domain_sums<<<1, 1, 0, ctx->stream>>>(ncell, terms, terms + ncell, d3);
+    k_domain_sums<<<1, 256, 0, ctx->stream>>>(ncell, terms, terms + ncell, d3);
     tm_status s = tm_internal_check_launch(ctx, "k_domain_sums");
     if (s != TM_OK) { cudaFree(d3); cudaFree(terms); return s; }
     double h3[3];

@@ -377,3 +377,20 @@ def test_cocircular_input_is_reported_degenerate():
     ctx.tm_voronoi_delaunay(bufs.tri, bufs.n_tri)
     st = ctx.tm_mesh_stats(xd, yd, bufs.tri, int(bufs.n_tri.item()))
     assert st.n_degenerate > 0
+
+
+@pytest.mark.parametrize("k", [1, 3, 5])
+def test_domain_constants_bitwise(k, cfg_cache):
+    """S0 (reading L7): c and h_avg come from a sequential row-major sum over the grid
+    cells with phi~(centre) < 0 -- the same order as the oracle's definition, so the
+    same bits (cfg5: 2048^2 cells, several staging tiles and a ragged last one)."""
+    import torch
+    import paper_2309_13824_b200 as T
+    c = cfg_cache(k)
+    dev = torch.device("cuda", 0)
+    to = lambda a: None if a is None else torch.from_numpy(a).to(dev)
+    ctx = T.Context(0)
+    gc, gh = ctx.tm_set_domain(c.box, to(c.phi), to(c.mu), to(c.rho), c.n)
+    ctx.close()
+    oc, oh = O.domain(O.FieldSet.from_config(c), c.n)
+    assert gc == oc and gh == oh, (gc, oc, gh, oh)
