@@ -38,7 +38,7 @@ using namespace tmg;
 #define TM_TMINB 5
 #endif
 #ifndef TM_OUT_MINB
-#define TM_OUT_MINB 1  // min resident 128-thread blocks per SM for k_output_t (register cap)
+#define TM_OUT_MINB 6  // min resident 128-thread blocks per SM for k_output_t (80-register cap: r3h A/B)
 #endif
 #ifndef TM_CVD_SPLIT
 #define TM_CVD_SPLIT 1  // 1: CVD centroid, quadrature, treatment in a second kernel over stored rings;
