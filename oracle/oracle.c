@@ -695,14 +695,14 @@ static line2 line_of(const cellctx *C, int32_t code) {
     return L;
 }
 
-/* Cramer intersection of two lines, relative coordinates, canonical form
- * (DESIGN.md §3): inv = fl(1/det), x = fl(num_x * inv), y = fl(num_y * inv).
- * Exactly symmetric in (A, B): det, inv and both numerators change sign. */
+/* Cramer intersection of two lines, relative coordinates, in the form SURVEY §8.0
+ * "Canonical wall vertices" writes down: det = n_a.x n_b.y - n_a.y n_b.x,
+ * x' = (r_a n_b.y - n_a.y r_b)/det, y' = (n_a.x r_b - r_a n_b.x)/det (correctly rounded
+ * divisions).  Exactly symmetric in (A, B): det and both numerators change sign. */
 static void cramer(line2 A, line2 B, double *x, double *y) {
     double det = A.nx * B.ny - A.ny * B.nx;
-    double inv = 1.0 / det;
-    *x = (A.r * B.ny - A.ny * B.r) * inv;
-    *y = (A.nx * B.r - A.r * B.nx) * inv;
+    *x = (A.r * B.ny - A.ny * B.r) / det;
+    *y = (A.nx * B.r - A.r * B.nx) / det;
 }
 
 typedef struct { int32_t la, lb; double x, y; } cvert;
