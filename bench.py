@@ -10,28 +10,43 @@ iterations.  One STEP = the whole schedule from the config's initial points
 Timing: W untimed warm-up steps, then K timed steps bracketed by a barrier +
 cuda.synchronize on both sides, CUDA events on the library's stream, max over
 ranks; L2 flushed (256 MiB write) before every step; SM clocks sampled with
-nvidia-smi during the timed region.  `e2e` repeats the measurement through
-the public API with pinned HOST buffers: H2D of the step's input points and
-D2H of the result (final points + triangle count) inside the timed region.
+nvidia-smi during the timed region.  Every iteration is bracketed by events too:
+the per-iteration time by mode is T_meas of SURVEY §8(d)'s per-iteration
+roofline (T_roof from the kernel's own work counters, an untimed counting pass).
 
---impl reference: the CPU oracle (oracle/, plain C, 1 thread) on a bounded
-sample of the same workload (one iteration per step, alternating DistMesh and
-CVD), printed as a JSON line with "impl": "reference".
+`e2e` repeats the measurement through the public API with pinned HOST buffers:
+H2D of the step's input points, then D2H of the result -- the final points, the
+triangle count and the final triangle list -- inside the timed region.
+
+cfg5 leg (`cfg5`): the uniform scaling workload, 1.6e7 and
+6.4e7 jittered points, 20 CVD iterations, ms/iteration and pts*it/s, so the
+driver's 1..8-GPU runs carry the north_star scaling config as well.
+
+cpu_baseline: the oracle (oracle/, plain C, as it stands) in a subprocess pinned
+to one core (`taskset -c 0`), the first 3 iterations of each phase of the cfg3
+schedule (3 DistMesh from the initial points, 3 CVD from the GPU's state after
+the 30 DistMesh iterations), ~20 s.
+
+--impl reference: the oracle on a bounded sample of the same workload (one
+iteration per step, alternating DistMesh and CVD), pinned to one core, printed
+as a JSON line with "impl": "reference".
 
 N > 1 (torchrun): the same mesh is split into N x-strips (x-quantiles of the
 initial points), one per GPU; every iteration exchanges a ghost halo and the
 migrating points with the neighbour strips over NCCL and all-reduces the two
 DistMesh edge sums -> "scaling": "strong" (total work fixed).
-`--strips` runs that path at N = 1 as well (smoke test of the code path).
+`--strips` runs that path at N = 1 as well.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import shutil
 import statistics
 import subprocess
 import sys
+import tempfile
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -43,6 +58,9 @@ WORKLOAD = "cfg3: annulus 0.3<|x|<1, adaptive h=min(0.002+0.3|sdf|,0.02), rho=h^
            "hybrid 30 DistMesh + 30 CVD iterations per step"
 METRIC = "points*iterations/s (Delaunay + CVD/DistMesh update), 10^6 pts"
 UNIT = "pts*it/s"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+# SURVEY §8(d) compulsory HBM bytes per point and iteration, by stage
+B_S1, B_FUSED, B_DM = 56.0, 69.0, 64.0
 
 
 def dist_env():
@@ -50,6 +68,18 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def host_info():
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return model, os.cpu_count()
 
 
 class ClockSampler:
@@ -105,59 +135,267 @@ def flush_l2(buf):
     buf.add_(1.0)  # 256 MiB read+write > 126 MB L2
 
 
+# ---------------------------------------------------------------- oracle timing (CPU)
+def _pin_cmd():
+    return ["taskset", "-c", "0"] if shutil.which("taskset") else []
+
+
+def cpu_worker(path):
+    """Child process: oracle iterations listed in the npz (pinned by the parent to core 0)."""
+    if not _pin_cmd() and hasattr(os, "sched_setaffinity"):
+        os.sched_setaffinity(0, {0})
+    import oracle as O
+    from inputs import configs
+    z = np.load(path)
+    c = configs.load(int(z["cfg"]))
+    fs = O.FieldSet.from_config(c)
+    out = []
+    for ph in ("dm", "cvd"):
+        x, y = z[f"{ph}_x"], z[f"{ph}_y"]
+        dp = z[f"{ph}_dp"] if z[f"{ph}_has_dp"] else None
+        for _ in range(int(z[f"{ph}_iters"])):
+            t0 = time.perf_counter()
+            r = O.iteration(fs, x, y, ph, d_prev=dp)
+            out.append({"mode": ph, "s": time.perf_counter() - t0, "n": c.n})
+            x, y, dp = r.x, r.y, r.d_prev
+    print(json.dumps(out), flush=True)
+
+
+def run_oracle_pinned(states: dict, cfg: int = 3):
+    """Times the oracle in a child process on core 0; states: {mode: (x, y, d_prev|None, iters)}."""
+    with tempfile.TemporaryDirectory() as td:
+        f = os.path.join(td, "states.npz")
+        kw = {"cfg": cfg}
+        for ph in ("dm", "cvd"):
+            x, y, dp, it = states.get(ph, (np.zeros(1), np.zeros(1), None, 0))
+            kw.update({f"{ph}_x": x, f"{ph}_y": y, f"{ph}_dp": dp if dp is not None else np.zeros(1),
+                       f"{ph}_has_dp": dp is not None, f"{ph}_iters": it})
+        np.savez(f, **kw)
+        cmd = _pin_cmd() + [sys.executable, os.path.abspath(__file__), "--cpu-worker", f]
+        r = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT)
+        if r.returncode != 0:
+            raise RuntimeError(f"oracle worker failed: {r.stderr[-2000:]}")
+        return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def cpu_desc(sample):
+    model, ncpu = host_info()
+    pin = "taskset -c 0" if _pin_cmd() else "sched_setaffinity({0})"
+    return {"cores": 1, "cores_available": ncpu, "cpu_model": model, "pinning": pin,
+            "threads_note": f"1 of {ncpu} cores ({model}), single-threaded plain C oracle", "sample": sample}
+
+
 # ---------------------------------------------------------------- reference arm
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    import oracle as O
     from inputs import configs
     c = configs.load(3)
-    fs = O.FieldSet.from_config(c)
-    modes = ["dm", "cvd"]
-    x, y, dp = c.x, c.y, None
-    times = []
     total = args.warmup + args.steps
-    for s in range(total):
-        mode = modes[s % 2]
-        t0 = time.perf_counter()
-        r = O.iteration(fs, x, y, mode, d_prev=dp)
-        dt = time.perf_counter() - t0
-        if s >= args.warmup:
-            times.append(dt)
-        x, y, dp = r.x, r.y, r.d_prev
+    modes = ["dm", "cvd"]
+    # one oracle iteration per step, alternating phases, chained from the config's points
+    states = {"dm": (c.x, c.y, None, (total + 1) // 2), "cvd": (c.x, c.y, None, total // 2)}
+    rec = run_oracle_pinned(states)
+    # interleave in step order dm, cvd, dm, ... and drop the warm-up ones
+    by = {m: [r for r in rec if r["mode"] == m] for m in modes}
+    seq = [by[modes[s % 2]][s // 2] for s in range(total)]
+    times = [r["s"] for r in seq[args.warmup:]]
     T = sum(times)
     value = c.n * len(times) / T
+    d = cpu_desc(f"{len(times)} timed oracle iterations of cfg3 (1e6 points), one per step, alternating "
+                 f"DistMesh/CVD from the config's points (after {args.warmup} warm-up ones)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / len(times),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "sample": "one oracle iteration per step (alternating DistMesh/CVD) "
                                                     "from the cfg3 initial points"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"{len(times)} single-threaded oracle iterations of cfg3 (1e6 points)"},
+        "cpu_baseline": dict(value=value, unit=UNIT, kind="oracle", **d),
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline_sample(pairs=2):
-    """Oracle (as it stands, 1 thread) on a bounded sample: `pairs` x (one DistMesh
-    then one CVD iteration) of cfg3 from its initial points (~10 s)."""
-    import oracle as O
+# ---------------------------------------------------------------- roofline
+def dp_peak():
+    """fp64 ALU peak (DP thread-instructions/s): the measured DFMA microbenchmark
+    (tools/fp64_peak.cu, profiles/fp64_peak.json), else 148 SMs x 64 lanes x clock."""
+    meas = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    if os.path.exists(meas):
+        try:
+            m = json.load(open(meas))
+            return float(m["dp_inst_per_s"]), "measured DFMA microbenchmark (tools/fp64_peak.cu, profiles/fp64_peak.json)"
+        except Exception:
+            pass
+    mhz = 1965.0
+    try:
+        mhz = float(json.load(open(PEAKS)).get("sm_max_mhz", mhz))
+    except Exception:
+        pass
+    return 148 * 64 * mhz * 1e6, f"derived 148 SMs x 64 FP64 lanes x {mhz:.0f} MHz"
+
+
+def hbm_peak():
+    try:
+        return float(json.load(open(PEAKS))["hbm_gbs"]) * 1e9, "MEASURED_PEAKS.json hbm_gbs (copy)"
+    except Exception:
+        return 6.56e12, "SURVEY §8(d) 6560 GB/s"
+
+
+def f_alg_cells(w, mode):
+    """SURVEY §8(d) DP instructions of the fused cell kernel, summed over cells:
+    4 n_cert + 5 deg V + 50 deg + 40 T_own + [6V+15 | 30 Q] + 20 (CVD update + projection test)."""
+    n = max(w.n_cells, 1)
+    f = 4 * w.n_cert + 5 * w.deg * (w.verts / n) + 50 * w.deg + 40 * w.t_own
+    if mode == "cvd":
+        f += 30 * w.quad_tris + 20 * w.n_cells  # quad_tris = V for uniform rho (the fan), Q otherwise
+    return f
+
+
+def count_work(T, c, ctx_device, schedule, dev):
+    """Untimed TM_F_COUNT_WORK pass over the schedule (its own context): per iteration the
+    oracle-pinned work counters of every cell (n_cert, deg, V, T_own, Q, E)."""
+    import torch
+    p = T.default_params()
+    p.flags |= T.TM_F_COUNT_WORK
+    cc = T.Context(ctx_device, params=p)
+    to = lambda a: None if a is None else torch.from_numpy(a).to(dev)
+    cc.tm_set_domain(c.box, to(c.phi), to(c.mu), to(c.rho), c.n)
+    bufs = T.IterBuffers.alloc(c.n, p.adj_stride, device=dev)
+    xs, ys = to(c.x), to(c.y)
+    xo, yo, do = torch.empty_like(xs), torch.empty_like(xs), torch.empty_like(xs)
+    dc = None
+    per = []
+    for mode in schedule:
+        cc.tm_grid_bin(xs, ys)
+        if mode == "cvd":
+            cc.tm_voronoi_delaunay(bufs.tri, bufs.n_tri, None, None, dc, xo, yo, do, bufs.status)
+        else:
+            cc.tm_voronoi_delaunay(bufs.tri, bufs.n_tri, bufs.adj, bufs.deg)
+        w = cc.tm_work_counts()
+        per.append((mode, w))
+        if mode == "dm":
+            cc.tm_distmesh_sums(bufs.adj, bufs.deg, bufs.sums2)
+            cc.tm_distmesh_step(bufs.adj, bufs.deg, bufs.sums2, None, dc, xo, yo, do, bufs.status)
+        xs, ys, dc = xo.clone(), yo.clone(), do.clone()
+    cc.tm_sync()
+    cc.close()
+    return per
+
+
+def iteration_roof(mode, w, n, P, BW):
+    """T_roof of one iteration: sum over stages of max(bytes/BW, DP/P_DP)."""
+    fc = f_alg_cells(w, mode)
+    t = n * B_S1 / BW + max(n * B_FUSED / BW, fc / P)
+    if mode == "dm":
+        t += max(n * B_DM / BW, 45.0 * w.ell / P)
+    return t, fc
+
+
+def roofline(per, cells_ms, it_ms):
+    """Dominant kernel (k_cells_t, the fused S2-S5 launch): algorithmic DP instructions per
+    launch / mean launch time (CUDA events on the launching stream).  Plus the per-iteration
+    T_roof / T_meas of SURVEY §8(d) by iteration type."""
+    P, how = dp_peak()
+    BW, bw_how = hbm_peak()
+    n = per[0][1].n_cells
+    by = {"dm": [], "cvd": []}
+    for mode, w in per:
+        by[mode].append(iteration_roof(mode, w, n, P, BW))
+    tot_f = sum(f for m in by for _, f in by[m])
+    nl = sum(len(v) for v in by.values())
+    tot_t = sum(sum(v) for v in cells_ms.values()) / max(1, sum(len(v) for v in cells_ms.values()))
+    achieved = (tot_f / nl) / (tot_t / 1e3)
+    traffic = None  # DRAM bytes per launch of the cell kernel from the committed ncu capture
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "kcells_traffic.json")))
+        nd = len(by["dm"])
+        traffic = (nd * tj["dm_bytes"] + len(by["cvd"]) * tj["cvd_bytes"]) / nl
+    except Exception:
+        pass
+    per_it = {}
+    for m in ("dm", "cvd"):
+        if not by[m] or not it_ms[m]:
+            continue
+        troof = statistics.mean(t for t, _ in by[m])
+        tmeas = statistics.mean(it_ms[m]) / 1e3
+        per_it[m] = {"T_roof_us": troof * 1e6, "T_meas_us": tmeas * 1e6, "frac": troof / tmeas,
+                     "alg_dp_inst_cells": statistics.mean(f for _, f in by[m]),
+                     "cells_ms": statistics.mean(cells_ms[m]) if cells_ms[m] else None}
+    wsum = {m: [0] * 12 for m in ("dm", "cvd")}
+    for mode, w in per:
+        wsum[mode] = [a + b for a, b in zip(wsum[mode], [getattr(w, k) for k, _ in w._fields_])]
+    names = [k for k, _ in per[0][1]._fields_]
+    sched_roof = sum(t for m in by for t, _ in by[m])
+    sched_meas = sum(sum(v) for v in it_ms.values()) / 1e3 / max(1, sum(len(v) for v in it_ms.values())) * nl
+    return {"bound": "alu", "achieved": achieved / 1e12, "peak": P / 1e12, "unit": "T DP-inst/s",
+            "frac": achieved / P, "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write)",
+            "kernel": "k_cells_t (S2+S3 cells/Delaunay, S4a/S5 in k_output_t for CVD)",
+            "algorithmic_dp_inst_per_launch": tot_f / nl, "peak_source": how, "hbm_peak_source": bw_how,
+            "per_iteration": per_it,
+            "schedule_T_roof_over_T_meas": sched_roof / sched_meas if sched_meas else None,
+            "work_per_cell_by_mode": {m: {k: round(v / max(1, wsum[m][0]), 3) for k, v in zip(names, wsum[m])}
+                                      for m in wsum if wsum[m][0]}}
+
+
+# ---------------------------------------------------------------- cfg5 leg
+def run_cfg5(T, dev, stream, n, iters=20, count=True):
+    """North-star scaling workload at N=1: jittered uniform square, n points, `iters` CVD
+    iterations; one untimed pass, then one timed pass (events per iteration)."""
+    import torch
     from inputs import configs
-    c = configs.load(3)
-    fs = O.FieldSet.from_config(c)
-    x, y, dp = c.x, c.y, None
-    t0 = time.perf_counter()
-    for _ in range(pairs):
-        r = O.iteration(fs, x, y, "dm", d_prev=dp)
-        r = O.iteration(fs, r.x, r.y, "cvd", d_prev=r.d_prev)
-        x, y, dp = r.x, r.y, r.d_prev
-    dt = time.perf_counter() - t0
-    return {"value": 2 * pairs * c.n / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{pairs} x (1 DistMesh + 1 CVD) oracle iterations of cfg3 (1e6 points), single thread",
-            "seconds": dt}
+    c = configs.config5(n=n, iters=iters)
+    ctx = T.Context(dev.index or 0, stream=stream)
+    ctx.tm_set_domain(c.box, torch.from_numpy(c.phi).to(dev), None, None, c.n)
+    x0, y0 = torch.from_numpy(c.x).to(dev), torch.from_numpy(c.y).to(dev)
+    del c
+    bufs = T.IterBuffers.alloc(n, 16, device=dev)
+    X = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(2)]
+    Y = [torch.empty_like(X[0]) for _ in range(2)]
+    D = [torch.empty_like(X[0]) for _ in range(2)]
+
+    def one(ev=None):
+        xc, yc, dc = x0, y0, None
+        for it in range(iters):
+            if ev is not None:
+                ev[it].record(stream)
+            T.iterate(ctx, xc, yc, dc, "cvd", bufs, X[it % 2], Y[it % 2], D[it % 2])
+            xc, yc, dc = X[it % 2], Y[it % 2], D[it % 2]
+        if ev is not None:
+            ev[iters].record(stream)
+        return xc, yc, dc
+    one()
+    ctx.tm_sync()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(iters + 1)]
+    torch.cuda.synchronize(dev)
+    xl, yl, dl = one(ev)
+    ev[-1].synchronize()
+    its = [ev[k].elapsed_time(ev[k + 1]) for k in range(iters)]
+    ctx.tm_sync()
+    tot = sum(its) / 1e3
+    out = {"n_points": n, "iterations": iters, "ms_per_iteration": statistics.mean(its),
+           "value": n * iters / tot, "unit": UNIT}
+    if count:
+        p = T.default_params()
+        p.flags |= T.TM_F_COUNT_WORK
+        cc = T.Context(dev.index or 0, stream=stream, params=p)
+        phi = torch.from_numpy(configs.box_phi((0.0, 0.0, 1.0, 1.0), 1024)).to(dev)
+        cc.tm_set_domain((0.0, 0.0, 1.0, 1.0), phi, None, None, n)
+        # warm lists on the last state, then the counted iteration on it
+        for _ in range(2):
+            cc.tm_grid_bin(xl, yl)
+            cc.tm_voronoi_delaunay(bufs.tri, bufs.n_tri, None, None, dl, X[0], Y[0], D[0], bufs.status)
+        w = cc.tm_work_counts()
+        P, _ = dp_peak()
+        BW, _ = hbm_peak()
+        troof, fc = iteration_roof("cvd", w, n, P, BW)
+        out["T_roof_us"] = troof * 1e6
+        out["frac_per_iteration"] = troof / (its[-1] / 1e3)
+        out["note"] = "T_roof of the last iteration's state vs its measured time (per GPU)"
+        cc.close()
+    ctx.close()
+    return out
 
 
 # ---------------------------------------------------------------- our arm
@@ -169,11 +407,14 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--strips", action="store_true", help="use the x-strip path even at N=1 (smoke test)")
-    ap.add_argument("--n-opt", type=float, default=None, help="override tm_params.n_opt (tuning)")
-    ap.add_argument("--cells", default="thread", choices=["thread", "group"],
-                    help="cell kernel: one thread per cell (default) or 16-lane groups (A/B)")
+    ap.add_argument("--no-cfg5", action="store_true")
+    ap.add_argument("--cfg5-sizes", default="16000000,64000000")
+    ap.add_argument("--strips", action="store_true", help="use the x-strip path even at N=1")
+    ap.add_argument("--flags", type=int, default=0, help="extra tm_params.flags (A/B)")
+    ap.add_argument("--cpu-worker", default=None, help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.cpu_worker:
+        return cpu_worker(args.cpu_worker)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -196,10 +437,7 @@ def main():
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
     params = T.default_params()
-    if args.cells == "group":
-        params.flags |= T.TM_F_GROUP_CELLS
-    if args.n_opt:
-        params.n_opt = args.n_opt
+    params.flags |= args.flags
     ctx = T.Context(local, params=params, stream=stream)
     box = c.box
     phi = torch.from_numpy(c.phi).to(dev)
@@ -214,11 +452,16 @@ def main():
     D = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(2)]
     flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device=dev)
     ev_cells = []  # (start, end, mode) around every tm_voronoi_delaunay in the timed region
+    ev_iter = []   # (start, end, mode) around every whole iteration in the timed region
+    saved = {}
 
-    def one_step_single(xin, yin, record=False):
+    def one_step_single(xin, yin, record=False, save=False):
         xc, yc, dc = xin, yin, None
         for it, mode in enumerate(schedule):
             xo, yo, do = X[it % 2], Y[it % 2], D[it % 2]
+            if record:
+                ei = torch.cuda.Event(enable_timing=True)
+                ei.record(stream)
             ctx.tm_grid_bin(xc, yc)
             if record:
                 e0 = torch.cuda.Event(enable_timing=True)
@@ -234,12 +477,16 @@ def main():
             if mode == "dm":
                 ctx.tm_distmesh_sums(bufs.adj, bufs.deg, bufs.sums2)
                 ctx.tm_distmesh_step(bufs.adj, bufs.deg, bufs.sums2, None, dc, xo, yo, do, bufs.status)
+            if record:
+                ej = torch.cuda.Event(enable_timing=True)
+                ej.record(stream)
+                ev_iter.append((ei, ej, mode))
             xc, yc, dc = xo, yo, do
+            if save and it + 1 < len(schedule) and schedule[it + 1] != mode:  # phase change: keep the state
+                saved["cvd"] = (xc.cpu().numpy(), yc.cpu().numpy(), dc.cpu().numpy())
         return xc, yc
 
-    # N > 1 (or --strips): x-strip decomposition of the same mesh: each rank owns the
-    # points of one x-quantile strip; per iteration a ghost halo (W = 2 S_max) goes to both neighbours
-    # over NCCL, the DistMesh edge sums are all-reduced, and points that left the strip migrate.
+    # N > 1 (or --strips): x-strip decomposition of the same mesh
     strip_mode = world > 1 or args.strips
     if strip_mode:
         from paper_2309_13824_b200 import strips as S
@@ -248,9 +495,8 @@ def main():
         W = S.ghost_width(ctx.c, params.fac_voro_bound, float(c.mu.max()) if c.mu is not None else 1.0)
         comm = S.TorchP2P(rank, world, dev)
         backend = S.GpuStripBackend(ctx, params.adj_stride, keep_tri=False)
-        n_own0 = st_init.x.shape[0]
 
-    def one_step_strips(xin, yin, record=False):
+    def one_step_strips(xin, yin, record=False, save=False):
         st = S.RankState(rank, xin, yin, st_init.gid, None)
         for mode in schedule:
             st = S.strip_iteration(st, strips, backend, comm.exchange, W, mode, allreduce=comm.allreduce_sum)
@@ -264,10 +510,10 @@ def main():
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    # warm-up
-    for _ in range(args.warmup):
+    # warm-up (the first one keeps the state at the DistMesh -> CVD switch for the CPU sample)
+    for w_ in range(args.warmup):
         flush_l2(flush)
-        one_step(xs0, ys0)
+        one_step(xs0, ys0, save=(w_ == 0 and not strip_mode))
     ctx.tm_sync()
     # timed (device, inputs resident)
     sampler = ClockSampler(local)
@@ -293,12 +539,15 @@ def main():
     t_max = float(t.item())
     value = n * iters * args.steps / t_max  # all ranks together mesh the n points (strips at N > 1)
 
-    # per-launch duration of the dominant kernel (k_cells), CUDA events on the launching stream
     cells_ms = {"dm": [], "cvd": []}
     for e0, e1, mode in ev_cells:
         cells_ms[mode].append(e0.elapsed_time(e1))
+    it_ms = {"dm": [], "cvd": []}
+    for e0, e1, mode in ev_iter:
+        it_ms[mode].append(e0.elapsed_time(e1))
 
-    # e2e through the public API with pinned host buffers
+    # e2e through the public API with pinned host buffers: points in; points, triangle
+    # count and triangle list out
     e2e = None
     if not args.no_e2e:
         hx = xs0.cpu().pin_memory()  # this rank's input points (all of them at N=1)
@@ -307,9 +556,10 @@ def main():
         rx = torch.empty(2 * n_in + 1024, dtype=torch.float64).pin_memory()
         ry = torch.empty(2 * n_in + 1024, dtype=torch.float64).pin_memory()
         rn = torch.empty(1, dtype=torch.int64).pin_memory()
+        rt = torch.empty((bufs.tri.shape[0], 3), dtype=torch.int32).pin_memory()
         dx = torch.empty(n_in, dtype=torch.float64, device=dev)
         dy = torch.empty(n_in, dtype=torch.float64, device=dev)
-        e2e_ms = []
+        e2e_ms, d2h = [], []
         barrier()
         for _ in range(args.steps):
             flush_l2(flush)
@@ -322,26 +572,45 @@ def main():
             rx[:xf.shape[0]].copy_(xf, non_blocking=True)
             ry[:yf.shape[0]].copy_(yf, non_blocking=True)
             rn.copy_(bufs.n_tri, non_blocking=True)
+            stream.synchronize()  # the caller needs the count to size the triangle copy
+            nt = int(rn.item()) if not strip_mode else 0
+            if nt:
+                rt[:nt].copy_(bufs.tri[:nt], non_blocking=True)
             s1.record(stream)
             s1.synchronize()
             e2e_ms.append(s0.elapsed_time(s1))
+            d2h.append(2 * 8 * xf.shape[0] + 8 + 12 * nt)
         barrier()
         te = torch.tensor([sum(e2e_ms) / 1e3], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": n * iters * args.steps / float(te.item()), "unit": UNIT,
-               "h2d_bytes_per_step": 2 * 8 * n, "d2h_bytes_per_step": 2 * 8 * n + 8}
+               "h2d_bytes_per_step": 2 * 8 * n_in, "d2h_bytes_per_step": int(statistics.mean(d2h)),
+               "d2h": "final points (x, y), triangle count, final triangle list (int32 x3)"}
 
-    # algorithmic DP instructions of the dominant kernel: work counters from an
-    # untimed counting pass over the same schedule (SURVEY §8(d) cost table)
     roof = None
     if rank == 0 and ev_cells:
-        roof = roofline(T, c, ctx, cells_ms, params.flags, params.n_opt)
+        per = count_work(T, c, local, schedule, dev)
+        roof = roofline(per, cells_ms, it_ms)
+
+    cfg5 = None
+    if not args.no_cfg5 and world == 1 and not strip_mode:
+        cfg5 = {}
+        for nn in [int(v) for v in args.cfg5_sizes.split(",") if v]:
+            torch.cuda.empty_cache()
+            cfg5[str(nn)] = run_cfg5(T, dev, stream, nn)
+        cfg5["workload"] = "cfg5: jittered uniform unit square, 20 CVD iterations per step (SURVEY §8(d) cfg5)"
 
     if rank == 0:
         cpu = None
-        if world == 1 and not args.no_cpu_baseline:
-            cpu = cpu_baseline_sample()
+        if world == 1 and not args.no_cpu_baseline and "cvd" in saved:
+            states = {"dm": (c.x, c.y, None, 3), "cvd": (*saved["cvd"], 3)}
+            rec = run_oracle_pinned(states)
+            tc = sum(r["s"] for r in rec)
+            cpu = dict(value=len(rec) * n / tc, unit=UNIT, kind="oracle", seconds=tc,
+                       per_iteration_s={m: [round(r["s"], 3) for r in rec if r["mode"] == m] for m in ("dm", "cvd")},
+                       **cpu_desc("the first 3 iterations of each phase of the cfg3 schedule: 3 DistMesh from the "
+                                  "config's points and 3 CVD from the GPU state after the 30 DistMesh iterations"))
         # binning: k_bin_keys, k_bin_levels, 2 x (k_scan_tiles, k_scan_top, k_scan_add), k_leaf_keys,
         # k_perm_scatter, k_leaf_sort_perm, k_gather_sorted = 12; cells: k_cells_t + the retry pass = 2,
         # + k_output_t in CVD mode; DistMesh: k_dm_sums, k_dm_final, k_dm_step = 3
@@ -357,93 +626,13 @@ def main():
                        "l2": "flushed before every step (256 MiB write); per-iteration working set ~90 MB"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
+            "ms_per_iteration": {m: (statistics.mean(v) if v else None) for m, v in it_ms.items()},
             "cells_ms_per_launch": {k: (statistics.mean(v) if v else None) for k, v in cells_ms.items()},
+            "cfg5": cfg5,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
-
-
-PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
-
-
-def dp_peak():
-    """fp64 ALU peak (DP thread-instructions/s) = SMs x 64 FP64 lanes x SM clock
-    (B200: 148 SMs; profiling guide max clock 1965 MHz, MEASURED_PEAKS.json)."""
-    mhz = 1965.0
-    try:
-        mhz = float(json.load(open(PEAKS)).get("sm_max_mhz", mhz))
-    except Exception:
-        pass
-    meas = os.path.join(ROOT, "profiles", "fp64_peak.json")
-    if os.path.exists(meas):
-        try:
-            m = json.load(open(meas))
-            return float(m["dp_inst_per_s"]), "measured DFMA microbenchmark (tools/fp64_peak.cu, profiles/fp64_peak.json)"
-        except Exception:
-            pass
-    return 148 * 64 * mhz * 1e6, f"derived 148 SMs x 64 FP64 lanes x {mhz:.0f} MHz"
-
-
-def roofline(T, c, ctx, cells_ms, flags=0, n_opt=None):
-    """achieved = algorithmic DP instructions per k_cells launch / mean launch time."""
-    import torch
-    p = T.default_params()
-    p.flags |= T.TM_F_COUNT_WORK | flags
-    if n_opt:
-        p.n_opt = n_opt
-    dev = torch.device("cuda", ctx.device)
-    cc = T.Context(ctx.device, params=p)
-    cc.tm_set_domain(c.box, torch.from_numpy(c.phi).to(dev), torch.from_numpy(c.mu).to(dev),
-                     torch.from_numpy(c.rho).to(dev), c.n)
-    bufs = T.IterBuffers.alloc(c.n, p.adj_stride, device=dev)
-    xs = torch.from_numpy(c.x).to(dev)
-    ys = torch.from_numpy(c.y).to(dev)
-    xo, yo, do = torch.empty_like(xs), torch.empty_like(xs), torch.empty_like(xs)
-    dc = None
-    flops = {"dm": [], "cvd": []}
-    wsum = {"dm": [0] * 11, "cvd": [0] * 11}
-    for mode in c.schedule:
-        cc.tm_grid_bin(xs, ys)
-        if mode == "cvd":
-            cc.tm_voronoi_delaunay(bufs.tri, bufs.n_tri, None, None, dc, xo, yo, do, bufs.status)
-        else:
-            cc.tm_voronoi_delaunay(bufs.tri, bufs.n_tri, bufs.adj, bufs.deg)
-        w = cc.tm_work_counts()
-        wsum[mode] = [a + b for a, b in zip(wsum[mode], [w.n_cells, w.n_cert, w.deg, w.verts, w.t_own, w.quad_tris,
-                                                          w.ell, w.candidates, w.clips, w.exact_calls, w.retries])]
-        # SURVEY §8(d): 4 n_cert + 5 deg V + 50 deg + 40 T_own + [6V+15 | 30 Q] + 20 (ELL/force cost is k_dm_step)
-        f = 4 * w.n_cert + 5 * w.deg * (w.verts / max(w.n_cells, 1)) + 50 * w.deg + 40 * w.t_own
-        if mode == "cvd":
-            f += 30 * w.quad_tris + 20 * w.n_cells
-        flops[mode].append(f)
-        if mode == "dm":
-            cc.tm_distmesh_sums(bufs.adj, bufs.deg, bufs.sums2)
-            cc.tm_distmesh_step(bufs.adj, bufs.deg, bufs.sums2, None, dc, xo, yo, do, bufs.status)
-        xs, ys, dc = xo.clone(), yo.clone(), do.clone()
-    cc.tm_sync()
-    cc.close()
-    peak, how = dp_peak()
-    traffic = None  # DRAM bytes per launch of the cell kernel from the committed ncu capture
-    try:
-        tj = json.load(open(os.path.join(ROOT, "profiles", "kcells_traffic.json")))
-        nd = sum(1 for m in c.schedule if m == "dm")
-        traffic = (nd * tj["dm_bytes"] + (len(c.schedule) - nd) * tj["cvd_bytes"]) / len(c.schedule)
-    except Exception:
-        pass
-    tot_f = sum(flops["dm"]) + sum(flops["cvd"])
-    tot_t = sum(sum(v) for v in cells_ms.values()) / max(1, len(cells_ms["dm"]) + len(cells_ms["cvd"]))
-    nl = len(c.schedule)
-    per_launch_f = tot_f / nl
-    achieved = per_launch_f / (tot_t / 1e3)
-    return {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "T DP-inst/s",
-            "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write)",
-            "kernel": "k_cells_t (S2+S3+S4a+S5 fused)",
-            "algorithmic_dp_inst_per_launch": per_launch_f, "peak_source": how,
-            "dp_inst_per_launch_by_mode": {k: (statistics.mean(v) if v else None) for k, v in flops.items()},
-            "work_per_cell_by_mode": {m: {k: round(v / max(1, wsum[m][0]), 3) for k, v in zip(
-                ["n_cells", "n_cert", "deg", "verts", "t_own", "quad_tris", "ell", "candidates", "clips",
-                 "exact_calls", "retries"], wsum[m])} for m in wsum}}
 
 
 if __name__ == "__main__":

@@ -18,7 +18,9 @@
  *    every function returns a tm_status; tm_last_error() explains the last
  *    failure.  Asynchronous device-side failures (capacity overflow, duplicate
  *    or outside points, CUDA faults) are latched in the context and reported
- *    by the next synchronising call (tm_sync, tm_mesh_stats).
+ *    by the next synchronising call (tm_sync, tm_mesh_stats), which then clears
+ *    them: after TM_E_CAPACITY the caller retries with the reported size on the
+ *    same context and gets TM_OK.
  *  - Point-indexed outputs are in the CALLER's input order; triangle vertex
  *    indices are caller indices, or gid[] values when gid was given to
  *    tm_grid_bin.  The DistMesh ELL adjacency (adj/deg) is the exception: it is
@@ -89,9 +91,12 @@ typedef struct {
 #define TM_F_TWO_LEVEL_BINS 0x1u  /* split dense bins into 2^r x 2^r sub-bins (adaptive rho) */
 #define TM_F_COUNT_WORK     0x2u  /* accumulate per-cell work counters (tm_work_counts)       */
 #define TM_F_GROUP_CELLS    0x4u  /* cells by 16-lane groups instead of one thread per cell  */
+#define TM_F_NO_WCERT       0x8u  /* warm-started launches: flat search instead of warm clips +
+                                     warp-cooperative certification (A/B and tests)        */
 
 /* Mesh quality (alpha = R_circ/(2 R_in), beta = l_max/l_min) and
- * the health counters of the last iteration. */
+ * the health counters accumulated since the previous synchronising call
+ * (tm_sync / tm_mesh_stats, which read and clear them). */
 typedef struct {
     int64_t n_tri, n_alpha_lt_1_2, n_alpha_lt_2;
     int64_t n_degenerate;   /* exact predicate zeros + inconsistent clips        */
@@ -116,7 +121,8 @@ void tm_params_default(tm_params *p);
 tm_status tm_create(int device, void *cuda_stream, const tm_params *p, tm_ctx **out);
 void tm_destroy(tm_ctx *ctx);
 const char *tm_last_error(const tm_ctx *ctx);
-/* host: blocks until the stream is idle, then reports latched device errors. synchronises */
+/* host: blocks until the stream is idle, then reports (and clears) latched device
+ * errors. synchronises */
 tm_status tm_sync(tm_ctx *ctx);
 
 /* S0: copy the grids, compute
@@ -178,7 +184,9 @@ tm_status tm_project_sdf(tm_ctx *ctx, const double *x_old, const double *y_old, 
                          int8_t *status);
 
 /* S6: quality of n_tri triangles (caller indices into x,y) and the
- * health counters of the last iteration.  out: host.  synchronises */
+ * health counters since the previous synchronising call; returns a latched
+ * error like tm_sync (out is filled either way).  The sums are fixed-order tree
+ * reductions (no atomics): bitwise reproducible.  out: host.  synchronises */
 tm_status tm_mesh_stats(tm_ctx *ctx, const double *x, const double *y, const int32_t *tri, int64_t n_tri,
                         tm_stats *out);
 

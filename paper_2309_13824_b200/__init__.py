@@ -29,6 +29,7 @@ STATUS_NAMES = ["TM_OK", "TM_E_ARG", "TM_E_CUDA", "TM_E_CAPACITY", "TM_E_DUPLICA
 TM_F_TWO_LEVEL_BINS = 0x1
 TM_F_COUNT_WORK = 0x2
 TM_F_GROUP_CELLS = 0x4
+TM_F_NO_WCERT = 0x8
 
 
 class TmError(RuntimeError):

@@ -2,6 +2,7 @@
 // statistics, S7 halo/migration packing and host-side hooks of libtrime_gpu.so.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stddef.h>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -88,12 +89,11 @@ tm_status tm_internal_check_launch(tm_ctx *ctx, const char *what) {
     return TM_OK;
 }
 
-extern "C" tm_status tm_sync(tm_ctx *ctx) {
-    if (!ctx) return TM_E_ARG;
-    TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
-    TM_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-    DevState s;
-    TM_CUDA_TRY(ctx, cudaMemcpy(&s, ctx->dst, sizeof(s), cudaMemcpyDeviceToHost));
+// Latched device errors (DevState, first seven fields) -> status.  The health and error
+// counters accumulate from one synchronising call (tm_sync, tm_mesh_stats) to the next,
+// which reports them and then clears them, so a caller that retries after an error
+// (e.g. a larger tri_cap after TM_E_CAPACITY) is not stuck with a stale error.
+static tm_status report_latched(tm_ctx *ctx, const DevState &s) {
     if (s.n_outside) TM_FAIL(ctx, TM_E_OUTSIDE, "%llu point(s) are NaN or outside the box B", s.n_outside);
     if (s.n_duplicate) TM_FAIL(ctx, TM_E_DUPLICATE, "%llu bitwise-duplicate point pair(s)", s.n_duplicate);
     if (s.n_overflow)
@@ -102,6 +102,22 @@ extern "C" tm_status tm_sync(tm_ctx *ctx) {
     if (s.n_tri_overflow) TM_FAIL(ctx, TM_E_CAPACITY, "triangle buffer too small (tri_cap)");
     if (s.n_adj_overflow) TM_FAIL(ctx, TM_E_CAPACITY, "ELL row wider than adj_stride=%d", ctx->p.adj_stride);
     return TM_OK;
+}
+
+static tm_status clear_latched(tm_ctx *ctx) {
+    TM_CUDA_TRY(ctx, cudaMemsetAsync(ctx->dst, 0, offsetof(DevState, work), ctx->stream));
+    return TM_OK;
+}
+
+extern "C" tm_status tm_sync(tm_ctx *ctx) {
+    if (!ctx) return TM_E_ARG;
+    TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    TM_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    DevState s;
+    TM_CUDA_TRY(ctx, cudaMemcpy(&s, ctx->dst, sizeof(s), cudaMemcpyDeviceToHost));
+    const tm_status r = report_latched(ctx, s);
+    const tm_status c = clear_latched(ctx);
+    return r != TM_OK ? r : c;
 }
 
 // ============================================================================ S0
@@ -638,15 +654,40 @@ extern "C" tm_status tm_project_sdf(tm_ctx *ctx, const double *x_old, const doub
 // ============================================================================ S6
 // acc layout: 0 n, 1 sum sqrt a, 2 sum sqrt b, 3 max a, 4 max b, 5 sum a, 6 sum a2, 7 sum b, 8 sum b2,
 //             9 #a<1.2, 10 #a<2
-__device__ __forceinline__ void atomic_max_pos(double *addr, double v) {
-    // non-negative doubles order like their bit patterns
-    atomicMax((unsigned long long *)addr, (unsigned long long)__double_as_longlong(v));
+// Deterministic: every block reduces its STATS_T triangles by a fixed shuffle tree and a
+// fixed warp order into one row of partials; one block then reduces the rows in a fixed
+// order (each thread a fixed stride of rows, then the same tree).  No atomics: the sums
+// have the same bits on every run (no atomics on results).
+constexpr int STATS_T = 256, STATS_K = 11;
+
+__device__ __forceinline__ double stats_op(int k, double a, double b) { return (k == 3 || k == 4) ? fmax(a, b) : a + b; }
+
+// block-wide fixed-order reduction of v[STATS_K]; result valid in thread 0
+__device__ __forceinline__ void stats_block_reduce(double v[STATS_K], double (*sm)[STATS_T / 32]) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < STATS_K; k++) {
+        double x = v[k];
+        for (int o = 16; o > 0; o >>= 1) x = stats_op(k, x, __shfl_xor_sync(0xffffffffu, x, o));
+        if (lane == 0) sm[k][w] = x;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < STATS_K; k++) {
+            double x = sm[k][0];
+            for (int ww = 1; ww < STATS_T / 32; ww++) x = stats_op(k, x, sm[k][ww]);
+            v[k] = x;
+        }
+    }
 }
 
-__global__ void k_stats(const double *__restrict__ x, const double *__restrict__ y, const int32_t *__restrict__ tri,
-                        int64_t nt, double *acc) {
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    double v[11] = {0};
+__global__ void __launch_bounds__(STATS_T) k_stats(const double *__restrict__ x, const double *__restrict__ y,
+                                                   const int32_t *__restrict__ tri, int64_t nt,
+                                                   double *__restrict__ part) {
+    __shared__ double sm[STATS_K][STATS_T / 32];
+    const int64_t t = (int64_t)blockIdx.x * STATS_T + threadIdx.x;
+    double v[STATS_K] = {0};
     if (t < nt) {
         int32_t a = tri[3 * t], b = tri[3 * t + 1], c = tri[3 * t + 2];
         double ax = x[a], ay = y[a], bx = x[b], by = y[b], cx = x[c], cy = y[c];
@@ -660,22 +701,24 @@ __global__ void k_stats(const double *__restrict__ x, const double *__restrict__
         v[0] = 1; v[1] = sqrt(al); v[2] = sqrt(be); v[3] = al; v[4] = be;
         v[5] = al; v[6] = al * al; v[7] = be; v[8] = be * be; v[9] = al < 1.2; v[10] = al < 2.0;
     }
-    for (int k = 0; k < 11; k++) {
-        double w = v[k];
-        for (int o = 16; o > 0; o >>= 1) {
-            double u = __shfl_xor_sync(0xffffffffu, w, o);
-            w = (k == 3 || k == 4) ? fmax(w, u) : w + u;
-        }
-        v[k] = w;
+    stats_block_reduce(v, sm);
+    if (threadIdx.x == 0)
+        for (int k = 0; k < STATS_K; k++) part[(int64_t)k * gridDim.x + blockIdx.x] = v[k];
+}
+
+__global__ void __launch_bounds__(STATS_T) k_stats_final(const double *__restrict__ part, int64_t nb,
+                                                         double *__restrict__ acc) {
+    __shared__ double sm[STATS_K][STATS_T / 32];
+    double v[STATS_K];
+#pragma unroll
+    for (int k = 0; k < STATS_K; k++) {
+        double x = 0.0;
+        for (int64_t b = threadIdx.x; b < nb; b += STATS_T) x = stats_op(k, x, part[k * nb + b]);
+        v[k] = x;
     }
-    if ((threadIdx.x & 31) == 0) {
-        for (int k = 0; k < 11; k++) {
-            if (k == 3 || k == 4)
-                atomic_max_pos(&acc[k], v[k]);
-            else
-                atomicAdd(&acc[k], v[k]);
-        }
-    }
+    stats_block_reduce(v, sm);
+    if (threadIdx.x == 0)
+        for (int k = 0; k < STATS_K; k++) acc[k] = v[k];
 }
 
 extern "C" tm_status tm_mesh_stats(tm_ctx *ctx, const double *x, const double *y, const int32_t *tri,
@@ -685,7 +728,16 @@ extern "C" tm_status tm_mesh_stats(tm_ctx *ctx, const double *x, const double *y
     TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
     TM_CUDA_TRY(ctx, cudaMemsetAsync(ctx->stat_acc, 0, 16 * sizeof(double), ctx->stream));
     if (n_tri > 0) {
-        k_stats<<<(unsigned)((n_tri + 255) / 256), 256, 0, ctx->stream>>>(x, y, tri, n_tri, ctx->stat_acc);
+        const int64_t nb = (n_tri + STATS_T - 1) / STATS_T;
+        if (nb * STATS_K > ctx->cap_partials) {  // cap_partials counts doubles (shared with DistMesh)
+            cudaFree(ctx->partials);
+            ctx->partials = nullptr;
+            const int64_t c = (nb + nb / 8 + 64) * STATS_K;
+            TM_CUDA_TRY(ctx, cudaMalloc(&ctx->partials, (size_t)c * sizeof(double)));
+            ctx->cap_partials = c;
+        }
+        k_stats<<<(unsigned)nb, STATS_T, 0, ctx->stream>>>(x, y, tri, n_tri, ctx->partials);
+        k_stats_final<<<1, STATS_T, 0, ctx->stream>>>(ctx->partials, nb, ctx->stat_acc);
         tm_status s = tm_internal_check_launch(ctx, "k_stats");
         if (s != TM_OK) return s;
     }
@@ -703,7 +755,9 @@ extern "C" tm_status tm_mesh_stats(tm_ctx *ctx, const double *x, const double *y
     out->n_degenerate = (int64_t)ds.n_degenerate;
     out->n_fallback = (int64_t)ds.n_fallback;
     out->n_overflow = (int64_t)ds.n_overflow;
-    return TM_OK;
+    const tm_status r = report_latched(ctx, ds);
+    const tm_status c = clear_latched(ctx);
+    return r != TM_OK ? r : c;
 }
 
 extern "C" tm_status tm_work_counts(tm_ctx *ctx, tm_work *out) {

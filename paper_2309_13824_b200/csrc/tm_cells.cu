@@ -20,6 +20,8 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <climits>
+
 #include "tm_cellcore.cuh"
 
 namespace cg = cooperative_groups;
@@ -182,78 +184,6 @@ __device__ __forceinline__ void bitonic_sort2(const Tile<G> &g, unsigned long lo
 }
 
 
-// adaptive quadrature centroid (Fig. 14; reading L13), relative to p_i
-template <int G>
-__device__ void quad_centroid(const Tile<G> &g, const VState &v, unsigned valid, double px, double py, double area,
-                              double h, double dprev, const CellArgs &A, double &cx, double &cy,
-                              unsigned long long &nq) {
-    const int lane = g.thread_rank();
-    const int nv = __popc(valid);
-    double eps = dprev >= 0.0 ? dprev / h : A.fac_pt;
-    if (eps < A.fac_end) eps = A.fac_end;
-    const double E = sqrt(area) * eps;
-    double prevx = 0.0, prevy = 0.0;
-    for (int L = 1; L <= A.quad_max; L++) {
-        const int depth = L - 1;
-        const int64_t nleaf = (int64_t)nv << depth;
-        double sw = 0.0, swx = 0.0, swy = 0.0;
-        for (int64_t base = 0; base < nleaf; base += G) {
-            int64_t t = base + lane;
-            bool ok = t < nleaf;
-            int f = ok ? (int)(t >> depth) : 0;
-            int fl = __fns(valid, 0, f + 1);  // lane of the f-th ring vertex (fan triangle f)
-            int fn = g.shfl(v.next, fl);
-            double x1 = g.shfl(v.vx, fl), y1 = g.shfl(v.vy, fl);
-            double x2 = g.shfl(v.vx, fn), y2 = g.shfl(v.vy, fn);
-            if (!ok) continue;
-            double P[3][2] = {{0.0, 0.0}, {x1, y1}, {x2, y2}};
-            int64_t path = t & (((int64_t)1 << depth) - 1);
-            for (int lev = depth - 1; lev >= 0; lev--) {
-                double best = -1.0;
-                int eidx = 0;
-#pragma unroll
-                for (int k = 0; k < 3; k++) {
-                    int k1 = k == 2 ? 0 : k + 1;
-                    double dx = csub(P[k1][0], P[k][0]), dy = csub(P[k1][1], P[k][1]);
-                    double Lk = cadd(cmul(dx, dx), cmul(dy, dy));
-                    if (Lk > best) { best = Lk; eidx = k; }
-                }
-                int ia = eidx, ib = eidx == 2 ? 0 : eidx + 1, ic = ib == 2 ? 0 : ib + 1;
-                double ax = P[ia][0], ay = P[ia][1], bx = P[ib][0], by = P[ib][1], qx = P[ic][0], qy = P[ic][1];
-                double mx = cmul(cadd(ax, bx), 0.5), my = cmul(cadd(ay, by), 0.5);
-                if ((path >> lev) & 1) {  // child 1 = (M, Pb, Pc)
-                    P[0][0] = mx; P[0][1] = my; P[1][0] = bx; P[1][1] = by;
-                } else {                  // child 0 = (Pa, M, Pc)
-                    P[0][0] = ax; P[0][1] = ay; P[1][0] = mx; P[1][1] = my;
-                }
-                P[2][0] = qx; P[2][1] = qy;
-            }
-            double cr = csub(cmul(csub(P[1][0], P[0][0]), csub(P[2][1], P[0][1])),
-                             cmul(csub(P[1][1], P[0][1]), csub(P[2][0], P[0][0])));
-            double At = cmul(0.5, cr);
-            double qx = cdiv(cadd(cadd(P[0][0], P[1][0]), P[2][0]), 3.0);
-            double qy = cdiv(cadd(cadd(P[0][1], P[1][1]), P[2][1]), 3.0);
-            double rho = bilinear(A.grid, A.rho, cadd(px, qx), cadd(py, qy), LdgLoad());
-            double wgt = At * rho;
-            sw += wgt;
-            swx += wgt * qx;
-            swy += wgt * qy;
-            nq++;
-        }
-        sw = tile_sum<G>(g, sw);
-        swx = tile_sum<G>(g, swx);
-        swy = tile_sum<G>(g, swy);
-        double curx = swx / sw, cury = swy / sw;
-        double dx = prevx - curx, dy = prevy - cury;
-        double dist = sqrt(dx * dx + dy * dy);
-        prevx = curx;
-        prevy = cury;
-        if (dist < E) break;
-    }
-    cx = prevx;
-    cy = prevy;
-}
-
 template <int G>
 __device__ __forceinline__ float fresh_R2(const Tile<G> &g, const VState &v, unsigned valid) {
     return tile_maxf<G>(g, ((valid >> g.thread_rank()) & 1u) ? vertex_r2f(v) : 0.0f);
@@ -265,6 +195,7 @@ template <int G, int MODE>
 __global__ void __launch_bounds__(BLOCK, (G == 16 ? TM_MINB : 1)) k_cells(CellArgs A, int32_t *retry_list, unsigned long long *retry_cnt) {
     constexpr int CPB = BLOCK / G;
     __shared__ int32_t sbuf_all[CPB][2 * G];
+    __shared__ double2 ring_smem[CPB][G];  // a finished ring in canonical order (S4a, lane 0)
     cg::thread_block block = cg::this_thread_block();
     Tile<G> g = cg::tiled_partition<G>(block);
     const int lane = g.thread_rank();
@@ -476,38 +407,71 @@ __global__ void __launch_bounds__(BLOCK, (G == 16 ? TM_MINB : 1)) k_cells(CellAr
                         }
                     }
                 }
+                // canonical ring order (from the smallest (incoming, outgoing) line pair, points
+                // named by their ids, as k_cells_t and the oracle): the ELL row, the warm-start
+                // neighbour list and the centroid sums below all walk the ring in this order, so
+                // every output is independent of which kernel computed the cell
+                const long long ckey =
+                    active ? (((long long)(v.la >= 0 ? __ldg(A.gids + v.la) : v.la) << 32) |
+                              (unsigned)(v.lb >= 0 ? __ldg(A.gids + v.lb) : v.lb))
+                           : LLONG_MAX;
+                const unsigned long long kmin = tile_min_u64<G>(g, (unsigned long long)ckey ^ 0x8000000000000000ull);
+                const int cstart =
+                    __ffs(g.ballot(active && ((unsigned long long)ckey ^ 0x8000000000000000ull) == kmin)) - 1;
                 // ---- DistMesh ELL row: neighbour a (incoming bisector of a vertex) borders a kept triangle
                 int ell = 0;
                 if (MODE & M_ELL) {
                     const bool kprev = g.shfl((int)kept, v.prev) != 0;
                     const bool nb = active && v.la >= 0 && (kept || kprev);
-                    const unsigned nm = g.ballot(nb);
-                    ell = __popc(nm);
-                    if (nb) {
-                        const int pos = __popc(nm & ((1u << lane) - 1u));
-                        if (pos < A.adj_stride) A.adj[(int64_t)pos * A.n_local + cell] = v.la;
+                    int walk = cstart;
+                    for (int q = 0; q < nv; q++) {
+                        const bool nbq = g.shfl((int)nb, walk) != 0;
+                        const int aq = g.shfl(v.la, walk);
+                        if (nbq) {
+                            if (lane == 0 && ell < A.adj_stride) A.adj[(int64_t)ell * A.n_local + cell] = aq;
+                            ell++;
+                        }
+                        walk = g.shfl(v.next, walk);
                     }
                     if (lane == 0) {
                         A.deg[cell] = (uint8_t)(ell < A.adj_stride ? ell : A.adj_stride);
                         if (ell > A.adj_stride) atomicAdd(&A.st->n_adj_overflow, 1ull);
                     }
                 }
+                // ---- warm-start neighbour list for the next launch (ids, canonical ring order,
+                // at most TM_NBR: a hint only, the next launch certifies its cells either way)
+                {
+                    const int32_t nid = A.nbr_by_gid ? gi : orig;
+                    if (A.nbr && A.nbr_cnt && nid >= 0 && (int64_t)nid < A.nbr_keys) {
+                        int walk = cstart, cnt = 0;
+                        for (int q = 0; q < nv; q++) {
+                            const int aq = g.shfl(v.la, walk);
+                            if (aq >= 0) {
+                                if (lane == 0 && cnt < TM_NBR)
+                                    A.nbr[(int64_t)nid * TM_NBR + cnt] = A.nbr_by_gid ? __ldg(A.gids + aq) : __ldg(A.perm + aq);
+                                cnt++;
+                            }
+                            walk = g.shfl(v.next, walk);
+                        }
+                        if (lane == 0) A.nbr_cnt[nid] = (uint8_t)(cnt < TM_NBR ? cnt : TM_NBR);
+                    }
+                }
                 // ---- S4a: centroid of C_i (relative to p_i)
                 if (MODE & (M_TREAT | M_HAT)) {
-                    const double x1 = g.shfl(v.vx, v.next), y1 = g.shfl(v.vy, v.next);
-                    const double cr = active ? v.vx * y1 - x1 * v.vy : 0.0;
-                    const double S2 = tile_sum<G>(g, cr);
-                    double cx, cy;
-                    if (A.rho == nullptr) {
-                        const double sx = tile_sum<G>(g, active ? cr * (v.vx + x1) : 0.0);
-                        const double sy = tile_sum<G>(g, active ? cr * (v.vy + y1) : 0.0);
-                        cx = sx / (3.0 * S2);
-                        cy = sy / (3.0 * S2);
-                        nq += nv;
-                    } else {
-                        const double dp = A.d_prev ? __ldg(A.d_prev + orig) : -1.0;
-                        quad_centroid<G>(g, v, valid, px, py, 0.5 * S2, h, dp, A, cx, cy, nq);
+                    // gather the ring in canonical order and let lane 0 sum it sequentially: the
+                    // same operations in the same order as k_output_t and the oracle's O4
+                    int walk = cstart;
+                    double2 *rb = ring_smem[threadIdx.x / G];
+                    for (int q = 0; q < nv; q++) {
+                        const double wx = g.shfl(v.vx, walk), wy = g.shfl(v.vy, walk);
+                        if (lane == 0) rb[q] = make_double2(wx, wy);
+                        walk = g.shfl(v.next, walk);
                     }
+                    g.sync();
+                    double cx = 0.0, cy = 0.0;
+                    if (lane == 0)
+                        ring_centroid(rb, 1, nv, px, py, h, A.d_prev ? __ldg(A.d_prev + orig) : -1.0, A, cx, cy, nq);
+                    g.sync();
                     if ((MODE & M_HAT) && lane == 0) {
                         A.x_hat[orig] = px + cx;
                         A.y_hat[orig] = py + cy;

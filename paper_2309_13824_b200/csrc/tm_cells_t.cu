@@ -59,6 +59,7 @@ namespace {
 constexpr int TB = TM_TB;
 constexpr int VMAX = TM_VMAX;
 static_assert(VMAX <= 31, "slot masks are 32-bit");
+static_assert(VMAX <= TM_NBR, "warm-start rows hold at most TM_NBR neighbours per point (ADVICE r1)");
 static_assert(TB <= 256 && (TB & (TB - 1)) == 0, "balancing keys hold the lane slot in 8 bits");
 #if TM_K_DOUBLE
 typedef double KT;  // filter constant storage
@@ -289,9 +290,9 @@ __device__ __forceinline__ void cswap(unsigned &a, unsigned &b) {
 // relative to p_i; same sub-triangle construction as quad_centroid
 __device__ void quad_centroid_t(const TPoly &P, int start, int nv, double px, double py, double area, double h,
                                 double dprev, const CellArgs &A, double &cx, double &cy, unsigned long long &nq) {
-    double eps = dprev >= 0.0 ? dprev / h : A.fac_pt;
+    double eps = dprev >= 0.0 ? cdiv(dprev, h) : A.fac_pt;
     if (eps < A.fac_end) eps = A.fac_end;
-    const double E = sqrt(area) * eps;
+    const double E = cmul(sqrt(area), eps);
     double prevx = 0.0, prevy = 0.0;
     for (int L = 1; L <= A.quad_max; L++) {
         const int depth = L - 1;
@@ -332,16 +333,16 @@ __device__ void quad_centroid_t(const TPoly &P, int start, int nv, double px, do
                 const double qx = div3(cadd(cadd(Q[0][0], Q[1][0]), Q[2][0]));
                 const double qy = div3(cadd(cadd(Q[0][1], Q[1][1]), Q[2][1]));
                 const double rho = bilinear(A.grid, A.rho, cadd(px, qx), cadd(py, qy), LdgLoad());
-                const double wgt = At * rho;
-                sw += wgt;
-                swx += wgt * qx;
-                swy += wgt * qy;
+                const double wgt = cmul(At, rho);
+                sw = cadd(sw, wgt);
+                swx = cadd(swx, cmul(wgt, qx));
+                swy = cadd(swy, cmul(wgt, qy));
                 nq++;
             }
         }
-        const double curx = swx / sw, cury = swy / sw;
-        const double dx = prevx - curx, dy = prevy - cury;
-        const double dist = sqrt(dx * dx + dy * dy);
+        const double curx = cdiv(swx, sw), cury = cdiv(swy, sw);
+        const double dx = csub(prevx, curx), dy = csub(prevy, cury);
+        const double dist = sqrt(cadd(cmul(dx, dx), cmul(dy, dy)));
         prevx = curx;
         prevy = cury;
         if (dist < E) break;
@@ -450,40 +451,46 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
         nly = bg.nby << rh;
         lsx = bg.sx / (double)(1 << rh);
         lsy = bg.sy / (double)(1 << rh);
-        // ring 1: the 8 neighbours nearest first (keys: d2 as float bits, low 3 bits = index)
-        const double gl = px - (bg.x0 + ux * lsx), gr = (bg.x0 + (ux + 1) * lsx) - px;
-        const double gd = py - (bg.y0 + uy * lsy), gu = (bg.y0 + (uy + 1) * lsy) - py;
-        const int ddx[8] = {-1, 1, 0, 0, -1, 1, -1, 1};
-        const int ddy[8] = {0, 0, -1, 1, -1, -1, 1, 1};
-#pragma unroll
-        for (int q = 0; q < 8; q++) {
-            const double gx = fmax(ddx[q] < 0 ? gl : (ddx[q] > 0 ? gr : 0.0), 0.0);
-            const double gy = fmax(ddy[q] < 0 ? gd : (ddy[q] > 0 ? gu : 0.0), 0.0);
-            const float d2 = __double2float_rd(gx * gx + gy * gy);
-            key[q] = (__float_as_uint(fmaxf(d2, 0.f)) & ~7u) | (unsigned)q;
+        if constexpr (!(MODE & M_WCERT)) {
+            // ring 1: the 8 neighbours nearest first (keys: d2 as float bits, low 3 bits = index)
+            const double gl = px - (bg.x0 + ux * lsx), gr = (bg.x0 + (ux + 1) * lsx) - px;
+            const double gd = py - (bg.y0 + uy * lsy), gu = (bg.y0 + (uy + 1) * lsy) - py;
+            const int ddx[8] = {-1, 1, 0, 0, -1, 1, -1, 1};
+            const int ddy[8] = {0, 0, -1, 1, -1, -1, 1, 1};
+    #pragma unroll
+            for (int q = 0; q < 8; q++) {
+                const double gx = fmax(ddx[q] < 0 ? gl : (ddx[q] > 0 ? gr : 0.0), 0.0);
+                const double gy = fmax(ddy[q] < 0 ? gd : (ddy[q] > 0 ? gu : 0.0), 0.0);
+                const float d2 = __double2float_rd(gx * gx + gy * gy);
+                key[q] = (__float_as_uint(fmaxf(d2, 0.f)) & ~7u) | (unsigned)q;
+            }
+            // 19-comparator sorting network for 8 keys
+            cswap(key[0], key[2]); cswap(key[1], key[3]); cswap(key[4], key[6]); cswap(key[5], key[7]);
+            cswap(key[0], key[4]); cswap(key[1], key[5]); cswap(key[2], key[6]); cswap(key[3], key[7]);
+            cswap(key[0], key[1]); cswap(key[2], key[3]); cswap(key[4], key[5]); cswap(key[6], key[7]);
+            cswap(key[2], key[4]); cswap(key[3], key[5]);
+            cswap(key[1], key[4]); cswap(key[3], key[6]);
+            cswap(key[1], key[2]); cswap(key[3], key[4]); cswap(key[5], key[6]);
+            // ring 0: the home leaf first
+            int st, cnt;
+            vleaf_range(A, ux, uy, rh, ux, uy, hb, hoff, st, cnt);
+            t = st;
+            tend = st + cnt;
+            // warm start: the cell's neighbours of the previous launch on the same point set
+            // (caller ids) are clipped first -- the ring is then nearly final and R_max small
+            // before the search; the search still certifies the cell (L11), so the result
+            // does not depend on them
+            wn = (A.warm && A.nbr_cnt && nid >= 0) ? min((int)A.nbr_cnt[nid], TM_NBR) : 0;
+            ph = fail ? 2 : (wn > 0 ? -1 : 0);
+            rr = 0;
+            if (ph == -1) { cvx = t; cend = tend; t = tend = 0; }  // home range parked until the warm list ends
+            if (ph == 2) t = tend;
+        } else {
+            wn = (A.warm && A.nbr_cnt && nid >= 0) ? min((int)A.nbr_cnt[nid], TM_NBR) : 0;
         }
-        // 19-comparator sorting network for 8 keys
-        cswap(key[0], key[2]); cswap(key[1], key[3]); cswap(key[4], key[6]); cswap(key[5], key[7]);
-        cswap(key[0], key[4]); cswap(key[1], key[5]); cswap(key[2], key[6]); cswap(key[3], key[7]);
-        cswap(key[0], key[1]); cswap(key[2], key[3]); cswap(key[4], key[5]); cswap(key[6], key[7]);
-        cswap(key[2], key[4]); cswap(key[3], key[5]);
-        cswap(key[1], key[4]); cswap(key[3], key[6]);
-        cswap(key[1], key[2]); cswap(key[3], key[4]); cswap(key[5], key[6]);
-        // ring 0: the home leaf first
-        int st, cnt;
-        vleaf_range(A, ux, uy, rh, ux, uy, hb, hoff, st, cnt);
-        t = st;
-        tend = st + cnt;
-        // warm start: the cell's neighbours of the previous launch on the same point set
-        // (caller ids) are clipped first -- the ring is then nearly final and R_max small
-        // before the search; the search still certifies the cell (L11), so the result
-        // does not depend on them
-        wn = (A.warm && A.nbr_cnt && nid >= 0) ? min((int)A.nbr_cnt[nid], TM_NBR) : 0;
-        ph = fail ? 2 : (wn > 0 ? -1 : 0);
-        rr = 0;
-        if (ph == -1) { cvx = t; cend = tend; t = tend = 0; }  // home range parked until the warm list ends
-        if (ph == 2) t = tend;
     }
+    unsigned trips = 0;
+    if constexpr (!(MODE & M_WCERT)) {
     // ---- flat candidate loop: one candidate per thread per trip, the warp
     // re-converges every trip (a per-thread nested loop lets lanes drift apart)
     // the iterator: advance to this thread's next candidate slot (-1 when done)
@@ -567,7 +574,6 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
         }
         return j;
     };
-    unsigned trips = 0;
     double lim2 = 4.0 * (double)R2 * MARG;  // (2 R_max)^2 with margin, updated with R_max
     // ---- (C) flat candidate loop
     int j = next_cand();
@@ -600,6 +606,146 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
             }
         }
     }
+    } else {
+        // ---- (A) warm clips, one thread per cell: the cell's neighbours of the previous
+        // launch on the same point set (ids -> slots of this binning; a stale id fails the
+        // check).  Every lane clips about the same number (~6) of lines: uniform work.
+        if (live && !fail) {
+            if (wn == 0) fail = -1;  // no warm list: the 32-lane pass computes the cell from scratch
+            for (int w = 0; w < wn && !fail; w++) {
+                const int id = A.nbr[(int64_t)nid * TM_NBR + w];
+                if (id < 0 || (int64_t)id >= A.nbr_keys) continue;
+                const int js = A.inv_perm[id];
+                if (js < 0 || (int64_t)js >= A.n_local || js == (int)cell ||
+                    (A.nbr_by_gid && __ldg(A.gids + js) != id))
+                    continue;
+                const double dx = csub(__ldg(A.xs + js), px), dy = csub(__ldg(A.ys + js), py);
+                if (dx == 0.0 && dy == 0.0) {
+                    atomicAdd(&A.st->n_duplicate, 1ull);
+                    continue;
+                }
+                fail = clip_t(P, js, bisector(dx, dy), cgm, A, cs);
+            }
+            R2 = poly_R2(P);
+        }
+        // ---- (B) certification (L11), one WARP per cell, cell by cell: every point within
+        // 2 R_max of p_c must be tested against the warm ring.  The lanes take the leaves of
+        // the box that can hold such points (home resolution, pruned by distance), then one
+        // candidate each: distance test, then the vertex test against the SAME ring (shared
+        // memory broadcast, a warp-uniform loop over its vertices).  A candidate that does not
+        // cut a ring cannot cut any later (smaller) ring, so only the rare cutters are clipped,
+        // sequentially, by the cell's own lane.
+        const int wbase = tid & ~31;
+        const unsigned todo = __ballot_sync(0xffffffffu, live && !fail);
+        for (unsigned mc = todo; mc; mc &= mc - 1) {
+            const int c = __ffs(mc) - 1;
+            const double pcx = __shfl_sync(0xffffffffu, px, c), pcy = __shfl_sync(0xffffffffu, py, c);
+            const int rhc = __shfl_sync(0xffffffffu, rh, c), uxc = __shfl_sync(0xffffffffu, ux, c);
+            const int uyc = __shfl_sync(0xffffffffu, uy, c), hbc = __shfl_sync(0xffffffffu, hb, c);
+            const int hoffc = __shfl_sync(0xffffffffu, hoff, c);
+            const int cellc = (int)__shfl_sync(0xffffffffu, (int)cell, c);
+            unsigned usedc = __shfl_sync(0xffffffffu, P.used, c), wallc = __shfl_sync(0xffffffffu, P.wall, c);
+            float r2c = __shfl_sync(0xffffffffu, R2, c);
+            const TPoly Pc = tpoly_bind(tsmem, wbase + c);
+            // leaf box at the home resolution that can hold a point closer than 2 R_max
+            const double rad = 2.0 * sqrt((double)r2c * MARG) * (1.0 + 1e-6);
+            const double lsxc = bg.sx / (double)(1 << rhc), lsyc = bg.sy / (double)(1 << rhc);
+            const double sxl = bg.isx * (double)(1 << rhc), syl = bg.isy * (double)(1 << rhc);
+            const int nlxc = bg.nbx << rhc, nlyc = bg.nby << rhc;
+            const int cxa = max(0, (int)floor((pcx - rad - bg.x0) * sxl));
+            const int cxb = min(nlxc - 1, (int)floor((pcx + rad - bg.x0) * sxl));
+            const int cya = max(0, (int)floor((pcy - rad - bg.y0) * syl));
+            const int cyb = min(nlyc - 1, (int)floor((pcy + rad - bg.y0) * syl));
+            const int nLx = cxb - cxa + 1, nL = nLx * (cyb - cya + 1);
+            bool dead = false;
+            unsigned long long ncand = 0;
+            for (int l0 = 0; l0 < nL && !dead; l0 += 32) {
+                const int l = l0 + lane;
+                int st = 0, cnt = 0;
+                if (l < nL) {
+                    const int vx = cxa + l % nLx, vy = cya + l / nLx;
+                    if (leaf_d2(bg, lsxc, lsyc, vx, vy, pcx, pcy) * (1.0 - 1e-9) < 4.0 * (double)r2c * MARG)
+                        vleaf_range(A, vx, vy, rhc, uxc, uyc, hbc, hoffc, st, cnt);
+                }
+                int incl = cnt;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int u = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += u;
+                }
+                const int tot = __shfl_sync(0xffffffffu, incl, 31);
+                ncand += (unsigned long long)tot;
+                for (int base = 0; base < tot && !dead; base += 32) {
+                    trips++;
+                    const int tt = base + lane;
+                    // leaf of candidate tt: the number of leaves whose inclusive count is <= tt
+                    int k = 0;
+#pragma unroll
+                    for (int s = 16; s > 0; s >>= 1)
+                        if (__shfl_sync(0xffffffffu, incl, k + s - 1) <= tt) k += s;
+                    const int kk = k < 31 ? k : 31;
+                    const int stk = __shfl_sync(0xffffffffu, st, kk);
+                    const int exk = __shfl_sync(0xffffffffu, incl - cnt, kk);
+                    const int j = stk + (tt - exk);
+                    bool flag = false;
+                    double dx = 0.0, dy = 0.0, d2 = 0.0;
+                    if (tt < tot && j != cellc) {
+                        dx = csub(__ldg(A.xs + j), pcx);
+                        dy = csub(__ldg(A.ys + j), pcy);
+                        d2 = dx * dx + dy * dy;
+                        if (dx == 0.0 && dy == 0.0) atomicAdd(&A.st->n_duplicate, 1ull);
+                        flag = d2 < 4.0 * (double)r2c * MARG && d2 > 0.0;
+                    }
+                    if (__any_sync(0xffffffffu, flag)) {
+                        const Line L = bisector(dx, dy);
+                        const double n1 = fabs(L.nx) + fabs(L.ny);
+                        const double c8 = 8.0 * EPS * n1 * n1;
+                        bool hit = false, isline = false;
+                        for (unsigned mm = usedc; mm; mm &= mm - 1) {  // warp-uniform: the same ring
+                            const int q = __ffs(mm) - 1;
+                            const double2 vv = Pc.v[q * TB];
+                            isline |= Pc.la[q * TB] == j;
+                            if ((wallc >> q) & 1u) {
+                                hit |= wall_out(L, vv.x, vv.y);
+                            } else {
+                                const double del = fma(L.nx, vv.x, L.ny * vv.y) - L.r;
+                                hit |= del > -fma(n1, (double)Pc.K[q * TB], c8);  // cut or undecided
+                            }
+                        }
+                        flag = flag && hit && !isline;  // a line of the ring never cuts it (L already bounds it)
+                    }
+                    // the rare (possible) cutters, nearest first, clipped by the cell's own lane; the
+                    // full clip test there also decides undecided vertices (-1: 32-lane pass)
+                    unsigned fl = __ballot_sync(0xffffffffu, flag);
+                    while (fl) {
+                        float best = __uint_as_float(0x7f800000u);
+                        int q = 0;
+                        for (unsigned m2 = fl; m2; m2 &= m2 - 1) {
+                            const int b = __ffs(m2) - 1;
+                            const float db = __shfl_sync(0xffffffffu, (float)d2, b);
+                            if (db < best) { best = db; q = b; }
+                        }
+                        fl &= ~(1u << q);
+                        const int jq = __shfl_sync(0xffffffffu, j, q);
+                        const double dxq = __shfl_sync(0xffffffffu, dx, q), dyq = __shfl_sync(0xffffffffu, dy, q);
+                        int fc = 0;
+                        if (lane == c) {
+                            const unsigned long long c0 = cs.clips;
+                            fc = clip_t(P, jq, bisector(dxq, dyq), cgm, A, cs);
+                            if (fc) fail = fc;
+                            else if (cs.clips != c0) R2 = poly_R2(P);
+                        }
+                        fc = __shfl_sync(0xffffffffu, fc, c);
+                        usedc = __shfl_sync(0xffffffffu, P.used, c);
+                        wallc = __shfl_sync(0xffffffffu, P.wall, c);
+                        r2c = __shfl_sync(0xffffffffu, R2, c);
+                        if (fc) { dead = true; break; }
+                    }
+                }
+            }
+            if (lane == c) sc.n_cand += ncand;
+        }
+    }
     if (live) {
         if (fail == -1) {
             // more than VMAX slots (or an undecided filter without TM_THREAD_EXACT):
@@ -619,15 +765,19 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
             live = false;
         }
     }
-    // canonical start vertex (smallest (incoming, outgoing) line pair): every ring
-    // traversal below -- neighbour lists, ELL rows, centroid sums -- is then
-    // independent of the order in which the cell was clipped
+    // canonical start vertex: the smallest (incoming, outgoing) line pair with points named
+    // by their ids (gid / caller index, walls by their negative codes) -- the oracle's
+    // canonical rotation (O2).  Every ring traversal below (neighbour lists, ELL rows,
+    // centroid and quadrature sums) is then independent of the clipping order AND of the
+    // binning, so the sums run in the oracle's order (bit-identical CVD, L25)
     int start = 0;
     if (live) {
         long long best = LLONG_MAX;
         for (unsigned m = P.used; m; m &= m - 1) {  // used slots only: a free slot's link is garbage
             const int k = __ffs(m) - 1;
-            const long long key = ((long long)P.la[k * TB] << 32) | (unsigned)P.la[P.nxt[k * TB] * TB];
+            const int la = P.la[k * TB], lb = P.la[P.nxt[k * TB] * TB];
+            const long long key = ((long long)(la >= 0 ? __ldg(A.gids + la) : la) << 32) |
+                                  (unsigned)(lb >= 0 ? __ldg(A.gids + lb) : lb);
             if (key < best) { best = key; start = k; }
         }
     }
@@ -741,20 +891,20 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
         for (int c = 0; c < nv; c++) {
             const int kn = P.nxt[k * TB];
             const double x0 = P.v[k * TB].x, y0 = P.v[k * TB].y, x1 = P.v[kn * TB].x, y1 = P.v[kn * TB].y;
-            const double cr = x0 * y1 - x1 * y0;
-            S2 += cr;
-            sx += cr * (x0 + x1);
-            sy += cr * (y0 + y1);
+            const double cr = csub(cmul(x0, y1), cmul(x1, y0));
+            S2 = cadd(S2, cr);
+            sx = cadd(sx, cmul(cr, cadd(x0, x1)));
+            sy = cadd(sy, cmul(cr, cadd(y0, y1)));
             k = kn;
         }
         double cx, cy;
         if (A.rho == nullptr) {
-            cx = sx / (3.0 * S2);
-            cy = sy / (3.0 * S2);
+            cx = cdiv(sx, cmul(3.0, S2));
+            cy = cdiv(sy, cmul(3.0, S2));
             nq += nv;
         } else {
             const double dp = A.d_prev ? __ldg(A.d_prev + orig) : -1.0;
-            quad_centroid_t(P, start, nv, px, py, 0.5 * S2, h, dp, A, cx, cy, nq);
+            quad_centroid_t(P, start, nv, px, py, cmul(0.5, S2), h, dp, A, cx, cy, nq);
         }
         if (MODE & M_HAT) {
             A.x_hat[orig] = px + cx;
@@ -808,124 +958,6 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
     }
 }
 
-
-// one longest-edge bisection of sub-triangle Q (Fig. 14): child `bit`
-// (0: (a, m, c), 1: (m, b, c) with ab the longest edge, m its midpoint)
-__device__ __forceinline__ void quad_split(const double Q[3][2], int bit, double C[3][2]) {
-    double best = -1.0;
-    int eidx = 0;
-#pragma unroll
-    for (int q = 0; q < 3; q++) {
-        const int q1 = q == 2 ? 0 : q + 1;
-        const double ddx = csub(Q[q1][0], Q[q][0]), ddy = csub(Q[q1][1], Q[q][1]);
-        const double Lq = cadd(cmul(ddx, ddx), cmul(ddy, ddy));
-        if (Lq > best) { best = Lq; eidx = q; }
-    }
-    // edge (a, b) = (Q[e], Q[e+1]), c the third vertex; selects, not indexing (registers)
-    const double ax = eidx == 0 ? Q[0][0] : (eidx == 1 ? Q[1][0] : Q[2][0]);
-    const double ay = eidx == 0 ? Q[0][1] : (eidx == 1 ? Q[1][1] : Q[2][1]);
-    const double bx = eidx == 0 ? Q[1][0] : (eidx == 1 ? Q[2][0] : Q[0][0]);
-    const double by = eidx == 0 ? Q[1][1] : (eidx == 1 ? Q[2][1] : Q[0][1]);
-    const double cx = eidx == 0 ? Q[2][0] : (eidx == 1 ? Q[0][0] : Q[1][0]);
-    const double cy = eidx == 0 ? Q[2][1] : (eidx == 1 ? Q[0][1] : Q[1][1]);
-    const double mx = cmul(cadd(ax, bx), 0.5), my = cmul(cadd(ay, by), 0.5);
-    if (bit) {
-        C[0][0] = mx; C[0][1] = my; C[1][0] = bx; C[1][1] = by;
-    } else {
-        C[0][0] = ax; C[0][1] = ay; C[1][0] = mx; C[1][1] = my;
-    }
-    C[2][0] = cx; C[2][1] = cy;
-}
-
-// sub-triangle of fan triangle (0, a, b) reached by `levels` bisections along `path`
-// (bit lev taken at level lev, from the top)
-__device__ __forceinline__ void quad_descend(const double2 a, const double2 b, int levels, int64_t path,
-                                             double Q[3][2]) {
-    Q[0][0] = 0.0; Q[0][1] = 0.0; Q[1][0] = a.x; Q[1][1] = a.y; Q[2][0] = b.x; Q[2][1] = b.y;
-    for (int lev = levels - 1; lev >= 0; lev--) {
-        double C[3][2];
-        quad_split(Q, (int)((path >> lev) & 1), C);
-#pragma unroll
-        for (int q = 0; q < 3; q++) { Q[q][0] = C[q][0]; Q[q][1] = C[q][1]; }
-    }
-}
-
-// area and centroid of a sub-triangle, and its density corners
-__device__ __forceinline__ void quad_leaf(const double Q[3][2], const CellArgs &A, double px, double py, double &At,
-                                          double &qx, double &qy, double &ss, double &tt, double f[4]) {
-    const double cr = csub(cmul(csub(Q[1][0], Q[0][0]), csub(Q[2][1], Q[0][1])),
-                           cmul(csub(Q[1][1], Q[0][1]), csub(Q[2][0], Q[0][0])));
-    At = cmul(0.5, cr);
-    qx = div3(cadd(cadd(Q[0][0], Q[1][0]), Q[2][0]));
-    qy = div3(cadd(cadd(Q[0][1], Q[1][1]), Q[2][1]));
-    int gi, gj;
-    grid_cell(A.grid, cadd(px, qx), cadd(py, qy), gi, gj, ss, tt);
-    const double *r0 = A.rho + (int64_t)gj * A.grid.nx + gi, *r1 = r0 + A.grid.nx;
-    f[0] = __ldg(r0);
-    f[1] = __ldg(r0 + 1);
-    f[2] = __ldg(r1);
-    f[3] = __ldg(r1 + 1);
-}
-
-// adaptive quadrature over a stored ring (ring order from the canonical vertex); the
-// same sub-triangles and sums, in the same order, as quad_centroid_t.  Sub-triangles
-// are taken two at a time with their density loads in flight together (the kernel is
-// bound by the latency of those loads); below level 1 the two are siblings, so the
-// descent to their parent is shared.
-__device__ void quad_centroid_g(const double2 *rv, int64_t ns, int nv, double px, double py, double area, double h,
-                                double dprev, const CellArgs &A, double &cx, double &cy, unsigned long long &nq) {
-    double eps = dprev >= 0.0 ? dprev / h : A.fac_pt;
-    if (eps < A.fac_end) eps = A.fac_end;
-    const double E = sqrt(area) * eps;
-    double prevx = 0.0, prevy = 0.0;
-    for (int L = 1; L <= A.quad_max; L++) {
-        const int depth = L - 1;
-        const int64_t ntot = (int64_t)nv << depth;
-        double sw = 0.0, swx = 0.0, swy = 0.0;
-        for (int64_t t0 = 0; t0 < ntot; t0 += 2) {
-            double At[2], qx[2], qy[2], ss[2], tt[2], f[2][4];
-            if (depth == 0) {  // fan triangles t0, t0 + 1 (the last one again for odd nv)
-#pragma unroll
-                for (int u = 0; u < 2; u++) {
-                    const int fi = (int)(t0 + u < ntot ? t0 + u : ntot - 1);
-                    double Q[3][2];
-                    quad_descend(rv[(int64_t)fi * ns], rv[(int64_t)(fi + 1 == nv ? 0 : fi + 1) * ns], 0, 0, Q);
-                    quad_leaf(Q, A, px, py, At[u], qx[u], qy[u], ss[u], tt[u], f[u]);
-                }
-            } else {           // siblings t0, t0 + 1 of parent t0 / 2
-                const int64_t par = t0 >> 1;
-                const int fi = (int)(par >> (depth - 1));
-                double Q[3][2];
-                quad_descend(rv[(int64_t)fi * ns], rv[(int64_t)(fi + 1 == nv ? 0 : fi + 1) * ns], depth - 1,
-                             par & (((int64_t)1 << (depth - 1)) - 1), Q);
-#pragma unroll
-                for (int u = 0; u < 2; u++) {
-                    double C[3][2];
-                    quad_split(Q, u, C);
-                    quad_leaf(C, A, px, py, At[u], qx[u], qy[u], ss[u], tt[u], f[u]);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < 2; u++) {
-                if (t0 + u >= ntot) break;
-                const double rho = clerp(clerp(f[u][0], f[u][1], ss[u]), clerp(f[u][2], f[u][3], ss[u]), tt[u]);
-                const double wgt = At[u] * rho;
-                sw += wgt;
-                swx += wgt * qx[u];
-                swy += wgt * qy[u];
-                nq++;
-            }
-        }
-        const double curx = swx / sw, cury = swy / sw;
-        const double dx = prevx - curx, dy = prevy - cury;
-        const double dist = sqrt(dx * dx + dy * dy);
-        prevx = curx;
-        prevy = cury;
-        if (dist < E) break;
-    }
-    cx = prevx;
-    cy = prevy;
-}
 
 // outputs of every stored ring: S3 triangles + keep rule and ELL rows, S4a centroid,
 // S5 treatment, warm-start neighbour lists, O8 counters -- one thread per cell
@@ -1034,23 +1066,8 @@ __global__ void __launch_bounds__(128, TM_OUT_MINB) k_output_t(CellArgs A, RingB
     }
     unsigned long long nq = 0;
     if (live && (MODE & (M_TREAT | M_HAT))) {
-        double S2 = 0.0, sx = 0.0, sy = 0.0;
-        for (int i = 0; i < nv; i++) {
-            const double2 a = RV(i), b = RV(i + 1 == nv ? 0 : i + 1);
-            const double cr = a.x * b.y - b.x * a.y;
-            S2 += cr;
-            sx += cr * (a.x + b.x);
-            sy += cr * (a.y + b.y);
-        }
         double cx, cy;
-        if (A.rho == nullptr) {
-            cx = sx / (3.0 * S2);
-            cy = sy / (3.0 * S2);
-            nq += nv;
-        } else {
-            const double dp = A.d_prev ? __ldg(A.d_prev + orig) : -1.0;
-            quad_centroid_g(rv0, ns, nv, px, py, 0.5 * S2, h, dp, A, cx, cy, nq);
-        }
+        ring_centroid(rv0, ns, nv, px, py, h, A.d_prev ? __ldg(A.d_prev + orig) : -1.0, A, cx, cy, nq);
         if (MODE & M_HAT) {
             A.x_hat[orig] = px + cx;
             A.y_hat[orig] = py + cy;
@@ -1101,7 +1118,7 @@ __global__ void __launch_bounds__(128, TM_OUT_MINB) k_output_t(CellArgs A, RingB
 namespace tmg {
 
 template <int MODE>
-tm_status launch_cells_thread(tm_ctx *ctx, const CellArgs &a) {
+static tm_status launch_cells_thread_impl(tm_ctx *ctx, const CellArgs &a) {
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         TM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_cells_t<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TSMEM));
@@ -1133,6 +1150,14 @@ tm_status launch_cells_thread(tm_ctx *ctx, const CellArgs &a) {
     b.nbr = nullptr;  // the neighbour lists were written by k_cells_t
     k_output_t<OMODE><<<(unsigned)((ctx->n_local + 127) / 128), 128, 0, ctx->stream>>>(b, R);
     return tm_internal_check_launch(ctx, "k_output_t");
+}
+
+// warm-started launches (neighbour lists of the previous launch on the same point set)
+// certify the warm rings warp-cooperatively (M_WCERT); cold ones run the flat search
+template <int MODE>
+tm_status launch_cells_thread(tm_ctx *ctx, const CellArgs &a) {
+    if (a.warm && !(ctx->p.flags & TM_F_NO_WCERT)) return launch_cells_thread_impl<MODE | M_WCERT>(ctx, a);
+    return launch_cells_thread_impl<MODE>(ctx, a);
 }
 
 #define TM_INST(M) template tm_status launch_cells_thread<M>(tm_ctx *, const CellArgs &);

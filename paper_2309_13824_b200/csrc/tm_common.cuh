@@ -57,15 +57,25 @@ TM_HD Line bisector(double dx, double dy) {
     return L;
 }
 
-// Cramer intersection of two lines, canonical: inv = fl(1/det),
-// x = fl(num_x * inv), y = fl(num_y * inv) -- one division per vertex and
-// exactly symmetric in (A, B).  Returns inv (for error bounds).
+// Cramer intersection of two lines in the canonical form of SURVEY §8.0 ("Canonical wall
+// vertices"): det = A.nx B.ny - A.ny B.nx, x = fl(num_x / det), y = fl(num_y / det), every
+// operation correctly rounded and uncontracted -- the same bits as the oracle's plain C,
+// and exactly symmetric in (A, B) (det and both numerators change sign).  Returns an upper
+// bound on 1/|det| for the vertex error bounds (a float reciprocal rounded up from a float
+// |det| rounded down: cheap, and +inf when |det| underflows, which only widens a filter).
+TM_HD double inv_det_bound(double det) {
+#if defined(__CUDA_ARCH__)
+    return (double)__frcp_ru(__double2float_rd(fabs(det)));
+#else
+    return (1.0 / fabs(det)) * (1.0 + 4.0 * 1.1102230246251565e-16);
+#endif
+}
+
 TM_HD double cramer(const Line &A, const Line &B, double &x, double &y) {
     double det = csub(cmul(A.nx, B.ny), cmul(A.ny, B.nx));
-    double inv = crcp(det);
-    x = cmul(csub(cmul(A.r, B.ny), cmul(A.ny, B.r)), inv);
-    y = cmul(csub(cmul(A.nx, B.r), cmul(A.r, B.nx)), inv);
-    return inv;
+    x = cdiv(csub(cmul(A.r, B.ny), cmul(A.ny, B.r)), det);
+    y = cdiv(csub(cmul(A.nx, B.r), cmul(A.r, B.nx)), det);
+    return inv_det_bound(det);
 }
 
 // wall codes: octagon side k (outward normal at 45k deg) -> -1-k;

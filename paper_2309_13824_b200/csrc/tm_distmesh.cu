@@ -158,11 +158,11 @@ extern "C" tm_status tm_distmesh_sums(tm_ctx *ctx, const int32_t *adj, const uin
     if (!adj || !deg || !sums2) TM_FAIL(ctx, TM_E_ARG, "null argument to tm_distmesh_sums");
     TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
     int64_t nblk = (ctx->n_local + DM_T - 1) / DM_T;
-    if (nblk > ctx->cap_partials) {
+    if (2 * nblk > ctx->cap_partials) {  // cap_partials counts doubles (shared with tm_mesh_stats)
         cudaFree(ctx->partials);
         ctx->partials = nullptr;
         TM_CUDA_TRY(ctx, cudaMalloc(&ctx->partials, 2 * nblk * sizeof(double)));
-        ctx->cap_partials = nblk;
+        ctx->cap_partials = 2 * nblk;
     }
     k_dm_sums<<<(unsigned)nblk, DM_T, 0, ctx->stream>>>(ctx->xs, ctx->ys, ctx->perm, ctx->gids, adj, deg,
                                                         ctx->n_local, ctx->n_owned, ctx->grid, ctx->mu,

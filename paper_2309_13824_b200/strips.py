@@ -54,6 +54,17 @@ class Strips:
         hi = self._cut(r + 1) if r < self.P - 1 else float("inf")
         return lo, hi
 
+    def check_width(self, W: float):
+        """Ghosts travel one strip only (to r-1 and r+1), so every interior strip must be at
+        least as wide as the halo W = 2 S_max: a point two strips away is then at least W >=
+        2 S_i from any cell it could otherwise cut (C_i lies in Oct_i, circumradius S_i).
+        Narrower strips would silently lose cells and triangles -- fail loudly instead."""
+        for r in range(1, self.P - 1):
+            lo, hi = self.bounds(r)
+            if not hi - lo >= W:
+                raise ValueError(f"strip {r} of {self.P} is {hi - lo:.3g} wide, narrower than the halo width "
+                                 f"W = {W:.3g}: use fewer strips (ghosts only reach the neighbouring strips)")
+
     def owner(self, x: torch.Tensor) -> torch.Tensor:
         if self.cuts is not None:
             c = torch.tensor(self.cuts, dtype=x.dtype, device=x.device)
@@ -271,6 +282,7 @@ def strip_iteration(st: RankState, strips: Strips, backend, exchange, W: float, 
                     allreduce=None) -> RankState:
     """One iteration on one rank.  `exchange(to_lo, to_hi) -> (from_lo, from_hi)`
     performs the neighbour exchange (collective over the ranks)."""
+    strips.check_width(W)
     lo, hi = strips.bounds(st.rank)
     h_lo, h_hi = backend.halo(st, lo, hi, W)
     g_lo, g_hi = exchange(h_lo, h_hi)
@@ -298,6 +310,7 @@ def loopback_iteration(states: List[RankState], strips: Strips, backends, W: flo
     Phases are run rank by rank with messages parked in a mailbox; the DistMesh
     sums are reduced across ranks between the two passes."""
     P = len(states)
+    strips.check_width(W)
     lb = Loopback(P)
     views = [lb.view(r) for r in range(P)]
     halos = []

@@ -70,10 +70,15 @@ def edges_from_adj(adj, deg):
     return E
 
 
-def compare(gpu, orc, box, mode, pos_tol=1e-12, ctx=""):
+def compare(gpu, orc, box, mode, pos_tol=1e-12, ctx="", exact_cvd=True):
     """Assert the parity bar: identical kept-triangle set (CCW, min first),
     identical ELL edge set (DistMesh), positions within pos_tol*diam(B) (L14),
-    identical status codes."""
+    identical status codes.  CVD positions are required to be BIT-identical
+    (exact_cvd): both sides build every cell vertex by the same correctly rounded
+    Cramer divisions and sum the centroid / quadrature in the same ring order
+    without contraction (L25), so the only remaining freedom is none.  DistMesh
+    positions differ by a few ulps (the force is a per-point gather on the GPU and
+    an edge loop in the oracle: another summation order)."""
     gt = tri_set(gpu["tri"])
     ot = tri_set(orc.tri)
     assert len(gt) == len(gpu["tri"]), f"{ctx}: duplicate GPU triangles"
@@ -89,6 +94,9 @@ def compare(gpu, orc, box, mode, pos_tol=1e-12, ctx=""):
     assert bad.size == 0, f"{ctx}: status differs at {bad[:5]} gpu={gpu['status'][bad[:5]]} or={orc.status[bad[:5]]}"
     derr = np.abs(gpu["d_prev"] - orc.d_prev)
     assert derr.max() <= pos_tol * diam, f"{ctx}: d_prev error {derr.max():.3e}"
+    if mode == "cvd" and exact_cvd:
+        nb = int(np.count_nonzero((gpu["x"] != orc.x) | (gpu["y"] != orc.y) | (gpu["d_prev"] != orc.d_prev)))
+        assert nb == 0, f"{ctx}: {nb} CVD positions not bit-identical (max error {err[k]:.3e})"
     if mode == "dm":
         ge = edges_from_adj(gpu["adj"], gpu["deg"])
         oe = set(map(tuple, orc.edges.tolist()))

@@ -94,3 +94,24 @@ def test_strips_gloo_matches_single_domain(world):
         # equal up to summation order (vertex rotation keys on local ids): the 1e-12*diam bar
         assert np.max(np.abs(xs - r.x)) < 1e-14 and np.max(np.abs(ys - r.y)) < 1e-14
         x, y, dp = r.x, r.y, r.d_prev
+
+
+def test_strip_narrower_than_halo_fails_loudly():
+    """ghosts only reach the neighbouring strips, so an interior strip narrower
+    than the halo width W would silently lose cells; the decomposition must refuse it.
+    n = 2000 points in the unit square split 8 ways: W = 2 * 5 * 2000^-1/2 = 0.22 > 1/8."""
+    import oracle as O
+    from inputs import configs
+    from paper_2309_13824_b200 import strips as S
+    n = 2000
+    box = (0.0, 0.0, 1.0, 1.0)
+    c, _ = O.domain(O.FieldSet(box, configs.box_phi(box, 64)), n)
+    W = S.ghost_width(c, 5.0)
+    assert W > 1.0 / 8
+    with pytest.raises(ValueError, match="narrower than the halo"):
+        S.Strips(0.0, 1.0, 8).check_width(W)
+    S.Strips(0.0, 1.0, 4).check_width(W)  # 0.25 >= 0.22: fine
+    x, y = configs.random_points(n, 3, box)
+    st = S.split_initial(torch.from_numpy(x), torch.from_numpy(y), S.Strips(0.0, 1.0, 8), 1)
+    with pytest.raises(ValueError):
+        S.strip_iteration(st, S.Strips(0.0, 1.0, 8), None, None, W, "cvd")
