@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(BLOCK, (G == 16 ? TM_MINB : 1)) k_cells(CellAr
             const int rh = __ldg(A.rlev + hby * bg.nbx + hbx);
             const int ux = leaf_coord(px, bg.x0, bg.isx, bg.nbx, rh), uy = leaf_coord(py, bg.y0, bg.isy, bg.nby, rh);
             const int nlx = bg.nbx << rh, nly = bg.nby << rh;
-            const double lsx = bg.sx / (double)(1 << rh), lsy = bg.sy / (double)(1 << rh);
+            const double lsx = bg.sx * pow2neg(rh), lsy = bg.sy * pow2neg(rh);
             for (int k = 1; !fail; k++) {
                 if (k > 1) {
                     double dl = px - (bg.x0 + (ux - k + 1) * lsx), dr = (bg.x0 + (ux + k) * lsx) - px;

@@ -68,6 +68,20 @@ typedef float KT;   // rounded up: still a valid bound
 #endif
 constexpr size_t TSMEM = (size_t)VMAX * TB * (16 + sizeof(KT) + (TM_R2_CACHE ? 4 : 0) + 4 + 1 + 1);
 
+// per-warp staging of the warm-certification phase (M_WCERT), after the rings: the warp's
+// cells (generator, prefilter data, ring masks, slot) and the queue of (cell, point) pairs
+struct WarpQ {
+    double cx[32], cy[32];
+    float4 cf[32];  // the group's cells relative to the group origin (float) and a (2 R_max)^2
+                    // bound rounded up with margin: a conservative prefilter, never the decision
+    unsigned used[32], wall[32];
+    int slot[32];
+    int qj[64];
+    uint8_t qc[64];
+};
+constexpr size_t TSMEM_W = TSMEM + (TB / 32) * sizeof(WarpQ);
+static_assert(TSMEM_W + 1024 <= 228 * 1024 / TM_TMINB, "5 blocks per SM must fit the shared memory");
+
 // this thread's view of the block's slot arrays (element k at [k * TB])
 struct TPoly {
     double2 *v;     // canonical coordinates relative to p_i
@@ -153,18 +167,26 @@ __device__ __forceinline__ int clip_t(TPoly &P, int code, const Line &L, const C
         for (int k = 0; k < VMAX; k++) dup |= (unsigned)(P.la[k * TB] == code) << k;
         if (dup & P.used) return 0;
     }
+    if (is_bis) {
 #pragma unroll
-    for (int k = 0; k < VMAX; k++) {
-        const double2 vv = P.v[k * TB];
-        const double del = fma(L.nx, vv.x, L.ny * vv.y) - L.r;
-        const double B = fma(n1, (double)P.K[k * TB], c8);
-        const bool pp = is_bis && !((P.wall >> k) & 1u);
-        const bool o = pp ? del > B : wall_out(L, vv.x, vv.y);
-        out |= (unsigned)o << k;
-        unc |= (unsigned)(pp && del <= B && del >= -B) << k;
+        for (int k = 0; k < VMAX; k++) {  // point-point filter on every slot (masked below)
+            const double2 vv = P.v[k * TB];
+            const double del = fma(L.nx, vv.x, L.ny * vv.y) - L.r;
+            const double B = fma(n1, (double)P.K[k * TB], c8);
+            out |= (unsigned)(del > B) << k;
+            unc |= (unsigned)(del <= B && del >= -B) << k;
+        }
     }
-    out &= P.used;
-    unc &= P.used;
+    // wall vertices (and every vertex when L is a wall): the canonical test (L25); interior
+    // cells have none once their neighbours bound them
+    const unsigned wset = is_bis ? (P.wall & P.used) : P.used;
+    out &= P.used & ~wset;
+    unc &= P.used & ~wset;
+    for (unsigned m = wset; m; m &= m - 1) {
+        const int k = __ffs(m) - 1;
+        const double2 vv = P.v[k * TB];
+        out |= (unsigned)wall_out(L, vv.x, vv.y) << k;
+    }
     // undecided point-point vertices (rare): exact incircle sign, outside the hot
     // loop -- or, with TM_THREAD_EXACT=0, the whole cell goes to the group kernel
 #if TM_THREAD_EXACT
@@ -358,8 +380,12 @@ struct RingBuf {
     uint8_t *n;                // vertices, 0 = no ring (ghost, failed, or retried)
 };
 
+#ifndef TM_WMINB
+#define TM_WMINB 5  // min resident blocks per SM of the warm-certification kernels (register cap)
+#endif
+
 template <int MODE>
-__global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *retry_list,
+__global__ void __launch_bounds__(TB, (MODE & M_WCERT) ? TM_WMINB : TM_TMINB) k_cells_t(CellArgs A, int32_t *retry_list,
                                                           unsigned long long *retry_cnt, RingBuf R) {
     // CVD split (TM_CVD_SPLIT): this kernel stores the ring and k_output_t computes the
     // centroid, quadrature and treatment -- a smaller kernel body for the search
@@ -449,8 +475,8 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
         uy = leaf_coord(py, bg.y0, bg.isy, bg.nby, rh);
         nlx = bg.nbx << rh;
         nly = bg.nby << rh;
-        lsx = bg.sx / (double)(1 << rh);
-        lsy = bg.sy / (double)(1 << rh);
+        lsx = bg.sx * pow2neg(rh);
+        lsy = bg.sy * pow2neg(rh);
         if constexpr (!(MODE & M_WCERT)) {
             // ring 1: the 8 neighbours nearest first (keys: d2 as float bits, low 3 bits = index)
             const double gl = px - (bg.x0 + ux * lsx), gr = (bg.x0 + (ux + 1) * lsx) - px;
@@ -628,44 +654,148 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
             }
             R2 = poly_R2(P);
         }
-        // ---- (B) certification (L11), one WARP per cell, cell by cell: every point within
-        // 2 R_max of p_c must be tested against the warm ring.  The lanes take the leaves of
-        // the box that can hold such points (home resolution, pruned by distance), then one
-        // candidate each: distance test, then the vertex test against the SAME ring (shared
-        // memory broadcast, a warp-uniform loop over its vertices).  A candidate that does not
-        // cut a ring cannot cut any later (smaller) ring, so only the rare cutters are clipped,
-        // sequentially, by the cell's own lane.
+        // ---- (B) certification (L11), warp-cooperative: every point within 2 R_max of p_c must be
+        // tested against cell c's warm ring.  The warp's cells are grouped by home leaf (cells are
+        // sorted by leaf); per group the lanes enumerate, once, the leaves of the union of the
+        // cells' 2 R_max boxes, take one candidate point each and distance-test it against every
+        // cell of the group.  The near (cell, point) pairs go to a per-warp queue; 32 at a time
+        // the lanes test one pair each against that cell's ring (shared memory).  A point that
+        // does not cut a ring cannot cut any later (smaller) ring, so only the rare cutters are
+        // clipped, by the cell's own lane, in any order: the cell is the same (exact topology).
+        WarpQ &W = reinterpret_cast<WarpQ *>(tsmem + TSMEM)[tid >> 5];
         const int wbase = tid & ~31;
-        const unsigned todo = __ballot_sync(0xffffffffu, live && !fail);
-        for (unsigned mc = todo; mc; mc &= mc - 1) {
-            const int c = __ffs(mc) - 1;
-            const double pcx = __shfl_sync(0xffffffffu, px, c), pcy = __shfl_sync(0xffffffffu, py, c);
-            const int rhc = __shfl_sync(0xffffffffu, rh, c), uxc = __shfl_sync(0xffffffffu, ux, c);
-            const int uyc = __shfl_sync(0xffffffffu, uy, c), hbc = __shfl_sync(0xffffffffu, hb, c);
-            const int hoffc = __shfl_sync(0xffffffffu, hoff, c);
-            const int cellc = (int)__shfl_sync(0xffffffffu, (int)cell, c);
-            unsigned usedc = __shfl_sync(0xffffffffu, P.used, c), wallc = __shfl_sync(0xffffffffu, P.wall, c);
-            float r2c = __shfl_sync(0xffffffffu, R2, c);
-            const TPoly Pc = tpoly_bind(tsmem, wbase + c);
-            // leaf box at the home resolution that can hold a point closer than 2 R_max
-            const double rad = 2.0 * sqrt((double)r2c * MARG) * (1.0 + 1e-6);
-            const double lsxc = bg.sx / (double)(1 << rhc), lsyc = bg.sy / (double)(1 << rhc);
-            const double sxl = bg.isx * (double)(1 << rhc), syl = bg.isy * (double)(1 << rhc);
-            const int nlxc = bg.nbx << rhc, nlyc = bg.nby << rhc;
-            const int cxa = max(0, (int)floor((pcx - rad - bg.x0) * sxl));
-            const int cxb = min(nlxc - 1, (int)floor((pcx + rad - bg.x0) * sxl));
-            const int cya = max(0, (int)floor((pcy - rad - bg.y0) * syl));
-            const int cyb = min(nlyc - 1, (int)floor((pcy + rad - bg.y0) * syl));
-            const int nLx = cxb - cxa + 1, nL = nLx * (cyb - cya + 1);
-            bool dead = false;
-            unsigned long long ncand = 0;
-            for (int l0 = 0; l0 < nL && !dead; l0 += 32) {
+        const bool act = live && !fail;
+        W.cx[lane] = px;
+        W.cy[lane] = py;
+        W.used[lane] = act ? P.used : 0u;
+        W.wall[lane] = P.wall;
+        W.slot[lane] = (int)cell;
+        const unsigned todo = __ballot_sync(0xffffffffu, act);
+        __syncwarp();
+        const unsigned lt = (1u << lane) - 1u;
+        int qn = 0;
+        // test the first m queued pairs (one per lane), clip the cutters, drop the tested pairs
+        auto flush = [&](int m) {
+            __syncwarp();
+            int cq = 0, jq = 0;
+            double dxq = 0.0, dyq = 0.0;
+            bool flq = false;
+            if (lane < m) {
+                jq = W.qj[lane];
+                cq = W.qc[lane];
+                const unsigned usedq = jq != W.slot[cq] ? W.used[cq] : 0u;
+                if (usedq) {
+                    dxq = csub(__ldg(A.xs + jq), W.cx[cq]);
+                    dyq = csub(__ldg(A.ys + jq), W.cy[cq]);
+                }
+                if (usedq && dxq == 0.0 && dyq == 0.0) {
+                    atomicAdd(&A.st->n_duplicate, 1ull);
+                } else if (usedq) {
+                    const Line L = bisector(dxq, dyq);
+                    const double n1 = fabs(L.nx) + fabs(L.ny);
+                    const double c8 = 8.0 * EPS * n1 * n1;
+                    const TPoly Pq = tpoly_bind(tsmem, wbase + cq);
+                    const unsigned wallq = W.wall[cq];
+                    unsigned hit = 0u, isl = 0u;
+#pragma unroll
+                    for (int k = 0; k < VMAX; k++) {  // all slots, masked: no divergence between rings
+                        const double2 vv = Pq.v[k * TB];
+                        isl |= (unsigned)(Pq.la[k * TB] == jq) << k;
+                        const double del = fma(L.nx, vv.x, L.ny * vv.y) - L.r;
+                        const bool o = ((wallq >> k) & 1u) ? wall_out(L, vv.x, vv.y)
+                                                           : del > -fma(n1, (double)Pq.K[k * TB], c8);
+                        hit |= (unsigned)o << k;
+                    }
+                    // cut or undecided, and not a line of the ring (a line already bounding it never cuts)
+                    flq = (hit & usedq) && !(isl & usedq);
+                }
+            }
+            __syncwarp();
+            // drop the tested pairs (qn - m < 32 remain)
+            int rj = 0, rc = 0;
+            const bool mv = lane < qn - m;
+            if (mv) { rj = W.qj[m + lane]; rc = W.qc[m + lane]; }
+            __syncwarp();
+            if (mv) { W.qj[lane] = rj; W.qc[lane] = (uint8_t)rc; }
+            qn -= m;
+            unsigned fb = __ballot_sync(0xffffffffu, flq);
+            while (fb) {
+                const int q = __ffs(fb) - 1;
+                fb &= fb - 1;
+                const int c = __shfl_sync(0xffffffffu, cq, q), j = __shfl_sync(0xffffffffu, jq, q);
+                const double dxc = __shfl_sync(0xffffffffu, dxq, q), dyc = __shfl_sync(0xffffffffu, dyq, q);
+                if (lane == c && !fail) {
+                    const unsigned long long c0 = cs.clips;
+                    const int fc = clip_t(P, j, bisector(dxc, dyc), cgm, A, cs);
+                    if (fc) {
+                        fail = fc;
+                        W.used[lane] = 0u;
+                    } else if (cs.clips != c0) {
+                        R2 = poly_R2(P);
+                        W.used[lane] = P.used;
+                        W.wall[lane] = P.wall;
+                    }
+                }
+                __syncwarp();
+            }
+        };
+        // groups: runs of lanes with the same home leaf
+        const unsigned long long lkey =
+            ((unsigned long long)rh << 48) | ((unsigned long long)(unsigned)ux << 24) | (unsigned)uy;
+        const unsigned long long lprev = __shfl_up_sync(0xffffffffu, lkey, 1);
+        for (unsigned hm = __ballot_sync(0xffffffffu, lane == 0 || lkey != lprev); hm;) {
+            const int g0 = __ffs(hm) - 1;
+            hm &= hm - 1;
+            const int g1 = hm ? __ffs(hm) - 1 : 32;
+            const unsigned gmask = (g1 == 32 ? 0xffffffffu : ((1u << g1) - 1u)) & ~((1u << g0) - 1u);
+            const unsigned gact = gmask & todo;
+            if (!gact) continue;
+            const int rhg = __shfl_sync(0xffffffffu, rh, g0), uxg = __shfl_sync(0xffffffffu, ux, g0);
+            const int uyg = __shfl_sync(0xffffffffu, uy, g0), hbg = __shfl_sync(0xffffffffu, hb, g0);
+            const int hoffg = __shfl_sync(0xffffffffu, hoff, g0);
+            const double lsxg = bg.sx * pow2neg(rhg), lsyg = bg.sy * pow2neg(rhg);
+            const double sxl = bg.isx * (double)(1 << rhg), syl = bg.isy * (double)(1 << rhg);
+            const int nlxg = bg.nbx << rhg, nlyg = bg.nby << rhg;
+            // union of the group's leaf boxes that can hold a point closer than 2 R_max
+            int bxa = INT_MAX, bxb = INT_MIN, bya = INT_MAX, byb = INT_MIN;
+            if ((gact >> lane) & 1u) {
+                const double rad = 2.0 * sqrt((double)R2 * MARG) * (1.0 + 1e-6);
+                bxa = max(0, (int)floor((px - rad - bg.x0) * sxl));
+                bxb = min(nlxg - 1, (int)floor((px + rad - bg.x0) * sxl));
+                bya = max(0, (int)floor((py - rad - bg.y0) * syl));
+                byb = min(nlyg - 1, (int)floor((py + rad - bg.y0) * syl));
+            }
+            bxa = __reduce_min_sync(0xffffffffu, bxa);
+            bxb = __reduce_max_sync(0xffffffffu, bxb);
+            bya = __reduce_min_sync(0xffffffffu, bya);
+            byb = __reduce_max_sync(0xffffffffu, byb);
+            // float prefilter data relative to the group origin (the first cell): distances of a
+            // few h are exact to ~1e-7 relative, far inside the 1e-4 margin of the bound
+            const double ox = __shfl_sync(0xffffffffu, px, g0), oy = __shfl_sync(0xffffffffu, py, g0);
+            if ((gact >> lane) & 1u)
+                W.cf[lane] = make_float4((float)(px - ox), (float)(py - oy),
+                                         __double2float_ru(4.0 * (double)R2 * MARG * (1.0 + 1e-4)), 0.f);
+            __syncwarp();
+            const float lxf = (float)(bg.x0 - ox), lyf = (float)(bg.y0 - oy);
+            const int nLx = bxb - bxa + 1, nL = nLx * (byb - bya + 1);
+            for (int l0 = 0; l0 < nL; l0 += 32) {
                 const int l = l0 + lane;
                 int st = 0, cnt = 0;
                 if (l < nL) {
-                    const int vx = cxa + l % nLx, vy = cya + l / nLx;
-                    if (leaf_d2(bg, lsxc, lsyc, vx, vy, pcx, pcy) * (1.0 - 1e-9) < 4.0 * (double)r2c * MARG)
-                        vleaf_range(A, vx, vy, rhc, uxc, uyc, hbc, hoffc, st, cnt);
+                    const int vy = l / nLx, vx = bxa + (l - vy * nLx);
+                    // any cell of the group within reach (float, conservative: the leaf is widened
+                    // by 1e-5 of its size, the bound carries a 1e-4 margin)
+                    const float ax = lxf + (float)(vx * lsxg), ay = lyf + (float)((bya + vy) * lsyg);
+                    const float wx = (float)lsxg, wy = (float)lsyg, ex = 1e-5f * wx, ey = 1e-5f * wy;
+                    bool need = false;
+                    for (unsigned m = gact; m; m &= m - 1) {
+                        const int c = __ffs(m) - 1;
+                        const float4 q = W.cf[c];
+                        const float gx = fmaxf(fmaxf(ax - ex - q.x, q.x - (ax + wx + ex)), 0.f);
+                        const float gy = fmaxf(fmaxf(ay - ey - q.y, q.y - (ay + wy + ey)), 0.f);
+                        need |= gx * gx + gy * gy < q.z;
+                    }
+                    if (need) vleaf_range(A, vx, bya + vy, rhg, uxg, uyg, hbg, hoffg, st, cnt);
                 }
                 int incl = cnt;
 #pragma unroll
@@ -674,77 +804,43 @@ __global__ void __launch_bounds__(TB, TM_TMINB) k_cells_t(CellArgs A, int32_t *r
                     if (lane >= o) incl += u;
                 }
                 const int tot = __shfl_sync(0xffffffffu, incl, 31);
-                ncand += (unsigned long long)tot;
-                for (int base = 0; base < tot && !dead; base += 32) {
+                if ((gact >> lane) & 1u) sc.n_cand += (unsigned long long)tot;
+                for (int base = 0; base < tot; base += 32) {
                     trips++;
                     const int tt = base + lane;
-                    // leaf of candidate tt: the number of leaves whose inclusive count is <= tt
-                    int k = 0;
+                    int k = 0;  // leaf of candidate tt: the leaves whose inclusive count is <= tt
 #pragma unroll
                     for (int s = 16; s > 0; s >>= 1)
                         if (__shfl_sync(0xffffffffu, incl, k + s - 1) <= tt) k += s;
                     const int kk = k < 31 ? k : 31;
                     const int stk = __shfl_sync(0xffffffffu, st, kk);
                     const int exk = __shfl_sync(0xffffffffu, incl - cnt, kk);
+                    const bool valid = tt < tot;
                     const int j = stk + (tt - exk);
-                    bool flag = false;
-                    double dx = 0.0, dy = 0.0, d2 = 0.0;
-                    if (tt < tot && j != cellc) {
-                        dx = csub(__ldg(A.xs + j), pcx);
-                        dy = csub(__ldg(A.ys + j), pcy);
-                        d2 = dx * dx + dy * dy;
-                        if (dx == 0.0 && dy == 0.0) atomicAdd(&A.st->n_duplicate, 1ull);
-                        flag = d2 < 4.0 * (double)r2c * MARG && d2 > 0.0;
-                    }
-                    if (__any_sync(0xffffffffu, flag)) {
-                        const Line L = bisector(dx, dy);
-                        const double n1 = fabs(L.nx) + fabs(L.ny);
-                        const double c8 = 8.0 * EPS * n1 * n1;
-                        bool hit = false, isline = false;
-                        for (unsigned mm = usedc; mm; mm &= mm - 1) {  // warp-uniform: the same ring
-                            const int q = __ffs(mm) - 1;
-                            const double2 vv = Pc.v[q * TB];
-                            isline |= Pc.la[q * TB] == j;
-                            if ((wallc >> q) & 1u) {
-                                hit |= wall_out(L, vv.x, vv.y);
-                            } else {
-                                const double del = fma(L.nx, vv.x, L.ny * vv.y) - L.r;
-                                hit |= del > -fma(n1, (double)Pc.K[q * TB], c8);  // cut or undecided
+                    float xjf = 3e38f, yjf = 3e38f;
+                    if (valid) { xjf = (float)(__ldg(A.xs + j) - ox); yjf = (float)(__ldg(A.ys + j) - oy); }
+                    for (unsigned m = gact; m; m &= m - 1) {
+                        const int c = __ffs(m) - 1;
+                        const float4 q = W.cf[c];
+                        const float dx = xjf - q.x, dy = yjf - q.y;
+                        // conservative: a few extra pairs are harmless, the ring test decides (the
+                        // cell's own point and exact duplicates are sorted out there)
+                        const bool near = fmaf(dx, dx, dy * dy) < q.z;
+                        const unsigned b = __ballot_sync(0xffffffffu, near);
+                        if (b) {
+                            if (near) {
+                                const int pos = qn + __popc(b & lt);
+                                W.qj[pos] = j;
+                                W.qc[pos] = (uint8_t)c;
                             }
+                            qn += __popc(b);
+                            if (qn >= 32) flush(32);
                         }
-                        flag = flag && hit && !isline;  // a line of the ring never cuts it (L already bounds it)
-                    }
-                    // the rare (possible) cutters, nearest first, clipped by the cell's own lane; the
-                    // full clip test there also decides undecided vertices (-1: 32-lane pass)
-                    unsigned fl = __ballot_sync(0xffffffffu, flag);
-                    while (fl) {
-                        float best = __uint_as_float(0x7f800000u);
-                        int q = 0;
-                        for (unsigned m2 = fl; m2; m2 &= m2 - 1) {
-                            const int b = __ffs(m2) - 1;
-                            const float db = __shfl_sync(0xffffffffu, (float)d2, b);
-                            if (db < best) { best = db; q = b; }
-                        }
-                        fl &= ~(1u << q);
-                        const int jq = __shfl_sync(0xffffffffu, j, q);
-                        const double dxq = __shfl_sync(0xffffffffu, dx, q), dyq = __shfl_sync(0xffffffffu, dy, q);
-                        int fc = 0;
-                        if (lane == c) {
-                            const unsigned long long c0 = cs.clips;
-                            fc = clip_t(P, jq, bisector(dxq, dyq), cgm, A, cs);
-                            if (fc) fail = fc;
-                            else if (cs.clips != c0) R2 = poly_R2(P);
-                        }
-                        fc = __shfl_sync(0xffffffffu, fc, c);
-                        usedc = __shfl_sync(0xffffffffu, P.used, c);
-                        wallc = __shfl_sync(0xffffffffu, P.wall, c);
-                        r2c = __shfl_sync(0xffffffffu, R2, c);
-                        if (fc) { dead = true; break; }
                     }
                 }
             }
-            if (lane == c) sc.n_cand += ncand;
         }
+        if (qn > 0) flush(qn);
     }
     if (live) {
         if (fail == -1) {
@@ -1120,8 +1216,9 @@ namespace tmg {
 template <int MODE>
 static tm_status launch_cells_thread_impl(tm_ctx *ctx, const CellArgs &a) {
     static bool attr_set = false;  // per instantiation
+    constexpr size_t smem = (MODE & M_WCERT) ? TSMEM_W : TSMEM;
     if (!attr_set) {
-        TM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_cells_t<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TSMEM));
+        TM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_cells_t<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set = true;
     }
     constexpr bool CSPLIT = !(MODE & M_COUNT) && ((TM_CVD_SPLIT >= 1 && (MODE & (M_TREAT | M_HAT))) ||
@@ -1143,7 +1240,7 @@ static tm_status launch_cells_thread_impl(tm_ctx *ctx, const CellArgs &a) {
         R.n = (uint8_t *)ctx->ring_n;
     }
     const unsigned blocks = (unsigned)((ctx->n_local + TB - 1) / TB);
-    k_cells_t<MODE><<<blocks, TB, TSMEM, ctx->stream>>>(a, ctx->retry_list, ctx->retry_cnt, R);
+    k_cells_t<MODE><<<blocks, TB, smem, ctx->stream>>>(a, ctx->retry_list, ctx->retry_cnt, R);
     tm_status s = tm_internal_check_launch(ctx, "k_cells_t");
     if (s != TM_OK || !CSPLIT) return s;
     CellArgs b = a;

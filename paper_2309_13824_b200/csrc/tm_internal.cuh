@@ -46,6 +46,16 @@ __host__ __device__ __forceinline__ uint32_t part1by1(uint32_t v) {
 }
 __host__ __device__ __forceinline__ uint32_t morton2(uint32_t x, uint32_t y) { return part1by1(x) | (part1by1(y) << 1); }
 
+// 2^-r for 0 <= r <= MAX_SUBLEVEL, exactly: leaf sizes bg.sx * 2^-r are the same bits as
+// bg.sx / 2^r (scaling by a power of two is exact), without a DP division
+__host__ __device__ __forceinline__ double pow2neg(int r) {
+#if defined(__CUDA_ARCH__)
+    return __longlong_as_double((long long)(1023 - r) << 52);
+#else
+    return 1.0 / (double)(1 << r);
+#endif
+}
+
 // leaf coordinate of x at depth r (consistent between binning and search):
 // floor((x-x0)*isx*2^r) clamped into the level-0 bin floor((x-x0)*isx)
 __device__ __forceinline__ int leaf_coord(double x, double x0, double is, int nb, int r) {
