@@ -380,6 +380,36 @@ struct RingBuf {
     uint8_t *n;                // vertices, 0 = no ring (ghost, failed, or retried)
 };
 
+// initial ring B ∩ Oct_i: the octagon (vertex k between sides k and k+1), clipped by the box
+// sides it crosses.  Returns the clip status (0 ok).
+__device__ __forceinline__ int init_ring(TPoly &P, const CellGeom &g, double S, const CellArgs &A, ClipStats &cs) {
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        // consecutive octagon sides have det = 1 exactly, so the canonical Cramer vertex is
+        // the numerators themselves (x / 1 = x): no division
+        const Line La = wall_line(-1 - k, g.px, g.py, g.r_oct, g.bx0, g.by0, g.bx1, g.by1);
+        const Line Lb = wall_line(-1 - ((k + 1) & 7), g.px, g.py, g.r_oct, g.bx0, g.by0, g.bx1, g.by1);
+        const double x = csub(cmul(La.r, Lb.ny), cmul(La.ny, Lb.r));
+        const double y = csub(cmul(La.nx, Lb.r), cmul(La.r, Lb.nx));
+        P.v[k * TB] = make_double2(x, y);
+        P.K[k * TB] = store_K(-1.0);
+        set_r2(P, k, x, y, -1.0);
+        P.la[k * TB] = -1 - k;
+        P.prv[k * TB] = (uint8_t)((k + 7) & 7);
+        P.nxt[k * TB] = (uint8_t)((k + 1) & 7);
+    }
+    P.used = 0xffu;
+    P.wall = 0xffu;
+    int fail = 0;
+    if (csub(g.px, g.bx0) < S || csub(g.bx1, g.px) < S || csub(g.py, g.by0) < S || csub(g.by1, g.py) < S) {
+        for (int b = 0; b < 4 && !fail; b++) {
+            const int code = -9 - b;
+            fail = clip_t(P, code, wall_line(code, g.px, g.py, g.r_oct, g.bx0, g.by0, g.bx1, g.by1), g, A, cs);
+        }
+    }
+    return fail;
+}
+
 #ifndef TM_WMINB
 #define TM_WMINB 5  // min resident blocks per SM of the warm-certification kernels (register cap)
 #endif
@@ -427,6 +457,7 @@ __global__ void __launch_bounds__(TB, (MODE & M_WCERT) ? TM_WMINB : TM_TMINB) k_
     int wi = 0, wn = 0;  // warm-start cursor (phase -1)
     int ph = 2, rr = 0, t = 0, tend = 0, cvx = 0, cvy = 0, cend = -1, cfix = 0, rk = 1, side = 4, kmax = 0;
     int bxa = 0, bxb = -1, bya = 0, byb = -1;
+    double r_oct = 0.0;
     if (live) {
         px = __ldg(A.xs + cell);
         py = __ldg(A.ys + cell);
@@ -436,33 +467,12 @@ __global__ void __launch_bounds__(TB, (MODE & M_WCERT) ? TM_WMINB : TM_TMINB) k_
         if (nid < 0 || (int64_t)nid >= A.nbr_keys) nid = -1;  // outside the key space: no warm start
         sc.px = px; sc.py = py; sc.cell = (int)cell;
         const double S = cmul(A.fac_voro, h);
-        const double r_oct = cmul(S, COS_PI8);
+        r_oct = cmul(S, COS_PI8);
         const double bx0 = A.grid.x0, by0 = A.grid.y0, bx1 = A.grid.x1, by1 = A.grid.y1;
         cgm = {px, py, r_oct, bx0, by0, bx1, by1};
-        // ---- initial ring: octagon, vertex k between sides k and k+1 (det = +-1: exact inverse)
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-            // consecutive octagon sides have det = 1 exactly, so the canonical Cramer
-            // vertex is the numerators themselves (x * fl(1/1) = x): no division
-            const Line La = wall_line(-1 - k, px, py, r_oct, bx0, by0, bx1, by1);
-            const Line Lb = wall_line(-1 - ((k + 1) & 7), px, py, r_oct, bx0, by0, bx1, by1);
-            const double x = csub(cmul(La.r, Lb.ny), cmul(La.ny, Lb.r));
-            const double y = csub(cmul(La.nx, Lb.r), cmul(La.r, Lb.nx));
-            P.v[k * TB] = make_double2(x, y);
-            P.K[k * TB] = store_K(-1.0);
-            set_r2(P, k, x, y, -1.0);
-            P.la[k * TB] = -1 - k;
-            P.prv[k * TB] = (uint8_t)((k + 7) & 7);
-            P.nxt[k * TB] = (uint8_t)((k + 1) & 7);
-        }
-        P.used = 0xffu;
-        P.wall = 0xffu;
-        if (csub(px, bx0) < S || csub(bx1, px) < S || csub(py, by0) < S || csub(by1, py) < S) {
-            for (int b = 0; b < 4 && !fail; b++) {
-                const int code = -9 - b;
-                fail = clip_t(P, code, wall_line(code, px, py, r_oct, bx0, by0, bx1, by1), cgm, A, cs);
-            }
-        }
+        // the flat search starts from B ∩ Oct_i; the warm path only when its direct
+        // construction fails (phase A below)
+        if constexpr (!(MODE & M_WCERT)) fail = init_ring(P, cgm, S, A, cs);
         R2 = poly_R2(P);
         // ---- candidate order over the two-level cell list (L11 stopping rule)
         int hbx = (int)floor((px - bg.x0) * bg.isx), hby = (int)floor((py - bg.y0) * bg.isy);
@@ -638,6 +648,7 @@ __global__ void __launch_bounds__(TB, (MODE & M_WCERT) ? TM_WMINB : TM_TMINB) k_
         // check).  Every lane clips about the same number (~6) of lines: uniform work.
         if (live && !fail) {
             if (wn == 0) fail = -1;  // no warm list: the 32-lane pass computes the cell from scratch
+            if (!fail) fail = init_ring(P, cgm, cmul(A.fac_voro, h), A, cs);
             for (int w = 0; w < wn && !fail; w++) {
                 const int id = A.nbr[(int64_t)nid * TM_NBR + w];
                 if (id < 0 || (int64_t)id >= A.nbr_keys) continue;
