@@ -248,20 +248,23 @@ extern "C" tm_status tm_set_domain(tm_ctx *ctx, const tm_fields *f, int64_t n_to
     if (e != cudaSuccess) TM_FAIL(ctx, TM_E_CUDA, "set_domain: %s", cudaGetErrorString(e));
     if (!(h3[2] > 0)) TM_FAIL(ctx, TM_E_ARG, "the SDF grid has no cell with phi < 0");
     // c = sqrt( sum_w * (dx*dy) / N ),  h_avg = c * (sum_mu / count)   (same order as the definition)
-    ctx->lip_mu = 0.0;
-    if (has_mu) {
+    // Lipschitz constants of the bilinear interpolants of mu (adaptive halo widths) and phi
+    // (keep-rule fast path of the cell kernels)
+    {
         unsigned long long *dl;
-        TM_CUDA_TRY(ctx, cudaMalloc(&dl, sizeof(unsigned long long)));
-        TM_CUDA_TRY(ctx, cudaMemsetAsync(dl, 0, sizeof(unsigned long long), ctx->stream));
-        k_lipschitz<<<(unsigned)((ncell + 255) / 256), 256, 0, ctx->stream>>>(g, ctx->mu, dl);
-        unsigned long long hl = 0;
-        cudaError_t e2 = cudaMemcpyAsync(&hl, dl, sizeof(hl), cudaMemcpyDeviceToHost, ctx->stream);
+        TM_CUDA_TRY(ctx, cudaMalloc(&dl, 2 * sizeof(unsigned long long)));
+        TM_CUDA_TRY(ctx, cudaMemsetAsync(dl, 0, 2 * sizeof(unsigned long long), ctx->stream));
+        if (has_mu) k_lipschitz<<<(unsigned)((ncell + 255) / 256), 256, 0, ctx->stream>>>(g, ctx->mu, dl);
+        k_lipschitz<<<(unsigned)((ncell + 255) / 256), 256, 0, ctx->stream>>>(g, ctx->phi, dl + 1);
+        unsigned long long hl[2] = {0, 0};
+        cudaError_t e2 = cudaMemcpyAsync(hl, dl, sizeof(hl), cudaMemcpyDeviceToHost, ctx->stream);
         if (e2 == cudaSuccess) e2 = cudaStreamSynchronize(ctx->stream);
         cudaFree(dl);
         if (e2 != cudaSuccess) TM_FAIL(ctx, TM_E_CUDA, "set_domain: %s", cudaGetErrorString(e2));
-        double L;
-        memcpy(&L, &hl, sizeof(L));
-        ctx->lip_mu = L;
+        double L[2];
+        memcpy(L, hl, sizeof(L));
+        ctx->lip_mu = has_mu ? L[0] : 0.0;
+        ctx->lip_phi = L[1];
     }
     ctx->c = sqrt(cdiv(cmul(h3[0], cmul(g.dx, g.dy)), (double)n_total));
     ctx->h_avg = cmul(ctx->c, cdiv(h3[1], h3[2]));
@@ -605,6 +608,7 @@ tm_status tm_internal_fill_cell_args(tm_ctx *ctx, CellArgs *a) {
     a->grid = ctx->grid;
     a->phi = ctx->phi; a->mu = ctx->mu; a->rho = ctx->rho;
     a->c = ctx->c; a->h_avg = ctx->h_avg;
+    a->lip_mu = ctx->lip_mu; a->lip_phi = ctx->lip_phi;
     a->fac_voro = ctx->p.fac_voro_bound; a->fac_pt = ctx->p.fac_pt_mvmt;
     a->fac_geps = ctx->p.fac_geps; a->fac_end = ctx->p.fac_end_mvmt;
     a->damping = ctx->p.newton_damping; a->keep_tol = ctx->p.keep_tol;

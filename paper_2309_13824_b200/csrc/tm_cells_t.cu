@@ -75,7 +75,6 @@ struct WarpQ {
     float4 cf[32];  // the group's cells relative to the group origin (float) and a (2 R_max)^2
                     // bound rounded up with margin: a conservative prefilter, never the decision
     unsigned used[32], wall[32];
-    int slot[32];
     int qj[64];
     uint8_t qc[64];
 };
@@ -410,6 +409,30 @@ __device__ __forceinline__ int init_ring(TPoly &P, const CellGeom &g, double S, 
     return fail;
 }
 
+// Keep rule fast path (S3, P:499-510 in reading L10): every Delaunay triangle around p_i is kept
+// when the cell is deep inside -- then the canonical keep_tri would return true for each of them,
+// so it need not run.  The triangle (i, a, b) of a point-point ring vertex has its exact
+// circumcentre c within R_i of p_i (R_i: the rounded-up max vertex distance plus error bound
+// the search uses) and |p_x - c| = |p_i - c| for x in {i, a, b}; its centroid lies within
+// 4 R_i / 3 of p_i (|p_a - p_i| <= 2 R_i).  So it is kept if
+//   * c stays inside B: p_i farther than R_i from every box side;
+//   * c is in the three octagons: R_i below their inradius r_x = fac h(p_x) cos(pi/8), with
+//     h(p_x) >= h(p_i) - c L_mu 2 R_i (h = c mu~, mu~ L_mu-Lipschitz);
+//   * phi~(g) < keep_tol: phi~(p_i) + L_phi 4 R_i / 3 < keep_tol (phi~ L_phi-Lipschitz).
+// All with relative margins (1e-9 .. 1e-6) far above the canonical arithmetic's rounding.
+__device__ __forceinline__ bool interior_keeps_all(const TPoly &P, const CellArgs &A, double px, double py, double h) {
+    if (P.wall & P.used) return false;
+    const double R = sqrt((double)poly_R2(P)) * (1.0 + 1e-9);
+    const Grid &g = A.grid;
+    if (!(px - g.x0 > R * (1.0 + 1e-9) + 1e-300 && g.x1 - px > R * (1.0 + 1e-9) && py - g.y0 > R * (1.0 + 1e-9) &&
+          g.y1 - py > R * (1.0 + 1e-9)))
+        return false;
+    const double hmin = (h - A.c * A.lip_mu * 2.0 * R) * (1.0 - 1e-9);
+    if (!(R < A.fac_voro * hmin * COS_PI8 * (1.0 - 1e-9))) return false;
+    const double ph = bilinear(g, A.phi, px, py, LdgLoad());
+    return ph + A.lip_phi * (4.0 / 3.0) * R * (1.0 + 1e-6) + 1e-12 * (1.0 + fabs(ph)) < A.keep_tol;
+}
+
 #ifndef TM_WMINB
 #define TM_WMINB 5  // min resident blocks per SM of the warm-certification kernels (register cap)
 #endif
@@ -680,7 +703,6 @@ __global__ void __launch_bounds__(TB, (MODE & M_WCERT) ? TM_WMINB : TM_TMINB) k_
         W.cy[lane] = py;
         W.used[lane] = act ? P.used : 0u;
         W.wall[lane] = P.wall;
-        W.slot[lane] = (int)cell;
         const unsigned todo = __ballot_sync(0xffffffffu, act);
         __syncwarp();
         const unsigned lt = (1u << lane) - 1u;
@@ -694,7 +716,7 @@ __global__ void __launch_bounds__(TB, (MODE & M_WCERT) ? TM_WMINB : TM_TMINB) k_
             if (lane < m) {
                 jq = W.qj[lane];
                 cq = W.qc[lane];
-                const unsigned usedq = jq != W.slot[cq] ? W.used[cq] : 0u;
+                const unsigned usedq = (int64_t)jq != (int64_t)blockIdx.x * TB + wbase + cq ? W.used[cq] : 0u;
                 if (usedq) {
                     dxq = csub(__ldg(A.xs + jq), W.cx[cq]);
                     dyq = csub(__ldg(A.ys + jq), W.cy[cq]);
@@ -729,25 +751,29 @@ __global__ void __launch_bounds__(TB, (MODE & M_WCERT) ? TM_WMINB : TM_TMINB) k_
             __syncwarp();
             if (mv) { W.qj[lane] = rj; W.qc[lane] = (uint8_t)rc; }
             qn -= m;
+            // cutters (rare): in rounds, the lowest flagged lane of every cell clips that cell --
+            // cells differ between the round's leaders, so they clip in parallel.  The ring's
+            // masks live in shared memory during the certification; the owners reload them after.
             unsigned fb = __ballot_sync(0xffffffffu, flq);
             while (fb) {
-                const int q = __ffs(fb) - 1;
-                fb &= fb - 1;
-                const int c = __shfl_sync(0xffffffffu, cq, q), j = __shfl_sync(0xffffffffu, jq, q);
-                const double dxc = __shfl_sync(0xffffffffu, dxq, q), dyc = __shfl_sync(0xffffffffu, dyq, q);
-                if (lane == c && !fail) {
-                    const unsigned long long c0 = cs.clips;
-                    const int fc = clip_t(P, j, bisector(dxc, dyc), cgm, A, cs);
-                    if (fc) {
-                        fail = fc;
-                        W.used[lane] = 0u;
-                    } else if (cs.clips != c0) {
-                        R2 = poly_R2(P);
-                        W.used[lane] = P.used;
-                        W.wall[lane] = P.wall;
+                const unsigned same = __match_any_sync(0xffffffffu, flq ? cq : -1 - lane);
+                if (flq && __ffs(same) - 1 == lane) {
+                    const int ct = wbase + cq;  // thread (and ring) of cell cq in this block
+                    TPoly Pc = tpoly_bind(tsmem, ct);
+                    Pc.used = W.used[cq];
+                    Pc.wall = W.wall[cq];
+                    if (Pc.used) {
+                        const double roc =
+                            cmul(cmul(A.fac_voro, __ldg(A.hs + (int64_t)blockIdx.x * TB + ct)), COS_PI8);
+                        const CellGeom gc = {W.cx[cq], W.cy[cq], roc, A.grid.x0, A.grid.y0, A.grid.x1, A.grid.y1};
+                        const int fc = clip_t(Pc, jq, bisector(dxq, dyq), gc, A, cs);
+                        W.used[cq] = fc ? 0u : Pc.used;  // 0: the cell failed, its code in wall
+                        W.wall[cq] = fc ? (unsigned)fc : Pc.wall;
                     }
+                    flq = false;
                 }
                 __syncwarp();
+                fb = __ballot_sync(0xffffffffu, flq);
             }
         };
         // groups: runs of lanes with the same home leaf
@@ -852,6 +878,15 @@ __global__ void __launch_bounds__(TB, (MODE & M_WCERT) ? TM_WMINB : TM_TMINB) k_
             }
         }
         if (qn > 0) flush(qn);
+        __syncwarp();
+        if (act) {  // the certified ring (or the failure) back to its owner
+            if (W.used[lane]) {
+                P.used = W.used[lane];
+                P.wall = W.wall[lane];
+            } else {
+                fail = (int)W.wall[lane];
+            }
+        }
     }
     if (live) {
         if (fail == -1) {
@@ -903,13 +938,17 @@ __global__ void __launch_bounds__(TB, (MODE & M_WCERT) ? TM_WMINB : TM_TMINB) k_
     int ell = 0;
     if (!TSPLIT && live && (MODE & (M_TRI | M_ELL))) {
         unsigned keptall = 0;  // for the ELL: kept, owned or not
+        const bool all_in = interior_keeps_all(P, A, px, py, h);
         int k = start;
         for (int c = 0; c < nv; c++) {
             const int kn = P.nxt[k * TB];
             const int a = P.la[k * TB], b = P.la[kn * TB];
             if (a >= 0 && b >= 0) {
                 const int32_t ga = __ldg(A.gids + a), gb = __ldg(A.gids + b);
-                if (gi < ga && gi < gb) {
+                if (all_in) {
+                    keptall |= 1u << k;
+                    if (gi < ga && gi < gb) keptmask |= 1u << k;
+                } else if (gi < ga && gi < gb) {
                     const int sv = ga < gb ? a : b, sw = ga < gb ? b : a;
                     if (keep_tri(A, (int)cell, sv, sw, cadd(px, P.v[k * TB].x), cadd(py, P.v[k * TB].y))) {
                         keptmask |= 1u << k;

@@ -83,6 +83,7 @@ struct CellArgs {
     Grid grid;
     const double *phi, *mu, *rho;
     double c, h_avg;
+    double lip_mu, lip_phi;  // Lipschitz constants of mu~ and phi~ (0 for uniform mu)
     double fac_voro, fac_pt, fac_geps, fac_end, damping, keep_tol;
     int32_t newton_max, quad_max;
     // outputs
@@ -111,6 +112,7 @@ struct tm_ctx {
     tmg::Grid grid;
     double c = 0, h_avg = 0;
     double lip_mu = 0;  // Lipschitz constant of mu~ (0 for uniform sizing): adaptive halo widths
+    double lip_phi = 0; // Lipschitz constant of phi~ (keep-rule fast path)
     int64_t n_total = 0;
     double *phi = nullptr, *mu = nullptr, *rho = nullptr;
     size_t grid_bytes = 0;
