@@ -93,6 +93,10 @@ typedef struct {
 #define TM_F_GROUP_CELLS    0x4u  /* cells by 16-lane groups instead of one thread per cell  */
 #define TM_F_NO_WCERT       0x8u  /* warm-started launches: flat search instead of warm clips +
                                      warp-cooperative certification (A/B and tests)        */
+#define TM_F_NO_PACKED_GRIDS 0x10u /* bilinear rho lookups from the node grid rows instead of the
+                                      packed 4-corner cells of tm_set_domain (A/B and tests)   */
+#define TM_F_NO_DEEP_PASS   0x20u  /* one output pass for every quadrature depth instead of
+                                      deferring deep cells to a compacted pass (A/B, tests) */
 
 /* Mesh quality (alpha = R_circ/(2 R_in), beta = l_max/l_min) and
  * the health counters accumulated since the previous synchronising call

@@ -30,6 +30,8 @@ TM_F_TWO_LEVEL_BINS = 0x1
 TM_F_COUNT_WORK = 0x2
 TM_F_GROUP_CELLS = 0x4
 TM_F_NO_WCERT = 0x8
+TM_F_NO_PACKED_GRIDS = 0x10
+TM_F_NO_DEEP_PASS = 0x20
 
 
 class TmError(RuntimeError):

@@ -72,12 +72,13 @@ extern "C" void tm_destroy(tm_ctx *ctx) {
     free_points(ctx);
     cudaFree(ctx->bin_count); cudaFree(ctx->rlev); cudaFree(ctx->leaf_off); cudaFree(ctx->block_sums);
     cudaFree(ctx->leaf_count); cudaFree(ctx->leaf_start);
-    cudaFree(ctx->phi); cudaFree(ctx->mu); cudaFree(ctx->rho);
+    cudaFree(ctx->phi); cudaFree(ctx->mu); cudaFree(ctx->rho); cudaFree(ctx->rho4);
     cudaFree(ctx->partials); cudaFree(ctx->stat_acc); cudaFree(ctx->dst);
     cudaFree(ctx->retry_list); cudaFree(ctx->retry_cnt);
     cudaFree(ctx->mig_keep); cudaFree(ctx->mig_cnt); cudaFree(ctx->mig_off);
     cudaFree(ctx->nbr); cudaFree(ctx->nbr_cnt); cudaFree(ctx->inv_id);
     cudaFree(ctx->ring_v); cudaFree(ctx->ring_la); cudaFree(ctx->ring_n);
+    cudaFree(ctx->deep_list); cudaFree(ctx->deep_cnt);
     delete ctx;
 }
 
@@ -191,6 +192,16 @@ __global__ void __launch_bounds__(256) k_domain_sums(int64_t n, const double *__
 // Lipschitz constant of the bilinear interpolant mu~ (continuous, bilinear per cell):
 // max over cells of |grad| <= sqrt(gx^2 + gy^2), gx = max(|f10-f00|,|f11-f01|)/dx, gy
 // likewise; kept as the bits of a positive double (atomicMax on the integer view)
+// the four corners of every grid cell contiguous: (f00, f10, f01, f11) of cell (i, j)
+__global__ void k_pack_corners(Grid g, const double *__restrict__ f, double4 *__restrict__ out) {
+    const int64_t ncx = g.nx - 1, ncy = g.ny - 1;
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= ncx * ncy) return;
+    const int64_t j = k / ncx, i = k % ncx;
+    const double *r0 = f + j * g.nx, *r1 = r0 + g.nx;
+    out[k] = make_double4(r0[i], r0[i + 1], r1[i], r1[i + 1]);
+}
+
 __global__ void k_lipschitz(Grid g, const double *mu, unsigned long long *out) {
     const int64_t ncx = g.nx - 1, ncy = g.ny - 1;
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -270,6 +281,15 @@ extern "C" tm_status tm_set_domain(tm_ctx *ctx, const tm_fields *f, int64_t n_to
     ctx->h_avg = cmul(ctx->c, cdiv(h3[1], h3[2]));
     if (!has_mu) { cudaFree(ctx->mu); ctx->mu = nullptr; ctx->grid_bytes = 0; }
     if (!has_rho) { cudaFree(ctx->rho); ctx->rho = nullptr; ctx->grid_bytes = 0; }
+    // S0 packing: each grid cell's four corners of rho contiguous, 32 bytes,
+    // so the quadrature's bilinear lookups cost one sector instead of two rows
+    cudaFree(ctx->rho4);
+    ctx->rho4 = nullptr;
+    if (has_rho) {
+        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->rho4, (size_t)ncell * sizeof(double4)));
+        k_pack_corners<<<(unsigned)((ncell + 255) / 256), 256, 0, ctx->stream>>>(g, ctx->rho, ctx->rho4);
+        TM_CUDA_TRY(ctx, cudaGetLastError());
+    }
     ctx->n_total = n_total;
     // level-0 bins: N_opt points per bin on average (P:343 without fac_grid; Listing P:651-654)
     double Lx = f->x1 - f->x0, Ly = f->y1 - f->y0;
@@ -607,6 +627,7 @@ tm_status tm_internal_fill_cell_args(tm_ctx *ctx, CellArgs *a) {
     a->n_local = ctx->n_local; a->n_owned = ctx->n_owned;
     a->grid = ctx->grid;
     a->phi = ctx->phi; a->mu = ctx->mu; a->rho = ctx->rho;
+    a->rho4 = (ctx->p.flags & TM_F_NO_PACKED_GRIDS) ? nullptr : ctx->rho4;
     a->c = ctx->c; a->h_avg = ctx->h_avg;
     a->lip_mu = ctx->lip_mu; a->lip_phi = ctx->lip_phi;
     a->fac_voro = ctx->p.fac_voro_bound; a->fac_pt = ctx->p.fac_pt_mvmt;

@@ -124,6 +124,15 @@ __device__ __forceinline__ void quad_leaf(const double Q[3][2], const CellArgs &
     qy = div3(cadd(cadd(Q[0][1], Q[1][1]), Q[2][1]));
     int gi, gj;
     grid_cell(A.grid, cadd(px, qx), cadd(py, qy), gi, gj, ss, tt);
+    if (A.rho4) {  // packed corners (S0): one 32-byte sector per lookup, the same four values
+        const double2 *c = reinterpret_cast<const double2 *>(A.rho4 + (int64_t)gj * (A.grid.nx - 1) + gi);
+        const double2 lo = __ldg(c), hi = __ldg(c + 1);
+        f[0] = lo.x;
+        f[1] = lo.y;
+        f[2] = hi.x;
+        f[3] = hi.y;
+        return;
+    }
     const double *r0 = A.rho + (int64_t)gj * A.grid.nx + gi, *r1 = r0 + A.grid.nx;
     f[0] = __ldg(r0);
     f[1] = __ldg(r0 + 1);
@@ -136,13 +145,17 @@ __device__ __forceinline__ void quad_leaf(const double Q[3][2], const CellArgs &
 // are taken two at a time with their density loads in flight together (the kernel is
 // bound by the latency of those loads); below level 1 the two are siblings, so the
 // descent to their parent is shared.
-static __device__ void quad_centroid_g(const double2 *rv, int64_t ns, int nv, double px, double py, double area, double h,
-                                double dprev, const CellArgs &A, double &cx, double &cy, unsigned long long &nq) {
+// Levels beyond `lmax` (< quad_max) are left to a later pass: returns false then (cx, cy unset).
+static __device__ bool quad_centroid_g(const double2 *rv, int64_t ns, int nv, double px, double py, double area,
+                                       double h, double dprev, const CellArgs &A, double &cx, double &cy,
+                                       unsigned long long &nq, int lmax) {
     double eps = dprev >= 0.0 ? cdiv(dprev, h) : A.fac_pt;
     if (eps < A.fac_end) eps = A.fac_end;
     const double E = cmul(sqrt(area), eps);
     double prevx = 0.0, prevy = 0.0;
+    bool done = false;
     for (int L = 1; L <= A.quad_max; L++) {
+        if (L > lmax) return false;
         const int depth = L - 1;
         const int64_t ntot = (int64_t)nv << depth;
         double sw = 0.0, swx = 0.0, swy = 0.0;
@@ -185,17 +198,24 @@ static __device__ void quad_centroid_g(const double2 *rv, int64_t ns, int nv, do
         const double dist = sqrt(cadd(cmul(dx, dx), cmul(dy, dy)));
         prevx = curx;
         prevy = cury;
-        if (dist < E) break;
+        if (dist < E) {
+            done = true;
+            break;
+        }
     }
+    (void)done;  // converged, or the level cap of the method (L13) reached
     cx = prevx;
     cy = prevy;
+    return true;
 }
 
 // S4a over a ring stored in canonical order rv[i * ns] (relative to p_i): the fan/shoelace
 // sums in ring order, uncontracted, as the oracle's O4; non-uniform rho takes the
 // adaptive quadrature.  Returns the centroid relative to p_i.
-static __device__ void ring_centroid(const double2 *rv, int64_t ns, int nv, double px, double py, double h,
-                                     double dprev, const CellArgs &A, double &cx, double &cy, unsigned long long &nq) {
+// lmax: see quad_centroid_g (false: the cell needs more quadrature levels than this pass does).
+static __device__ bool ring_centroid(const double2 *rv, int64_t ns, int nv, double px, double py, double h,
+                                     double dprev, const CellArgs &A, double &cx, double &cy, unsigned long long &nq,
+                                     int lmax = 1 << 30) {
     double S2 = 0.0, sx = 0.0, sy = 0.0;
     for (int i = 0; i < nv; i++) {
         const double2 a = rv[(int64_t)i * ns], b = rv[(int64_t)(i + 1 == nv ? 0 : i + 1) * ns];
@@ -209,8 +229,9 @@ static __device__ void ring_centroid(const double2 *rv, int64_t ns, int nv, doub
         cy = cdiv(sy, cmul(3.0, S2));
         nq += nv;
     } else {
-        quad_centroid_g(rv, ns, nv, px, py, cmul(0.5, S2), h, dprev, A, cx, cy, nq);
+        return quad_centroid_g(rv, ns, nv, px, py, cmul(0.5, S2), h, dprev, A, cx, cy, nq, lmax);
     }
+    return true;
 }
 
 // thread-per-cell launcher (tm_cells_t.cu), explicitly instantiated for every mode

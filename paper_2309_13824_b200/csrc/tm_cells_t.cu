@@ -1107,8 +1107,52 @@ __global__ void __launch_bounds__(TB, (MODE & M_WCERT) ? TM_WMINB : TM_TMINB) k_
 
 // outputs of every stored ring: S3 triangles + keep rule and ELL rows, S4a centroid,
 // S5 treatment, warm-start neighbour lists, O8 counters -- one thread per cell
+#ifndef TM_QLEV1
+#define TM_QLEV1 2  // quadrature levels done by k_output_t; deeper cells go to k_output_deep
+#endif
+
+// S4a result -> x_hat (tm_cvd_step) or S5 treatment (fused CVD update), caller order
 template <int MODE>
-__global__ void __launch_bounds__(128, TM_OUT_MINB) k_output_t(CellArgs A, RingBuf R) {
+__device__ __forceinline__ void cell_update(const CellArgs &A, int32_t orig, double px, double py, double h,
+                                            double cx, double cy) {
+    if (MODE & M_HAT) {
+        A.x_hat[orig] = px + cx;
+        A.y_hat[orig] = py + cy;
+    }
+    if (MODE & M_TREAT) {
+        double qx, qy, dpo;
+        const int s = treat_point(A.grid, A.phi, h, A.h_avg, A.fac_pt, A.fac_geps, A.damping, A.newton_max, px, py,
+                                  px + cx, py + cy, qx, qy, dpo, LdgLoad());
+        A.x_out[orig] = qx;
+        A.y_out[orig] = qy;
+        A.d_prev_out[orig] = dpo;
+        A.status[orig] = (int8_t)s;
+        if (s & 2) atomicAdd(&A.st->n_fallback, 1ull);
+    }
+}
+
+// the cells whose adaptive quadrature needs more than TM_QLEV1 levels, compacted: the same
+// sub-triangles and sums in the same order (levels recomputed from 1), one thread per cell
+template <int MODE>
+__global__ void __launch_bounds__(128, TM_OUT_MINB) k_output_deep(CellArgs A, RingBuf R, const int32_t *list,
+                                                                  const unsigned long long *cnt) {
+    const int64_t n = (int64_t)*cnt;
+    for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < n; it += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t cell = list[it];
+        const int nv = (int)R.n[cell];
+        const int32_t orig = __ldg(A.perm + cell);
+        const double px = __ldg(A.xs + cell), py = __ldg(A.ys + cell), h = __ldg(A.hs + cell);
+        double cx, cy;
+        unsigned long long nq = 0;
+        ring_centroid(R.v + cell, A.n_local, nv, px, py, h, A.d_prev ? __ldg(A.d_prev + orig) : -1.0, A, cx, cy, nq);
+        cell_update<MODE>(A, orig, px, py, h, cx, cy);
+        if (MODE & M_COUNT) atomicAdd(&A.st->work[5], nq);
+    }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(128, TM_OUT_MINB) k_output_t(CellArgs A, RingBuf R, int32_t *deep_list,
+                                                               unsigned long long *deep_cnt) {
     const int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const int nv = cell < A.n_local ? (int)R.n[cell] : 0;
@@ -1213,23 +1257,18 @@ __global__ void __launch_bounds__(128, TM_OUT_MINB) k_output_t(CellArgs A, RingB
     unsigned long long nq = 0;
     if (live && (MODE & (M_TREAT | M_HAT))) {
         double cx, cy;
-        ring_centroid(rv0, ns, nv, px, py, h, A.d_prev ? __ldg(A.d_prev + orig) : -1.0, A, cx, cy, nq);
-        if (MODE & M_HAT) {
-            A.x_hat[orig] = px + cx;
-            A.y_hat[orig] = py + cy;
+        // levels beyond TM_QLEV1: deferred to k_output_deep over a compacted list, so that the
+        // few cells that refine deep do not hold their whole warp (lane divergence)
+        unsigned long long nq1 = 0;
+        const bool done = ring_centroid(rv0, ns, nv, px, py, h, A.d_prev ? __ldg(A.d_prev + orig) : -1.0, A, cx, cy,
+                                        nq1, deep_list ? TM_QLEV1 : (1 << 30));
+        if (done) {
+            nq += nq1;
+            cell_update<MODE>(A, orig, px, py, h, cx, cy);
+        } else {
+            deep_list[atomicAdd(deep_cnt, 1ull)] = (int32_t)cell;
         }
-        if (MODE & M_TREAT) {
-            double qx, qy, dpo;
-            const int s = treat_point(A.grid, A.phi, h, A.h_avg, A.fac_pt, A.fac_geps, A.damping, A.newton_max, px,
-                                      py, px + cx, py + cy, qx, qy, dpo, LdgLoad());
-            A.x_out[orig] = qx;
-            A.y_out[orig] = qy;
-            A.d_prev_out[orig] = dpo;
-            A.status[orig] = (int8_t)s;
-            if (s & 2) atomicAdd(&A.st->n_fallback, 1ull);
-        }
-    }
-    if ((MODE & M_COUNT) && live) {
+    }    if ((MODE & M_COUNT) && live) {
         float R2f = 0.f;
         for (int i = 0; i < nv; i++) R2f = fmaxf(R2f, vertex_r2f_t(RV(i).x, RV(i).y, -1.0));
         const double rad = 2.0 * sqrt((double)R2f);
@@ -1295,8 +1334,23 @@ static tm_status launch_cells_thread_impl(tm_ctx *ctx, const CellArgs &a) {
     if (s != TM_OK || !CSPLIT) return s;
     CellArgs b = a;
     b.nbr = nullptr;  // the neighbour lists were written by k_cells_t
-    k_output_t<OMODE><<<(unsigned)((ctx->n_local + 127) / 128), 128, 0, ctx->stream>>>(b, R);
-    return tm_internal_check_launch(ctx, "k_output_t");
+    const bool deep = b.rho != nullptr && (OMODE & (M_TREAT | M_HAT)) && !(ctx->p.flags & TM_F_NO_DEEP_PASS);
+    if (deep) {
+        if (!ctx->deep_cnt) TM_CUDA_TRY(ctx, cudaMalloc(&ctx->deep_cnt, sizeof(unsigned long long)));
+        if (ctx->cap_deep < ctx->n_local) {
+            cudaFree(ctx->deep_list);
+            ctx->deep_list = nullptr;
+            TM_CUDA_TRY(ctx, cudaMalloc(&ctx->deep_list, ctx->cap_ring * sizeof(int32_t)));
+            ctx->cap_deep = ctx->cap_ring;
+        }
+        TM_CUDA_TRY(ctx, cudaMemsetAsync(ctx->deep_cnt, 0, sizeof(unsigned long long), ctx->stream));
+    }
+    k_output_t<OMODE><<<(unsigned)((ctx->n_local + 127) / 128), 128, 0, ctx->stream>>>(
+        b, R, deep ? ctx->deep_list : nullptr, ctx->deep_cnt);
+    s = tm_internal_check_launch(ctx, "k_output_t");
+    if (s != TM_OK || !deep) return s;
+    k_output_deep<OMODE><<<148 * TM_OUT_MINB, 128, 0, ctx->stream>>>(b, R, ctx->deep_list, ctx->deep_cnt);
+    return tm_internal_check_launch(ctx, "k_output_deep");
 }
 
 // warm-started launches (neighbour lists of the previous launch on the same point set)

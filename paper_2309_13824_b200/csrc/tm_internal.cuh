@@ -82,6 +82,7 @@ struct CellArgs {
     int64_t n_local, n_owned;
     Grid grid;
     const double *phi, *mu, *rho;
+    const double4 *rho4;     // rho's grid cells with their 4 corners packed (f00, f10, f01, f11), or NULL
     double c, h_avg;
     double lip_mu, lip_phi;  // Lipschitz constants of mu~ and phi~ (0 for uniform mu)
     double fac_voro, fac_pt, fac_geps, fac_end, damping, keep_tol;
@@ -115,6 +116,7 @@ struct tm_ctx {
     double lip_phi = 0; // Lipschitz constant of phi~ (keep-rule fast path)
     int64_t n_total = 0;
     double *phi = nullptr, *mu = nullptr, *rho = nullptr;
+    double4 *rho4 = nullptr;  // packed corners of rho (S0, one sector per bilinear lookup)
     size_t grid_bytes = 0;
     tmg::BinGeom bg;
     // sorted state (S1)
@@ -144,6 +146,10 @@ struct tm_ctx {
     // CVD split: stored rings (slot-major, see tm_cells_t.cu RingBuf)
     void *ring_v = nullptr, *ring_la = nullptr, *ring_n = nullptr;
     int64_t cap_ring = 0;
+    // cells whose adaptive quadrature goes deeper than k_output_t's levels (k_output_deep)
+    int32_t *deep_list = nullptr;
+    unsigned long long *deep_cnt = nullptr;
+    int64_t cap_deep = 0;
     // strip migration scratch (stable partition)
     double *mig_keep = nullptr;
     int32_t *mig_cnt = nullptr, *mig_off = nullptr;
