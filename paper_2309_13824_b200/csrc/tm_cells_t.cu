@@ -1110,6 +1110,9 @@ __global__ void __launch_bounds__(TB, (MODE & M_WCERT) ? TM_WMINB : TM_TMINB) k_
 #ifndef TM_QLEV1
 #define TM_QLEV1 2  // quadrature levels done by k_output_t; deeper cells go to k_output_deep
 #endif
+#ifndef TM_DEEP_G
+#define TM_DEEP_G 8  // lanes per deep cell in k_output_deep
+#endif
 
 // S4a result -> x_hat (tm_cvd_step) or S5 treatment (fused CVD update), caller order
 template <int MODE>
@@ -1131,22 +1134,77 @@ __device__ __forceinline__ void cell_update(const CellArgs &A, int32_t orig, dou
     }
 }
 
-// the cells whose adaptive quadrature needs more than TM_QLEV1 levels, compacted: the same
-// sub-triangles and sums in the same order (levels recomputed from 1), one thread per cell
-template <int MODE>
-__global__ void __launch_bounds__(128, TM_OUT_MINB) k_output_deep(CellArgs A, RingBuf R, const int32_t *list,
-                                                                  const unsigned long long *cnt) {
+// the cells whose adaptive quadrature needs more than TM_QLEV1 levels, compacted, G lanes per
+// cell: the lanes compute the sub-triangle terms of a level G at a time (descent, area,
+// centroid, density lookup, the products w, w qx, w qy), the group's first lane adds them in
+// sub-triangle order -- the same operations in the same order as k_output_t and the oracle
+// (bit-identical), with the long serial chain of lookups of a deep cell cut G-fold
+template <int MODE, int G>
+__global__ void __launch_bounds__(128) k_output_deep(CellArgs A, RingBuf R, const int32_t *list,
+                                                     const unsigned long long *cnt) {
     const int64_t n = (int64_t)*cnt;
-    for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < n; it += (int64_t)gridDim.x * blockDim.x) {
+    const int gl = threadIdx.x % G;  // lane in the group
+    const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+    const int64_t ngroups = (int64_t)gridDim.x * (blockDim.x / G);
+    for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; it < n; it += ngroups) {
         const int64_t cell = list[it];
         const int nv = (int)R.n[cell];
         const int32_t orig = __ldg(A.perm + cell);
         const double px = __ldg(A.xs + cell), py = __ldg(A.ys + cell), h = __ldg(A.hs + cell);
-        double cx, cy;
+        const double2 *rv = R.v + cell;
+        const int64_t ns = A.n_local;
+        // area by the shoelace in ring order (every lane the same, as ring_centroid)
+        double S2 = 0.0;
+        for (int i = 0; i < nv; i++) {
+            const double2 a = rv[(int64_t)i * ns], b = rv[(int64_t)(i + 1 == nv ? 0 : i + 1) * ns];
+            S2 = cadd(S2, csub(cmul(a.x, b.y), cmul(b.x, a.y)));
+        }
+        const double dprev = A.d_prev ? __ldg(A.d_prev + orig) : -1.0;
+        double eps = dprev >= 0.0 ? cdiv(dprev, h) : A.fac_pt;
+        if (eps < A.fac_end) eps = A.fac_end;
+        const double E = cmul(sqrt(cmul(0.5, S2)), eps);
+        double prevx = 0.0, prevy = 0.0;
         unsigned long long nq = 0;
-        ring_centroid(R.v + cell, A.n_local, nv, px, py, h, A.d_prev ? __ldg(A.d_prev + orig) : -1.0, A, cx, cy, nq);
-        cell_update<MODE>(A, orig, px, py, h, cx, cy);
-        if (MODE & M_COUNT) atomicAdd(&A.st->work[5], nq);
+        for (int L = 1; L <= A.quad_max; L++) {
+            const int depth = L - 1;
+            const int64_t ntot = (int64_t)nv << depth;
+            double sw = 0.0, swx = 0.0, swy = 0.0;
+            for (int64_t base = 0; base < ntot; base += G) {
+                const int64_t t = base + gl;
+                double w = 0.0, wx = 0.0, wy = 0.0;
+                if (t < ntot) {
+                    const int fi = (int)(t >> depth);
+                    double Q[3][2];
+                    quad_descend(rv[(int64_t)fi * ns], rv[(int64_t)(fi + 1 == nv ? 0 : fi + 1) * ns], depth,
+                                 t & (((int64_t)1 << depth) - 1), Q);
+                    double At, qx, qy, ss, tt, f[4];
+                    quad_leaf(Q, A, px, py, At, qx, qy, ss, tt, f);
+                    const double rho = clerp(clerp(f[0], f[1], ss), clerp(f[2], f[3], ss), tt);
+                    w = cmul(At, rho);
+                    wx = cmul(w, qx);
+                    wy = cmul(w, qy);
+                }
+                const int m = (int)(ntot - base < G ? ntot - base : G);
+                for (int k = 0; k < m; k++) {  // in sub-triangle order
+                    const double a = __shfl_sync(gmask, w, k, G), b = __shfl_sync(gmask, wx, k, G),
+                                 c = __shfl_sync(gmask, wy, k, G);
+                    sw = cadd(sw, a);
+                    swx = cadd(swx, b);
+                    swy = cadd(swy, c);
+                }
+                nq += (unsigned long long)m;
+            }
+            const double curx = cdiv(swx, sw), cury = cdiv(swy, sw);
+            const double dx = csub(prevx, curx), dy = csub(prevy, cury);
+            const double dist = sqrt(cadd(cmul(dx, dx), cmul(dy, dy)));
+            prevx = curx;
+            prevy = cury;
+            if (dist < E) break;
+        }
+        if (gl == 0) {
+            cell_update<MODE>(A, orig, px, py, h, prevx, prevy);
+            if (MODE & M_COUNT) atomicAdd(&A.st->work[5], nq);
+        }
     }
 }
 
@@ -1349,7 +1407,7 @@ static tm_status launch_cells_thread_impl(tm_ctx *ctx, const CellArgs &a) {
         b, R, deep ? ctx->deep_list : nullptr, ctx->deep_cnt);
     s = tm_internal_check_launch(ctx, "k_output_t");
     if (s != TM_OK || !deep) return s;
-    k_output_deep<OMODE><<<148 * TM_OUT_MINB, 128, 0, ctx->stream>>>(b, R, ctx->deep_list, ctx->deep_cnt);
+    k_output_deep<OMODE, TM_DEEP_G><<<148 * 8, 128, 0, ctx->stream>>>(b, R, ctx->deep_list, ctx->deep_cnt);
     return tm_internal_check_launch(ctx, "k_output_deep");
 }
 
