@@ -486,24 +486,36 @@ def main():
                 saved["cvd"] = (xc.cpu().numpy(), yc.cpu().numpy(), dc.cpu().numpy())
         return xc, yc
 
-    # N > 1 (or --strips): x-strip decomposition of the same mesh
+    # N > 1 (or --strips): x-strip decomposition of the same mesh, the sync-free
+    # protocol of paper_2309_13824_b200.strips (fixed-size messages, device counts)
     strip_mode = world > 1 or args.strips
     if strip_mode:
         from paper_2309_13824_b200 import strips as S
         strips = S.Strips.from_quantiles(torch.from_numpy(c.x), world, box[0], box[2])
-        st_init = S.split_initial(x0, y0, strips, rank)
         W = S.ghost_width(ctx.c, params.fac_voro_bound, float(c.mu.max()) if c.mu is not None else 1.0)
+        # capacities: the owned share with slack; the messages sized from the initial halo
+        # (a one-off measurement before timing: 4x the larger side, at most the owned capacity)
+        cap_own, _ = S.capacities(n, world, 0)
+        S0 = S.split_initial(x0, y0, strips, rank, cap_own, cap_own)
+        lo_, hi_ = strips.bounds(rank)
+        S.GpuStripBackend(ctx, params.adj_stride).halo_pack(S0, lo_, hi_, W)
+        ghosts0 = max(S0.h_send[0].count(), S0.h_send[1].count())
+        cap_msg = min(cap_own, 4 * ghosts0 + 4096)
+        S0 = S.split_initial(x0, y0, strips, rank, cap_own, cap_msg)
+        xo_, yo_, go_, _ = S0.owned()
+        x_own, y_own, g_own = xo_.clone(), yo_.clone(), go_.clone()
+        counts0 = S0.counts.clone()
         comm = S.TorchP2P(rank, world, dev)
-        backend = S.GpuStripBackend(ctx, params.adj_stride, keep_tri=False)
+        backend = S.GpuStripBackend(ctx, params.adj_stride)
 
     def one_step_strips(xin, yin, record=False, save=False):
-        st = S.RankState(rank, xin, yin, st_init.gid, None)
+        S0.reset(xin, yin, g_own, counts0)
         for mode in schedule:
-            st = S.strip_iteration(st, strips, backend, comm.exchange, W, mode, allreduce=comm.allreduce_sum)
-        return st.x, st.y
+            S.strip_step(S0, strips, backend, comm, W, mode)
+        return S0.X, S0.Y  # owned points at [0, n_owned) (count on the device)
 
     one_step = one_step_strips if strip_mode else one_step_single
-    xs0, ys0 = (st_init.x, st_init.y) if strip_mode else (x0, y0)
+    xs0, ys0 = (x_own, y_own) if strip_mode else (x0, y0)
 
     def barrier():
         if world > 1:
@@ -556,7 +568,8 @@ def main():
         rx = torch.empty(2 * n_in + 1024, dtype=torch.float64).pin_memory()
         ry = torch.empty(2 * n_in + 1024, dtype=torch.float64).pin_memory()
         rn = torch.empty(1, dtype=torch.int64).pin_memory()
-        rt = torch.empty((bufs.tri.shape[0], 3), dtype=torch.int32).pin_memory()
+        rt = torch.empty(((backend.bufs if strip_mode else bufs).tri.shape[0], 3), dtype=torch.int32).pin_memory()
+        rc = torch.empty(2, dtype=torch.int64).pin_memory()
         dx = torch.empty(n_in, dtype=torch.float64, device=dev)
         dy = torch.empty(n_in, dtype=torch.float64, device=dev)
         e2e_ms, d2h = [], []
@@ -569,17 +582,21 @@ def main():
             dx.copy_(hx, non_blocking=True)
             dy.copy_(hy, non_blocking=True)
             xf, yf = one_step(dx, dy)
-            rx[:xf.shape[0]].copy_(xf, non_blocking=True)
-            ry[:yf.shape[0]].copy_(yf, non_blocking=True)
-            rn.copy_(bufs.n_tri, non_blocking=True)
-            stream.synchronize()  # the caller needs the count to size the triangle copy
-            nt = int(rn.item()) if not strip_mode else 0
+            tb = backend.bufs if strip_mode else bufs
+            rn.copy_(tb.n_tri, non_blocking=True)
+            if strip_mode:
+                rc.copy_(S0.counts, non_blocking=True)
+            stream.synchronize()  # the caller needs the counts to size the copies
+            npt = int(rc[0].item()) if strip_mode else xf.shape[0]
+            nt = int(rn.item())
+            rx[:npt].copy_(xf[:npt], non_blocking=True)
+            ry[:npt].copy_(yf[:npt], non_blocking=True)
             if nt:
-                rt[:nt].copy_(bufs.tri[:nt], non_blocking=True)
+                rt[:nt].copy_(tb.tri[:nt], non_blocking=True)
             s1.record(stream)
             s1.synchronize()
             e2e_ms.append(s0.elapsed_time(s1))
-            d2h.append(2 * 8 * xf.shape[0] + 8 + 12 * nt)
+            d2h.append(2 * 8 * npt + 8 + 12 * nt + (16 if strip_mode else 0))
         barrier()
         te = torch.tensor([sum(e2e_ms) / 1e3], dtype=torch.float64, device=dev)
         if world > 1:

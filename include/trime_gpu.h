@@ -221,6 +221,38 @@ tm_status tm_migrate_pack(tm_ctx *ctx, double *x, double *y, int32_t *gid, doubl
                           double strip_lo, double strip_hi, double *out_lo, double *out_hi, int64_t cap,
                           int64_t *cnt3);
 
+/* ---- device-count variants: the strip path without host synchronisation --------
+ * The ghost and migrant counts of a strip iteration are known only on the device (they
+ * arrive with the NCCL messages).  These calls take them from device memory, so one
+ * iteration issues no host sync; array arguments are then CAPACITIES (host, fixed).
+ *
+ * tm_grid_bin_dc: as tm_grid_bin, with d_counts = device int64[2] {n_owned, n_local}
+ * (the first n_owned of the n_local points are owned) and cap_local >= n_local the
+ * capacity of x/y/gid (gid required).  Every later call of the iteration (cells,
+ * DistMesh passes, adjacency export) uses these live counts; ELL rows and rings are
+ * strided by cap_local. */
+tm_status tm_grid_bin_dc(tm_ctx *ctx, const double *x, const double *y, int64_t cap_local, const int64_t *d_counts,
+                         const int32_t *gid);
+/* tm_halo_pack with the owned count *d_n_owned (device) and capacity cap_owned; the two
+ * counts go to cnt_lo / cnt_hi (device int64, e.g. the headers of the two messages).
+ * Counts beyond cap are still counted (the receiver's tm_append_points latches the
+ * overflow, TM_E_CAPACITY at the next synchronising call). */
+tm_status tm_halo_pack_dc(tm_ctx *ctx, const double *x, const double *y, const int32_t *gid,
+                          const int64_t *d_n_owned, int64_t cap_owned, double strip_lo, double strip_hi,
+                          double width, double *send_lo, double *send_hi, int64_t cap, int64_t *cnt_lo,
+                          int64_t *cnt_hi);
+/* tm_migrate_pack with the owned count *d_n_owned (device, capacity cap_owned): the kept
+ * count is written back to *d_n_owned, the leaver counts to cnt_lo / cnt_hi. */
+tm_status tm_migrate_pack_dc(tm_ctx *ctx, double *x, double *y, int32_t *gid, double *d_prev, int64_t *d_n_owned,
+                             int64_t cap_owned, double strip_lo, double strip_hi, double *out_lo, double *out_hi,
+                             int64_t cap, int64_t *cnt_lo, int64_t *cnt_hi);
+/* Append a received message -- segments [x | y | gid (int32) | d_prev] of capacity
+ * msg_cap holding *msg_count entries (d_prev: NULL = no such segment) -- after the
+ * *d_count points of x/y/gid/d_prev (capacity cap), and advance *d_count; overflow
+ * latches TM_E_CAPACITY.  Device pointers, no host sync. */
+tm_status tm_append_points(tm_ctx *ctx, double *x, double *y, int32_t *gid, double *d_prev, int64_t *d_count,
+                           int64_t cap, const double *msg, const int64_t *msg_count, int64_t msg_cap);
+
 /* ---- host-side predicate hooks (no GPU needed; same code as the kernels) -- */
 /* sign of incircle(a,b,c,d) (>0: d inside circle(a,b,c), a,b,c CCW) by the
  * kernels' exact expansion arithmetic, and by the kernels' full filtered path */

@@ -79,7 +79,8 @@ _lib = None
 EXPORTED = ["tm_params_default", "tm_create", "tm_destroy", "tm_last_error", "tm_sync", "tm_set_domain",
             "tm_grid_bin", "tm_voronoi_delaunay", "tm_cvd_step", "tm_distmesh_sums", "tm_distmesh_step",
             "tm_project_sdf", "tm_mesh_stats", "tm_adjacency_export", "tm_work_counts", "tm_halo_pack",
-            "tm_migrate_pack", "tm_host_incircle_exact", "tm_host_cramer", "tm_host_bilinear"]
+            "tm_migrate_pack", "tm_grid_bin_dc", "tm_halo_pack_dc", "tm_migrate_pack_dc", "tm_append_points",
+            "tm_host_incircle_exact", "tm_host_cramer", "tm_host_bilinear"]
 
 
 def load_library(path: str = LIB_PATH, build_if_missing: bool = True):
@@ -112,6 +113,10 @@ def load_library(path: str = LIB_PATH, build_if_missing: bool = True):
         "tm_work_counts": (st, [vp, ctypes.POINTER(tm_work)]),
         "tm_halo_pack": (st, [vp, vp, vp, vp, i64, dbl, dbl, dbl, vp, vp, i64, vp]),
         "tm_migrate_pack": (st, [vp, vp, vp, vp, vp, i64, dbl, dbl, vp, vp, i64, vp]),
+        "tm_grid_bin_dc": (st, [vp, vp, vp, i64, vp, vp]),
+        "tm_halo_pack_dc": (st, [vp, vp, vp, vp, vp, i64, dbl, dbl, dbl, vp, vp, i64, vp, vp]),
+        "tm_migrate_pack_dc": (st, [vp, vp, vp, vp, vp, vp, i64, dbl, dbl, vp, vp, i64, vp, vp]),
+        "tm_append_points": (st, [vp, vp, vp, vp, vp, vp, i64, vp, vp, i64]),
         "tm_host_incircle_exact": (ctypes.c_int, [vp, vp, vp, vp]),
         "tm_host_cramer": (None, [vp, vp, vp]),
         "tm_host_bilinear": (dbl, [i32, i32, dbl, dbl, dbl, dbl, vp, dbl, dbl]),
@@ -132,6 +137,13 @@ def _ptr(t: Optional[torch.Tensor]):
     if not t.is_contiguous():
         raise TmError(TM_E_ARG, "tensor must be contiguous")
     return ctypes.c_void_p(t.data_ptr())
+
+
+def _addr(a):
+    """A raw device address (int) or a CUDA tensor -> c_void_p."""
+    if isinstance(a, torch.Tensor):
+        return _ptr(a)
+    return ctypes.c_void_p(int(a))
 
 
 def default_params(**kw) -> tm_params:
@@ -236,6 +248,27 @@ class Context:
     def tm_migrate_pack(self, x, y, gid, d_prev, n_owned, lo, hi, out_lo, out_hi, cap, cnt3):
         self._check(self.L.tm_migrate_pack(self.h, _ptr(x), _ptr(y), _ptr(gid), _ptr(d_prev), int(n_owned), lo, hi,
                                            _ptr(out_lo), _ptr(out_hi), int(cap), _ptr(cnt3)))
+
+    # device-count variants (strip path without host synchronisation); *_p arguments are raw
+    # device addresses (int), e.g. a message header inside a byte buffer
+    def tm_grid_bin_dc(self, x, y, cap_local, counts, gid):
+        self._check(self.L.tm_grid_bin_dc(self.h, _ptr(x), _ptr(y), int(cap_local), _ptr(counts), _ptr(gid)))
+
+    def tm_halo_pack_dc(self, x, y, gid, n_owned_p, cap_owned, lo, hi, width, send_lo_p, send_hi_p, cap, cnt_lo_p,
+                        cnt_hi_p):
+        self._check(self.L.tm_halo_pack_dc(self.h, _ptr(x), _ptr(y), _ptr(gid), _addr(n_owned_p), int(cap_owned), lo,
+                                           hi, width, _addr(send_lo_p), _addr(send_hi_p), int(cap), _addr(cnt_lo_p),
+                                           _addr(cnt_hi_p)))
+
+    def tm_migrate_pack_dc(self, x, y, gid, d_prev, n_owned_p, cap_owned, lo, hi, out_lo_p, out_hi_p, cap, cnt_lo_p,
+                           cnt_hi_p):
+        self._check(self.L.tm_migrate_pack_dc(self.h, _ptr(x), _ptr(y), _ptr(gid), _ptr(d_prev), _addr(n_owned_p),
+                                              int(cap_owned), lo, hi, _addr(out_lo_p), _addr(out_hi_p), int(cap),
+                                              _addr(cnt_lo_p), _addr(cnt_hi_p)))
+
+    def tm_append_points(self, x, y, gid, d_prev, count_p, cap, msg_p, msg_count_p, msg_cap):
+        self._check(self.L.tm_append_points(self.h, _ptr(x), _ptr(y), _ptr(gid), _ptr(d_prev), _addr(count_p),
+                                            int(cap), _addr(msg_p), _addr(msg_count_p), int(msg_cap)))
 
 
 # ------------------------------------------------------------------ driver

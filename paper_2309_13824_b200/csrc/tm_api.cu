@@ -78,7 +78,7 @@ extern "C" void tm_destroy(tm_ctx *ctx) {
     cudaFree(ctx->mig_keep); cudaFree(ctx->mig_cnt); cudaFree(ctx->mig_off);
     cudaFree(ctx->nbr); cudaFree(ctx->nbr_cnt); cudaFree(ctx->inv_id);
     cudaFree(ctx->ring_v); cudaFree(ctx->ring_la); cudaFree(ctx->ring_n);
-    cudaFree(ctx->deep_list); cudaFree(ctx->deep_cnt);
+    cudaFree(ctx->deep_list); cudaFree(ctx->deep_cnt); cudaFree(ctx->scratch_n);
     delete ctx;
 }
 
@@ -102,6 +102,9 @@ static tm_status report_latched(tm_ctx *ctx, const DevState &s) {
                 ctx->p.max_cell_vertices);
     if (s.n_tri_overflow) TM_FAIL(ctx, TM_E_CAPACITY, "triangle buffer too small (tri_cap)");
     if (s.n_adj_overflow) TM_FAIL(ctx, TM_E_CAPACITY, "ELL row wider than adj_stride=%d", ctx->p.adj_stride);
+    if (s.n_strip_overflow)
+        TM_FAIL(ctx, TM_E_CAPACITY, "%llu strip halo/migration message(s) or append(s) beyond capacity",
+                s.n_strip_overflow);
     return TM_OK;
 }
 
@@ -313,9 +316,9 @@ extern "C" tm_status tm_set_domain(tm_ctx *ctx, const tm_fields *f, int64_t n_to
 // ============================================================================ S1
 __global__ void k_bin_keys(const double *__restrict__ x, const double *__restrict__ y, int64_t n, BinGeom bg,
                            double bx0, double by0, double bx1, double by1, int32_t *__restrict__ key,
-                           int32_t *__restrict__ count, DevState *st) {
+                           int32_t *__restrict__ count, DevState *st, const int64_t *dn) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    if (i >= (dn ? dn[1] : n)) return;
     double px = x[i], py = y[i];
     if (!(px >= bx0 && px <= bx1 && py >= by0 && py <= by1)) {
         atomicAdd(&st->n_outside, 1ull);
@@ -350,9 +353,9 @@ __global__ void k_bin_levels(const int32_t *__restrict__ count, int64_t nb, doub
 __global__ void k_leaf_keys(const double *__restrict__ x, const double *__restrict__ y, int64_t n, BinGeom bg,
                             double bx0, double by0, double bx1, double by1, int32_t *__restrict__ key,
                             const uint8_t *__restrict__ rlev, const int32_t *__restrict__ leaf_off,
-                            int32_t *__restrict__ leaf_count, int32_t *__restrict__ rank) {
+                            int32_t *__restrict__ leaf_count, int32_t *__restrict__ rank, const int64_t *dn) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    if (i >= (dn ? dn[1] : n)) return;
     double px = fmin(fmax(x[i] == x[i] ? x[i] : bx0, bx0), bx1);
     double py = fmin(fmax(y[i] == y[i] ? y[i] : by0, by0), by1);
     int32_t b = key[i];
@@ -445,9 +448,9 @@ __global__ void k_scan_add(int32_t *out, const int32_t *tile_sums, int64_t n) {
 // sorted (4-byte keys only) and the point data gathered once into slot order with
 // coalesced stores: the in-leaf order is the caller order, deterministic.
 __global__ void k_perm_scatter(int64_t n, const int32_t *__restrict__ key, const int32_t *__restrict__ rank,
-                               const int32_t *__restrict__ start, int32_t *__restrict__ perm) {
+                               const int32_t *__restrict__ start, int32_t *__restrict__ perm, const int64_t *dn) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    if (i >= (dn ? dn[1] : n)) return;
     perm[(int64_t)start[key[i]] + rank[i]] = (int32_t)i;
 }
 
@@ -476,9 +479,9 @@ __global__ void k_gather_sorted(const double *__restrict__ x, const double *__re
                                 const int32_t *__restrict__ gid, int64_t n, const int32_t *__restrict__ perm,
                                 double bx0, double by0, double bx1, double by1, Grid g, const double *__restrict__ mu,
                                 double c, double *__restrict__ xs, double *__restrict__ ys, double *__restrict__ hs,
-                                int32_t *__restrict__ gids) {
+                                int32_t *__restrict__ gids, const int64_t *dn) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= n) return;
+    if (s >= (dn ? dn[1] : n)) return;
     const int32_t i = perm[s];
     double px = x[i], py = y[i];
     px = fmin(fmax(px == px ? px : bx0, bx0), bx1);
@@ -550,8 +553,9 @@ static tm_status scan_counts(tm_ctx *ctx, const int32_t *in, int32_t *out, int64
     return tm_internal_check_launch(ctx, "scan");
 }
 
-extern "C" tm_status tm_grid_bin(tm_ctx *ctx, const double *x, const double *y, int64_t n_local, int64_t n_owned,
-                                 const int32_t *gid) {
+// n_local: the number of points, or with dcnt (device {n_owned, n_local}) the capacity of x/y/gid
+static tm_status grid_bin_impl(tm_ctx *ctx, const double *x, const double *y, int64_t n_local, int64_t n_owned,
+                               const int32_t *gid, const int64_t *dcnt) {
     if (!ctx) return TM_E_ARG;
     if (!ctx->have_domain) TM_FAIL(ctx, TM_E_STATE, "tm_grid_bin before tm_set_domain");
     if (!x || !y) TM_FAIL(ctx, TM_E_ARG, "null x/y");
@@ -588,7 +592,7 @@ extern "C" tm_status tm_grid_bin(tm_ctx *ctx, const double *x, const double *y, 
     const Grid &g = ctx->grid;
     unsigned blocks = (unsigned)((n_local + 255) / 256);
     k_bin_keys<<<blocks, 256, 0, ctx->stream>>>(x, y, n_local, ctx->bg, g.x0, g.y0, g.x1, g.y1, ctx->key,
-                                                ctx->bin_count, ctx->dst);
+                                                ctx->bin_count, ctx->dst, dcnt);
     if ((s = tm_internal_check_launch(ctx, "k_bin_keys")) != TM_OK) return s;
     // per-bin level and number of leaves (reuses leaf_count as scratch), scan -> leaf_off
     k_bin_levels<<<(unsigned)((nb + 255) / 256), 256, 0, ctx->stream>>>(
@@ -596,21 +600,34 @@ extern "C" tm_status tm_grid_bin(tm_ctx *ctx, const double *x, const double *y, 
     if ((s = scan_counts(ctx, ctx->leaf_count, ctx->leaf_off, nb)) != TM_OK) return s;
     TM_CUDA_TRY(ctx, cudaMemsetAsync(ctx->leaf_count, 0, nleaves_max * sizeof(int32_t), ctx->stream));
     k_leaf_keys<<<blocks, 256, 0, ctx->stream>>>(x, y, n_local, ctx->bg, g.x0, g.y0, g.x1, g.y1, ctx->key, ctx->rlev,
-                                                 ctx->leaf_off, ctx->leaf_count, ctx->rank);
+                                                 ctx->leaf_off, ctx->leaf_count, ctx->rank, dcnt);
     if ((s = tm_internal_check_launch(ctx, "k_leaf_keys")) != TM_OK) return s;
     if ((s = scan_counts(ctx, ctx->leaf_count, ctx->leaf_start, nleaves_max)) != TM_OK) return s;
-    k_perm_scatter<<<blocks, 256, 0, ctx->stream>>>(n_local, ctx->key, ctx->rank, ctx->leaf_start, ctx->perm);
+    k_perm_scatter<<<blocks, 256, 0, ctx->stream>>>(n_local, ctx->key, ctx->rank, ctx->leaf_start, ctx->perm, dcnt);
     k_leaf_sort_perm<<<(unsigned)((nleaves_max + 255) / 256), 256, 0, ctx->stream>>>(ctx->leaf_start, nleaves_max,
                                                                                    ctx->perm, gid, nkey, ctx->inv_id);
     k_gather_sorted<<<blocks, 256, 0, ctx->stream>>>(x, y, gid, n_local, ctx->perm, g.x0, g.y0, g.x1, g.y1, g, ctx->mu,
-                                                     ctx->c, ctx->xs, ctx->ys, ctx->hs, ctx->gids);
+                                                     ctx->c, ctx->xs, ctx->ys, ctx->hs, ctx->gids, dcnt);
     if ((s = tm_internal_check_launch(ctx, "k_gather_sorted")) != TM_OK) return s;
     ctx->have_gid = gid != nullptr;
     ctx->n_local = n_local;
     ctx->n_owned = n_owned;
+    ctx->dcnt = dcnt;
     ctx->have_bins = true;
     ctx->have_cells = false;
     return TM_OK;
+}
+
+extern "C" tm_status tm_grid_bin(tm_ctx *ctx, const double *x, const double *y, int64_t n_local, int64_t n_owned,
+                                 const int32_t *gid) {
+    return grid_bin_impl(ctx, x, y, n_local, n_owned, gid, nullptr);
+}
+
+extern "C" tm_status tm_grid_bin_dc(tm_ctx *ctx, const double *x, const double *y, int64_t cap_local,
+                                    const int64_t *d_counts, const int32_t *gid) {
+    if (!ctx) return TM_E_ARG;
+    if (!d_counts || !gid) TM_FAIL(ctx, TM_E_ARG, "tm_grid_bin_dc needs device counts and global ids");
+    return grid_bin_impl(ctx, x, y, cap_local, cap_local, gid, d_counts);
 }
 
 tm_status tm_internal_fill_cell_args(tm_ctx *ctx, CellArgs *a) {
@@ -625,6 +642,7 @@ tm_status tm_internal_fill_cell_args(tm_ctx *ctx, CellArgs *a) {
     a->rlev = ctx->rlev; a->leaf_off = ctx->leaf_off; a->leaf_start = ctx->leaf_start;
     a->bg = ctx->bg;
     a->n_local = ctx->n_local; a->n_owned = ctx->n_owned;
+    a->dcnt = ctx->dcnt;
     a->grid = ctx->grid;
     a->phi = ctx->phi; a->mu = ctx->mu; a->rho = ctx->rho;
     a->rho4 = (ctx->p.flags & TM_F_NO_PACKED_GRIDS) ? nullptr : ctx->rho4;
@@ -806,12 +824,12 @@ extern "C" tm_status tm_work_counts(tm_ctx *ctx, tm_work *out) {
 // ============================================================================ exports
 __global__ void k_adj_export(const int32_t *__restrict__ adj, const uint8_t *__restrict__ deg,
                              const int32_t *__restrict__ perm, const int32_t *__restrict__ gids, int64_t n_local,
-                             int64_t n_owned, int stride, int32_t *__restrict__ adj_out,
+                             int64_t n_owned, const int64_t *dcnt, int stride, int32_t *__restrict__ adj_out,
                              uint8_t *__restrict__ deg_out) {
     int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= n_local) return;
+    if (s >= (dcnt ? dcnt[1] : n_local)) return;
     int32_t o = perm[s];
-    if (o >= n_owned) return;
+    if (o >= (dcnt ? dcnt[0] : n_owned)) return;
     int d = deg[s];
     deg_out[o] = (uint8_t)d;
     for (int k = 0; k < stride; k++)
@@ -825,24 +843,28 @@ extern "C" tm_status tm_adjacency_export(tm_ctx *ctx, const int32_t *adj, const 
     if (!adj || !deg || !adj_out || !deg_out) TM_FAIL(ctx, TM_E_ARG, "null argument to tm_adjacency_export");
     TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
     k_adj_export<<<(unsigned)((ctx->n_local + 255) / 256), 256, 0, ctx->stream>>>(
-        adj, deg, ctx->perm, ctx->gids, ctx->n_local, ctx->n_owned, ctx->p.adj_stride, adj_out, deg_out);
+        adj, deg, ctx->perm, ctx->gids, ctx->n_local, ctx->n_owned, ctx->dcnt, ctx->p.adj_stride, adj_out, deg_out);
     return tm_internal_check_launch(ctx, "k_adj_export");
 }
 
 // ============================================================================ S7 packing
+static double strip_edge(double v) { return v < -1e300 ? -1e300 : (v > 1e300 ? 1e300 : v); }
+
 // Halo selection.  A point j of this strip can cut the cell of a point i
 // across the edge only if |p_j - p_i| < 2 S_i (C_i lies in Oct_i).  With w > 0 the band
 // is the fixed width w = 2 S_max.  With w < 0 the width is per point: S = fac h and h =
 // c mu~ is Lipschitz with constant c L, so S_i <= S_j + fac c L d and d < 2 S_i implies
 // d < 2 S_j / (1 - 2 fac c L) when 2 fac c L < 1; the band is the smaller of that and |w|.
+// n: the owned count, or with dn the device one (*dn) and n the capacity.
 __global__ void k_halo_pack(const double *__restrict__ x, const double *__restrict__ y,
-                            const int32_t *__restrict__ gid, int64_t n, double lo, double hi, double w,
-                            Grid g, const double *__restrict__ mu, double c, double fac, double lip,
-                            double *send_lo, double *send_hi, int64_t cap, unsigned long long *cnt) {
+                            const int32_t *__restrict__ gid, int64_t n, const int64_t *dn, double lo, double hi,
+                            double w, Grid g, const double *__restrict__ mu, double c, double fac, double lip,
+                            double *send_lo, double *send_hi, int64_t cap, unsigned long long *cnt_lo,
+                            unsigned long long *cnt_hi) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
-    const double px = i < n ? x[i] : 0.0;
-    const bool in_n = i < n;
+    const bool in_n = i < (dn ? *dn : n);
+    const double px = in_n ? x[i] : 0.0;
     double wi = w;
     if (w < 0.0) {
         const double k = 2.0 * fac * c * lip;
@@ -861,7 +883,7 @@ __global__ void k_halo_pack(const double *__restrict__ x, const double *__restri
         const unsigned m = __ballot_sync(0xffffffffu, sel);
         if (!m) continue;
         unsigned long long base = 0;
-        if (lane == __ffs(m) - 1) base = atomicAdd(&cnt[side], (unsigned long long)__popc(m));
+        if (lane == __ffs(m) - 1) base = atomicAdd(side == 0 ? cnt_lo : cnt_hi, (unsigned long long)__popc(m));
         base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
         if (sel) {
             const unsigned long long k = base + __popc(m & ((1u << lane) - 1u));
@@ -875,39 +897,59 @@ __global__ void k_halo_pack(const double *__restrict__ x, const double *__restri
     }
 }
 
+static tm_status halo_pack_impl(tm_ctx *ctx, const double *x, const double *y, const int32_t *gid, int64_t n,
+                                const int64_t *dn, double lo, double hi, double width, double *send_lo,
+                                double *send_hi, int64_t cap, int64_t *cnt_lo, int64_t *cnt_hi) {
+    TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    TM_CUDA_TRY(ctx, cudaMemsetAsync(cnt_lo, 0, sizeof(int64_t), ctx->stream));
+    TM_CUDA_TRY(ctx, cudaMemsetAsync(cnt_hi, 0, sizeof(int64_t), ctx->stream));
+    if (n == 0) return TM_OK;
+    if (width < 0.0 && !ctx->have_domain) TM_FAIL(ctx, TM_E_STATE, "adaptive halo width needs tm_set_domain");
+    k_halo_pack<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(
+        x, y, gid, n, dn, strip_edge(lo), strip_edge(hi), width, ctx->grid, ctx->mu, ctx->c, ctx->p.fac_voro_bound,
+        ctx->lip_mu, send_lo, send_hi, cap, (unsigned long long *)cnt_lo, (unsigned long long *)cnt_hi);
+    return tm_internal_check_launch(ctx, "k_halo_pack");
+}
+
 extern "C" tm_status tm_halo_pack(tm_ctx *ctx, const double *x, const double *y, const int32_t *gid,
                                   int64_t n_owned, double strip_lo, double strip_hi, double width, double *send_lo,
                                   double *send_hi, int64_t cap, int64_t *cnt2) {
     if (!ctx) return TM_E_ARG;
     if (!x || !y || !send_lo || !send_hi || !cnt2 || n_owned < 0 || cap < 0)
         TM_FAIL(ctx, TM_E_ARG, "null argument to tm_halo_pack");
-    TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
-    TM_CUDA_TRY(ctx, cudaMemsetAsync(cnt2, 0, 2 * sizeof(int64_t), ctx->stream));
-    if (n_owned == 0) return TM_OK;
-    if (width < 0.0 && !ctx->have_domain) TM_FAIL(ctx, TM_E_STATE, "adaptive halo width needs tm_set_domain");
-    k_halo_pack<<<(unsigned)((n_owned + 255) / 256), 256, 0, ctx->stream>>>(
-        x, y, gid, n_owned, strip_lo, strip_hi, width, ctx->grid, ctx->mu, ctx->c, ctx->p.fac_voro_bound,
-        ctx->lip_mu, send_lo, send_hi, cap, (unsigned long long *)cnt2);
-    return tm_internal_check_launch(ctx, "k_halo_pack");
+    return halo_pack_impl(ctx, x, y, gid, n_owned, nullptr, strip_lo, strip_hi, width, send_lo, send_hi, cap, cnt2,
+                          cnt2 + 1);
+}
+
+extern "C" tm_status tm_halo_pack_dc(tm_ctx *ctx, const double *x, const double *y, const int32_t *gid,
+                                     const int64_t *d_n_owned, int64_t cap_owned, double strip_lo, double strip_hi,
+                                     double width, double *send_lo, double *send_hi, int64_t cap, int64_t *cnt_lo,
+                                     int64_t *cnt_hi) {
+    if (!ctx) return TM_E_ARG;
+    if (!x || !y || !d_n_owned || !send_lo || !send_hi || !cnt_lo || !cnt_hi || cap_owned < 0 || cap < 0)
+        TM_FAIL(ctx, TM_E_ARG, "null argument to tm_halo_pack_dc");
+    return halo_pack_impl(ctx, x, y, gid, cap_owned, d_n_owned, strip_lo, strip_hi, width, send_lo, send_hi, cap,
+                          cnt_lo, cnt_hi);
 }
 
 // Stable 3-way partition of the owned points after an update (SURVEY §8(e)
 // step 4): category 0 stays, 1 leaves to the lower strip, 2 to the upper one.
 // Per-block counts -> exclusive scan -> per-block ranks by warp ballots: the
 // order inside every category is the input order (deterministic, no atomics).
+// n: the owned count, or with dn the device one (*dn; n = capacity).
 constexpr int MIG_T = 256;
 
 __device__ __forceinline__ int mig_cat(double px, double lo, double hi) {
     return px < lo ? 1 : (px >= hi ? 2 : 0);
 }
 
-__global__ void __launch_bounds__(MIG_T) k_migrate_count(const double *__restrict__ x, int64_t n, double lo,
-                                                         double hi, int32_t *__restrict__ bc, int64_t nblk) {
+__global__ void __launch_bounds__(MIG_T) k_migrate_count(const double *__restrict__ x, int64_t n, const int64_t *dn,
+                                                         double lo, double hi, int32_t *__restrict__ bc, int64_t nblk) {
     __shared__ int sc[3];
     if (threadIdx.x < 3) sc[threadIdx.x] = 0;
     __syncthreads();
     const int64_t i = (int64_t)blockIdx.x * MIG_T + threadIdx.x;
-    const int c = i < n ? mig_cat(x[i], lo, hi) : -1;
+    const int c = i < (dn ? *dn : n) ? mig_cat(x[i], lo, hi) : -1;
 #pragma unroll
     for (int cc = 0; cc < 3; cc++) {
         const unsigned m = __ballot_sync(0xffffffffu, c == cc);
@@ -919,14 +961,16 @@ __global__ void __launch_bounds__(MIG_T) k_migrate_count(const double *__restric
 
 __global__ void __launch_bounds__(MIG_T) k_migrate_scatter(const double *__restrict__ x, const double *__restrict__ y,
                                                            const int32_t *__restrict__ gid,
-                                                           const double *__restrict__ dp, int64_t n, double lo,
-                                                           double hi, const int32_t *__restrict__ off, int64_t nblk,
+                                                           const double *__restrict__ dp, int64_t n,
+                                                           const int64_t *dn, double lo, double hi,
+                                                           const int32_t *__restrict__ off, int64_t nblk,
                                                            double *keep, double *out_lo, double *out_hi, int64_t cap,
-                                                           unsigned long long *cnt) {
+                                                           unsigned long long *c0, unsigned long long *c1,
+                                                           unsigned long long *c2) {
     __shared__ int wc[3][MIG_T / 32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t i = (int64_t)blockIdx.x * MIG_T + threadIdx.x;
-    const int c = i < n ? mig_cat(x[i], lo, hi) : -1;
+    const int c = i < (dn ? *dn : n) ? mig_cat(x[i], lo, hi) : -1;
     int rank = 0;
 #pragma unroll
     for (int cc = 0; cc < 3; cc++) {
@@ -947,8 +991,10 @@ __global__ void __launch_bounds__(MIG_T) k_migrate_scatter(const double *__restr
             dst[3 * cc_cap + pos] = dp ? dp[i] : 0.0;
         }
     }
-    if (blockIdx.x == 0 && threadIdx.x < 3)
-        cnt[threadIdx.x] = (unsigned long long)(off[(threadIdx.x + 1) * nblk] - off[threadIdx.x * nblk]);
+    if (blockIdx.x == 0 && threadIdx.x < 3) {
+        unsigned long long *dcnt = threadIdx.x == 0 ? c0 : (threadIdx.x == 1 ? c1 : c2);
+        *dcnt = (unsigned long long)(off[(threadIdx.x + 1) * nblk] - off[threadIdx.x * nblk]);
+    }
 }
 
 __global__ void k_migrate_unpack(const double *keep, int64_t n, const unsigned long long *cnt, double *x, double *y,
@@ -961,20 +1007,23 @@ __global__ void k_migrate_unpack(const double *keep, int64_t n, const unsigned l
     if (dp) dp[k] = keep[3 * n + k];
 }
 
-extern "C" tm_status tm_migrate_pack(tm_ctx *ctx, double *x, double *y, int32_t *gid, double *d_prev,
-                                     int64_t n_owned, double strip_lo, double strip_hi, double *out_lo,
-                                     double *out_hi, int64_t cap, int64_t *cnt3) {
-    if (!ctx) return TM_E_ARG;
-    if (!x || !y || !gid || !out_lo || !out_hi || !cnt3 || n_owned < 0 || cap < 0)
-        TM_FAIL(ctx, TM_E_ARG, "null argument to tm_migrate_pack");
+// n: count (host) or capacity with dn (device count, read before anything is written: the
+// kept count may be written to the same location, c_kept == dn is allowed)
+static tm_status migrate_impl(tm_ctx *ctx, double *x, double *y, int32_t *gid, double *d_prev, int64_t n,
+                              const int64_t *dn, double lo, double hi, double *out_lo, double *out_hi, int64_t cap,
+                              int64_t *c_kept, int64_t *c_lo, int64_t *c_hi) {
     TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
-    TM_CUDA_TRY(ctx, cudaMemsetAsync(cnt3, 0, 3 * sizeof(int64_t), ctx->stream));
-    if (n_owned == 0) return TM_OK;
-    const int64_t nblk = (n_owned + MIG_T - 1) / MIG_T;
-    if (n_owned > ctx->cap_mig) {
+    if (!dn) {
+        TM_CUDA_TRY(ctx, cudaMemsetAsync(c_kept, 0, sizeof(int64_t), ctx->stream));
+        TM_CUDA_TRY(ctx, cudaMemsetAsync(c_lo, 0, sizeof(int64_t), ctx->stream));
+        TM_CUDA_TRY(ctx, cudaMemsetAsync(c_hi, 0, sizeof(int64_t), ctx->stream));
+    }
+    if (n == 0) return TM_OK;
+    const int64_t nblk = (n + MIG_T - 1) / MIG_T;
+    if (n > ctx->cap_mig) {
         cudaFree(ctx->mig_keep);
         ctx->mig_keep = nullptr;
-        const int64_t c = n_owned + n_owned / 8 + 1024;
+        const int64_t c = n + n / 8 + 1024;
         TM_CUDA_TRY(ctx, cudaMalloc(&ctx->mig_keep, 4 * c * sizeof(double)));
         ctx->cap_mig = c;
     }
@@ -987,17 +1036,81 @@ extern "C" tm_status tm_migrate_pack(tm_ctx *ctx, double *x, double *y, int32_t 
         TM_CUDA_TRY(ctx, cudaMalloc(&ctx->mig_off, c * sizeof(int32_t)));
         ctx->cap_mig_blk = c;
     }
+    const int64_t *src_n = nullptr;
+    if (dn) {  // the source count, copied: the kept count may overwrite *dn
+        if (!ctx->scratch_n) TM_CUDA_TRY(ctx, cudaMalloc(&ctx->scratch_n, 2 * sizeof(int64_t)));
+        TM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->scratch_n, dn, sizeof(int64_t), cudaMemcpyDeviceToDevice, ctx->stream));
+        src_n = ctx->scratch_n;
+    }
     tm_status s = ensure_scan_scratch(ctx, 3 * nblk);
     if (s != TM_OK) return s;
-    // keep is n_owned-strided: the scatter writes [x | y | gid | d_prev] segments of stride n_owned
-    k_migrate_count<<<(unsigned)nblk, MIG_T, 0, ctx->stream>>>(x, n_owned, strip_lo, strip_hi, ctx->mig_cnt, nblk);
+    // keep is n-strided: the scatter writes [x | y | gid | d_prev] segments of stride n
+    k_migrate_count<<<(unsigned)nblk, MIG_T, 0, ctx->stream>>>(x, n, src_n, lo, hi, ctx->mig_cnt, nblk);
     if ((s = scan_counts(ctx, ctx->mig_cnt, ctx->mig_off, 3 * nblk)) != TM_OK) return s;
-    k_migrate_scatter<<<(unsigned)nblk, MIG_T, 0, ctx->stream>>>(x, y, gid, d_prev, n_owned, strip_lo, strip_hi,
-                                                                 ctx->mig_off, nblk, ctx->mig_keep, out_lo, out_hi,
-                                                                 cap, (unsigned long long *)cnt3);
-    k_migrate_unpack<<<(unsigned)nblk, MIG_T, 0, ctx->stream>>>(ctx->mig_keep, n_owned,
-                                                                (const unsigned long long *)cnt3, x, y, gid, d_prev);
+    k_migrate_scatter<<<(unsigned)nblk, MIG_T, 0, ctx->stream>>>(
+        x, y, gid, d_prev, n, src_n, lo, hi, ctx->mig_off, nblk, ctx->mig_keep, out_lo, out_hi, cap,
+        (unsigned long long *)c_kept, (unsigned long long *)c_lo, (unsigned long long *)c_hi);
+    k_migrate_unpack<<<(unsigned)nblk, MIG_T, 0, ctx->stream>>>(ctx->mig_keep, n, (const unsigned long long *)c_kept,
+                                                                x, y, gid, d_prev);
     return tm_internal_check_launch(ctx, "k_migrate");
+}
+
+extern "C" tm_status tm_migrate_pack(tm_ctx *ctx, double *x, double *y, int32_t *gid, double *d_prev,
+                                     int64_t n_owned, double strip_lo, double strip_hi, double *out_lo,
+                                     double *out_hi, int64_t cap, int64_t *cnt3) {
+    if (!ctx) return TM_E_ARG;
+    if (!x || !y || !gid || !out_lo || !out_hi || !cnt3 || n_owned < 0 || cap < 0)
+        TM_FAIL(ctx, TM_E_ARG, "null argument to tm_migrate_pack");
+    return migrate_impl(ctx, x, y, gid, d_prev, n_owned, nullptr, strip_edge(strip_lo), strip_edge(strip_hi), out_lo,
+                        out_hi, cap, cnt3, cnt3 + 1, cnt3 + 2);
+}
+
+extern "C" tm_status tm_migrate_pack_dc(tm_ctx *ctx, double *x, double *y, int32_t *gid, double *d_prev,
+                                        int64_t *d_n_owned, int64_t cap_owned, double strip_lo, double strip_hi,
+                                        double *out_lo, double *out_hi, int64_t cap, int64_t *cnt_lo,
+                                        int64_t *cnt_hi) {
+    if (!ctx) return TM_E_ARG;
+    if (!x || !y || !gid || !d_n_owned || !out_lo || !out_hi || !cnt_lo || !cnt_hi || cap_owned < 0 || cap < 0)
+        TM_FAIL(ctx, TM_E_ARG, "null argument to tm_migrate_pack_dc");
+    return migrate_impl(ctx, x, y, gid, d_prev, cap_owned, d_n_owned, strip_edge(strip_lo), strip_edge(strip_hi),
+                        out_lo, out_hi, cap, d_n_owned, cnt_lo, cnt_hi);
+}
+
+// Append a received strip message (segments [x | y | gid (| d_prev)] of capacity msg_cap,
+// *msg_count entries) after the *d_count points of x/y/gid(/d_prev) (capacity cap), then
+// advance *d_count: all on the device (no host sync).  Beyond a capacity nothing is written
+// and TM_E_CAPACITY is latched.
+__global__ void k_append(double *__restrict__ x, double *__restrict__ y, int32_t *__restrict__ gid,
+                         double *__restrict__ dp, const int64_t *d_count, int64_t cap, const double *__restrict__ src,
+                         const int64_t *src_count, int64_t src_cap) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t k = *src_count, base = *d_count;
+    if (i >= k || i >= src_cap || base + i >= cap) return;
+    x[base + i] = src[i];
+    y[base + i] = src[src_cap + i];
+    gid[base + i] = ((const int32_t *)(src + 2 * src_cap))[i];
+    if (dp) dp[base + i] = src[3 * src_cap + i];
+}
+
+__global__ void k_append_count(int64_t *d_count, int64_t cap, const int64_t *src_count, int64_t src_cap,
+                               DevState *st) {
+    const int64_t k = *src_count, base = *d_count;
+    if (k > src_cap || base + k > cap) atomicAdd(&st->n_strip_overflow, 1ull);
+    *d_count = min(base + min(k, src_cap), cap);
+}
+
+extern "C" tm_status tm_append_points(tm_ctx *ctx, double *x, double *y, int32_t *gid, double *d_prev,
+                                      int64_t *d_count, int64_t cap, const double *msg, const int64_t *msg_count,
+                                      int64_t msg_cap) {
+    if (!ctx) return TM_E_ARG;
+    if (!x || !y || !gid || !d_count || !msg || !msg_count || cap < 0 || msg_cap < 0)
+        TM_FAIL(ctx, TM_E_ARG, "null argument to tm_append_points");
+    TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    if (msg_cap > 0)
+        k_append<<<(unsigned)((msg_cap + 255) / 256), 256, 0, ctx->stream>>>(x, y, gid, d_prev, d_count, cap, msg,
+                                                                          msg_count, msg_cap);
+    k_append_count<<<1, 1, 0, ctx->stream>>>(d_count, cap, msg_count, msg_cap, ctx->dst);
+    return tm_internal_check_launch(ctx, "k_append");
 }
 
 extern "C" int tm_host_incircle_exact(const double *a, const double *b, const double *c, const double *d) {

@@ -201,12 +201,12 @@ __global__ void __launch_bounds__(BLOCK, (G == 16 ? TM_MINB : 1)) k_cells(CellAr
     const int lane = g.thread_rank();
     const int gib = threadIdx.x / G;
     int32_t *sbuf = sbuf_all[gib];
-    const int64_t nitems = (MODE & M_RETRY) ? (int64_t)*retry_cnt : A.n_local;
+    const int64_t nitems = (MODE & M_RETRY) ? (int64_t)*retry_cnt : live_local(A);
     const int64_t stride = (MODE & M_RETRY) ? (int64_t)gridDim.x * CPB : 0;
     for (int64_t item = (int64_t)blockIdx.x * CPB + gib; item < nitems; item += stride) {
         const int64_t cell = (MODE & M_RETRY) ? (int64_t)retry_list[item] : item;
         const int32_t orig = __ldg(A.perm + cell);
-        if (orig < A.n_owned) {
+        if (orig < live_owned(A)) {
             const double px = __ldg(A.xs + cell), py = __ldg(A.ys + cell);
             const double h = __ldg(A.hs + cell);
             const int32_t gi = __ldg(A.gids + cell);

@@ -452,9 +452,10 @@ __global__ void __launch_bounds__(TB, (MODE & M_WCERT) ? TM_WMINB : TM_TMINB) k_
     TPoly P = tpoly_bind(tsmem, tid);
     bool live = false;
     int32_t orig = 0;
-    if (cell < A.n_local) {
+    const int64_t n_live = live_local(A);
+    if (cell < n_live) {
         orig = __ldg(A.perm + cell);
-        live = orig < A.n_owned;
+        live = orig < live_owned(A);
     }
     // ---- per-cell results consumed by the warp-collective emission below
     int t_own = 0;
@@ -562,7 +563,7 @@ __global__ void __launch_bounds__(TB, (MODE & M_WCERT) ? TM_WMINB : TM_TMINB) k_
                 const int id = A.nbr[(int64_t)nid * TM_NBR + wi++];
                 if (id < 0 || (int64_t)id >= A.nbr_keys) continue;
                 const int js = A.inv_perm[id];  // stale for a gid not binned here: checked
-                if (js < 0 || (int64_t)js >= A.n_local || (A.nbr_by_gid && __ldg(A.gids + js) != id)) continue;
+                if (js < 0 || (int64_t)js >= n_live || (A.nbr_by_gid && __ldg(A.gids + js) != id)) continue;
                 j = js;
                 P.lmask |= 1ull << (j & 63);
                 break;
@@ -676,7 +677,7 @@ __global__ void __launch_bounds__(TB, (MODE & M_WCERT) ? TM_WMINB : TM_TMINB) k_
                 const int id = A.nbr[(int64_t)nid * TM_NBR + w];
                 if (id < 0 || (int64_t)id >= A.nbr_keys) continue;
                 const int js = A.inv_perm[id];
-                if (js < 0 || (int64_t)js >= A.n_local || js == (int)cell ||
+                if (js < 0 || (int64_t)js >= n_live || js == (int)cell ||
                     (A.nbr_by_gid && __ldg(A.gids + js) != id))
                     continue;
                 const double dx = csub(__ldg(A.xs + js), px), dy = csub(__ldg(A.ys + js), py);

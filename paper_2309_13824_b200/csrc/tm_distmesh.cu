@@ -26,12 +26,13 @@ __device__ __forceinline__ double mu_at(const Grid &g, const double *mu, double 
 __global__ void __launch_bounds__(DM_T) k_dm_sums(const double *__restrict__ xs, const double *__restrict__ ys,
                                                   const int32_t *__restrict__ perm, const int32_t *__restrict__ gids,
                                                   const int32_t *__restrict__ adj, const uint8_t *__restrict__ deg,
-                                                  int64_t n_local, int64_t n_owned, Grid g,
+                                                  int64_t n_local, int64_t n_owned, const int64_t *dcnt, Grid g,
                                                   const double *__restrict__ mu, double *__restrict__ partials) {
     __shared__ double red[2][DM_T / 32];
     int64_t s = (int64_t)blockIdx.x * DM_T + threadIdx.x;
     double l2 = 0.0, m2 = 0.0;
-    if (s < n_local && perm[s] < n_owned) {
+    const int64_t n_live = dcnt ? dcnt[1] : n_local, n_own = dcnt ? dcnt[0] : n_owned;
+    if (s < n_live && perm[s] < n_own) {
         const double xi = xs[s], yi = ys[s];
         const int32_t gi = gids[s];
         const int d = deg[s];
@@ -105,9 +106,9 @@ __global__ void __launch_bounds__(DM_T) k_dm_step(CellArgs A, const int32_t *__r
                                                   const uint8_t *__restrict__ deg, const double *__restrict__ sums2,
                                                   const uint8_t *__restrict__ fixed, double fscale, double dt_k) {
     int64_t s = (int64_t)blockIdx.x * DM_T + threadIdx.x;
-    if (s >= A.n_local) return;
+    if (s >= live_local(A)) return;
     int32_t orig = A.perm[s];
-    if (orig >= A.n_owned) return;
+    if (orig >= live_owned(A)) return;
     double fac_mu = sqrt(sums2[0] / sums2[1]);
     double xi = A.xs[s], yi = A.ys[s];
     double Fx = 0.0, Fy = 0.0;
@@ -165,7 +166,7 @@ extern "C" tm_status tm_distmesh_sums(tm_ctx *ctx, const int32_t *adj, const uin
         ctx->cap_partials = 2 * nblk;
     }
     k_dm_sums<<<(unsigned)nblk, DM_T, 0, ctx->stream>>>(ctx->xs, ctx->ys, ctx->perm, ctx->gids, adj, deg,
-                                                        ctx->n_local, ctx->n_owned, ctx->grid, ctx->mu,
+                                                        ctx->n_local, ctx->n_owned, ctx->dcnt, ctx->grid, ctx->mu,
                                                         ctx->partials);
     k_dm_final<<<1, DM_T, 0, ctx->stream>>>(ctx->partials, nblk, sums2);
     return tm_internal_check_launch(ctx, "k_dm_sums");

@@ -22,6 +22,7 @@ struct DevState {
     unsigned long long n_tri_overflow; // triangles beyond tri_cap
     unsigned long long n_adj_overflow; // ELL rows beyond adj_stride
     unsigned long long n_fallback;     // projection fallbacks
+    unsigned long long n_strip_overflow; // strip messages / appends beyond their capacity
     unsigned long long work[11];       // tm_work fields n_cells .. exact_calls, then warp_trips
 };
 
@@ -79,7 +80,8 @@ struct CellArgs {
     const uint8_t *rlev;
     const int32_t *leaf_off, *leaf_start;
     BinGeom bg;
-    int64_t n_local, n_owned;
+    int64_t n_local, n_owned;  // capacity (array stride) and owned bound; the live counts are
+    const int64_t *dcnt;       // device {n_owned, n_local} when binned by tm_grid_bin_dc, else NULL
     Grid grid;
     const double *phi, *mu, *rho;
     const double4 *rho4;     // rho's grid cells with their 4 corners packed (f00, f10, f01, f11), or NULL
@@ -157,6 +159,8 @@ struct tm_ctx {
     // device health counters
     tmg::DevState *dst = nullptr;
     bool have_cells = false;
+    const int64_t *dcnt = nullptr;  // device {n_owned, n_local} of the last tm_grid_bin_dc, else NULL
+    int64_t *scratch_n = nullptr;   // device scratch count (migration source size)
 };
 
 #define TM_CUDA_TRY(ctx, call)                                                                       \
@@ -174,6 +178,11 @@ struct tm_ctx {
         snprintf((ctx)->err, sizeof((ctx)->err), __VA_ARGS__);    \
         return (code);                                            \
     } while (0)
+
+// live counts of the binned point set: host values, or device ones (tm_grid_bin_dc: the
+// multi-GPU strip path learns its ghost and migrant counts on the device, no host sync)
+__device__ __forceinline__ int64_t live_local(const tmg::CellArgs &A) { return A.dcnt ? __ldg(A.dcnt + 1) : A.n_local; }
+__device__ __forceinline__ int64_t live_owned(const tmg::CellArgs &A) { return A.dcnt ? __ldg(A.dcnt) : A.n_owned; }
 
 // internal helpers implemented in tm_api.cu
 tm_status tm_internal_fill_cell_args(tm_ctx *ctx, tmg::CellArgs *a);

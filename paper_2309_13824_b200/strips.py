@@ -5,26 +5,34 @@ Rank r owns the points with x in [X_r, X_{r+1}).  Per iteration:
   1. halo: every rank sends the owned points within W of each strip edge to
      the neighbour across it (x, y, gid), W = 2 * S_max = 2 * fac_voro * h_max
      (a cell lies inside its octagon of circumradius S, so only points within
-     2S can cut it);
-  2. the rank bins owned + ghosts (tm_grid_bin with n_owned < n_local and the
-     global ids) and computes cells for its OWNED points only; a triangle is
-     emitted by the owner of its smallest-id vertex, so every triangle appears
-     exactly once over all ranks;
+     2S can cut it); strips narrower than W are refused (Strips.check_width);
+  2. the rank bins owned + ghosts (global ids) and computes cells for its OWNED
+     points only; a triangle is emitted by the owner of its smallest-id vertex,
+     so every triangle appears exactly once over all ranks;
   3. (DistMesh) the two edge sums are all-reduced (each edge counted by the
      rank owning its smaller-id endpoint);
   4. migrate: updated points that left the strip go to the neighbour.
 
-The arithmetic runs in the backend (GpuStripBackend: the C-ABI kernels); the
-exchange runs in an exchanger: TorchP2P (torch.distributed send/recv, NCCL
-over NVLink on GPUs or gloo on CPU) or Loopback (P ranks inside one process,
-for single-GPU emulation and tests).  This module only orchestrates.
+No host synchronisation inside an iteration: every message has a FIXED size
+(capacity `cap_msg`, an int64 count header followed by SoA segments), the
+counts live on the device, and the library's device-count calls
+(tm_halo_pack_dc, tm_append_points, tm_grid_bin_dc, tm_migrate_pack_dc) take
+them from there.  All buffers are allocated once (StripState).  Overflow of a
+capacity is latched by the library and raised at the next synchronising call.
+
+The arithmetic runs in a backend (GpuStripBackend: the C ABI; the CPU test
+double in tests/strip_cpu_backend.py); the exchange runs in an exchanger:
+TorchP2P (torch.distributed send/recv, NCCL over NVLink on GPUs or gloo on
+CPU) or the in-process loopback of `loopback_step`.  This module orchestrates.
 """
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from typing import List, Optional
 
 import torch
+
+HALO_SEGS, MIG_SEGS = 3, 4  # message segments: x | y | gid (| d_prev)
 
 
 @dataclass
@@ -73,76 +81,123 @@ class Strips:
         return torch.clamp(((x - self.x0) / w).floor().to(torch.int64), 0, self.P - 1)
 
 
-@dataclass
-class RankState:
-    """Owned points of one rank (device or host tensors)."""
-    rank: int
-    x: torch.Tensor
-    y: torch.Tensor
-    gid: torch.Tensor          # int32 global ids
-    d_prev: Optional[torch.Tensor] = None
-    tri: Optional[torch.Tensor] = None   # triangles emitted by this rank (global ids)
-    extra: dict = field(default_factory=dict)
+def ghost_width(c: float, fac_voro: float = 5.0, mu_max: float = 1.0) -> float:
+    """W = 2 S_max, S = fac_voro * h, h = c * mu (reading L34)."""
+    return 2.0 * fac_voro * c * mu_max
 
 
-def split_initial(x, y, strips: Strips, rank: int, d_prev=None) -> RankState:
+class Msg:
+    """A fixed-size strip message: int64 count header, then `segs` SoA segments of `cap`
+    (doubles; the gid segment holds int32).  Sent and received whole: the receiver never
+    needs the count on the host."""
+
+    def __init__(self, cap: int, segs: int, device):
+        self.cap, self.segs = cap, segs
+        self.buf = torch.zeros(1 + segs * cap, dtype=torch.float64, device=device)
+
+    @property
+    def header(self) -> torch.Tensor:
+        return self.buf[:1].view(torch.int64)
+
+    def addr(self) -> int:
+        return self.buf.data_ptr()
+
+    def payload_addr(self) -> int:
+        return self.buf.data_ptr() + 8
+
+    def count(self) -> int:  # tests / diagnostics only (synchronises)
+        return int(self.header.item())
+
+    def segment(self, k: int, n: int, dtype=torch.float64) -> torch.Tensor:
+        seg = self.buf[1 + k * self.cap: 1 + (k + 1) * self.cap]
+        return seg.view(torch.int32)[:n] if dtype == torch.int32 else seg[:n]
+
+
+class StripState:
+    """Persistent per-rank state: owned points at [0, n_owned), ghosts after them, with
+    device counts {n_owned, n_local}; the update's outputs in a second set of arrays (swapped
+    after migration); the four halo and four migration messages."""
+
+    def __init__(self, rank: int, x: torch.Tensor, y: torch.Tensor, gid: torch.Tensor, cap_own: int, cap_msg: int,
+                 d_prev: Optional[torch.Tensor] = None):
+        dev = x.device
+        n = x.shape[0]
+        if n > cap_own:
+            raise ValueError(f"rank {rank}: {n} owned points exceed the capacity {cap_own}")
+        self.rank, self.cap_own, self.cap_msg = rank, cap_own, cap_msg
+        self.cap_local = cap_own + 2 * cap_msg
+        f64 = dict(dtype=torch.float64, device=dev)
+        self.X, self.Y, self.D = (torch.zeros(self.cap_local, **f64) for _ in range(3))
+        self.Xo, self.Yo, self.Do = (torch.zeros(self.cap_local, **f64) for _ in range(3))
+        self.G = torch.zeros(self.cap_local, dtype=torch.int32, device=dev)
+        self.status = torch.zeros(self.cap_local, dtype=torch.int8, device=dev)
+        self.X[:n], self.Y[:n], self.G[:n] = x, y, gid
+        self.have_dprev = d_prev is not None
+        if d_prev is not None:
+            self.D[:n] = d_prev
+        self.counts = torch.tensor([n, n], dtype=torch.int64, device=dev)  # n_owned, n_local
+        self.h_send = [Msg(cap_msg, HALO_SEGS, dev) for _ in range(2)]
+        self.h_recv = [Msg(cap_msg, HALO_SEGS, dev) for _ in range(2)]
+        self.m_send = [Msg(cap_msg, MIG_SEGS, dev) for _ in range(2)]
+        self.m_recv = [Msg(cap_msg, MIG_SEGS, dev) for _ in range(2)]
+        self.extra = {}
+
+    def reset(self, x: torch.Tensor, y: torch.Tensor, gid: torch.Tensor, counts: torch.Tensor):
+        """Restart from the given owned points (device copies, no host sync): counts is a
+        device int64[2] {n, n}."""
+        n = x.shape[0]
+        self.X[:n], self.Y[:n], self.G[:n] = x, y, gid
+        self.counts.copy_(counts)
+        self.have_dprev = False
+
+    def swap(self):
+        self.X, self.Xo = self.Xo, self.X
+        self.Y, self.Yo = self.Yo, self.Y
+        self.D, self.Do = self.Do, self.D
+        self.have_dprev = True
+
+    def owned(self):
+        """The owned points (host-visible views; synchronises): x, y, gid, d_prev."""
+        n = int(self.counts[0].item())
+        return self.X[:n], self.Y[:n], self.G[:n], (self.D[:n] if self.have_dprev else None)
+
+
+def split_initial(x, y, strips: Strips, rank: int, cap_own: int, cap_msg: int, d_prev=None) -> StripState:
     own = strips.owner(x) == rank
     gid = torch.nonzero(own, as_tuple=False).flatten().to(torch.int32)
-    return RankState(rank, x[own].contiguous(), y[own].contiguous(), gid.contiguous(),
-                     None if d_prev is None else d_prev[own].contiguous())
+    return StripState(rank, x[own].contiguous(), y[own].contiguous(), gid.contiguous(), cap_own, cap_msg,
+                      None if d_prev is None else d_prev[own].contiguous())
+
+
+def capacities(n_total: int, P: int, n_ghost_est: int, slack: float = 1.15):
+    """Owned and message capacities: the owned share with slack for migration, and a halo
+    message sized for the estimated ghosts per side (at most the owned capacity)."""
+    cap_own = int(slack * n_total / P) + 1024
+    cap_msg = min(cap_own, int(4 * n_ghost_est) + 4096)
+    return cap_own, cap_msg
 
 
 # ---------------------------------------------------------------- exchangers
 class TorchP2P:
-    """Neighbour exchange with torch.distributed (NCCL or gloo): counts first,
-    then the SoA payload, to ranks r-1 and r+1 (grouped send/recv)."""
+    """Neighbour exchange of fixed-size messages with torch.distributed (NCCL or gloo):
+    one grouped send/recv round per exchange; with NCCL the waits are stream-ordered (the
+    host does not block)."""
 
     def __init__(self, rank: int, world: int, device):
         self.rank, self.world, self.device = rank, world, device
 
-    def _pair(self, send: List[Optional[torch.Tensor]], recv_like):
+    def exchange(self, send_lo: Msg, send_hi: Msg, recv_lo: Msg, recv_hi: Msg):
         import torch.distributed as dist
-        ops, recv = [], [None, None]
-        nbr = [self.rank - 1, self.rank + 1]
-        for side in (0, 1):
-            if 0 <= nbr[side] < self.world:
-                ops.append(dist.P2POp(dist.isend, send[side], nbr[side]))
-                recv[side] = recv_like(side)
-                ops.append(dist.P2POp(dist.irecv, recv[side], nbr[side]))
+        ops = []
+        if self.rank > 0:
+            ops += [dist.P2POp(dist.isend, send_lo.buf, self.rank - 1),
+                    dist.P2POp(dist.irecv, recv_lo.buf, self.rank - 1)]
+        if self.rank < self.world - 1:
+            ops += [dist.P2POp(dist.isend, send_hi.buf, self.rank + 1),
+                    dist.P2POp(dist.irecv, recv_hi.buf, self.rank + 1)]
         if ops:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
-        return recv
-
-    def exchange(self, to_lo: List[torch.Tensor], to_hi: List[torch.Tensor]):
-        """to_lo/to_hi: lists of 1-D tensors of equal length (same dtypes on both sides).
-        Returns (from_lo, from_hi) lists (None where there is no neighbour).  Two rounds:
-        the element counts, then every array of a side packed into one byte buffer."""
-        dev = self.device
-        n = [torch.tensor([to_lo[0].shape[0]], dtype=torch.int64, device=dev),
-             torch.tensor([to_hi[0].shape[0]], dtype=torch.int64, device=dev)]
-        cnt = self._pair(n, lambda s: torch.empty(1, dtype=torch.int64, device=dev))
-        dts = [t.dtype for t in to_lo]
-        esz = [torch.empty(0, dtype=d).element_size() for d in dts]
-        order = sorted(range(len(dts)), key=lambda i: -esz[i])  # widest first: every view stays aligned
-
-        def pack(lst):
-            if not lst[0].numel():
-                return torch.empty(0, dtype=torch.uint8, device=dev)
-            return torch.cat([lst[i].contiguous().view(torch.uint8) for i in order])
-        k = [None if c is None else int(c.item()) for c in cnt]
-        got = self._pair([pack(to_lo), pack(to_hi)],
-                         lambda s: torch.empty(k[s] * sum(esz), dtype=torch.uint8, device=dev))
-        out = [None, None]
-        for side in (0, 1):
-            if got[side] is None:
-                continue
-            parts, off = [None] * len(dts), 0
-            for i in order:
-                parts[i] = got[side][off:off + k[side] * esz[i]].view(dts[i])
-                off += k[side] * esz[i]
-            out[side] = parts
-        return out[0], out[1]
 
     def allreduce_sum(self, t: torch.Tensor):
         import torch.distributed as dist
@@ -151,195 +206,124 @@ class TorchP2P:
         return t
 
 
-class Loopback:
-    """P ranks in one process: exchange() is called once per rank in order with
-    the same call pattern; messages are parked until the matching rank reads."""
-
-    def __init__(self, P: int):
-        self.P = P
-        self.box = {}
-
-    def view(self, rank: int):
-        return _LoopbackView(self, rank)
-
-
-class _LoopbackView:
-    def __init__(self, lb: Loopback, rank: int):
-        self.lb, self.rank = lb, rank
-
-    def post(self, tag, to_lo, to_hi):
-        if self.rank > 0:
-            self.lb.box[(tag, self.rank, self.rank - 1)] = [t.clone() for t in to_lo]
-        if self.rank < self.lb.P - 1:
-            self.lb.box[(tag, self.rank, self.rank + 1)] = [t.clone() for t in to_hi]
-
-    def collect(self, tag):
-        a = self.lb.box.pop((tag, self.rank - 1, self.rank), None)
-        b = self.lb.box.pop((tag, self.rank + 1, self.rank), None)
-        return a, b
-
-
 # ---------------------------------------------------------------- backend (GPU)
 class GpuStripBackend:
-    """The per-rank arithmetic through the C ABI (no CPU work)."""
+    """The per-rank arithmetic through the C ABI (no CPU work, no host synchronisation)."""
 
-    def __init__(self, ctx, adj_stride=16, keep_tri=True, adaptive_halo=True):
+    def __init__(self, ctx, adj_stride=16, adaptive_halo=True):
+        import paper_2309_13824_b200 as T
+        self.T = T
         self.ctx = ctx
         self.adj_stride = adj_stride
         self.adaptive_halo = adaptive_halo  # per-point halo width from the Lipschitz bound of mu~
-        self.keep_tri = keep_tri  # False: leave the triangles in the device buffers (no count readback)
-        self.bufs = {}
+        self.bufs = None
 
-    def _buf(self, name, numel, dtype, dev):
-        """Persistent scratch (grown on demand): no per-iteration allocation."""
-        b = self.bufs.get(name)
-        if b is None or b.numel() < numel or b.device != dev:
-            b = torch.empty(int(numel * 1.125) + 1024, dtype=dtype, device=dev)
-            self.bufs[name] = b
-        return b
+    def _bufs(self, S: StripState):
+        if self.bufs is None or self.bufs.n != S.cap_local:
+            self.bufs = self.T.IterBuffers.alloc(S.cap_local, self.adj_stride, device=S.X.device)
+        return self.bufs
 
-    def halo(self, st: RankState, lo, hi, W):
-        dev = st.x.device
-        n = st.x.shape[0]
-        cap = n
-        send_lo = self._buf("send_lo", 3 * cap + 1, torch.float64, dev)
-        send_hi = self._buf("send_hi", 3 * cap + 1, torch.float64, dev)
-        cnt = self._buf("hcnt", 2, torch.int64, dev)[:2]
-        self.ctx.tm_halo_pack(st.x, st.y, st.gid, n, lo if lo > -1e300 else -1e300, hi if hi < 1e300 else 1e300,
-                              -W if self.adaptive_halo else W, send_lo, send_hi, cap, cnt)
-        c = cnt.tolist()
+    def halo_pack(self, S: StripState, lo, hi, W):
+        self.ctx.tm_halo_pack_dc(S.X, S.Y, S.G, S.counts.data_ptr(), S.cap_own, lo, hi,
+                                 -W if self.adaptive_halo else W, S.h_send[0].payload_addr(),
+                                 S.h_send[1].payload_addr(), S.cap_msg, S.h_send[0].addr(), S.h_send[1].addr())
 
-        def seg(buf, k):
-            return [buf[:k].clone(), buf[cap:cap + k].clone(),
-                    buf[2 * cap:2 * cap + (k + 1) // 2 + 1].view(torch.int32)[:k].clone()]
-        return seg(send_lo, c[0]), seg(send_hi, c[1])
+    def append_ghosts(self, S: StripState):
+        S.counts[1:2].copy_(S.counts[0:1])
+        for m in S.h_recv:
+            self.ctx.tm_append_points(S.X, S.Y, S.G, None, S.counts.data_ptr() + 8, S.cap_local, m.payload_addr(),
+                                      m.addr(), m.cap)
 
-    def cells_begin(self, st: RankState, ghosts, mode: str):
-        """Bin owned + ghosts, compute the owned cells.  CVD completes here;
-        DistMesh stops after pass 1 and returns its local edge sums."""
-        import paper_2309_13824_b200 as T
-        xs = [st.x] + [g[0] for g in ghosts if g is not None]
-        ys = [st.y] + [g[1] for g in ghosts if g is not None]
-        gs = [st.gid] + [g[2] for g in ghosts if g is not None]
-        xl, yl, gl = torch.cat(xs).contiguous(), torch.cat(ys).contiguous(), torch.cat(gs).contiguous()
-        n_own, n_loc = st.x.shape[0], xl.shape[0]
-        ctx = self.ctx
-        ctx.tm_grid_bin(xl, yl, n_own, gl)
-        bufs = T.IterBuffers.alloc(n_loc, self.adj_stride, device=xl.device)
-        h = {"bufs": bufs, "st": st, "mode": mode,
-             "xo": torch.empty(n_own, dtype=torch.float64, device=xl.device)}
-        h["yo"], h["do"] = torch.empty_like(h["xo"]), torch.empty_like(h["xo"])
-        h["status"] = torch.empty(n_own, dtype=torch.int8, device=xl.device)
+    def cells_begin(self, S: StripState, mode: str):
+        """Bin owned + ghosts, compute the owned cells.  CVD completes here; DistMesh stops
+        after pass 1 and returns its local edge sums (device)."""
+        c = self.ctx
+        b = self._bufs(S)
+        c.tm_grid_bin_dc(S.X, S.Y, S.cap_local, S.counts, S.G)
         if mode == "cvd":
-            ctx.tm_voronoi_delaunay(bufs.tri, bufs.n_tri, None, None, st.d_prev, h["xo"], h["yo"], h["do"],
-                                    h["status"])
-            return h, None
-        ctx.tm_voronoi_delaunay(bufs.tri, bufs.n_tri, bufs.adj, bufs.deg)
-        ctx.tm_distmesh_sums(bufs.adj, bufs.deg, bufs.sums2)
-        return h, bufs.sums2
+            c.tm_voronoi_delaunay(b.tri, b.n_tri, None, None, S.D if S.have_dprev else None, S.Xo, S.Yo, S.Do,
+                                  S.status)
+            return None
+        c.tm_voronoi_delaunay(b.tri, b.n_tri, b.adj, b.deg)
+        c.tm_distmesh_sums(b.adj, b.deg, b.sums2)
+        return b.sums2
 
-    def cells_end(self, h, sums2=None):
-        bufs, st = h["bufs"], h["st"]
-        if h["mode"] == "dm":
-            if sums2 is not None and sums2 is not bufs.sums2:
-                bufs.sums2.copy_(sums2)
-            self.ctx.tm_distmesh_step(bufs.adj, bufs.deg, bufs.sums2, None, st.d_prev, h["xo"], h["yo"], h["do"],
-                                      h["status"])
-        if not self.keep_tri:
-            return None, h["xo"], h["yo"], h["do"], h["status"]
-        nt = int(bufs.n_tri.item())
-        return bufs.tri[:nt].clone(), h["xo"], h["yo"], h["do"], h["status"]
+    def cells_end(self, S: StripState, mode: str, sums2=None):
+        if mode != "dm":
+            return
+        b = self.bufs
+        if sums2 is not None and sums2 is not b.sums2:
+            b.sums2.copy_(sums2)
+        self.ctx.tm_distmesh_step(b.adj, b.deg, b.sums2, None, S.D if S.have_dprev else None, S.Xo, S.Yo, S.Do,
+                                  S.status)
 
-    def migrate(self, st: RankState, lo, hi):
-        """Partition the updated owned points (stable, in place in st's arrays,
-        which this iteration produced): kept ones stay at the front, leavers are
-        packed for the neighbours."""
-        dev = st.x.device
-        n = st.x.shape[0]
-        out_lo = self._buf("out_lo", 4 * n + 1, torch.float64, dev)
-        out_hi = self._buf("out_hi", 4 * n + 1, torch.float64, dev)
-        cnt = self._buf("mcnt", 3, torch.int64, dev)[:3]
-        dp = st.d_prev if st.d_prev is not None else torch.zeros(n, dtype=torch.float64, device=dev)
-        x, y, g = st.x, st.y, st.gid.clone()  # gid is shared with the previous state
-        self.ctx.tm_migrate_pack(x, y, g, dp, n, lo if lo > -1e300 else -1e300, hi if hi < 1e300 else 1e300,
-                                 out_lo, out_hi, n, cnt)
-        k, a, b = cnt.tolist()
+    def migrate_pack(self, S: StripState, lo, hi):
+        """Owned outputs that left the strip go to the messages; the rest are compacted in
+        place (Xo, Yo, G, Do) and counts[0] becomes the kept count."""
+        self.ctx.tm_migrate_pack_dc(S.Xo, S.Yo, S.G, S.Do, S.counts.data_ptr(), S.cap_own, lo, hi,
+                                    S.m_send[0].payload_addr(), S.m_send[1].payload_addr(), S.cap_msg,
+                                    S.m_send[0].addr(), S.m_send[1].addr())
 
-        def seg(buf, m):
-            return [buf[:m].clone(), buf[n:n + m].clone(),
-                    buf[2 * n:2 * n + (m + 1) // 2 + 1].view(torch.int32)[:m].clone(), buf[3 * n:3 * n + m].clone()]
-        keep = [x[:k], y[:k], g[:k], dp[:k]]
-        return keep, seg(out_lo, a), seg(out_hi, b)
+    def append_migrants(self, S: StripState):
+        for m in S.m_recv:
+            self.ctx.tm_append_points(S.Xo, S.Yo, S.G, S.Do, S.counts.data_ptr(), S.cap_own, m.payload_addr(),
+                                      m.addr(), m.cap)
+
+    def triangles(self):
+        """This rank's emitted triangles (global ids; synchronises)."""
+        nt = int(self.bufs.n_tri.item())
+        return self.bufs.tri[:nt]
 
 
 # ---------------------------------------------------------------- one iteration
-def ghost_width(c: float, fac_voro: float = 5.0, mu_max: float = 1.0) -> float:
-    """W = 2 S_max, S = fac_voro * h, h = c * mu (reading L34)."""
-    return 2.0 * fac_voro * c * mu_max
-
-
-def strip_iteration(st: RankState, strips: Strips, backend, exchange, W: float, mode: str = "cvd",
-                    allreduce=None) -> RankState:
-    """One iteration on one rank.  `exchange(to_lo, to_hi) -> (from_lo, from_hi)`
-    performs the neighbour exchange (collective over the ranks)."""
+def strip_step(S: StripState, strips: Strips, backend, comm, W: float, mode: str = "cvd"):
+    """One iteration on one rank; `comm` is a TorchP2P (collective over the ranks)."""
     strips.check_width(W)
-    lo, hi = strips.bounds(st.rank)
-    h_lo, h_hi = backend.halo(st, lo, hi, W)
-    g_lo, g_hi = exchange(h_lo, h_hi)
-    hnd, sums2 = backend.cells_begin(st, [g_lo, g_hi], mode)
-    if sums2 is not None and allreduce is not None:
-        allreduce(sums2)
-    tri, xo, yo, do, status = backend.cells_end(hnd, sums2)
-    nst = RankState(st.rank, xo, yo, st.gid, do, tri)
-    nst.extra["status"] = status
-    keep, m_lo, m_hi = backend.migrate(nst, lo, hi)
-    r_lo, r_hi = exchange(m_lo, m_hi)
-    parts = [keep] + [r for r in (r_lo, r_hi) if r is not None]
-    out = RankState(st.rank, torch.cat([p[0] for p in parts]).contiguous(),
-                    torch.cat([p[1] for p in parts]).contiguous(),
-                    torch.cat([p[2] for p in parts]).contiguous(),
-                    torch.cat([p[3] for p in parts]).contiguous(), tri)
-    out.extra["status"] = status
-    out.extra["n_ghosts"] = sum(0 if g is None else g[0].shape[0] for g in (g_lo, g_hi))
-    out.extra["n_migrated_in"] = sum(0 if r is None else r[0].shape[0] for r in (r_lo, r_hi))
-    return out
+    lo, hi = strips.bounds(S.rank)
+    backend.halo_pack(S, lo, hi, W)
+    comm.exchange(S.h_send[0], S.h_send[1], S.h_recv[0], S.h_recv[1])
+    backend.append_ghosts(S)
+    sums2 = backend.cells_begin(S, mode)
+    if sums2 is not None:
+        comm.allreduce_sum(sums2)
+    backend.cells_end(S, mode, sums2)
+    backend.migrate_pack(S, lo, hi)
+    comm.exchange(S.m_send[0], S.m_send[1], S.m_recv[0], S.m_recv[1])
+    backend.append_migrants(S)
+    S.swap()
 
 
-def loopback_iteration(states: List[RankState], strips: Strips, backends, W: float, mode: str = "cvd"):
-    """All P ranks of one iteration inside one process (single-GPU emulation).
-    Phases are run rank by rank with messages parked in a mailbox; the DistMesh
-    sums are reduced across ranks between the two passes."""
+def _loop_exchange(states: List[StripState], send, recv):
+    """In-process exchange among logical ranks: rank r's low message to r-1's high slot."""
     P = len(states)
+    for r, S in enumerate(states):
+        if r > 0:
+            recv(states[r - 1])[1].buf.copy_(send(S)[0].buf)
+        if r < P - 1:
+            recv(states[r + 1])[0].buf.copy_(send(S)[1].buf)
+
+
+def loopback_step(states: List[StripState], strips: Strips, backends, W: float, mode: str = "cvd"):
+    """All P ranks of one iteration inside one process (single-GPU emulation): the same
+    phases as strip_step, each run for every rank before the exchange that follows it; the
+    DistMesh sums are reduced across ranks between the two passes."""
     strips.check_width(W)
-    lb = Loopback(P)
-    views = [lb.view(r) for r in range(P)]
-    halos = []
-    for r, st in enumerate(states):
-        lo, hi = strips.bounds(r)
-        h_lo, h_hi = backends[r].halo(st, lo, hi, W)
-        views[r].post("halo", h_lo, h_hi)
-    for r in range(P):
-        halos.append(views[r].collect("halo"))
-    begun = [backends[r].cells_begin(st, list(halos[r]), mode) for r, st in enumerate(states)]
+    for r, S in enumerate(states):
+        backends[r].halo_pack(S, *strips.bounds(r), W)
+    _loop_exchange(states, lambda S: S.h_send, lambda S: S.h_recv)
+    sums = []
+    for r, S in enumerate(states):
+        backends[r].append_ghosts(S)
+        sums.append(backends[r].cells_begin(S, mode))
     total = None
-    if mode == "dm":  # all-reduce of the two DistMesh sums across the ranks
-        total = sum(b[1] for b in begun)
-    results = [backends[r].cells_end(begun[r][0], total) for r in range(P)]
-    migr = []
-    for r, st in enumerate(states):
-        tri, xo, yo, do, status = results[r]
-        nst = RankState(r, xo, yo, st.gid, do, tri)
-        lo, hi = strips.bounds(r)
-        keep, m_lo, m_hi = backends[r].migrate(nst, lo, hi)
-        views[r].post("mig", m_lo, m_hi)
-        migr.append((keep, status, tri))
-    out = []
-    for r in range(P):
-        keep, status, tri = migr[r]
-        r_lo, r_hi = views[r].collect("mig")
-        parts = [keep] + [p for p in (r_lo, r_hi) if p is not None]
-        s = RankState(r, torch.cat([p[0] for p in parts]).contiguous(), torch.cat([p[1] for p in parts]).contiguous(),
-                      torch.cat([p[2] for p in parts]).contiguous(), torch.cat([p[3] for p in parts]).contiguous(), tri)
-        s.extra["status"] = status
-        out.append(s)
-    return out
+    if mode == "dm":
+        total = sums[0].clone()
+        for s in sums[1:]:
+            total += s
+    for r, S in enumerate(states):
+        backends[r].cells_end(S, mode, total)
+        backends[r].migrate_pack(S, *strips.bounds(r))
+    _loop_exchange(states, lambda S: S.m_send, lambda S: S.m_recv)
+    for r, S in enumerate(states):
+        backends[r].append_migrants(S)
+        S.swap()

@@ -1,10 +1,11 @@
 """x-strip decomposition on ONE GPU: P logical ranks run the
-GPU strip backend (tm_halo_pack, ghost binning with global ids, owner-emits
-triangles, tm_migrate_pack) through the Loopback exchanger.  The union of the
-per-rank triangle sets must equal the oracle's single-domain result, every
+sync-free GPU strip protocol (tm_halo_pack_dc -> fixed-size messages ->
+tm_append_points -> tm_grid_bin_dc with device counts, owner-emits triangles,
+tm_migrate_pack_dc) through the in-process loopback exchanger.  The union of
+the per-rank triangle sets must equal the oracle's single-domain result, every
 triangle must be emitted exactly once and every point owned once, and the
-owned positions must equal the oracle's update (CVD) / agree within the
-parity bar (DistMesh, where the edge-sum reduction order differs)."""
+owned positions must equal the oracle's update (CVD bit for bit) / agree within
+the parity bar (DistMesh, where the edge-sum reduction order differs)."""
 import numpy as np
 import pytest
 import torch
@@ -15,7 +16,32 @@ import oracle as O
 from inputs import configs
 
 
-def _run(P, n, seed, modes, box=(0.0, 0.0, 1.0, 1.0)):
+def _gather(states, backends, n):
+    got, seen = [], np.zeros(n, bool)
+    xs, ys, ds = np.empty(n), np.empty(n), np.empty(n)
+    for st, be in zip(states, backends):
+        x, y, g, d = st.owned()
+        gid = g.cpu().numpy().astype(np.int64)
+        assert not seen[gid].any(), "a point is owned by two ranks"
+        seen[gid] = True
+        xs[gid], ys[gid], ds[gid] = x.cpu().numpy(), y.cpu().numpy(), d.cpu().numpy()
+        got += [tuple(t) for t in be.triangles().cpu().numpy().tolist()]
+    assert seen.all(), "a point is owned by no rank"
+    return got, xs, ys, ds
+
+
+def _make(P, box, phid, n, mu=None, rho=None, adaptive=True):
+    import paper_2309_13824_b200 as T
+    from paper_2309_13824_b200 import strips as S
+    backends = []
+    for r in range(P):
+        ctx = T.Context(0)
+        c, _ = ctx.tm_set_domain(box, phid, mu, rho, n)
+        backends.append(S.GpuStripBackend(ctx, adaptive_halo=adaptive))
+    return backends, c
+
+
+def _run(P, n, seed, modes, box=(0.0, 0.0, 1.0, 1.0), chained=False):
     import paper_2309_13824_b200 as T
     from paper_2309_13824_b200 import strips as S
     phi = configs.box_phi(box, 128)
@@ -23,42 +49,61 @@ def _run(P, n, seed, modes, box=(0.0, 0.0, 1.0, 1.0)):
     x, y = configs.random_points(n, seed, box)
     strips = S.Strips(box[0], box[2], P)
     dev = torch.device("cuda", 0)
-    phid = torch.from_numpy(phi).to(dev)
-    backends = []
-    for r in range(P):
-        ctx = T.Context(0)
-        c, _ = ctx.tm_set_domain(box, phid, None, None, n)
-        backends.append(S.GpuStripBackend(ctx))
+    backends, c = _make(P, box, torch.from_numpy(phi).to(dev), n)
     W = S.ghost_width(c, 5.0)
-    xd, yd = torch.from_numpy(x).to(dev), torch.from_numpy(y).to(dev)
-    states = [S.split_initial(xd, yd, strips, r) for r in range(P)]
+    cap_own, cap_msg = S.capacities(n, P, n // P)
+    to = lambda a: torch.from_numpy(a).to(dev)
+    states = [S.split_initial(to(x), to(y), strips, r, cap_own, cap_msg) for r in range(P)]
     dp = None
     for it, mode in enumerate(modes):
         ref = O.iteration(fs, x, y, mode, d_prev=dp)
-        states = S.loopback_iteration(states, strips, backends, W, mode)
-        got, seen = [], np.zeros(n, bool)
-        xs, ys, ds = np.empty(n), np.empty(n), np.empty(n)
-        for st in states:
-            gid = st.gid.cpu().numpy().astype(np.int64)
-            assert not seen[gid].any()
-            seen[gid] = True
-            xs[gid], ys[gid], ds[gid] = st.x.cpu().numpy(), st.y.cpu().numpy(), st.d_prev.cpu().numpy()
-            got += [tuple(t) for t in st.tri.cpu().numpy().tolist()]
-        assert seen.all()
+        S.loopback_step(states, strips, backends, W, mode)
+        backends[0].ctx.tm_sync()
+        got, xs, ys, ds = _gather(states, backends, n)
         assert len(got) == len(set(got)), "a triangle was emitted by two ranks"
         assert set(got) == set(map(tuple, ref.tri.tolist())), f"P={P} it={it} {mode}: triangle sets differ"
         diam = np.hypot(box[2] - box[0], box[3] - box[1])
         err = np.hypot(xs - ref.x, ys - ref.y).max()
         assert err <= 1e-12 * diam, f"P={P} it={it} {mode}: position error {err:.3e}"
-        x, y, dp = ref.x, ref.y, ref.d_prev
-        # continue from the oracle's state so that both sides start each iteration identically
-        states = [S.split_initial(torch.from_numpy(x).to(dev), torch.from_numpy(y).to(dev), strips, r,
-                                  d_prev=torch.from_numpy(dp).to(dev)) for r in range(P)]
+        if mode == "cvd":
+            assert np.array_equal(xs, ref.x) and np.array_equal(ys, ref.y), f"P={P} it={it}: CVD not bit-identical"
+        if chained:  # continue from the ranks' own state (migration, warm start across iterations)
+            x, y, dp = xs, ys, ds
+        else:        # continue from the oracle's state so that both sides start identically
+            x, y, dp = ref.x, ref.y, ref.d_prev
+            states = [S.split_initial(to(x), to(y), strips, r, cap_own, cap_msg, d_prev=to(dp)) for r in range(P)]
 
 
 @pytest.mark.parametrize("P", [2, 3, 8])
 def test_gpu_strips_loopback_match_single_domain(P):
     _run(P, 20000, 21 + P, ["cvd", "dm", "cvd"])
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_gpu_strips_chained_iterations(P):
+    """Five iterations on the ranks' own state: points migrate between strips, warm starts
+    key on global ids, and every iteration still equals the oracle run on the gathered
+    state (the parity protocol of SURVEY §8(c), per iteration)."""
+    _run(P, 30000, 41 + P, ["cvd", "cvd", "dm", "cvd", "cvd"], chained=True)
+
+
+def test_gpu_strips_capacity_overflow_is_loud():
+    """A halo message capacity far below the ghost count latches TM_E_CAPACITY."""
+    import paper_2309_13824_b200 as T
+    from paper_2309_13824_b200 import strips as S
+    box = (0.0, 0.0, 1.0, 1.0)
+    n, P = 20000, 2
+    phi = configs.box_phi(box, 128)
+    dev = torch.device("cuda", 0)
+    backends, c = _make(P, box, torch.from_numpy(phi).to(dev), n)
+    x, y = configs.random_points(n, 3, box)
+    strips = S.Strips(0.0, 1.0, P)
+    to = lambda a: torch.from_numpy(a).to(dev)
+    states = [S.split_initial(to(x), to(y), strips, r, n, 16) for r in range(P)]
+    S.loopback_step(states, strips, backends, S.ghost_width(c, 5.0), "cvd")
+    with pytest.raises(T.TmError) as e:
+        backends[0].ctx.tm_sync()
+    assert e.value.code == T.TM_E_CAPACITY
 
 
 def test_gpu_strips_adaptive_halo():
@@ -67,43 +112,30 @@ def test_gpu_strips_adaptive_halo():
     the per-point halo width from the Lipschitz bound of mu~ (tm_halo_pack width < 0).
     The union of the rank results equals the oracle's single-domain iteration, and the
     adaptive band sends fewer ghosts than the fixed 2 S_max band."""
-    import paper_2309_13824_b200 as T
     from paper_2309_13824_b200 import strips as S
     c = configs.config3(n=400000, grid=512)
     n, P = c.n, 4
     fs = O.FieldSet.from_config(c)
     dev = torch.device("cuda", 0)
     to = lambda a: torch.from_numpy(a).to(dev)
-    xd, yd = to(c.x), to(c.y)
-    strips = S.Strips.from_quantiles(xd, P, c.box[0], c.box[2])
+    strips = S.Strips.from_quantiles(to(c.x), P, c.box[0], c.box[2])
     results = {}
     for adaptive in (True, False):
-        backends = []
-        for r in range(P):
-            ctx = T.Context(0)
-            cc, _ = ctx.tm_set_domain(c.box, to(c.phi), to(c.mu), to(c.rho), n)
-            backends.append(S.GpuStripBackend(ctx, adaptive_halo=adaptive))
+        backends, cc = _make(P, c.box, to(c.phi), n, to(c.mu), to(c.rho), adaptive)
         W = S.ghost_width(cc, 5.0, float(c.mu.max()))
-        states = [S.split_initial(xd, yd, strips, r) for r in range(P)]
+        cap_own, cap_msg = S.capacities(n, P, n // P)
+        states = [S.split_initial(to(c.x), to(c.y), strips, r, cap_own, cap_msg) for r in range(P)]
         ghosts = 0
         x, y, dp = c.x, c.y, None
         for mode in ("dm", "cvd"):
             ref = O.iteration(fs, x, y, mode, d_prev=dp)
-            states = S.loopback_iteration(states, strips, backends, W, mode)
-            got, xs, ys = [], np.empty(n), np.empty(n)
-            for st in states:
-                gid = st.gid.cpu().numpy().astype(np.int64)
-                xs[gid], ys[gid] = st.x.cpu().numpy(), st.y.cpu().numpy()
-                got += [tuple(t) for t in st.tri.cpu().numpy().tolist()]
+            S.loopback_step(states, strips, backends, W, mode)
+            ghosts += sum(m.count() for st in states for m in st.h_recv)
+            got, xs, ys, ds = _gather(states, backends, n)
             assert len(got) == len(set(got))
             assert set(got) == set(map(tuple, ref.tri.tolist())), f"adaptive={adaptive} {mode}: triangles differ"
             assert np.hypot(xs - ref.x, ys - ref.y).max() <= 1e-12 * 2.2 * np.sqrt(2)
             x, y, dp = ref.x, ref.y, ref.d_prev
-            states = [S.split_initial(to(x), to(y), strips, r, d_prev=to(dp)) for r in range(P)]
-            # ghosts sent for this state
-            for r, st in enumerate(states):
-                lo, hi = strips.bounds(r)
-                h_lo, h_hi = backends[r].halo(st, lo, hi, W)
-                ghosts += h_lo[0].shape[0] + h_hi[0].shape[0]
+            states = [S.split_initial(to(x), to(y), strips, r, cap_own, cap_msg, d_prev=to(dp)) for r in range(P)]
         results[adaptive] = ghosts
     assert results[True] < results[False], results

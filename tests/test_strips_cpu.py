@@ -36,15 +36,17 @@ def _worker(rank, world, port, n, seed, iters, q):
         x, y = configs.random_points(n, seed, box)
         c, _ = O.domain(fs, n)
         strips = S.Strips(0.0, 1.0, world)
-        st = S.split_initial(torch.from_numpy(x), torch.from_numpy(y), strips, rank)
-        st.d_prev = None
+        cap_own, cap_msg = S.capacities(n, world, n // world)
+        st = S.split_initial(torch.from_numpy(x), torch.from_numpy(y), strips, rank, cap_own, cap_msg)
         comm = S.TorchP2P(rank, world, torch.device("cpu"))
         be = CpuStripBackend(fs, n)
         W = S.ghost_width(c, 5.0)
         out = []
         for it in range(iters):
-            st = S.strip_iteration(st, strips, be, comm.exchange, W, "cvd")
-            out.append((st.tri.numpy(), st.gid.numpy(), st.x.numpy(), st.y.numpy(), st.extra["n_ghosts"]))
+            S.strip_step(st, strips, be, comm, W, "cvd")
+            ng = sum(m.count() for m in st.h_recv)
+            px, py, g, _ = st.owned()
+            out.append((be.triangles().numpy(), g.numpy().copy(), px.numpy().copy(), py.numpy().copy(), ng))
         res = [None] * world
         dist.all_gather_object(res, out)
         if rank == 0:
@@ -112,6 +114,6 @@ def test_strip_narrower_than_halo_fails_loudly():
         S.Strips(0.0, 1.0, 8).check_width(W)
     S.Strips(0.0, 1.0, 4).check_width(W)  # 0.25 >= 0.22: fine
     x, y = configs.random_points(n, 3, box)
-    st = S.split_initial(torch.from_numpy(x), torch.from_numpy(y), S.Strips(0.0, 1.0, 8), 1)
     with pytest.raises(ValueError):
-        S.strip_iteration(st, S.Strips(0.0, 1.0, 8), None, None, W, "cvd")
+        st = S.split_initial(torch.from_numpy(x), torch.from_numpy(y), S.Strips(0.0, 1.0, 8), 1, n, n)
+        S.strip_step(st, S.Strips(0.0, 1.0, 8), None, None, W, "cvd")
