@@ -253,6 +253,19 @@ tm_status tm_migrate_pack_dc(tm_ctx *ctx, double *x, double *y, int32_t *gid, do
 tm_status tm_append_points(tm_ctx *ctx, double *x, double *y, int32_t *gid, double *d_prev, int64_t *d_count,
                            int64_t cap, const double *msg, const int64_t *msg_count, int64_t msg_cap);
 
+/* ---- CUDA Graphs: capture a sequence of the calls above once, replay it many times ----
+ * tm_graph_begin starts capturing the context's stream (thread-local capture mode);
+ * every call until tm_graph_end is recorded instead of run (its status reports argument
+ * and state errors as usual).  Synchronising calls (tm_sync, tm_set_domain, tm_mesh_stats,
+ * tm_work_counts) are refused with TM_E_STATE while capturing.  Buffers must not grow
+ * during a capture: run the same sequence once before (warm-up).  A replay repeats the
+ * recorded kernels with the recorded arguments (same buffers) on the context's stream. */
+typedef struct tm_graph tm_graph;
+tm_status tm_graph_begin(tm_ctx *ctx);
+tm_status tm_graph_end(tm_ctx *ctx, tm_graph **out);
+tm_status tm_graph_launch(tm_ctx *ctx, tm_graph *g);
+void tm_graph_destroy(tm_graph *g);
+
 /* ---- host-side predicate hooks (no GPU needed; same code as the kernels) -- */
 /* sign of incircle(a,b,c,d) (>0: d inside circle(a,b,c), a,b,c CCW) by the
  * kernels' exact expansion arithmetic, and by the kernels' full filtered path */

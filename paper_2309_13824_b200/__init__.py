@@ -80,6 +80,7 @@ EXPORTED = ["tm_params_default", "tm_create", "tm_destroy", "tm_last_error", "tm
             "tm_grid_bin", "tm_voronoi_delaunay", "tm_cvd_step", "tm_distmesh_sums", "tm_distmesh_step",
             "tm_project_sdf", "tm_mesh_stats", "tm_adjacency_export", "tm_work_counts", "tm_halo_pack",
             "tm_migrate_pack", "tm_grid_bin_dc", "tm_halo_pack_dc", "tm_migrate_pack_dc", "tm_append_points",
+            "tm_graph_begin", "tm_graph_end", "tm_graph_launch", "tm_graph_destroy",
             "tm_host_incircle_exact", "tm_host_cramer", "tm_host_bilinear"]
 
 
@@ -117,6 +118,10 @@ def load_library(path: str = LIB_PATH, build_if_missing: bool = True):
         "tm_halo_pack_dc": (st, [vp, vp, vp, vp, vp, i64, dbl, dbl, dbl, vp, vp, i64, vp, vp]),
         "tm_migrate_pack_dc": (st, [vp, vp, vp, vp, vp, vp, i64, dbl, dbl, vp, vp, i64, vp, vp]),
         "tm_append_points": (st, [vp, vp, vp, vp, vp, vp, i64, vp, vp, i64]),
+        "tm_graph_begin": (st, [vp]),
+        "tm_graph_end": (st, [vp, ctypes.POINTER(vp)]),
+        "tm_graph_launch": (st, [vp, vp]),
+        "tm_graph_destroy": (None, [vp]),
         "tm_host_incircle_exact": (ctypes.c_int, [vp, vp, vp, vp]),
         "tm_host_cramer": (None, [vp, vp, vp]),
         "tm_host_bilinear": (dbl, [i32, i32, dbl, dbl, dbl, dbl, vp, dbl, dbl]),
@@ -249,6 +254,24 @@ class Context:
         self._check(self.L.tm_migrate_pack(self.h, _ptr(x), _ptr(y), _ptr(gid), _ptr(d_prev), int(n_owned), lo, hi,
                                            _ptr(out_lo), _ptr(out_hi), int(cap), _ptr(cnt3)))
 
+    # CUDA Graphs: record a sequence of calls once, replay it (same buffers, same arguments)
+    def capture(self, fn) -> "Graph":
+        """Run fn() under stream capture and return the instantiated graph.  fn must issue
+        library calls (and torch work) on this context's stream only, must not synchronise
+        and must not grow any buffer (run it once before, as a warm-up)."""
+        self._check(self.L.tm_graph_begin(self.h))
+        try:
+            fn()
+        except BaseException:
+            g = ctypes.c_void_p()
+            self.L.tm_graph_end(self.h, ctypes.byref(g))
+            if g.value:
+                self.L.tm_graph_destroy(g)
+            raise
+        g = ctypes.c_void_p()
+        self._check(self.L.tm_graph_end(self.h, ctypes.byref(g)))
+        return Graph(self, g)
+
     # device-count variants (strip path without host synchronisation); *_p arguments are raw
     # device addresses (int), e.g. a message header inside a byte buffer
     def tm_grid_bin_dc(self, x, y, cap_local, counts, gid):
@@ -269,6 +292,27 @@ class Context:
     def tm_append_points(self, x, y, gid, d_prev, count_p, cap, msg_p, msg_count_p, msg_cap):
         self._check(self.L.tm_append_points(self.h, _ptr(x), _ptr(y), _ptr(gid), _ptr(d_prev), _addr(count_p),
                                             int(cap), _addr(msg_p), _addr(msg_count_p), int(msg_cap)))
+
+
+class Graph:
+    """An instantiated capture of library calls (tm_graph); launch() replays it."""
+
+    def __init__(self, ctx: "Context", handle):
+        self.ctx, self.h = ctx, handle
+
+    def launch(self):
+        self.ctx._check(self.ctx.L.tm_graph_launch(self.ctx.h, self.h))
+
+    def close(self):
+        if self.h:
+            self.ctx.L.tm_graph_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 # ------------------------------------------------------------------ driver

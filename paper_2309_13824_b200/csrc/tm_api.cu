@@ -115,6 +115,7 @@ static tm_status clear_latched(tm_ctx *ctx) {
 
 extern "C" tm_status tm_sync(tm_ctx *ctx) {
     if (!ctx) return TM_E_ARG;
+    if (ctx->capturing) TM_FAIL(ctx, TM_E_STATE, "tm_sync while capturing a graph");
     TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
     TM_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     DevState s;
@@ -219,6 +220,7 @@ __global__ void k_lipschitz(Grid g, const double *mu, unsigned long long *out) {
 
 extern "C" tm_status tm_set_domain(tm_ctx *ctx, const tm_fields *f, int64_t n_total, double *c_out,
                                    double *h_avg_out) {
+    if (ctx && ctx->capturing) TM_FAIL(ctx, TM_E_STATE, "tm_set_domain while capturing a graph");
     if (!ctx || !f || !f->phi) return ctx ? (snprintf(ctx->err, sizeof(ctx->err), "null argument"), TM_E_ARG) : TM_E_ARG;
     if (f->nx < 2 || f->ny < 2 || !(f->x1 > f->x0) || !(f->y1 > f->y0) || n_total < 1)
         TM_FAIL(ctx, TM_E_ARG, "bad domain: grid %dx%d, box [%g,%g]x[%g,%g], n_total %lld", f->nx, f->ny, f->x0,
@@ -767,6 +769,7 @@ __global__ void __launch_bounds__(STATS_T) k_stats_final(const double *__restric
 extern "C" tm_status tm_mesh_stats(tm_ctx *ctx, const double *x, const double *y, const int32_t *tri,
                                    int64_t n_tri, tm_stats *out) {
     if (!ctx) return TM_E_ARG;
+    if (ctx->capturing) TM_FAIL(ctx, TM_E_STATE, "tm_mesh_stats while capturing a graph");
     if (!x || !y || (!tri && n_tri > 0) || !out || n_tri < 0) TM_FAIL(ctx, TM_E_ARG, "null argument to tm_mesh_stats");
     TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
     TM_CUDA_TRY(ctx, cudaMemsetAsync(ctx->stat_acc, 0, 16 * sizeof(double), ctx->stream));
@@ -805,6 +808,7 @@ extern "C" tm_status tm_mesh_stats(tm_ctx *ctx, const double *x, const double *y
 
 extern "C" tm_status tm_work_counts(tm_ctx *ctx, tm_work *out) {
     if (!ctx || !out) return TM_E_ARG;
+    if (ctx->capturing) TM_FAIL(ctx, TM_E_STATE, "tm_work_counts while capturing a graph");
     TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
     DevState ds;
     TM_CUDA_TRY(ctx, cudaMemcpyAsync(&ds, ctx->dst, sizeof(ds), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1111,6 +1115,53 @@ extern "C" tm_status tm_append_points(tm_ctx *ctx, double *x, double *y, int32_t
                                                                           msg_count, msg_cap);
     k_append_count<<<1, 1, 0, ctx->stream>>>(d_count, cap, msg_count, msg_cap, ctx->dst);
     return tm_internal_check_launch(ctx, "k_append");
+}
+
+// ============================================================================ CUDA Graphs
+struct tm_graph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+};
+
+extern "C" tm_status tm_graph_begin(tm_ctx *ctx) {
+    if (!ctx) return TM_E_ARG;
+    if (ctx->capturing) TM_FAIL(ctx, TM_E_STATE, "tm_graph_begin while capturing");
+    TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    if (!ctx->stream) TM_FAIL(ctx, TM_E_ARG, "graph capture needs a non-default stream");
+    TM_CUDA_TRY(ctx, cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    ctx->capturing = true;
+    return TM_OK;
+}
+
+extern "C" tm_status tm_graph_end(tm_ctx *ctx, tm_graph **out) {
+    if (!ctx || !out) return TM_E_ARG;
+    if (!ctx->capturing) TM_FAIL(ctx, TM_E_STATE, "tm_graph_end without tm_graph_begin");
+    ctx->capturing = false;
+    tm_graph *g = new (std::nothrow) tm_graph();
+    if (!g) return TM_E_ARG;
+    cudaError_t e = cudaStreamEndCapture(ctx->stream, &g->graph);
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&g->exec, g->graph, 0);
+    if (e != cudaSuccess) {
+        if (g->graph) cudaGraphDestroy(g->graph);
+        delete g;
+        cudaGetLastError();
+        TM_FAIL(ctx, TM_E_CUDA, "graph capture failed: %s", cudaGetErrorString(e));
+    }
+    *out = g;
+    return TM_OK;
+}
+
+extern "C" tm_status tm_graph_launch(tm_ctx *ctx, tm_graph *g) {
+    if (!ctx || !g) return TM_E_ARG;
+    TM_CUDA_TRY(ctx, cudaGraphLaunch(g->exec, ctx->stream));
+    return TM_OK;
+}
+
+extern "C" void tm_graph_destroy(tm_graph *g) {
+    if (!g) return;
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    delete g;
 }
 
 extern "C" int tm_host_incircle_exact(const double *a, const double *b, const double *c, const double *d) {

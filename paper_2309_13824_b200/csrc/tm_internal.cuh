@@ -160,6 +160,7 @@ struct tm_ctx {
     tmg::DevState *dst = nullptr;
     bool have_cells = false;
     const int64_t *dcnt = nullptr;  // device {n_owned, n_local} of the last tm_grid_bin_dc, else NULL
+    bool capturing = false;         // tm_graph_begin .. tm_graph_end
     int64_t *scratch_n = nullptr;   // device scratch count (migration source size)
 };
 

@@ -468,3 +468,46 @@ def test_domain_constants_bitwise(k, cfg_cache):
     ctx.close()
     oc, oh = O.domain(O.FieldSet.from_config(c), c.n)
     assert gc == oc and gh == oh, (gc, oc, gh, oh)
+
+
+def test_graph_replay_equals_eager(cfg_cache):
+    """A captured DistMesh + CVD iteration pair (tm_graph_begin/end) replays to the same
+    bits as the eager calls; synchronising calls are refused while capturing."""
+    import torch
+    import paper_2309_13824_b200 as T
+    c = cfg_cache(2)
+    stream = torch.cuda.Stream()
+    ctx = T.Context(0, stream=stream)
+    with torch.cuda.stream(stream):
+        ctx.tm_set_domain(c.box, torch.from_numpy(c.phi).cuda(), None, None, c.n)
+        x0, y0 = torch.from_numpy(c.x).cuda(), torch.from_numpy(c.y).cuda()
+        bufs = T.IterBuffers.alloc(c.n)
+        X = [torch.empty_like(x0) for _ in range(6)]
+
+        def two():
+            T.iterate(ctx, x0, y0, None, "dm", bufs, X[0], X[1], X[2])
+            T.iterate(ctx, X[0], X[1], X[2], "cvd", bufs, X[3], X[4], X[5])
+
+        two()  # warm-up (allocations, warm-start lists)
+        two()
+        ctx.tm_sync()
+        eager = [t.cpu().numpy().copy() for t in X] + [bufs.tri[:int(bufs.n_tri.item())].cpu().numpy().copy()]
+        assert np.all(np.isfinite(eager[3]))
+        g = ctx.capture(two)
+        for t in X:
+            t.zero_()
+        g.launch()
+        ctx.tm_sync()
+        replay = [t.cpu().numpy() for t in X] + [bufs.tri[:int(bufs.n_tri.item())].cpu().numpy()]
+        for a, b in zip(eager[:6], replay[:6]):
+            assert np.array_equal(a, b)
+        assert tri_set_eq(eager[6], replay[6])
+        T.load_library().tm_graph_begin(ctx.h)
+        with pytest.raises(T.TmError) as e:
+            ctx.tm_sync()
+        assert e.value.code == T.TM_E_STATE
+        import ctypes
+        h = ctypes.c_void_p()
+        T.load_library().tm_graph_end(ctx.h, ctypes.byref(h))
+        T.load_library().tm_graph_destroy(h)
+        g.close()
