@@ -50,7 +50,8 @@ class Params(ctypes.Structure):
                 ("fac_geps", ctypes.c_double), ("fac_end_mvmt", ctypes.c_double),
                 ("newton_damping", ctypes.c_double), ("newton_max", ctypes.c_int32),
                 ("quad_max_level", ctypes.c_int32), ("fscale", ctypes.c_double),
-                ("dt_k", ctypes.c_double), ("keep_tol", ctypes.c_double)]
+                ("dt_k", ctypes.c_double), ("keep_tol", ctypes.c_double),
+                ("projection", ctypes.c_int32), ("trace_max", ctypes.c_int32), ("fac_retria", ctypes.c_double)]
 
 
 class Info(ctypes.Structure):
@@ -65,7 +66,7 @@ def default_params(**kw) -> Params:
     """Table B.1 defaults plus the L3/L10/L13 readings."""
     p = Params(fac_voro_bound=5.0, fac_pt_mvmt=0.4, fac_geps=0.01, fac_end_mvmt=0.001,
                newton_damping=1.0, newton_max=10, quad_max_level=10, fscale=1.2, dt_k=0.2,
-               keep_tol=0.0)
+               keep_tol=0.0, projection=0, trace_max=64, fac_retria=0.1)
     for k, v in kw.items():
         setattr(p, k, v)
     return p
@@ -118,6 +119,11 @@ def lib():
         L.or_treat.argtypes = [ctypes.POINTER(Fields), ctypes.POINTER(Params), ctypes.c_double,
                                ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                ctypes.c_double, D, D, D]
+        L.or_distmesh_lazy.restype = ctypes.c_int
+        L.or_distmesh_lazy.argtypes = [ctypes.POINTER(Fields), ctypes.POINTER(Params), ctypes.c_int64, ctypes.c_int64,
+                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int32)]
         L.or_triangle_quality.restype = None
         L.or_triangle_quality.argtypes = [D, D, D, D, D]
         L.or_stats.restype = None
@@ -303,6 +309,33 @@ def treat(fs: FieldSet, c, h_avg, old, new, params=None):
     st = lib().or_treat(ctypes.byref(fs.c), ctypes.byref(params), c, h_avg, old[0], old[1], new[0], new[1],
                         ctypes.byref(xn), ctypes.byref(yn), ctypes.byref(dp))
     return (xn.value, yn.value), dp.value, int(st)
+
+
+@dataclass
+class LazyResult:
+    x: np.ndarray
+    y: np.ndarray
+    d_prev: np.ndarray
+    status: np.ndarray
+    retria: bool
+
+
+def distmesh_lazy(fs: FieldSet, x, y, edges, x_tria, y_tria, params=None, n_total: int = 0) -> LazyResult:
+    """NEXT-1: one DistMesh update on the stale triangulation `edges` (Alg. 1), treatment,
+    and the re-triangulation flag (any |p_new - p_tria| > fac_retria h(p_tria))."""
+    params = params or default_params()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    e = np.ascontiguousarray(edges, dtype=np.int32)
+    xt = np.ascontiguousarray(x_tria, dtype=np.float64)
+    yt = np.ascontiguousarray(y_tria, dtype=np.float64)
+    n = x.shape[0]
+    xo, yo, dp = np.empty(n), np.empty(n), np.empty(n)
+    st = np.empty(n, dtype=np.int8)
+    flag = ctypes.c_int32()
+    lib().or_distmesh_lazy(ctypes.byref(fs.c), ctypes.byref(params), n, n_total, _p(x), _p(y), e.shape[0], _p(e),
+                           _p(xt), _p(yt), _p(xo), _p(yo), _p(dp), _p(st), ctypes.byref(flag))
+    return LazyResult(xo, yo, dp, st, bool(flag.value))
 
 
 def triangle_quality(a, b, c):

@@ -1060,6 +1060,80 @@ void or_distmesh(const or_fields *f, const or_params *p, int64_t n, const double
 /* ========================================================================== */
 static double clampd(double v, double lo, double hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
+/* NEXT-1: the paper's projection of escaped points (Fig. 13).
+ * Sphere tracing ([hart1995]): from the inner p_old toward p_new, step by the circle of
+ * radius |sdf(q)| around the current point q, q <- q + |sdf(q)| u (u the unit direction of the
+ * segment, a step never passing p_new), until |sdf(q)| <= geps; at most trace_max steps (L39). */
+static int sphere_trace(const or_fields *f, const or_params *p, double xo, double yo, double xn, double yn,
+                        double geps, double *qx_out, double *qy_out) {
+    double dx = xn - xo, dy = yn - yo;
+    double len = sqrt(dx * dx + dy * dy);
+    double ux = dx / len, uy = dy / len;
+    double qx = xo, qy = yo, s = 0.0;
+    for (int k = 0; k < p->trace_max; k++) {
+        double v = or_field_value(f, f->phi, qx, qy);
+        near_tie(fabs(v), geps, geps);
+        if (fabs(v) <= geps) { *qx_out = qx; *qy_out = qy; return 1; }
+        double r = fabs(v);
+        if (s + r > len) r = len - s;
+        s = s + r;
+        qx = qx + r * ux;
+        qy = qy + r * uy;
+    }
+    double v = or_field_value(f, f->phi, qx, qy);
+    *qx_out = qx; *qy_out = qy;
+    return fabs(v) <= geps;
+}
+
+/* Finite-difference derivatives of sdf~ with step d ("approximated with the finite
+ * difference method of step size deps"): central differences (reading L41). */
+static void fd_derivs(const or_fields *f, double x, double y, double d, double *fx, double *fy,
+                      double *fxx, double *fyy, double *fxy) {
+    const double *F = f->phi;
+    double f0 = or_field_value(f, F, x, y);
+    double fxp = or_field_value(f, F, x + d, y), fxm = or_field_value(f, F, x - d, y);
+    double fyp = or_field_value(f, F, x, y + d), fym = or_field_value(f, F, x, y - d);
+    double fpp = or_field_value(f, F, x + d, y + d), fpm = or_field_value(f, F, x + d, y - d);
+    double fmp = or_field_value(f, F, x - d, y + d), fmm = or_field_value(f, F, x - d, y - d);
+    *fx = (fxp - fxm) / (2.0 * d);
+    *fy = (fyp - fym) / (2.0 * d);
+    *fxx = ((fxp - 2.0 * f0) + fxm) / (d * d);
+    *fyy = ((fyp - 2.0 * f0) + fym) / (d * d);
+    *fxy = (((fpp - fpm) - fmp) + fmm) / (4.0 * d * d);
+}
+
+/* Point projection by the damped Newton method: solve
+ * L(p) = [sdf(p), (p - p_new) x grad sdf(p)] = 0 (Eq. projection_point_requirement, written
+ * with the gradient at p as its Jacobian Eq. projection_Newton_Jacobian requires, L36), from
+ * p_new, p <- p - alpha J^-1 L (Eq. projection_pt_update), clamped into B, until
+ * |sdf(p)| <= geps or newton_max steps. */
+static int newton_project(const or_fields *f, const or_params *p, double xn, double yn, double geps,
+                          double deps, double *qx_out, double *qy_out) {
+    double x = xn, y = yn;
+    int ok = 0;
+    for (int k = 0; k < p->newton_max; k++) {
+        double fx, fy, fxx, fyy, fxy;
+        fd_derivs(f, x, y, deps, &fx, &fy, &fxx, &fyy, &fxy);
+        double L1 = or_field_value(f, f->phi, x, y);
+        double ex = x - xn, ey = y - yn;
+        double L2 = ex * fy - ey * fx;
+        double J11 = fx, J12 = fy;
+        double J21 = (fy + ex * fxy) - ey * fxx;
+        double J22 = (-fx - ey * fxy) + ex * fyy;
+        double det = J11 * J22 - J12 * J21;
+        if (!(det != 0.0)) break;
+        double sx = (L1 * J22 - J12 * L2) / det;
+        double sy = (J11 * L2 - J21 * L1) / det;
+        x = clampd(x - p->newton_damping * sx, f->x0, f->x1);
+        y = clampd(y - p->newton_damping * sy, f->y0, f->y1);
+        double v = or_field_value(f, f->phi, x, y);
+        near_tie(fabs(v), geps, geps);
+        if (fabs(v) <= geps) { ok = 1; break; }
+    }
+    *qx_out = x; *qy_out = y;
+    return ok;
+}
+
 int or_treat(const or_fields *f, const or_params *p, double c, double h_avg,
              double xo, double yo, double xh, double yh, double *xn, double *yn, double *dprev) {
     int status = 0;
@@ -1073,22 +1147,38 @@ int or_treat(const or_fields *f, const or_params *p, double c, double h_avg,
         status |= 4;
     }
     double qx = clampd(xo + dx, f->x0, f->x1), qy = clampd(yo + dy, f->y0, f->y1);
-    double geps = p->fac_geps * (h < h_avg ? h : h_avg);
+    double hm = h < h_avg ? h : h_avg;
+    double geps = p->fac_geps * hm;
     double ph = or_field_value(f, f->phi, qx, qy);
     near_tie(ph, geps, geps);
     if (!(ph <= geps)) {
         int ok = 0;
-        for (int it = 0; it < p->newton_max; it++) {
-            double gx, gy;
-            or_field_grad(f, f->phi, qx, qy, &gx, &gy);
-            double g2 = gx * gx + gy * gy;
-            if (!(g2 > 0.0)) break;
-            double st = p->newton_damping * ph / g2;
-            qx = clampd(qx - st * gx, f->x0, f->x1);
-            qy = clampd(qy - st * gy, f->y0, f->y1);
-            ph = or_field_value(f, f->phi, qx, qy);
-            near_tie(fabs(ph), geps, geps);
-            if (fabs(ph) <= geps) { ok = 1; break; }
+        if (p->projection == 1) {
+            /* Fig. 13: an inner p_old (sdf < -geps) is sphere-traced toward p_new;
+             * a boundary (or outside) p_old projects p_new by the 2x2 damped Newton method */
+            double po = or_field_value(f, f->phi, xo, yo);
+            double px_, py_;
+            if (po < -geps) {
+                ok = sphere_trace(f, p, xo, yo, qx, qy, geps, &px_, &py_);
+                status |= 8;
+            } else {
+                double deps = 1.4901161193847656e-08 * hm;  /* sqrt(DBL_EPSILON) min(h, h_avg) */
+                ok = newton_project(f, p, qx, qy, geps, deps, &px_, &py_);
+            }
+            qx = px_; qy = py_;
+        } else {
+            for (int it = 0; it < p->newton_max; it++) {
+                double gx, gy;
+                or_field_grad(f, f->phi, qx, qy, &gx, &gy);
+                double g2 = gx * gx + gy * gy;
+                if (!(g2 > 0.0)) break;
+                double st = p->newton_damping * ph / g2;
+                qx = clampd(qx - st * gx, f->x0, f->x1);
+                qy = clampd(qy - st * gy, f->y0, f->y1);
+                ph = or_field_value(f, f->phi, qx, qy);
+                near_tie(fabs(ph), geps, geps);
+                if (fabs(ph) <= geps) { ok = 1; break; }
+            }
         }
         if (ok) status |= 1;
         else { qx = xo; qy = yo; status = (status & 4) | 2; }
@@ -1097,6 +1187,30 @@ int or_treat(const or_fields *f, const or_params *p, double c, double h_avg,
     double ex = qx - xo, ey = qy - yo;
     *dprev = sqrt(ex * ex + ey * ey);
     return status;
+}
+
+int or_distmesh_lazy(const or_fields *f, const or_params *p, int64_t n, int64_t n_total,
+                     const double *x, const double *y, int64_t ne, const int32_t *edges,
+                     const double *x_tria, const double *y_tria,
+                     double *x_out, double *y_out, double *d_prev_out, int8_t *status, int32_t *retria) {
+    double c, h_avg;
+    or_domain(f, n_total > 0 ? n_total : n, &c, &h_avg);
+    double *xh = (double *)malloc(sizeof(double) * (size_t)n);
+    double *yh = (double *)malloc(sizeof(double) * (size_t)n);
+    or_distmesh(f, p, n, x, y, ne, edges, NULL, xh, yh, NULL);
+    int32_t flag = 0;
+    for (int64_t i = 0; i < n; i++) {
+        status[i] = (int8_t)or_treat(f, p, c, h_avg, x[i], y[i], xh[i], yh[i], &x_out[i], &y_out[i], &d_prev_out[i]);
+        /* movement since the last triangulation against T_retria = fac_retria h(p_tria) */
+        double ex = x_out[i] - x_tria[i], ey = y_out[i] - y_tria[i];
+        double d = sqrt(ex * ex + ey * ey);
+        double T = p->fac_retria * h_of(f, c, x_tria[i], y_tria[i]);
+        near_tie(d, T, T);
+        if (d > T) flag = 1;
+    }
+    *retria = flag;
+    free(xh); free(yh);
+    return 0;
 }
 
 /* ========================================================================== */

@@ -38,6 +38,13 @@ typedef struct {
     double fscale;          /* 1.2                                     */
     double dt_k;            /* 0.2   L3                                        */
     double keep_tol;        /* 0.0   L10                                       */
+    /* NEXT-1: the paper's treatment of escaped points, Fig. 13:
+     * 0 = the L22 reading (gradient Newton from p_new), 1 = sphere tracing from an inner
+     * p_old / damped 2x2 Newton on L(p) with FD derivatives from a boundary p_old
+     * (Eqs. projection_*) */
+    int32_t projection;
+    int32_t trace_max;      /* 64    sphere-tracing step cap (paper silent, L39)            */
+    double fac_retria;      /* 0.1   P:1098 lazy re-triangulation threshold fac * h (Alg. 1) */
 } or_params;
 
 typedef struct {
@@ -109,6 +116,15 @@ void or_distmesh(const or_fields *f, const or_params *p, int64_t n, const double
 /* O6 treatment of one point */
 int or_treat(const or_fields *f, const or_params *p, double c, double h_avg,
              double xo, double yo, double xh, double yh, double *xn, double *yn, double *dprev);
+/* NEXT-1, Alg. 1 lines 7-11 with P:446: one DistMesh update on a STALE
+ * triangulation -- forces over the unique edges of the last triangulation at the current
+ * positions (O5), the treatment (O6), and the re-triangulation test: *retria = 1 iff some
+ * point's displacement since that triangulation exceeds fac_retria * h(p_tria) (L40).
+ * x_tria/y_tria: the positions the edges were computed at.  Returns 0. */
+int or_distmesh_lazy(const or_fields *f, const or_params *p, int64_t n, int64_t n_total,
+                     const double *x, const double *y, int64_t ne, const int32_t *edges,
+                     const double *x_tria, const double *y_tria,
+                     double *x_out, double *y_out, double *d_prev_out, int8_t *status, int32_t *retria);
 /* O7 quality of one triangle and reductions over a list */
 void or_triangle_quality(const double *a, const double *b, const double *c, double *alpha, double *beta);
 void or_stats(int64_t n_tri, const int32_t *tri, const double *x, const double *y, double *out12);
