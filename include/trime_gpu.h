@@ -86,6 +86,13 @@ typedef struct {
     int32_t adj_stride;        /* 16    ELL row width for DistMesh                      */
     int32_t max_cell_vertices; /* 32    cell vertex capacity (one warp lane per vertex) */
     uint32_t flags;            /* TM_F_* below                                          */
+    /* NEXT-1 */
+    int32_t projection;        /* 0     escaped points: L22 gradient Newton from p_new;
+                                  1     the paper's Fig. 13: sphere tracing from an
+                                        inner p_old (status |= 8), 2x2 damped Newton with FD
+                                        derivatives from a boundary p_old                       */
+    int32_t trace_max;         /* 64    sphere-tracing step cap (L39)                           */
+    double fac_retria;         /* 0.1   P:1098 lazy re-triangulation threshold fac * h (Alg. 1) */
 } tm_params;
 
 #define TM_F_TWO_LEVEL_BINS 0x1u  /* split dense bins into 2^r x 2^r sub-bins (adaptive rho) */
@@ -193,6 +200,16 @@ tm_status tm_project_sdf(tm_ctx *ctx, const double *x_old, const double *y_old, 
  * reductions (no atomics): bitwise reproducible.  out: host.  synchronises */
 tm_status tm_mesh_stats(tm_ctx *ctx, const double *x, const double *y, const int32_t *tri, int64_t n_tri,
                         tm_stats *out);
+
+/* NEXT-1, Alg. 1: DistMesh iterations on a stale triangulation.
+ * tm_refresh_positions: new positions (caller order, the point set of the last tm_grid_bin)
+ *   replace the binned ones without re-binning -- the ELL rows of the last triangulation
+ *   then act on the current positions (tm_distmesh_sums / tm_distmesh_step).
+ * tm_retria_check: *flag (device int32) |= 1 iff some point's position x_new/y_new (caller
+ *   order) is farther than fac_retria * h(p_tria) from its position p_tria at the last
+ *   tm_voronoi_delaunay with adj (re-triangulate in the next iteration). */
+tm_status tm_refresh_positions(tm_ctx *ctx, const double *x, const double *y);
+tm_status tm_retria_check(tm_ctx *ctx, const double *x_new, const double *y_new, int32_t *flag);
 
 /* Copy of the ELL adjacency in caller order with caller ids (tests/export):
  * adj_out int32[n_owned*adj_stride], deg_out uint8[n_owned] (device). */

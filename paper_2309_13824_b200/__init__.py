@@ -54,7 +54,8 @@ class tm_params(ctypes.Structure):
                 ("newton_max", ctypes.c_int32), ("quad_max_level", ctypes.c_int32),
                 ("fscale", ctypes.c_double), ("dt_k", ctypes.c_double), ("keep_tol", ctypes.c_double),
                 ("adj_stride", ctypes.c_int32), ("max_cell_vertices", ctypes.c_int32),
-                ("flags", ctypes.c_uint32)]
+                ("flags", ctypes.c_uint32), ("projection", ctypes.c_int32), ("trace_max", ctypes.c_int32),
+                ("fac_retria", ctypes.c_double)]
 
 
 class tm_stats(ctypes.Structure):
@@ -80,7 +81,8 @@ EXPORTED = ["tm_params_default", "tm_create", "tm_destroy", "tm_last_error", "tm
             "tm_grid_bin", "tm_voronoi_delaunay", "tm_cvd_step", "tm_distmesh_sums", "tm_distmesh_step",
             "tm_project_sdf", "tm_mesh_stats", "tm_adjacency_export", "tm_work_counts", "tm_halo_pack",
             "tm_migrate_pack", "tm_grid_bin_dc", "tm_halo_pack_dc", "tm_migrate_pack_dc", "tm_append_points",
-            "tm_graph_begin", "tm_graph_end", "tm_graph_launch", "tm_graph_destroy",
+            "tm_graph_begin", "tm_graph_end", "tm_graph_launch", "tm_graph_destroy", "tm_refresh_positions",
+            "tm_retria_check",
             "tm_host_incircle_exact", "tm_host_cramer", "tm_host_bilinear"]
 
 
@@ -118,6 +120,8 @@ def load_library(path: str = LIB_PATH, build_if_missing: bool = True):
         "tm_halo_pack_dc": (st, [vp, vp, vp, vp, vp, i64, dbl, dbl, dbl, vp, vp, i64, vp, vp]),
         "tm_migrate_pack_dc": (st, [vp, vp, vp, vp, vp, vp, i64, dbl, dbl, vp, vp, i64, vp, vp]),
         "tm_append_points": (st, [vp, vp, vp, vp, vp, vp, i64, vp, vp, i64]),
+        "tm_refresh_positions": (st, [vp, vp, vp]),
+        "tm_retria_check": (st, [vp, vp, vp, vp]),
         "tm_graph_begin": (st, [vp]),
         "tm_graph_end": (st, [vp, ctypes.POINTER(vp)]),
         "tm_graph_launch": (st, [vp, vp]),
@@ -254,6 +258,12 @@ class Context:
         self._check(self.L.tm_migrate_pack(self.h, _ptr(x), _ptr(y), _ptr(gid), _ptr(d_prev), int(n_owned), lo, hi,
                                            _ptr(out_lo), _ptr(out_hi), int(cap), _ptr(cnt3)))
 
+    def tm_refresh_positions(self, x, y):
+        self._check(self.L.tm_refresh_positions(self.h, _ptr(x), _ptr(y)))
+
+    def tm_retria_check(self, x_new, y_new, flag):
+        self._check(self.L.tm_retria_check(self.h, _ptr(x_new), _ptr(y_new), _ptr(flag)))
+
     # CUDA Graphs: record a sequence of calls once, replay it (same buffers, same arguments)
     def capture(self, fn) -> "Graph":
         """Run fn() under stream capture and return the instantiated graph.  fn must issue
@@ -336,6 +346,36 @@ class IterBuffers:
                    deg=torch.empty(n, dtype=torch.uint8, device=device),
                    sums2=torch.empty(2, dtype=torch.float64, device=device),
                    status=torch.empty(n, dtype=torch.int8, device=device))
+
+
+class LazyDistMesh:
+    """NEXT-1: DistMesh with lazy re-triangulation (Alg. 1): the Voronoi/Delaunay
+    step runs only in an iteration after some point moved more than fac_retria h since the
+    last triangulation; the other iterations reuse its ELL rows at the current
+    positions (tm_refresh_positions).  One 4-byte device-to-host read per iteration (the
+    re-triangulation flag decides which calls the next iteration issues)."""
+
+    def __init__(self, ctx: "Context", n: int):
+        self.ctx = ctx
+        self.bufs = IterBuffers.alloc(n, ctx.params.adj_stride)
+        self.flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.retria = True
+        self.triangulations = 0
+
+    def step(self, x, y, d_prev, x_out, y_out, d_prev_out):
+        c, b = self.ctx, self.bufs
+        if self.retria:
+            c.tm_grid_bin(x, y)
+            c.tm_voronoi_delaunay(b.tri, b.n_tri, b.adj, b.deg)
+            self.triangulations += 1
+        else:
+            c.tm_refresh_positions(x, y)
+        c.tm_distmesh_sums(b.adj, b.deg, b.sums2)
+        c.tm_distmesh_step(b.adj, b.deg, b.sums2, None, d_prev, x_out, y_out, d_prev_out, b.status)
+        self.flag.zero_()
+        c.tm_retria_check(x_out, y_out, self.flag)
+        self.retria = bool(self.flag.item())
+        return self.retria
 
 
 def iterate(ctx: Context, x, y, d_prev, mode: str, bufs: IterBuffers, x_out, y_out, d_prev_out):

@@ -28,6 +28,9 @@ extern "C" void tm_params_default(tm_params *p) {
     p->adj_stride = 16;
     p->max_cell_vertices = 32;
     p->flags = TM_F_TWO_LEVEL_BINS;
+    p->projection = 0;         // L22 (north_star "gradient projection"); 1 = the paper's Fig. 13
+    p->trace_max = 64;         // L39
+    p->fac_retria = 0.1;
 }
 
 extern "C" tm_status tm_create(int device, void *cuda_stream, const tm_params *p, tm_ctx **out) {
@@ -42,7 +45,8 @@ extern "C" tm_status tm_create(int device, void *cuda_stream, const tm_params *p
     else
         tm_params_default(&ctx->p);
     if (ctx->p.max_cell_vertices != 32 || ctx->p.adj_stride < 1 || ctx->p.adj_stride > 255 ||
-        ctx->p.quad_max_level < 1 || ctx->p.quad_max_level > 20 || ctx->p.newton_max < 0) {
+        ctx->p.quad_max_level < 1 || ctx->p.quad_max_level > 20 || ctx->p.newton_max < 0 ||
+        (ctx->p.projection != 0 && ctx->p.projection != 1) || ctx->p.trace_max < 0) {
         delete ctx;
         return TM_E_ARG;
     }
@@ -79,6 +83,7 @@ extern "C" void tm_destroy(tm_ctx *ctx) {
     cudaFree(ctx->nbr); cudaFree(ctx->nbr_cnt); cudaFree(ctx->inv_id);
     cudaFree(ctx->ring_v); cudaFree(ctx->ring_la); cudaFree(ctx->ring_n);
     cudaFree(ctx->deep_list); cudaFree(ctx->deep_cnt); cudaFree(ctx->scratch_n);
+    cudaFree(ctx->xs_tria); cudaFree(ctx->ys_tria); cudaFree(ctx->hs_tria);
     delete ctx;
 }
 
@@ -608,6 +613,7 @@ static tm_status grid_bin_impl(tm_ctx *ctx, const double *x, const double *y, in
     k_perm_scatter<<<blocks, 256, 0, ctx->stream>>>(n_local, ctx->key, ctx->rank, ctx->leaf_start, ctx->perm, dcnt);
     k_leaf_sort_perm<<<(unsigned)((nleaves_max + 255) / 256), 256, 0, ctx->stream>>>(ctx->leaf_start, nleaves_max,
                                                                                    ctx->perm, gid, nkey, ctx->inv_id);
+    ctx->gids_in = gid;
     k_gather_sorted<<<blocks, 256, 0, ctx->stream>>>(x, y, gid, n_local, ctx->perm, g.x0, g.y0, g.x1, g.y1, g, ctx->mu,
                                                      ctx->c, ctx->xs, ctx->ys, ctx->hs, ctx->gids, dcnt);
     if ((s = tm_internal_check_launch(ctx, "k_gather_sorted")) != TM_OK) return s;
@@ -654,6 +660,7 @@ tm_status tm_internal_fill_cell_args(tm_ctx *ctx, CellArgs *a) {
     a->fac_geps = ctx->p.fac_geps; a->fac_end = ctx->p.fac_end_mvmt;
     a->damping = ctx->p.newton_damping; a->keep_tol = ctx->p.keep_tol;
     a->newton_max = ctx->p.newton_max; a->quad_max = ctx->p.quad_max_level;
+    a->projection = ctx->p.projection; a->trace_max = ctx->p.trace_max;
     a->adj_stride = ctx->p.adj_stride;
     a->st = ctx->dst;
     return TM_OK;
@@ -665,14 +672,14 @@ __global__ void k_project(Grid g, const double *__restrict__ phi, const double *
                           const double *__restrict__ xo, const double *__restrict__ yo,
                           const double *__restrict__ xh, const double *__restrict__ yh, int64_t n,
                           double *__restrict__ x_out, double *__restrict__ y_out, double *__restrict__ d_out,
-                          int8_t *__restrict__ status, DevState *st) {
+                          int8_t *__restrict__ status, DevState *st, int projection, int trace_max) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double px = xo[i], py = yo[i];
     double h = mu ? cmul(c, bilinear(g, mu, px, py, LdgLoad())) : c;
     double qx, qy, dp;
     int s = treat_point(g, phi, h, h_avg, fac_pt, fac_geps, damping, newton_max, px, py, xh[i], yh[i], qx, qy, dp,
-                        LdgLoad());
+                        LdgLoad(), projection, trace_max);
     x_out[i] = qx;
     y_out[i] = qy;
     d_out[i] = dp;
@@ -692,7 +699,7 @@ extern "C" tm_status tm_project_sdf(tm_ctx *ctx, const double *x_old, const doub
     k_project<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(
         ctx->grid, ctx->phi, ctx->mu, ctx->c, ctx->h_avg, ctx->p.fac_pt_mvmt, ctx->p.fac_geps,
         ctx->p.newton_damping, ctx->p.newton_max, x_old, y_old, x_hat, y_hat, n, x_out, y_out, d_prev_out,
-        status, ctx->dst);
+        status, ctx->dst, ctx->p.projection, ctx->p.trace_max);
     return tm_internal_check_launch(ctx, "k_project");
 }
 
@@ -1115,6 +1122,49 @@ extern "C" tm_status tm_append_points(tm_ctx *ctx, double *x, double *y, int32_t
                                                                           msg_count, msg_cap);
     k_append_count<<<1, 1, 0, ctx->stream>>>(d_count, cap, msg_count, msg_cap, ctx->dst);
     return tm_internal_check_launch(ctx, "k_append");
+}
+
+// ============================================================================ NEXT-1: lazy re-triangulation
+extern "C" tm_status tm_refresh_positions(tm_ctx *ctx, const double *x, const double *y) {
+    if (!ctx) return TM_E_ARG;
+    if (!ctx->have_bins) TM_FAIL(ctx, TM_E_STATE, "tm_refresh_positions before tm_grid_bin");
+    if (!x || !y) TM_FAIL(ctx, TM_E_ARG, "null x/y");
+    if (ctx->dcnt) TM_FAIL(ctx, TM_E_STATE, "tm_refresh_positions on a device-count binning");
+    TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    const Grid &g = ctx->grid;
+    // the binning's gather with the same permutation: sorted positions and h(p) of the new
+    // positions, slots (and so the ELL rows) unchanged
+    k_gather_sorted<<<(unsigned)((ctx->n_local + 255) / 256), 256, 0, ctx->stream>>>(
+        x, y, ctx->have_gid ? ctx->gids_in : nullptr, ctx->n_local, ctx->perm, g.x0, g.y0, g.x1, g.y1, g, ctx->mu,
+        ctx->c, ctx->xs, ctx->ys, ctx->hs, ctx->gids, nullptr);
+    return tm_internal_check_launch(ctx, "k_gather_sorted");
+}
+
+__global__ void k_retria(const double *__restrict__ x, const double *__restrict__ y, const int32_t *__restrict__ perm,
+                         const double *__restrict__ xt, const double *__restrict__ yt,
+                         const double *__restrict__ ht, int64_t n, int64_t n_owned, double fac, int32_t *flag) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool big = false;
+    if (s < n) {
+        const int32_t i = perm[s];
+        if (i < n_owned) {
+            // movement since the triangulation vs T_retria = fac h(p_tria), as the oracle
+            const double ex = csub(x[i], xt[s]), ey = csub(y[i], yt[s]);
+            big = sqrt(cadd(cmul(ex, ex), cmul(ey, ey))) > cmul(fac, ht[s]);
+        }
+    }
+    if (__any_sync(0xffffffffu, big) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+extern "C" tm_status tm_retria_check(tm_ctx *ctx, const double *x_new, const double *y_new, int32_t *flag) {
+    if (!ctx) return TM_E_ARG;
+    if (!x_new || !y_new || !flag) TM_FAIL(ctx, TM_E_ARG, "null argument to tm_retria_check");
+    if (!ctx->have_tria) TM_FAIL(ctx, TM_E_STATE, "tm_retria_check before a triangulation with adjacency");
+    TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    k_retria<<<(unsigned)((ctx->n_local + 255) / 256), 256, 0, ctx->stream>>>(
+        x_new, y_new, ctx->perm, ctx->xs_tria, ctx->ys_tria, ctx->hs_tria, ctx->n_local, ctx->n_owned,
+        ctx->p.fac_retria, flag);
+    return tm_internal_check_launch(ctx, "k_retria");
 }
 
 // ============================================================================ CUDA Graphs

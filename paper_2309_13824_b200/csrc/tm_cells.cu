@@ -480,7 +480,8 @@ __global__ void __launch_bounds__(BLOCK, (G == 16 ? TM_MINB : 1)) k_cells(CellAr
                     if ((MODE & M_TREAT) && lane == 0) {
                         double qx, qy, dpo;
                         const int s = treat_point(A.grid, A.phi, h, A.h_avg, A.fac_pt, A.fac_geps, A.damping,
-                                                  A.newton_max, px, py, px + cx, py + cy, qx, qy, dpo, LdgLoad());
+                                                  A.newton_max, px, py, px + cx, py + cy, qx, qy, dpo, LdgLoad(),
+                                                  A.projection, A.trace_max);
                         A.x_out[orig] = qx;
                         A.y_out[orig] = qy;
                         A.d_prev_out[orig] = dpo;
@@ -599,6 +600,23 @@ extern "C" tm_status tm_voronoi_delaunay(tm_ctx *ctx, int32_t *tri, int64_t tri_
         ctx->have_cells = true;
         // neighbour lists written (thread kernel only): warm start for the next launch
         ctx->nbr_n = (a.nbr && !(ctx->p.flags & TM_F_GROUP_CELLS)) ? a.nbr_keys : -1;
+    }
+    if (s == TM_OK && adj && !ctx->dcnt) {
+        // positions and h of this triangulation, for tm_retria_check (NEXT-1, Alg. 1)
+        if (ctx->cap_tria < ctx->n_local) {
+            cudaFree(ctx->xs_tria); cudaFree(ctx->ys_tria); cudaFree(ctx->hs_tria);
+            ctx->xs_tria = ctx->ys_tria = ctx->hs_tria = nullptr;
+            const int64_t c = ctx->cap_points;
+            TM_CUDA_TRY(ctx, cudaMalloc(&ctx->xs_tria, c * sizeof(double)));
+            TM_CUDA_TRY(ctx, cudaMalloc(&ctx->ys_tria, c * sizeof(double)));
+            TM_CUDA_TRY(ctx, cudaMalloc(&ctx->hs_tria, c * sizeof(double)));
+            ctx->cap_tria = c;
+        }
+        const size_t nb = (size_t)ctx->n_local * sizeof(double);
+        TM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->xs_tria, ctx->xs, nb, cudaMemcpyDeviceToDevice, ctx->stream));
+        TM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->ys_tria, ctx->ys, nb, cudaMemcpyDeviceToDevice, ctx->stream));
+        TM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->hs_tria, ctx->hs, nb, cudaMemcpyDeviceToDevice, ctx->stream));
+        ctx->have_tria = true;
     }
     return s;
 }

@@ -1060,7 +1060,7 @@ __global__ void __launch_bounds__(TB, (MODE & M_WCERT) ? TM_WMINB : TM_TMINB) k_
         if (MODE & M_TREAT) {
             double qx, qy, dpo;
             const int s = treat_point(A.grid, A.phi, h, A.h_avg, A.fac_pt, A.fac_geps, A.damping, A.newton_max, px,
-                                      py, px + cx, py + cy, qx, qy, dpo, LdgLoad());
+                                      py, px + cx, py + cy, qx, qy, dpo, LdgLoad(), A.projection, A.trace_max);
             A.x_out[orig] = qx;
             A.y_out[orig] = qy;
             A.d_prev_out[orig] = dpo;
@@ -1126,7 +1126,7 @@ __device__ __forceinline__ void cell_update(const CellArgs &A, int32_t orig, dou
     if (MODE & M_TREAT) {
         double qx, qy, dpo;
         const int s = treat_point(A.grid, A.phi, h, A.h_avg, A.fac_pt, A.fac_geps, A.damping, A.newton_max, px, py,
-                                  px + cx, py + cy, qx, qy, dpo, LdgLoad());
+                                  px + cx, py + cy, qx, qy, dpo, LdgLoad(), A.projection, A.trace_max);
         A.x_out[orig] = qx;
         A.y_out[orig] = qy;
         A.d_prev_out[orig] = dpo;

@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(DM_T) k_dm_step(CellArgs A, const int32_t *__r
     }
     double qx, qy, dpo;
     int st = treat_point(A.grid, A.phi, A.hs[s], A.h_avg, A.fac_pt, A.fac_geps, A.damping, A.newton_max, xi, yi, xh,
-                         yh, qx, qy, dpo, LdgLoad());
+                         yh, qx, qy, dpo, LdgLoad(), A.projection, A.trace_max);
     A.x_out[orig] = qx;
     A.y_out[orig] = qy;
     A.d_prev_out[orig] = dpo;

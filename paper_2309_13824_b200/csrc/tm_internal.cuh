@@ -89,6 +89,7 @@ struct CellArgs {
     double lip_mu, lip_phi;  // Lipschitz constants of mu~ and phi~ (0 for uniform mu)
     double fac_voro, fac_pt, fac_geps, fac_end, damping, keep_tol;
     int32_t newton_max, quad_max;
+    int32_t projection, trace_max;  // treatment scheme (NEXT-1), see treat_point
     // outputs
     int32_t *tri;
     int64_t tri_cap;
@@ -161,6 +162,11 @@ struct tm_ctx {
     bool have_cells = false;
     const int64_t *dcnt = nullptr;  // device {n_owned, n_local} of the last tm_grid_bin_dc, else NULL
     bool capturing = false;         // tm_graph_begin .. tm_graph_end
+    const int32_t *gids_in = nullptr;  // the caller's gid array of the last tm_grid_bin (or NULL)
+    // positions and h of the last triangulation with adjacency (lazy re-triangulation, NEXT-1)
+    double *xs_tria = nullptr, *ys_tria = nullptr, *hs_tria = nullptr;
+    int64_t cap_tria = 0;
+    bool have_tria = false;
     int64_t *scratch_n = nullptr;   // device scratch count (migration source size)
 };
 
@@ -191,12 +197,90 @@ tm_status tm_internal_check_launch(tm_ctx *ctx, const char *what);
 
 namespace tmg {
 
-// S5 treatment of one point (L20-L22); returns status
+// NEXT-1: the paper's projection of escaped points (Fig. 13), the same operations
+// in the same order as the oracle (canonical, uncontracted: identical bits).
+// Sphere tracing from the inner p_old toward p_new: q <- q + |phi~(q)| u, a step never
+// passing p_new, until |phi~(q)| <= geps, at most trace_max steps (L39).
+template <typename Load>
+__device__ __noinline__ bool sphere_trace(const Grid &g, const double *phi, double xo, double yo, double xn,
+                                          double yn, double geps, int trace_max, double &qx_out, double &qy_out,
+                                          Load ld) {
+    const double dx = csub(xn, xo), dy = csub(yn, yo);
+    const double len = sqrt(cadd(cmul(dx, dx), cmul(dy, dy)));
+    const double ux = cdiv(dx, len), uy = cdiv(dy, len);
+    double qx = xo, qy = yo, s = 0.0;
+    for (int k = 0; k < trace_max; k++) {
+        const double v = bilinear(g, phi, qx, qy, ld);
+        if (fabs(v) <= geps) {
+            qx_out = qx;
+            qy_out = qy;
+            return true;
+        }
+        double r = fabs(v);
+        if (cadd(s, r) > len) r = csub(len, s);
+        s = cadd(s, r);
+        qx = cadd(qx, cmul(r, ux));
+        qy = cadd(qy, cmul(r, uy));
+    }
+    qx_out = qx;
+    qy_out = qy;
+    return fabs(bilinear(g, phi, qx, qy, ld)) <= geps;
+}
+
+// Damped Newton projection: L(p) = [phi~(p), (p - p_new) x grad phi~(p)] = 0 from
+// p_new, the Jacobian of Eq. projection_Newton_Jacobian with central finite differences of step
+// deps (L36, L41), p <- p - alpha J^-1 L clamped into B, until |phi~| <= geps.
+template <typename Load>
+__device__ __noinline__ bool newton_project(const Grid &g, const double *phi, double xn, double yn, double geps,
+                                            double deps, double damping, int newton_max, double &qx_out,
+                                            double &qy_out, Load ld) {
+    double x = xn, y = yn;
+    bool ok = false;
+    for (int k = 0; k < newton_max; k++) {
+        const double d = deps;
+        const double f0 = bilinear(g, phi, x, y, ld);
+        const double xp = cadd(x, d), xm = csub(x, d), yp = cadd(y, d), ym = csub(y, d);
+        const double fxp = bilinear(g, phi, xp, y, ld), fxm = bilinear(g, phi, xm, y, ld);
+        const double fyp = bilinear(g, phi, x, yp, ld), fym = bilinear(g, phi, x, ym, ld);
+        const double fpp = bilinear(g, phi, xp, yp, ld), fpm = bilinear(g, phi, xp, ym, ld);
+        const double fmp = bilinear(g, phi, xm, yp, ld), fmm = bilinear(g, phi, xm, ym, ld);
+        const double fx = cdiv(csub(fxp, fxm), cmul(2.0, d)), fy = cdiv(csub(fyp, fym), cmul(2.0, d));
+        const double dd = cmul(d, d);
+        const double fxx = cdiv(cadd(csub(fxp, cmul(2.0, f0)), fxm), dd);
+        const double fyy = cdiv(cadd(csub(fyp, cmul(2.0, f0)), fym), dd);
+        const double fxy = cdiv(cadd(csub(csub(fpp, fpm), fmp), fmm), cmul(cmul(4.0, d), d));
+        const double L1 = f0;
+        const double ex = csub(x, xn), ey = csub(y, yn);
+        const double L2 = csub(cmul(ex, fy), cmul(ey, fx));
+        const double J11 = fx, J12 = fy;
+        const double J21 = csub(cadd(fy, cmul(ex, fxy)), cmul(ey, fxx));
+        const double J22 = cadd(csub(-fx, cmul(ey, fxy)), cmul(ex, fyy));
+        const double det = csub(cmul(J11, J22), cmul(J12, J21));
+        if (!(det != 0.0)) break;
+        const double sx = cdiv(csub(cmul(L1, J22), cmul(J12, L2)), det);
+        const double sy = cdiv(csub(cmul(J11, L2), cmul(J21, L1)), det);
+        const double nx = csub(x, cmul(damping, sx)), ny = csub(y, cmul(damping, sy));
+        x = nx < g.x0 ? g.x0 : (nx > g.x1 ? g.x1 : nx);
+        y = ny < g.y0 ? g.y0 : (ny > g.y1 ? g.y1 : ny);
+        if (fabs(bilinear(g, phi, x, y, ld)) <= geps) {
+            ok = true;
+            break;
+        }
+    }
+    qx_out = x;
+    qy_out = y;
+    return ok;
+}
+
+// S5 treatment of one point (L20-L22); returns status.
+// projection 0: the L22 reading (1-D gradient Newton from p_new); 1: the paper's Fig. 13
+// (sphere tracing from an inner p_old, status + 8; 2x2 FD Newton from a boundary p_old).
 template <typename Load>
 __device__ __forceinline__ int treat_point(const Grid &g, const double *phi, double h, double h_avg,
                                            double fac_pt, double fac_geps, double damping, int newton_max,
                                            double xo, double yo, double xh, double yh, double &qx_out,
-                                           double &qy_out, double &dprev, Load ld) {
+                                           double &qy_out, double &dprev, Load ld, int projection = 0,
+                                           int trace_max = 64) {
     int status = 0;
     double T = cmul(fac_pt, h);
     double dx = csub(xh, xo), dy = csub(yh, yo);
@@ -209,9 +293,30 @@ __device__ __forceinline__ int treat_point(const Grid &g, const double *phi, dou
     }
     double qx = fmin(fmax(cadd(xo, dx), g.x0), g.x1);
     double qy = fmin(fmax(cadd(yo, dy), g.y0), g.y1);
-    double geps = cmul(fac_geps, h < h_avg ? h : h_avg);
+    const double hm = h < h_avg ? h : h_avg;
+    double geps = cmul(fac_geps, hm);
     double ph = bilinear(g, phi, qx, qy, ld);
-    if (!(ph <= geps)) {
+    if (!(ph <= geps) && projection == 1) {
+        const double po = bilinear(g, phi, xo, yo, ld);
+        double tx, ty;
+        bool ok;
+        if (po < -geps) {
+            ok = sphere_trace(g, phi, xo, yo, qx, qy, geps, trace_max, tx, ty, ld);
+            status |= 8;
+        } else {
+            ok = newton_project(g, phi, qx, qy, geps, cmul(1.4901161193847656e-08, hm), damping, newton_max, tx, ty,
+                                ld);
+        }
+        if (ok) {
+            qx = tx;
+            qy = ty;
+            status |= 1;
+        } else {
+            qx = xo;
+            qy = yo;
+            status = (status & 4) | 2;
+        }
+    } else if (!(ph <= geps)) {
         bool ok = false;
         for (int it = 0; it < newton_max; it++) {
             double gx, gy;
