@@ -96,12 +96,8 @@ def run(k, warm=4, timed=5):
         graph_ms = g0.elapsed_time(g1) / (3 * timed)
         g.close()
         # work counters of a warm-started launch: the counting context on S0, then on its output
-        cctx.tm_grid_bin(x, y)
         xo2, yo2, do2 = torch.empty_like(x), torch.empty_like(x), torch.empty_like(x)
-        if mode == "cvd":
-            cctx.tm_voronoi_delaunay(bufs.tri, bufs.n_tri, None, None, dp, xo2, yo2, do2, bufs.status)
-        else:
-            cctx.tm_voronoi_delaunay(bufs.tri, bufs.n_tri, bufs.adj, bufs.deg)
+        T.iterate(cctx, x, y, dp, mode, bufs, xo2, yo2, do2)
         cctx.tm_grid_bin(xo2, yo2)
         if mode == "cvd":
             cctx.tm_voronoi_delaunay(bufs.tri, bufs.n_tri, None, None, do2, *B[0], bufs.status)
