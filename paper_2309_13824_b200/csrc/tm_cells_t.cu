@@ -56,6 +56,16 @@ using namespace tmg;
 
 namespace {
 
+// which outputs leave k_cells_t for k_output_t (measured per mode, round 2): CVD's centroid,
+// quadrature and treatment always; DistMesh's triangles and ELL rows (-6 % per DistMesh
+// iteration on cfg3/cfg4); CVD's triangles stay (+4 % if moved)
+__host__ __device__ constexpr bool split_tris(int mode) {
+    return !(mode & M_COUNT) && (TM_CVD_SPLIT >= 2 || ((mode & M_ELL) && TM_CVD_SPLIT >= 1));
+}
+__host__ __device__ constexpr bool split_rings(int mode) {
+    return !(mode & M_COUNT) && ((TM_CVD_SPLIT >= 1 && (mode & (M_TREAT | M_HAT))) || split_tris(mode));
+}
+
 constexpr int TB = TM_TB;
 constexpr int VMAX = TM_VMAX;
 static_assert(VMAX <= 31, "slot masks are 32-bit");
@@ -420,9 +430,7 @@ __device__ __forceinline__ int init_ring(TPoly &P, const CellGeom &g, double S, 
 //     h(p_x) >= h(p_i) - c L_mu 2 R_i (h = c mu~, mu~ L_mu-Lipschitz);
 //   * phi~(g) < keep_tol: phi~(p_i) + L_phi 4 R_i / 3 < keep_tol (phi~ L_phi-Lipschitz).
 // All with relative margins (1e-9 .. 1e-6) far above the canonical arithmetic's rounding.
-__device__ __forceinline__ bool interior_keeps_all(const TPoly &P, const CellArgs &A, double px, double py, double h) {
-    if (P.wall & P.used) return false;
-    const double R = sqrt((double)poly_R2(P)) * (1.0 + 1e-9);
+__device__ __forceinline__ bool interior_keeps_all_R(const CellArgs &A, double px, double py, double h, double R) {
     const Grid &g = A.grid;
     if (!(px - g.x0 > R * (1.0 + 1e-9) + 1e-300 && g.x1 - px > R * (1.0 + 1e-9) && py - g.y0 > R * (1.0 + 1e-9) &&
           g.y1 - py > R * (1.0 + 1e-9)))
@@ -433,6 +441,11 @@ __device__ __forceinline__ bool interior_keeps_all(const TPoly &P, const CellArg
     return ph + A.lip_phi * (4.0 / 3.0) * R * (1.0 + 1e-6) + 1e-12 * (1.0 + fabs(ph)) < A.keep_tol;
 }
 
+__device__ __forceinline__ bool interior_keeps_all(const TPoly &P, const CellArgs &A, double px, double py, double h) {
+    if (P.wall & P.used) return false;
+    return interior_keeps_all_R(A, px, py, h, sqrt((double)poly_R2(P)) * (1.0 + 1e-9));
+}
+
 #ifndef TM_WMINB
 #define TM_WMINB 5  // min resident blocks per SM of the warm-certification kernels (register cap)
 #endif
@@ -440,11 +453,11 @@ __device__ __forceinline__ bool interior_keeps_all(const TPoly &P, const CellArg
 template <int MODE>
 __global__ void __launch_bounds__(TB, (MODE & M_WCERT) ? TM_WMINB : TM_TMINB) k_cells_t(CellArgs A, int32_t *retry_list,
                                                           unsigned long long *retry_cnt, RingBuf R) {
-    // CVD split (TM_CVD_SPLIT): this kernel stores the ring and k_output_t computes the
-    // centroid, quadrature and treatment -- a smaller kernel body for the search
-    constexpr bool CSPLIT = !(MODE & M_COUNT) && ((TM_CVD_SPLIT >= 1 && (MODE & (M_TREAT | M_HAT))) ||
-                                                  (TM_CVD_SPLIT >= 2 && (MODE & M_ELL)));
-    constexpr bool TSPLIT = CSPLIT && TM_CVD_SPLIT >= 2;  // triangles / ELL rows in k_output_t too
+    // output split: this kernel stores the ring and k_output_t computes the centroid, quadrature
+    // and treatment (CVD), or the triangles and ELL rows (DistMesh) -- a smaller kernel body
+    // (instruction cache) for the search
+    constexpr bool CSPLIT = split_rings(MODE);
+    constexpr bool TSPLIT = split_tris(MODE);
     extern __shared__ __align__(16) unsigned char tsmem[];
     const int tid = threadIdx.x;
     const int64_t cell = (int64_t)blockIdx.x * TB + tid;
@@ -1245,11 +1258,24 @@ __global__ void __launch_bounds__(128, TM_OUT_MINB) k_output_t(CellArgs A, RingB
     unsigned keptmask = 0;
     if (live && (MODE & (M_TRI | M_ELL))) {
         unsigned keptall = 0;
+        // keep-rule fast path (see interior_keeps_all): no wall line in the ring, and R from the
+        // stored vertices with a 1e-9 margin (far above their error bound)
+        bool all_in = true;
+        double R2 = 0.0;
+        for (int i = 0; i < nv; i++) {
+            const double2 v = RV(i);
+            R2 = fmax(R2, v.x * v.x + v.y * v.y);
+            all_in = all_in && RL(i) >= 0;
+        }
+        all_in = all_in && interior_keeps_all_R(A, px, py, h, sqrt(R2) * (1.0 + 1e-9));
         for (int i = 0; i < nv; i++) {
             const int a = RL(i), b = RL(i + 1 == nv ? 0 : i + 1);
             if (a >= 0 && b >= 0) {
                 const int32_t ga = __ldg(A.gids + a), gb = __ldg(A.gids + b);
-                if (gi < ga && gi < gb) {
+                if (all_in) {
+                    keptall |= 1u << i;
+                    if (gi < ga && gi < gb) keptmask |= 1u << i;
+                } else if (gi < ga && gi < gb) {
                     const int sv = ga < gb ? a : b, sw = ga < gb ? b : a;
                     const double2 v = RV(i);
                     if (keep_tri(A, (int)cell, sv, sw, cadd(px, v.x), cadd(py, v.y))) {
@@ -1369,9 +1395,8 @@ static tm_status launch_cells_thread_impl(tm_ctx *ctx, const CellArgs &a) {
         TM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_cells_t<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set = true;
     }
-    constexpr bool CSPLIT = !(MODE & M_COUNT) && ((TM_CVD_SPLIT >= 1 && (MODE & (M_TREAT | M_HAT))) ||
-                                                  (TM_CVD_SPLIT >= 2 && (MODE & M_ELL)));
-    constexpr int OMODE = TM_CVD_SPLIT >= 2 ? (MODE & (M_TRI | M_ELL | M_TREAT | M_HAT)) : (MODE & (M_TREAT | M_HAT));
+    constexpr bool CSPLIT = split_rings(MODE);
+    constexpr int OMODE = split_tris(MODE) ? (MODE & (M_TRI | M_ELL | M_TREAT | M_HAT)) : (MODE & (M_TREAT | M_HAT));
     RingBuf R = {};
     if (CSPLIT) {
         if (ctx->n_local > ctx->cap_ring) {
