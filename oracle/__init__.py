@@ -51,7 +51,8 @@ class Params(ctypes.Structure):
                 ("newton_damping", ctypes.c_double), ("newton_max", ctypes.c_int32),
                 ("quad_max_level", ctypes.c_int32), ("fscale", ctypes.c_double),
                 ("dt_k", ctypes.c_double), ("keep_tol", ctypes.c_double),
-                ("projection", ctypes.c_int32), ("trace_max", ctypes.c_int32), ("fac_retria", ctypes.c_double)]
+                ("projection", ctypes.c_int32), ("trace_max", ctypes.c_int32), ("fac_retria", ctypes.c_double),
+                ("validity", ctypes.c_int32), ("t_circ", ctypes.c_double)]
 
 
 class Info(ctypes.Structure):
@@ -66,7 +67,8 @@ def default_params(**kw) -> Params:
     """Table B.1 defaults plus the L3/L10/L13 readings."""
     p = Params(fac_voro_bound=5.0, fac_pt_mvmt=0.4, fac_geps=0.01, fac_end_mvmt=0.001,
                newton_damping=1.0, newton_max=10, quad_max_level=10, fscale=1.2, dt_k=0.2,
-               keep_tol=0.0, projection=0, trace_max=64, fac_retria=0.1)
+               keep_tol=0.0, projection=0, trace_max=64, fac_retria=0.1,
+               validity=0, t_circ=0.4)
     for k, v in kw.items():
         setattr(p, k, v)
     return p
@@ -129,6 +131,17 @@ def lib():
         L.or_stats.restype = None
         L.or_stats.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                ctypes.c_void_p]
+        L.or_keep_triangle.restype = ctypes.c_int
+        L.or_keep_triangle.argtypes = [ctypes.POINTER(Fields), ctypes.POINTER(Params), ctypes.c_double,
+                                       ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32,
+                                       ctypes.c_int32, ctypes.c_int32]
+        L.or_move_count.restype = ctypes.c_int64
+        L.or_move_count.argtypes = [ctypes.POINTER(Fields), ctypes.POINTER(Params), ctypes.c_double, ctypes.c_double,
+                                    ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        L.or_point_addition.restype = ctypes.c_int64
+        L.or_point_addition.argtypes = [ctypes.POINTER(Fields), ctypes.c_double, ctypes.c_int64, ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                        ctypes.c_void_p, D]
         _lib = L
     return _lib
 
@@ -351,3 +364,113 @@ def stats(tri, x, y):
     out = np.zeros(12)
     lib().or_stats(tri.shape[0], _p(tri), _p(x), _p(y), _p(out))
     return out
+
+
+# ---------------------------------------------------------------- NEXT-2 / NEXT-3
+def keep_triangle(fs: FieldSet, c, h_avg, x, y, tri, params=None) -> bool:
+    """O3 keep rule on one triangle (indices into x, y)."""
+    params = params or default_params()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    return bool(lib().or_keep_triangle(ctypes.byref(fs.c), ctypes.byref(params), c, h_avg, _p(x), _p(y),
+                                       int(tri[0]), int(tri[1]), int(tri[2])))
+
+
+def move_count(fs: FieldSet, c, h_avg, x_old, y_old, d_prev, params=None) -> int:
+    """Inner points (phi~(p_old) < -geps) whose move is not below fac_end_mvmt*h(p_old)."""
+    params = params or default_params()
+    xo = np.ascontiguousarray(x_old, dtype=np.float64)
+    yo = np.ascontiguousarray(y_old, dtype=np.float64)
+    dp = np.ascontiguousarray(d_prev, dtype=np.float64)
+    return int(lib().or_move_count(ctypes.byref(fs.c), ctypes.byref(params), c, h_avg, xo.shape[0], _p(xo), _p(yo),
+                                   _p(dp)))
+
+
+def point_addition(fs: FieldSet, c, tri, x, y, n_add):
+    """centroids of the n_add triangles with the largest R_circ/h(g), in (u, v) order
+    of their triangles (reading L46).  Returns (x_new, y_new, smallest selected ratio)."""
+    tri = np.ascontiguousarray(tri, dtype=np.int32)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    k = max(0, min(int(n_add), tri.shape[0]))
+    xn, yn = np.empty(k), np.empty(k)
+    r = ctypes.c_double(0.0)
+    m = lib().or_point_addition(ctypes.byref(fs.c), c, tri.shape[0], _p(tri), _p(x), _p(y), k, _p(xn), _p(yn),
+                                ctypes.byref(r))
+    return xn[:m], yn[:m], r.value
+
+
+@dataclass
+class ControlParams:
+    """Table B.1 thresholds of the meshing controller."""
+    t_add_quality: float = 0.002     # P:1093  T^add_quality
+    fac_add: float = 0.6             # P:1095  fac_add
+    t_end_quality: float = 0.001     # P:1111  T^end_quality
+    t_end_alpha_max: float = 0.005   # P:1113  T^end_alpha_max
+    t_switch_quality: float = 0.0015 # P:1121  T^switch_quality
+    max_iterations: int = 1000       # safety cap (paper silent)
+
+
+class Controller:
+    """The iterate-to-termination controller (NEXT-2, NEXT-3 trigger), step by step as the paper
+    states it (reading L45):
+
+    * quality of iteration n: the 1/2-means M_a, M_b of alpha and beta and max alpha over the kept
+      triangles T_n at the positions p_n they were computed from (Eqs. aspect/edge ratios, 1/2-mean,
+      P:415-427); relative change r(X) = |X_n - X_{n-1}| / X_{n-1} between consecutive iterations
+      at the same N_current (the history restarts after a point addition);
+    * N_current < N_total: add points when r(M_a) < T_add and r(M_b) < T_add, N_add =
+      min(floor(fac_add N_current), N_total - N_current) (P:430);
+    * N_current = N_total, hybrid, still DistMesh: switch to CVD from the next iteration when
+      r(M_a) < T_switch (P:555);
+    * N_current = N_total, CVD (or DistMesh-only meshing): terminate when r(M_a) < T_end and
+      r(M_b) < T_end and r(max alpha) < T_end_alpha, or when no inner point moved by at
+      least fac_end h (move_count == 0).
+
+    update() returns a dict {"action": "continue"|"add"|"switch"|"terminate", "n_add": k}."""
+
+    def __init__(self, n_total, n_current, method="hybrid", cp: Optional[ControlParams] = None):
+        self.cp = cp or ControlParams()
+        self.n_total = int(n_total)
+        self.n_current = int(n_current)
+        self.method = method                       # "cvd", "distmesh", "hybrid"
+        self.mode = "cvd" if method == "cvd" else "dm"
+        self.prev = None
+        self.iterations = 0
+
+    @staticmethod
+    def _rel(a, b):
+        return abs(a - b) / b
+
+    def update(self, half_alpha, half_beta, max_alpha, move_count):
+        cp = self.cp
+        self.iterations += 1
+        cur = (float(half_alpha), float(half_beta), float(max_alpha))
+        prev, self.prev = self.prev, cur
+        if self.iterations >= cp.max_iterations:
+            return {"action": "terminate", "n_add": 0, "reason": "max_iterations"}
+        if self.n_current < self.n_total:
+            if prev is not None and self._rel(cur[0], prev[0]) < cp.t_add_quality and \
+                    self._rel(cur[1], prev[1]) < cp.t_add_quality:
+                k = min(int(np.floor(cp.fac_add * self.n_current)), self.n_total - self.n_current)
+                self.n_current += k
+                self.prev = None
+                return {"action": "add", "n_add": k}
+            return {"action": "continue", "n_add": 0}
+        if self.method == "hybrid" and self.mode == "dm":
+            if prev is not None and self._rel(cur[0], prev[0]) < cp.t_switch_quality:
+                self.mode = "cvd"
+                return {"action": "switch", "n_add": 0}
+            return {"action": "continue", "n_add": 0}
+        if move_count == 0:
+            return {"action": "terminate", "n_add": 0, "reason": "movement"}
+        if prev is not None and self._rel(cur[0], prev[0]) < cp.t_end_quality and \
+                self._rel(cur[1], prev[1]) < cp.t_end_quality and self._rel(cur[2], prev[2]) < cp.t_end_alpha_max:
+            return {"action": "terminate", "n_add": 0, "reason": "quality"}
+        return {"action": "continue", "n_add": 0}
+
+
+def quality_of(st):
+    """(1/2-mean alpha, 1/2-mean beta, max alpha) from stats() (Eq. 1/2-mean)."""
+    n = st[0]
+    return (st[1] / n) ** 2, (st[2] / n) ** 2, st[3]

@@ -894,9 +894,43 @@ static int in_octagon(double cx, double cy, double qx, double qy, double r) {
     return fabs(dx) < r && fabs(dy) < r && fabs(dx + dy) < r2 && fabs(dx - dy) < r2;
 }
 
-/* t = {u<v<w}: keep iff c_t strictly in B and in all three octagons and phi~(g_t) < tau */
-static int keep_triangle(const or_fields *f, const or_params *p, double c, const double *x, const double *y,
-                         int32_t u, int32_t v, int32_t w) {
+/* geps(x) = fac_geps * min(h(x), h_avg)   (reading L20 evaluated at x) */
+static double geps_at(const or_fields *f, const or_params *p, double c, double h_avg, double x, double y) {
+    const double h = c * (f->mu ? or_field_value(f, f->mu, x, y) : 1.0);
+    return p->fac_geps * (h < h_avg ? h : h_avg);
+}
+
+/* NEXT-2: the paper's validity tests on a triangle whose circumcentre passed the bounded-cell
+ * conditions (§4.1, reading L43).  (ox, oy): canonical circumcentre relative to p_u.
+ *   Test 1: the centroid g; discard iff phi~(g) > geps(g).
+ *   Test 2: count the edge midpoints m with phi~(m) <= geps(m); valid iff >= 2.
+ *   Test 3: otherwise discard iff |phi~(c_circ)| / R_circ > T^tria. */
+static int validity_tests(const or_fields *f, const or_params *p, double c, double h_avg, const double *x,
+                          const double *y, int32_t u, int32_t v, int32_t w, double ox, double oy) {
+    const double gx = ((x[u] + x[v]) + x[w]) / 3.0, gy = ((y[u] + y[v]) + y[w]) / 3.0;
+    const double pg = or_field_value(f, f->phi, gx, gy), eg = geps_at(f, p, c, h_avg, gx, gy);
+    near_tie(pg, eg, eg);
+    if (pg > eg) return 0;                                   /* Test 1: centroid outside */
+    const int32_t q[3] = {u, v, w};
+    int count = 0;
+    for (int k = 0; k < 3; k++) {                            /* Test 2: edges (u,v), (v,w), (w,u) */
+        const int32_t a = q[k], b = q[(k + 1) % 3];
+        const double mx = (x[a] + x[b]) * 0.5, my = (y[a] + y[b]) * 0.5;
+        const double pm = or_field_value(f, f->phi, mx, my), em = geps_at(f, p, c, h_avg, mx, my);
+        near_tie(pm, em, em);
+        if (pm <= em) count++;
+    }
+    if (count >= 2) return 1;
+    const double R = sqrt(ox * ox + oy * oy);                /* Test 3: circumcentre */
+    const double pc = or_field_value(f, f->phi, x[u] + ox, y[u] + oy);
+    near_tie(fabs(pc) / R, p->t_circ, 1.0);
+    return !(fabs(pc) / R > p->t_circ);
+}
+
+/* t = {u<v<w}: keep iff c_t strictly in B and in all three octagons and phi~(g_t) < tau
+ * (validity 0, L10), or the paper's Tests 1-3 (validity 1, NEXT-2) */
+static int keep_triangle(const or_fields *f, const or_params *p, double c, double h_avg, const double *x,
+                         const double *y, int32_t u, int32_t v, int32_t w) {
     /* canonical circumcentre relative to p_u, as the Cramer intersection of the two bisectors */
     line2 A, B;
     A.nx = x[v] - x[u]; A.ny = y[v] - y[u]; A.r = 0.5 * (A.nx * A.nx + A.ny * A.ny);
@@ -915,6 +949,7 @@ static int keep_triangle(const or_fields *f, const or_params *p, double c, const
         near_tie(fabs(dx + dy), OR_SQRT2 * r, r); near_tie(fabs(dx - dy), OR_SQRT2 * r, r);
         if (!in_octagon(cx, cy, x[q[k]], y[q[k]], r)) return 0;
     }
+    if (p->validity) return validity_tests(f, p, c, h_avg, x, y, u, v, w, ox, oy);
     double gx = ((x[u] + x[v]) + x[w]) / 3.0, gy = ((y[u] + y[v]) + y[w]) / 3.0;
     const double ph = or_field_value(f, f->phi, gx, gy);
     near_tie(ph, p->keep_tol, sqrt(ox * ox + oy * oy));
@@ -1327,7 +1362,7 @@ int or_iteration(const or_fields *f, const or_params *p, int64_t n, int64_t n_to
     for (int64_t t = 0; t < nd; t++) {
         int32_t u = D[3 * t], v = D[3 * t + 1], w = D[3 * t + 2]; /* u is the min, CCW */
         int32_t lo = v < w ? v : w, hi = v < w ? w : v;
-        if (keep_triangle(f, p, c, x, y, u, lo, hi)) {
+        if (keep_triangle(f, p, c, inf.h_avg, x, y, u, lo, hi)) {
             if (nk < tri_cap) { tri_out[3 * nk] = u; tri_out[3 * nk + 1] = v; tri_out[3 * nk + 2] = w; }
             if (own) own[u]++;
             nk++;
@@ -1412,4 +1447,83 @@ int or_iteration(const or_fields *f, const or_params *p, int64_t n, int64_t n_to
     free(D); free(own); free(E); free(erow); free(g.start); free(g.nb);
     if (counts) { free(cg.start); free(cg.idx); }
     return 0;
+}
+
+/* ========================================================================== */
+/* NEXT-2 / NEXT-3: controller inputs and point addition          */
+/* ========================================================================== */
+/* the keep rule (O3) on one triangle, for pin tests: u, v, w any order */
+int or_keep_triangle(const or_fields *f, const or_params *p, double c, double h_avg, const double *x,
+                     const double *y, int32_t u, int32_t v, int32_t w) {
+    int32_t q[3] = {u, v, w};
+    for (int a = 0; a < 2; a++)
+        for (int b = 0; b < 2 - a; b++)
+            if (q[b] > q[b + 1]) { int32_t t = q[b]; q[b] = q[b + 1]; q[b + 1] = t; }
+    return keep_triangle(f, p, c, h_avg, x, y, q[0], q[1], q[2]);
+}
+
+/* Movement termination input (P:447 T^end_mvmt,i = fac_end * h_i): the number of
+ * inner points whose move in this iteration is NOT below its local threshold.  A point is
+ * inner iff phi~(p_old) < -geps(p_old) (the tagging rule P:410, reading L38); its move is
+ * d_prev = |p_new - p_old| (L32) and its threshold fac_end_mvmt * h(p_old).  Meshing may
+ * terminate on movements iff the count is 0. */
+int64_t or_move_count(const or_fields *f, const or_params *p, double c, double h_avg, int64_t n,
+                      const double *x_old, const double *y_old, const double *d_prev) {
+    int64_t cnt = 0;
+    for (int64_t i = 0; i < n; i++) {
+        const double h = h_of(f, c, x_old[i], y_old[i]);
+        const double geps = p->fac_geps * (h < h_avg ? h : h_avg);
+        const double ph = or_field_value(f, f->phi, x_old[i], y_old[i]);
+        if (!(ph < -geps)) continue;                     /* boundary or outside point */
+        if (!(d_prev[i] < p->fac_end_mvmt * h)) cnt++;
+    }
+    return cnt;
+}
+
+/* Point addition (§3.6, after Alliez et al.): rank the triangles by
+ * R_circum / h(g) and add one point at the centroid g of each of the n_add largest.
+ * Reading L46: a triangle is taken as {u < v < w} (caller indices); its circumcentre is the
+ * canonical Cramer intersection of the bisectors of (u,v) and (u,w) relative to p_u (as in the
+ * keep rule), R = |c - p_u|, g = ((p_u + p_v) + p_w) / 3, h(g) = c mu~(g).  Ties of the ratio
+ * are broken by (u, v) ascending; the new points are written in (u, v) ascending order of their
+ * triangles.  Returns the number written (min(n_add, n_tri)). */
+typedef struct { double r; int32_t u, v; double gx, gy; } pa_item;
+static int cmp_pa_rank(const void *a, const void *b) {
+    const pa_item *A = (const pa_item *)a, *B = (const pa_item *)b;
+    if (A->r != B->r) return A->r > B->r ? -1 : 1;
+    if (A->u != B->u) return A->u < B->u ? -1 : 1;
+    return A->v < B->v ? -1 : (A->v > B->v);
+}
+static int cmp_pa_uv(const void *a, const void *b) {
+    const pa_item *A = (const pa_item *)a, *B = (const pa_item *)b;
+    if (A->u != B->u) return A->u < B->u ? -1 : 1;
+    return A->v < B->v ? -1 : (A->v > B->v);
+}
+int64_t or_point_addition(const or_fields *f, double c, int64_t n_tri, const int32_t *tri, const double *x,
+                          const double *y, int64_t n_add, double *x_new, double *y_new, double *ratio_out) {
+    if (n_add > n_tri) n_add = n_tri;
+    if (n_add <= 0) return 0;
+    pa_item *it = (pa_item *)malloc(sizeof(pa_item) * (size_t)n_tri);
+    for (int64_t t = 0; t < n_tri; t++) {
+        int32_t q[3] = {tri[3 * t], tri[3 * t + 1], tri[3 * t + 2]};
+        for (int a = 0; a < 2; a++)
+            for (int b = 0; b < 2 - a; b++)
+                if (q[b] > q[b + 1]) { int32_t s = q[b]; q[b] = q[b + 1]; q[b + 1] = s; }
+        const int32_t u = q[0], v = q[1], w = q[2];
+        line2 A, B;
+        A.nx = x[v] - x[u]; A.ny = y[v] - y[u]; A.r = 0.5 * (A.nx * A.nx + A.ny * A.ny);
+        B.nx = x[w] - x[u]; B.ny = y[w] - y[u]; B.r = 0.5 * (B.nx * B.nx + B.ny * B.ny);
+        double ox, oy;
+        cramer(A, B, &ox, &oy);
+        const double R = sqrt(ox * ox + oy * oy);
+        const double gx = ((x[u] + x[v]) + x[w]) / 3.0, gy = ((y[u] + y[v]) + y[w]) / 3.0;
+        const double h = h_of(f, c, gx, gy);
+        it[t].r = R / h; it[t].u = u; it[t].v = v; it[t].gx = gx; it[t].gy = gy;
+    }
+    qsort(it, (size_t)n_tri, sizeof(pa_item), cmp_pa_rank);
+    if (ratio_out) ratio_out[0] = it[n_add - 1].r;  /* the smallest selected ratio */
+    qsort(it, (size_t)n_add, sizeof(pa_item), cmp_pa_uv);
+    for (int64_t k = 0; k < n_add; k++) { x_new[k] = it[k].gx; y_new[k] = it[k].gy; }
+    free(it);
+    return n_add;
 }

@@ -45,6 +45,13 @@ typedef struct {
     int32_t projection;
     int32_t trace_max;      /* 64    sphere-tracing step cap (paper silent, L39)            */
     double fac_retria;      /* 0.1   P:1098 lazy re-triangulation threshold fac * h (Alg. 1) */
+    /* NEXT-2: the triangle validity tests, P:499-521 (§4.1).
+     * 0 = Test 1 only in the L10 reading (keep iff phi~(g) < keep_tol);
+     * 1 = the paper's Tests 1-3 (reading L43): discard iff phi~(g) > geps(g) (Test 1); keep iff
+     *     at least two edge midpoints have phi~(m) <= geps(m) (Test 2); otherwise keep iff
+     *     |phi~(c_circ)| / R_circ <= t_circ (Test 3).  geps(x) = fac_geps * min(h(x), h_avg). */
+    int32_t validity;
+    double t_circ;          /* 0.4   P:1118 circumcentre test threshold T^tria_ccircum          */
 } or_params;
 
 typedef struct {
@@ -128,6 +135,18 @@ int or_distmesh_lazy(const or_fields *f, const or_params *p, int64_t n, int64_t 
 /* O7 quality of one triangle and reductions over a list */
 void or_triangle_quality(const double *a, const double *b, const double *c, double *alpha, double *beta);
 void or_stats(int64_t n_tri, const int32_t *tri, const double *x, const double *y, double *out12);
+
+/* ---- NEXT-2 / NEXT-3 ------------------------------------- */
+/* keep rule O3 on one triangle (any vertex order), for pin tests */
+int or_keep_triangle(const or_fields *f, const or_params *p, double c, double h_avg, const double *x,
+                     const double *y, int32_t u, int32_t v, int32_t w);
+/* inner points (phi~(p_old) < -geps) whose move d_prev is not below fac_end_mvmt*h(p_old) */
+int64_t or_move_count(const or_fields *f, const or_params *p, double c, double h_avg, int64_t n,
+                      const double *x_old, const double *y_old, const double *d_prev);
+/* point addition: centroids of the n_add triangles of largest R_circ/h(g), in (u,v)
+ * order; ratio_out[0] = smallest selected ratio.  Returns the count written. */
+int64_t or_point_addition(const or_fields *f, double c, int64_t n_tri, const int32_t *tri, const double *x,
+                          const double *y, int64_t n_add, double *x_new, double *y_new, double *ratio_out);
 
 #ifdef __cplusplus
 }

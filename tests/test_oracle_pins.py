@@ -149,6 +149,10 @@ def test_oracle_defaults_are_table_b1():
         assert getattr(p, k) == tb[k]["value"], k
     # readings where the paper is silent (SURVEY §8(c) ledger)
     assert p.dt_k == 0.2 and p.keep_tol == 0.0 and p.quad_max_level == 10  # L3, L10, L13
+    assert p.t_circ == tb["t_tria_ccircum"]["value"] and p.fac_retria == tb["fac_retria_mvmt"]["value"]
+    cp = O.ControlParams()
+    for k in ["t_add_quality", "fac_add", "t_end_quality", "t_end_alpha_max", "t_switch_quality"]:
+        assert getattr(cp, k) == tb[k]["value"], k
 
 
 def test_library_defaults_are_table_b1():
