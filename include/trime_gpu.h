@@ -93,6 +93,12 @@ typedef struct {
                                         derivatives from a boundary p_old                       */
     int32_t trace_max;         /* 64    sphere-tracing step cap (L39)                           */
     double fac_retria;         /* 0.1   P:1098 lazy re-triangulation threshold fac * h (Alg. 1) */
+    /* NEXT-2 */
+    int32_t validity;          /* 0     keep rule: L10 Test 1 (phi~(g) < keep_tol);
+                                  1     the paper's Tests 1-3 (reading L43): discard iff
+                                        phi~(g) > geps(g); keep iff >= 2 edge midpoints have
+                                        phi~(m) <= geps(m); else keep iff |phi~(c_circ)|/R_circ <= t_circ */
+    double t_circ;             /* 0.4   P:1118 circumcentre test threshold T^tria_ccircum        */
 } tm_params;
 
 #define TM_F_TWO_LEVEL_BINS 0x1u  /* split dense bins into 2^r x 2^r sub-bins (adaptive rho) */
@@ -277,6 +283,70 @@ tm_status tm_append_points(tm_ctx *ctx, double *x, double *y, int32_t *gid, doub
  * tm_work_counts) are refused with TM_E_STATE while capturing.  Buffers must not grow
  * during a capture: run the same sequence once before (warm-up).  A replay repeats the
  * recorded kernels with the recorded arguments (same buffers) on the context's stream. */
+/* ---- NEXT-2 / NEXT-3: meshing to termination ------------------------------ */
+/* Movement termination input (T^end_mvmt,i = fac_end_mvmt * h_i): *d_count
+ * (device int64) = the number of inner points -- phi~(p_old) < -geps(p_old), the tagging rule of
+ * P:410 (reading L38) -- whose move d_prev[i] (= |p_new - p_old|, L32) is NOT below
+ * fac_end_mvmt * h(p_old).  x_old, y_old, d_prev: device, caller order, n entries.  Asynchronous;
+ * exact (integer count). */
+tm_status tm_move_count(tm_ctx *ctx, const double *x_old, const double *y_old, const double *d_prev, int64_t n,
+                        int64_t *d_count);
+
+/* Resolution update after point addition (reading L44): c, h_avg and the level-0 bins are
+ * recomputed for N = n_total from the sums of tm_set_domain (equal to scaling the adaptive
+ * quantities by sqrt(N_old / N_current) up to rounding).  Invalidates the warm start.  c_out /
+ * h_avg_out: host, may be NULL.  Host arithmetic only. */
+tm_status tm_set_n_total(tm_ctx *ctx, int64_t n_total, double *c_out, double *h_avg_out);
+
+/* Point addition (§3.6, after Alliez et al.; reading L46): rank the n_tri triangles
+ * (caller indices into x, y: the mesh T_n at its positions p_n) by R_circ / h(g) -- R_circ the
+ * distance from p_u (u the smallest index) to the canonical circumcentre of the keep rule, g =
+ * ((p_u + p_v) + p_w) / 3 with u < v < w, h(g) = c mu~(g) -- and write the centroids g of the
+ * n_add largest (ties by (u, v) ascending) to x_new/y_new (device, n_add entries) in (u, v)
+ * ascending order of their triangles.  *ratio_min (host, may be NULL) = the smallest selected
+ * ratio.  0 <= n_add <= n_tri.  Uses scratch memory of ~56 bytes per triangle.  synchronises */
+tm_status tm_point_addition(tm_ctx *ctx, const int32_t *tri, int64_t n_tri, const double *x, const double *y,
+                            int64_t n_add, double *x_new, double *y_new, double *ratio_min);
+
+/* The iterate-to-termination controller (host state machine; P:483-485, P:430, P:555,
+ * thresholds Table B.1; reading L45).  After each iteration n, tm_control_update
+ * takes the quality of the mesh (T_n, p_n) from tm_mesh_stats -- M_a, M_b the 1/2-means of
+ * alpha and beta (Eq. 1/2-mean), A = max alpha -- and the movement count, compares them
+ * with the previous iteration at the same N_current (relative changes r(X) = |X_n - X_{n-1}| /
+ * X_{n-1}), and returns the action:
+ *   N_current < N_total:            ADD (n_add = min(floor(fac_add N_current), N_total - N_current))
+ *                                   when r(M_a) < T_add and r(M_b) < T_add;
+ *   hybrid, still DistMesh:         SWITCH to CVD when r(M_a) < T_switch;
+ *   otherwise:                      TERMINATE_MOVES when move_count == 0,
+ *                                   TERMINATE_QUALITY when r(M_a), r(M_b) < T_end and
+ *                                   r(A) < T_end_alpha;
+ *   any:                            TERMINATE_CAP after max_iterations updates. */
+#define TM_METHOD_CVD 0
+#define TM_METHOD_DISTMESH 1
+#define TM_METHOD_HYBRID 2
+#define TM_ACT_CONTINUE 0
+#define TM_ACT_ADD 1
+#define TM_ACT_SWITCH 2
+#define TM_ACT_TERMINATE_QUALITY 3
+#define TM_ACT_TERMINATE_MOVES 4
+#define TM_ACT_TERMINATE_CAP 5
+typedef struct {
+    int64_t n_total, n_current;
+    int32_t method;            /* TM_METHOD_*                                   */
+    int32_t mode;              /* current: TM_METHOD_CVD or TM_METHOD_DISTMESH   */
+    int32_t have_prev, iterations;
+    double prev[3];            /* M_a, M_b, max alpha of the previous iteration  */
+    double t_add_quality;      /* 0.002 */
+    double fac_add;            /* 0.6 */
+    double t_end_quality;      /* 0.001 */
+    double t_end_alpha_max;    /* 0.005 */
+    double t_switch_quality;   /* 0.0015 P:1121 */
+    int32_t max_iterations;    /* 1000   safety cap (paper silent) */
+} tm_control;
+void tm_control_init(tm_control *c, int64_t n_total, int64_t n_current, int32_t method);
+/* returns TM_ACT_*; *n_add (host, may be NULL) receives the points to add for TM_ACT_ADD */
+int32_t tm_control_update(tm_control *c, const tm_stats *s, int64_t move_count, int64_t *n_add);
+
 typedef struct tm_graph tm_graph;
 tm_status tm_graph_begin(tm_ctx *ctx);
 tm_status tm_graph_end(tm_ctx *ctx, tm_graph **out);

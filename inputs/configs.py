@@ -264,3 +264,25 @@ def box_phi(box, n):
 def disk_phi(box, n, r=1.0):
     X, Y = _grid(box, n)
     return np.sqrt(X * X + Y * Y) - r
+
+
+# ---------------------------------------------------------------- NEXT-2 test input
+def validity_strip():
+    """left half of the unit square (phi = x - 1/2, exactly bilinear on 33^2 nodes); a jittered
+    interior lattice, a strip of points alternating just outside (phi = +4e-4 <= geps) and just
+    inside (-2e-4) the boundary, and a few points outside (phi = 0.1): boundary triangles whose
+    centroid lies in (0, geps] (Tests 1-2 keep, the L10 reading discards) and triangles decided
+    by Test 3."""
+    rng = np.random.default_rng(21)
+    g = np.arange(0.03, 0.44, 0.05)
+    X, Y = np.meshgrid(g, np.arange(0.03, 0.98, 0.05))
+    xi = (X + rng.uniform(-0.01, 0.01, X.shape)).ravel(); yi = (Y + rng.uniform(-0.01, 0.01, Y.shape)).ravel()
+    k = np.arange(0, 20)
+    xo = 0.5004 + rng.uniform(-5e-5, 5e-5, k.size); yo = 0.30 + 0.02 * k + rng.uniform(-2e-3, 2e-3, k.size)
+    xa = 0.4998 + rng.uniform(-5e-5, 5e-5, k.size - 1); ya = 0.31 + 0.02 * k[:-1] + rng.uniform(-2e-3, 2e-3, k.size - 1)
+    xf = np.array([0.6, 0.62, 0.6]); yf = np.array([0.12, 0.80, 0.92])
+    x = np.concatenate([xi, xo, xa, xf]); y = np.concatenate([yi, yo, ya, yf])
+    box = (0.0, 0.0, 1.0, 1.0)
+    gx = node_coords(0, 1, 33)
+    PX, PY = np.meshgrid(gx, gx)
+    return box, PX - 0.5, x, y

@@ -55,7 +55,7 @@ class tm_params(ctypes.Structure):
                 ("fscale", ctypes.c_double), ("dt_k", ctypes.c_double), ("keep_tol", ctypes.c_double),
                 ("adj_stride", ctypes.c_int32), ("max_cell_vertices", ctypes.c_int32),
                 ("flags", ctypes.c_uint32), ("projection", ctypes.c_int32), ("trace_max", ctypes.c_int32),
-                ("fac_retria", ctypes.c_double)]
+                ("fac_retria", ctypes.c_double), ("validity", ctypes.c_int32), ("t_circ", ctypes.c_double)]
 
 
 class tm_stats(ctypes.Structure):
@@ -66,6 +66,18 @@ class tm_stats(ctypes.Structure):
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+TM_METHOD_CVD, TM_METHOD_DISTMESH, TM_METHOD_HYBRID = 0, 1, 2
+TM_ACT_NAMES = ["continue", "add", "switch", "terminate_quality", "terminate_moves", "terminate_cap"]
+
+
+class tm_control(ctypes.Structure):
+    _fields_ = [("n_total", ctypes.c_int64), ("n_current", ctypes.c_int64), ("method", ctypes.c_int32),
+                ("mode", ctypes.c_int32), ("have_prev", ctypes.c_int32), ("iterations", ctypes.c_int32),
+                ("prev", ctypes.c_double * 3), ("t_add_quality", ctypes.c_double), ("fac_add", ctypes.c_double),
+                ("t_end_quality", ctypes.c_double), ("t_end_alpha_max", ctypes.c_double),
+                ("t_switch_quality", ctypes.c_double), ("max_iterations", ctypes.c_int32)]
 
 
 class tm_work(ctypes.Structure):
@@ -82,7 +94,8 @@ EXPORTED = ["tm_params_default", "tm_create", "tm_destroy", "tm_last_error", "tm
             "tm_project_sdf", "tm_mesh_stats", "tm_adjacency_export", "tm_work_counts", "tm_halo_pack",
             "tm_migrate_pack", "tm_grid_bin_dc", "tm_halo_pack_dc", "tm_migrate_pack_dc", "tm_append_points",
             "tm_graph_begin", "tm_graph_end", "tm_graph_launch", "tm_graph_destroy", "tm_refresh_positions",
-            "tm_retria_check",
+            "tm_retria_check", "tm_move_count", "tm_set_n_total", "tm_point_addition", "tm_control_init",
+            "tm_control_update",
             "tm_host_incircle_exact", "tm_host_cramer", "tm_host_bilinear"]
 
 
@@ -114,6 +127,12 @@ def load_library(path: str = LIB_PATH, build_if_missing: bool = True):
         "tm_mesh_stats": (st, [vp, vp, vp, vp, i64, ctypes.POINTER(tm_stats)]),
         "tm_adjacency_export": (st, [vp, vp, vp, vp, vp]),
         "tm_work_counts": (st, [vp, ctypes.POINTER(tm_work)]),
+        "tm_move_count": (st, [vp, vp, vp, vp, i64, vp]),
+        "tm_set_n_total": (st, [vp, i64, ctypes.POINTER(dbl), ctypes.POINTER(dbl)]),
+        "tm_point_addition": (st, [vp, vp, i64, vp, vp, i64, vp, vp, ctypes.POINTER(dbl)]),
+        "tm_control_init": (None, [ctypes.POINTER(tm_control), i64, i64, i32]),
+        "tm_control_update": (i32, [ctypes.POINTER(tm_control), ctypes.POINTER(tm_stats), i64,
+                                    ctypes.POINTER(i64)]),
         "tm_halo_pack": (st, [vp, vp, vp, vp, i64, dbl, dbl, dbl, vp, vp, i64, vp]),
         "tm_migrate_pack": (st, [vp, vp, vp, vp, vp, i64, dbl, dbl, vp, vp, i64, vp]),
         "tm_grid_bin_dc": (st, [vp, vp, vp, i64, vp, vp]),
@@ -241,6 +260,22 @@ class Context:
         s = tm_stats()
         self._check(self.L.tm_mesh_stats(self.h, _ptr(x), _ptr(y), _ptr(tri), int(n_tri), ctypes.byref(s)))
         return s
+
+    def tm_move_count(self, x_old, y_old, d_prev, d_count):
+        self._check(self.L.tm_move_count(self.h, _ptr(x_old), _ptr(y_old), _ptr(d_prev), int(x_old.shape[0]),
+                                         _ptr(d_count)))
+
+    def tm_set_n_total(self, n_total: int):
+        c, ha = ctypes.c_double(), ctypes.c_double()
+        self._check(self.L.tm_set_n_total(self.h, int(n_total), ctypes.byref(c), ctypes.byref(ha)))
+        self.c, self.h_avg = c.value, ha.value
+        return self.c, self.h_avg
+
+    def tm_point_addition(self, tri, n_tri: int, x, y, n_add: int, x_new, y_new) -> float:
+        r = ctypes.c_double()
+        self._check(self.L.tm_point_addition(self.h, _ptr(tri), int(n_tri), _ptr(x), _ptr(y), int(n_add),
+                                             _ptr(x_new), _ptr(y_new), ctypes.byref(r)))
+        return r.value
 
     def tm_adjacency_export(self, adj, deg, adj_out, deg_out):
         self._check(self.L.tm_adjacency_export(self.h, _ptr(adj), _ptr(deg), _ptr(adj_out), _ptr(deg_out)))
@@ -391,3 +426,91 @@ def iterate(ctx: Context, x, y, d_prev, mode: str, bufs: IterBuffers, x_out, y_o
         ctx.tm_distmesh_step(bufs.adj, bufs.deg, bufs.sums2, None, d_prev, x_out, y_out, d_prev_out, bufs.status)
     else:
         raise ValueError(mode)
+
+
+# ---------------------------------------------------------------- NEXT-2 / NEXT-3
+class Controller:
+    """The library's iterate-to-termination controller (tm_control_init / tm_control_update)."""
+
+    def __init__(self, n_total: int, n_current: int, method: str = "hybrid"):
+        self.L = load_library()
+        self.c = tm_control()
+        m = {"cvd": TM_METHOD_CVD, "dm": TM_METHOD_DISTMESH, "distmesh": TM_METHOD_DISTMESH,
+             "hybrid": TM_METHOD_HYBRID}[method]
+        self.L.tm_control_init(ctypes.byref(self.c), int(n_total), int(n_current), m)
+
+    @property
+    def mode(self) -> str:
+        return "cvd" if self.c.mode == TM_METHOD_CVD else "dm"
+
+    def update(self, stats: tm_stats, move_count: int):
+        k = ctypes.c_int64(0)
+        a = self.L.tm_control_update(ctypes.byref(self.c), ctypes.byref(stats), int(move_count), ctypes.byref(k))
+        return TM_ACT_NAMES[a], int(k.value)
+
+
+@dataclass
+class MeshResult:
+    x: torch.Tensor
+    y: torch.Tensor
+    tri: torch.Tensor
+    iterations: int
+    history: list
+
+
+def mesh(ctx: Context, x, y, n_total: Optional[int] = None, method: str = "hybrid", max_iterations: int = 1000,
+         on_iteration=None) -> MeshResult:
+    """Mesh to termination (NEXT-2/NEXT-3): iterate (Procedure 1 +
+    Alg. 1 or Alg. 2), read the quality of (T_n, p_n) and the movement count, and let the
+    library's controller add points, switch DistMesh -> CVD, or stop.  x, y: the N_current
+    initial points (device); n_total: N_total (default: no point addition).  ctx's domain must
+    have been set for n_total = len(x) (c follows N_current).  Returns the final points, the
+    last iteration's kept triangles (at the positions it was computed from) and a per-iteration
+    history.  on_iteration(dict) runs after each iteration and decision, before points are added
+    (tests: the iteration's inputs, outputs, triangles and the controller's action)."""
+    n = int(x.shape[0])
+    n_total = int(n_total or n)
+    ctl = Controller(n_total, n, method)
+    ctl.c.max_iterations = int(max_iterations)
+    bufs = IterBuffers.alloc(n, ctx.params.adj_stride, device=x.device)
+    cnt = torch.zeros(1, dtype=torch.int64, device=x.device)
+    dp = None
+    hist = []
+    it = 0
+    tri_last = None
+    while True:
+        mode = ctl.mode
+        xo, yo, do = torch.empty_like(x), torch.empty_like(x), torch.empty_like(x)
+        iterate(ctx, x, y, dp, mode, bufs, xo, yo, do)
+        ctx.tm_move_count(x, y, do, cnt)
+        nt = int(bufs.n_tri.item())
+        st = ctx.tm_mesh_stats(x, y, bufs.tri, nt)
+        action, k = ctl.update(st, int(cnt.item()))
+        hist.append({"it": it, "mode": mode, "n": n, "n_tri": nt, "action": action, "n_add": k,
+                     "half_alpha": (st.sum_sqrt_alpha / nt) ** 2, "half_beta": (st.sum_sqrt_beta / nt) ** 2,
+                     "max_alpha": st.max_alpha, "moves": int(cnt.item())})
+        if on_iteration is not None:
+            on_iteration({"it": it, "mode": mode, "x": x, "y": y, "d_prev_in": dp, "x_out": xo, "y_out": yo,
+                          "d_prev_out": do, "status": bufs.status[:n], "tri": bufs.tri[:nt], "action": action,
+                          "n_add": k, "moves": int(cnt.item()), "stats": st})
+        it += 1
+        if action.startswith("terminate"):
+            tri_last = bufs.tri[:nt].clone()
+            x, y = xo, yo
+            break
+        if action == "add":
+            x2 = torch.empty(n + k, dtype=x.dtype, device=x.device)
+            y2 = torch.empty_like(x2)
+            d2 = torch.full((n + k,), -1.0, dtype=x.dtype, device=x.device)  # new points: no previous move
+            x2[:n].copy_(xo)
+            y2[:n].copy_(yo)
+            d2[:n].copy_(do)
+            # centroids of the mesh (T_n, p_n) (reading L46)
+            ctx.tm_point_addition(bufs.tri, nt, x, y, k, x2[n:], y2[n:])
+            n += k
+            ctx.tm_set_n_total(n)
+            bufs = IterBuffers.alloc(n, ctx.params.adj_stride, device=x.device)
+            x, y, dp = x2, y2, d2
+        else:
+            x, y, dp = xo, yo, do
+    return MeshResult(x, y, tri_last, it, hist)

@@ -31,6 +31,8 @@ extern "C" void tm_params_default(tm_params *p) {
     p->projection = 0;         // L22 (north_star "gradient projection"); 1 = the paper's Fig. 13
     p->trace_max = 64;         // L39
     p->fac_retria = 0.1;
+    p->validity = 0;           // L10 (north_star Test 1); 1 = the paper's Tests 1-3 (NEXT-2)
+    p->t_circ = 0.4;
 }
 
 extern "C" tm_status tm_create(int device, void *cuda_stream, const tm_params *p, tm_ctx **out) {
@@ -287,6 +289,9 @@ extern "C" tm_status tm_set_domain(tm_ctx *ctx, const tm_fields *f, int64_t n_to
         ctx->lip_mu = has_mu ? L[0] : 0.0;
         ctx->lip_phi = L[1];
     }
+    ctx->dom_sums[0] = h3[0];
+    ctx->dom_sums[1] = h3[1];
+    ctx->dom_sums[2] = h3[2];
     ctx->c = sqrt(cdiv(cmul(h3[0], cmul(g.dx, g.dy)), (double)n_total));
     ctx->h_avg = cmul(ctx->c, cdiv(h3[1], h3[2]));
     if (!has_mu) { cudaFree(ctx->mu); ctx->mu = nullptr; ctx->grid_bytes = 0; }
@@ -300,17 +305,7 @@ extern "C" tm_status tm_set_domain(tm_ctx *ctx, const tm_fields *f, int64_t n_to
         k_pack_corners<<<(unsigned)((ncell + 255) / 256), 256, 0, ctx->stream>>>(g, ctx->rho, ctx->rho4);
         TM_CUDA_TRY(ctx, cudaGetLastError());
     }
-    ctx->n_total = n_total;
-    // level-0 bins: N_opt points per bin on average (P:343 without fac_grid; Listing P:651-654)
-    double Lx = f->x1 - f->x0, Ly = f->y1 - f->y0;
-    double lam = sqrt((double)n_total / (ctx->p.n_opt * Lx * Ly));
-    int32_t nbx = (int32_t)ceil(lam * Lx), nby = (int32_t)ceil(lam * Ly);
-    if (nbx < 1) nbx = 1;
-    if (nby < 1) nby = 1;
-    ctx->bg.nbx = nbx; ctx->bg.nby = nby;
-    ctx->bg.x0 = f->x0; ctx->bg.y0 = f->y0;
-    ctx->bg.sx = Lx / nbx; ctx->bg.sy = Ly / nby;
-    ctx->bg.isx = nbx / Lx; ctx->bg.isy = nby / Ly;
+    tm_internal_set_n_total(ctx, n_total);
     ctx->have_domain = true;
     ctx->nbr_n = -1;
     ctx->have_bins = false;
@@ -318,6 +313,29 @@ extern "C" tm_status tm_set_domain(tm_ctx *ctx, const tm_fields *f, int64_t n_to
     if (c_out) *c_out = ctx->c;
     if (h_avg_out) *h_avg_out = ctx->h_avg;
     return TM_OK;
+}
+
+// c = sqrt( sum_w * (dx*dy) / N ), h_avg = c * (sum_mu / count) for N = n_total, and the level-0
+// bins for N points: N_opt points per bin on average (P:343 without fac_grid; Listing P:651-654).
+// Point addition (NEXT-3) calls it with N_current: the adaptive quantities follow the resolution
+// (reading L44: recomputed for N_current = scaled by sqrt(N_old / N_current) up to rounding)
+void tm_internal_set_n_total(tm_ctx *ctx, int64_t n_total) {
+    const Grid &g = ctx->grid;
+    ctx->c = sqrt(cdiv(cmul(ctx->dom_sums[0], cmul(g.dx, g.dy)), (double)n_total));
+    ctx->h_avg = cmul(ctx->c, cdiv(ctx->dom_sums[1], ctx->dom_sums[2]));
+    ctx->n_total = n_total;
+    double Lx = g.x1 - g.x0, Ly = g.y1 - g.y0;
+    double lam = sqrt((double)n_total / (ctx->p.n_opt * Lx * Ly));
+    int32_t nbx = (int32_t)ceil(lam * Lx), nby = (int32_t)ceil(lam * Ly);
+    if (nbx < 1) nbx = 1;
+    if (nby < 1) nby = 1;
+    ctx->bg.nbx = nbx; ctx->bg.nby = nby;
+    ctx->bg.x0 = g.x0; ctx->bg.y0 = g.y0;
+    ctx->bg.sx = Lx / nbx; ctx->bg.sy = Ly / nby;
+    ctx->bg.isx = nbx / Lx; ctx->bg.isy = nby / Ly;
+    ctx->nbr_n = -1;  // warm-start lists are keyed by a point set of the old size
+    ctx->have_bins = false;
+    ctx->have_cells = false;
 }
 
 // ============================================================================ S1
@@ -659,6 +677,7 @@ tm_status tm_internal_fill_cell_args(tm_ctx *ctx, CellArgs *a) {
     a->fac_voro = ctx->p.fac_voro_bound; a->fac_pt = ctx->p.fac_pt_mvmt;
     a->fac_geps = ctx->p.fac_geps; a->fac_end = ctx->p.fac_end_mvmt;
     a->damping = ctx->p.newton_damping; a->keep_tol = ctx->p.keep_tol;
+    a->validity = ctx->p.validity; a->t_circ = ctx->p.t_circ;
     a->newton_max = ctx->p.newton_max; a->quad_max = ctx->p.quad_max_level;
     a->projection = ctx->p.projection; a->trace_max = ctx->p.trace_max;
     a->adj_stride = ctx->p.adj_stride;

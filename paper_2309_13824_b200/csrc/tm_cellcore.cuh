@@ -54,20 +54,49 @@ __device__ __forceinline__ bool in_oct(double cx, double cy, double qx, double q
     return fabs(dx) < r && fabs(dy) < r && fabs(cadd(dx, dy)) < r2 && fabs(csub(dx, dy)) < r2;
 }
 
-static __device__ bool keep_tri(const CellArgs &A, int su, int sv, int sw, double cx, double cy) {
-    // su,sv,sw: slots ordered by gid (u smallest); (cx,cy) canonical circumcentre (rel. p_u, made absolute)
-    if (!(cx > A.grid.x0 && cx < A.grid.x1 && cy > A.grid.y0 && cy < A.grid.y1)) return false;
+// geps(x) = fac_geps * min(h(x), h_avg), h(x) = c mu~(x)   (reading L20 evaluated at x)
+static __device__ __forceinline__ double geps_at(const CellArgs &A, double x, double y) {
+    const double h = A.mu ? cmul(A.c, bilinear(A.grid, A.mu, x, y, LdgLoad())) : A.c;
+    return cmul(A.fac_geps, h < A.h_avg ? h : A.h_avg);
+}
+
+// NEXT-2: the paper's validity tests (reading L43) after the bounded-cell conditions:
+// Test 1 discards iff phi~(g) > geps(g); Test 2 keeps iff >= 2 edge midpoints have phi~(m) <=
+// geps(m); Test 3 keeps iff |phi~(c)| / R_circ <= t_circ.  Same operations as the oracle.
+static __device__ __noinline__ bool validity_tests(const CellArgs &A, const double X[3], const double Y[3], double gx,
+                                            double gy, double ox, double oy, double cx, double cy) {
+    if (bilinear(A.grid, A.phi, gx, gy, LdgLoad()) > geps_at(A, gx, gy)) return false;  // Test 1
+    int count = 0;
+#pragma unroll
+    for (int k = 0; k < 3; k++) {  // Test 2: edges (u,v), (v,w), (w,u)
+        const int b = k == 2 ? 0 : k + 1;
+        const double mx = cmul(cadd(X[k], X[b]), 0.5), my = cmul(cadd(Y[k], Y[b]), 0.5);
+        count += bilinear(A.grid, A.phi, mx, my, LdgLoad()) <= geps_at(A, mx, my) ? 1 : 0;
+    }
+    if (count >= 2) return true;
+    const double R = sqrt(cadd(cmul(ox, ox), cmul(oy, oy)));  // Test 3
+    return !(cdiv(fabs(bilinear(A.grid, A.phi, cx, cy, LdgLoad())), R) > A.t_circ);
+}
+
+// su,sv,sw: slots ordered by gid (u smallest); (ox,oy): canonical circumcentre relative to p_u
+static __device__ bool keep_tri(const CellArgs &A, int su, int sv, int sw, double ox, double oy) {
     const int s3[3] = {su, sv, sw};
     double X[3], Y[3];
 #pragma unroll
     for (int k = 0; k < 3; k++) {
         X[k] = __ldg(A.xs + s3[k]);
         Y[k] = __ldg(A.ys + s3[k]);
+    }
+    const double cx = cadd(X[0], ox), cy = cadd(Y[0], oy);
+    if (!(cx > A.grid.x0 && cx < A.grid.x1 && cy > A.grid.y0 && cy < A.grid.y1)) return false;
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
         double r = cmul(cmul(A.fac_voro, __ldg(A.hs + s3[k])), COS_PI8);
         if (!in_oct(cx, cy, X[k], Y[k], r)) return false;
     }
     double gx = cdiv(cadd(cadd(X[0], X[1]), X[2]), 3.0);
     double gy = cdiv(cadd(cadd(Y[0], Y[1]), Y[2]), 3.0);
+    if (A.validity) return validity_tests(A, X, Y, gx, gy, ox, oy, cx, cy);
     return bilinear(A.grid, A.phi, gx, gy, LdgLoad()) < A.keep_tol;
 }
 

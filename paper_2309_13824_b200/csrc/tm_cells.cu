@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(BLOCK, (G == 16 ? TM_MINB : 1)) k_cells(CellAr
                         owned = gi < ga && gi < gb;
                         if (owned) {
                             const int sv = ga < gb ? v.la : v.lb, sw = ga < gb ? v.lb : v.la;
-                            kept = keep_tri(A, (int)cell, sv, sw, cadd(px, v.vx), cadd(py, v.vy));
+                            kept = keep_tri(A, (int)cell, sv, sw, v.vx, v.vy);
                         } else if (MODE & M_ELL) {
                             // canonical circumcentre relative to the smallest-id vertex
                             int s3[3] = {(int)cell, v.la, v.lb};
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(BLOCK, (G == 16 ? TM_MINB : 1)) k_cells(CellAr
                             const Line B2 = bisector(csub(__ldg(A.xs + s3[2]), uxx), csub(__ldg(A.ys + s3[2]), uyy));
                             double ox, oy;
                             cramer(B1, B2, ox, oy);
-                            kept = keep_tri(A, s3[0], s3[1], s3[2], cadd(uxx, ox), cadd(uyy, oy));
+                            kept = keep_tri(A, s3[0], s3[1], s3[2], ox, oy);
                         }
                     }
                     if (MODE & M_TRI) {

@@ -438,6 +438,8 @@ __device__ __forceinline__ bool interior_keeps_all_R(const CellArgs &A, double p
     const double hmin = (h - A.c * A.lip_mu * 2.0 * R) * (1.0 - 1e-9);
     if (!(R < A.fac_voro * hmin * COS_PI8 * (1.0 - 1e-9))) return false;
     const double ph = bilinear(g, A.phi, px, py, LdgLoad());
+    // validity 1 (Tests 1-3): every midpoint (within 2R of p_i) and centroid inside keeps the triangle
+    if (A.validity) return ph + A.lip_phi * 2.0 * R * (1.0 + 1e-6) + 1e-12 * (1.0 + fabs(ph)) < 0.0;
     return ph + A.lip_phi * (4.0 / 3.0) * R * (1.0 + 1e-6) + 1e-12 * (1.0 + fabs(ph)) < A.keep_tol;
 }
 
@@ -964,7 +966,7 @@ __global__ void __launch_bounds__(TB, (MODE & M_WCERT) ? TM_WMINB : TM_TMINB) k_
                     if (gi < ga && gi < gb) keptmask |= 1u << k;
                 } else if (gi < ga && gi < gb) {
                     const int sv = ga < gb ? a : b, sw = ga < gb ? b : a;
-                    if (keep_tri(A, (int)cell, sv, sw, cadd(px, P.v[k * TB].x), cadd(py, P.v[k * TB].y))) {
+                    if (keep_tri(A, (int)cell, sv, sw, P.v[k * TB].x, P.v[k * TB].y)) {
                         keptmask |= 1u << k;
                         keptall |= 1u << k;
                     }
@@ -982,7 +984,7 @@ __global__ void __launch_bounds__(TB, (MODE & M_WCERT) ? TM_WMINB : TM_TMINB) k_
                     const Line B2 = bisector(csub(__ldg(A.xs + s3[2]), uxx), csub(__ldg(A.ys + s3[2]), uyy));
                     double ox, oy;
                     cramer(B1, B2, ox, oy);
-                    if (keep_tri(A, s3[0], s3[1], s3[2], cadd(uxx, ox), cadd(uyy, oy))) keptall |= 1u << k;
+                    if (keep_tri(A, s3[0], s3[1], s3[2], ox, oy)) keptall |= 1u << k;
                 }
             }
             k = kn;
@@ -1278,7 +1280,7 @@ __global__ void __launch_bounds__(128, TM_OUT_MINB) k_output_t(CellArgs A, RingB
                 } else if (gi < ga && gi < gb) {
                     const int sv = ga < gb ? a : b, sw = ga < gb ? b : a;
                     const double2 v = RV(i);
-                    if (keep_tri(A, (int)cell, sv, sw, cadd(px, v.x), cadd(py, v.y))) {
+                    if (keep_tri(A, (int)cell, sv, sw, v.x, v.y)) {
                         keptmask |= 1u << i;
                         keptall |= 1u << i;
                     }
@@ -1296,7 +1298,7 @@ __global__ void __launch_bounds__(128, TM_OUT_MINB) k_output_t(CellArgs A, RingB
                     const Line B2 = bisector(csub(__ldg(A.xs + s3[2]), uxx), csub(__ldg(A.ys + s3[2]), uyy));
                     double ox, oy;
                     cramer(B1, B2, ox, oy);
-                    if (keep_tri(A, s3[0], s3[1], s3[2], cadd(uxx, ox), cadd(uyy, oy))) keptall |= 1u << i;
+                    if (keep_tri(A, s3[0], s3[1], s3[2], ox, oy)) keptall |= 1u << i;
                 }
             }
         }

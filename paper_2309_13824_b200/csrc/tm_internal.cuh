@@ -90,6 +90,8 @@ struct CellArgs {
     double fac_voro, fac_pt, fac_geps, fac_end, damping, keep_tol;
     int32_t newton_max, quad_max;
     int32_t projection, trace_max;  // treatment scheme (NEXT-1), see treat_point
+    int32_t validity;               // keep rule: 0 Test 1 (L10), 1 the paper's Tests 1-3 (NEXT-2)
+    double t_circ;
     // outputs
     int32_t *tri;
     int64_t tri_cap;
@@ -115,6 +117,7 @@ struct tm_ctx {
     bool have_domain = false;
     tmg::Grid grid;
     double c = 0, h_avg = 0;
+    double dom_sums[3] = {0, 0, 0};  // S0 sums: sum mu~^-2, sum mu~, count over the inside cells
     double lip_mu = 0;  // Lipschitz constant of mu~ (0 for uniform sizing): adaptive halo widths
     double lip_phi = 0; // Lipschitz constant of phi~ (keep-rule fast path)
     int64_t n_total = 0;
@@ -194,6 +197,7 @@ __device__ __forceinline__ int64_t live_owned(const tmg::CellArgs &A) { return A
 // internal helpers implemented in tm_api.cu
 tm_status tm_internal_fill_cell_args(tm_ctx *ctx, tmg::CellArgs *a);
 tm_status tm_internal_check_launch(tm_ctx *ctx, const char *what);
+void tm_internal_set_n_total(tm_ctx *ctx, int64_t n_total);
 
 namespace tmg {
 
