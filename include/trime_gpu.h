@@ -347,6 +347,43 @@ void tm_control_init(tm_control *c, int64_t n_total, int64_t n_current, int32_t 
 /* returns TM_ACT_*; *n_add (host, may be NULL) receives the points to add for TM_ACT_ADD */
 int32_t tm_control_update(tm_control *c, const tm_stats *s, int64_t move_count, int64_t *n_add);
 
+/* ---- NEXT-4: the set-up pipeline ---------------------------------------------- */
+/* Geometry grid size: lambda = sqrt(N_total / (N_opt A)), n = ceil(lambda L),
+ * n_geo = fac_grid * n per axis (N_total = 5000 on the unit square, N_opt = 3.3,
+ * fac_grid = 5 -> 195 x 195).  Host arithmetic. */
+void tm_geometry_grid_dims(int64_t n_total, double n_opt, int32_t fac_grid, double x0, double y0, double x1,
+                           double y1, int32_t *nx, int32_t *ny);
+/* Geometry grid cell categories over the domain box of tm_set_domain, nxg x nyg cells:
+ * cat[j*nxg+i] (device int8) = 1 (boundary) iff |phi~(m)| <= l_diag (m the midpoint, l_diag the
+ * cell diagonal), else 0 (inner) iff phi~(m) < 0, else 2 (outer).  Asynchronous. */
+tm_status tm_geometry_categories(tm_ctx *ctx, int32_t nxg, int32_t nyg, int8_t *cat);
+/* Contour SDF: segs (device, n_seg x {x1, y1, x2, y2}) a closed loop in clockwise
+ * order (segment k ends where k+1 starts; the last closes on the first).  phi (device, [ny][nx]
+ * at the nodes x0 + i (x1-x0)/(nx-1), y likewise) = the distance to the closest segment point p*
+ * (found by the outward layer search in a segment grid of ~mean-segment-length cells),
+ * negative iff (p - p*).n > 0 for the inward normal n (right-hand normal of the clockwise
+ * direction, averaged over both segments at a shared endpoint); ties of the distance:
+ * the smallest segment index (reading L48).  synchronises */
+tm_status tm_contour_sdf(tm_ctx *ctx, const double *segs, int64_t n_seg, int32_t nx, int32_t ny, double x0,
+                         double y0, double x1, double y1, double *phi);
+/* SDF set operations, elementwise on device arrays: op 0 union min(a,b),
+ * 1 difference max(a,-b), 2 intersection max(a,b).  Asynchronous. */
+tm_status tm_sdf_combine(tm_ctx *ctx, int32_t op, const double *a, const double *b, int64_t n, double *out);
+/* Point initialisation (reading L47).  cat: the categories of tm_geometry_categories.
+ * Valid cells: inner, and boundary cells with phi~(m) <= eta min(dx, dy) (eta 0.5).
+ * Expected counts n_E = rho_norm * n_init with rho = rho~(m) (1 without rho) normalised over the
+ * valid cells; Floyd-Steinberg dithering over the valid cells, rows from the top (largest y),
+ * each left to right: count = max(0, floor(v + 1/2)) of v = n_E + received residual, the residual
+ * spread equally over the valid not-yet-visited neighbours among right, below-left, below,
+ * below-right (serial by construction: host code).  counts (device int32 [nyg][nxg]) receives the
+ * counts and *n_out (host) their total.  Then, if x, y are given and cap >= total, point k (loop
+ * order of cells, then within the cell) is cell-uniform from the counter-based generator
+ * splitmix64(seed + (2k + comp + 1) * 0x9E3779B97F4A7C15) >> 11 * 2^-53 (comp 0: x, 1: y) and, if
+ * phi~ > geps there, projected onto the boundary by the treatment's 2x2 damped Newton.
+ * TM_E_CAPACITY if cap is too small (*n_out tells the size).  synchronises */
+tm_status tm_init_points(tm_ctx *ctx, int32_t nxg, int32_t nyg, const int8_t *cat, double n_init, double eta,
+                         uint64_t seed, int32_t *counts, double *x, double *y, int64_t cap, int64_t *n_out);
+
 typedef struct tm_graph tm_graph;
 tm_status tm_graph_begin(tm_ctx *ctx);
 tm_status tm_graph_end(tm_ctx *ctx, tm_graph **out);

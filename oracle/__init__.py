@@ -142,6 +142,24 @@ def lib():
         L.or_point_addition.argtypes = [ctypes.POINTER(Fields), ctypes.c_double, ctypes.c_int64, ctypes.c_void_p,
                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
                                         ctypes.c_void_p, D]
+        I32P = ctypes.POINTER(ctypes.c_int32)
+        L.or_geometry_grid_dims.restype = None
+        L.or_geometry_grid_dims.argtypes = [ctypes.c_int64, ctypes.c_double, ctypes.c_int32, ctypes.c_double,
+                                            ctypes.c_double, ctypes.c_double, ctypes.c_double, I32P, I32P]
+        L.or_geometry_categories.restype = None
+        L.or_geometry_categories.argtypes = [ctypes.POINTER(Fields), ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p]
+        L.or_contour_sdf_point.restype = ctypes.c_double
+        L.or_contour_sdf_point.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_double]
+        L.or_contour_sdf.restype = None
+        L.or_contour_sdf.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
+                                     ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_void_p]
+        L.or_init_counts.restype = ctypes.c_int64
+        L.or_init_counts.argtypes = [ctypes.POINTER(Fields), ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p,
+                                     ctypes.c_double, ctypes.c_double, ctypes.c_void_p]
+        L.or_init_points.restype = ctypes.c_int64
+        L.or_init_points.argtypes = [ctypes.POINTER(Fields), ctypes.POINTER(Params), ctypes.c_double, ctypes.c_double,
+                                     ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_uint64,
+                                     ctypes.c_void_p, ctypes.c_void_p]
         _lib = L
     return _lib
 
@@ -474,3 +492,52 @@ def quality_of(st):
     """(1/2-mean alpha, 1/2-mean beta, max alpha) from stats() (Eq. 1/2-mean)."""
     n = st[0]
     return (st[1] / n) ** 2, (st[2] / n) ** 2, st[3]
+
+
+# ---------------------------------------------------------------- NEXT-4
+def geometry_grid_dims(n_total, box, n_opt=3.3, fac_grid=5):
+    """P:338-346."""
+    nx, ny = ctypes.c_int32(), ctypes.c_int32()
+    lib().or_geometry_grid_dims(int(n_total), float(n_opt), int(fac_grid), box[0], box[1], box[2], box[3],
+                                ctypes.byref(nx), ctypes.byref(ny))
+    return nx.value, ny.value
+
+
+def geometry_categories(fs: FieldSet, nxg, nyg):
+    """[nyg, nxg] int8, 0 inner / 1 boundary / 2 outer."""
+    cat = np.empty(nxg * nyg, dtype=np.int8)
+    lib().or_geometry_categories(ctypes.byref(fs.c), int(nxg), int(nyg), _p(cat))
+    return cat.reshape(nyg, nxg)
+
+
+def contour_sdf(segs, nx, ny, box):
+    """SDF of a closed clockwise loop of segments [n, 4] on the (ny, nx) node grid."""
+    s = np.ascontiguousarray(segs, dtype=np.float64)
+    phi = np.empty(nx * ny)
+    lib().or_contour_sdf(_p(s), s.shape[0], int(nx), int(ny), box[0], box[1], box[2], box[3], _p(phi))
+    return phi.reshape(ny, nx)
+
+
+def contour_sdf_point(segs, x, y):
+    s = np.ascontiguousarray(segs, dtype=np.float64)
+    return lib().or_contour_sdf_point(_p(s), s.shape[0], float(x), float(y))
+
+
+def init_counts(fs: FieldSet, cat, n_init, eta=0.5):
+    """P:380-406 Floyd-Steinberg counts [nyg, nxg] and their total."""
+    nyg, nxg = cat.shape
+    c8 = np.ascontiguousarray(cat, dtype=np.int8)
+    cnt = np.empty(nxg * nyg, dtype=np.int32)
+    tot = lib().or_init_counts(ctypes.byref(fs.c), int(nxg), int(nyg), _p(c8), float(n_init), float(eta), _p(cnt))
+    return cnt.reshape(nyg, nxg), int(tot)
+
+
+def init_points(fs: FieldSet, counts, seed, c, h_avg, params=None):
+    params = params or default_params()
+    nyg, nxg = counts.shape
+    cn = np.ascontiguousarray(counts, dtype=np.int32)
+    n = int(cn.sum())
+    x, y = np.empty(n), np.empty(n)
+    lib().or_init_points(ctypes.byref(fs.c), ctypes.byref(params), c, h_avg, int(nxg), int(nyg), _p(cn), int(seed),
+                         _p(x), _p(y))
+    return x, y

@@ -1527,3 +1527,187 @@ int64_t or_point_addition(const or_fields *f, double c, int64_t n_tri, const int
     free(it);
     return n_add;
 }
+
+/* ========================================================================== */
+/* NEXT-4: the set-up pipeline                                   */
+/* ========================================================================== */
+/* Geometry grid size: lambda = sqrt(N/(N_opt A)), n = ceil(lambda L), n_geo = fac n. */
+void or_geometry_grid_dims(int64_t n_total, double n_opt, int32_t fac_grid, double x0, double y0, double x1,
+                           double y1, int32_t *nx, int32_t *ny) {
+    const double lx = x1 - x0, ly = y1 - y0;
+    const double lam = sqrt((double)n_total / (n_opt * (lx * ly)));
+    *nx = fac_grid * (int32_t)ceil(lam * lx);
+    *ny = fac_grid * (int32_t)ceil(lam * ly);
+}
+
+/* Cell categories: m the cell midpoint, l_diag its diagonal; boundary (1) iff
+ * |sdf(m)| <= l_diag, else inner (0) iff sdf(m) < 0, else outer (2).  sdf = phi~ (bilinear). */
+void or_geometry_categories(const or_fields *f, int32_t nxg, int32_t nyg, int8_t *cat) {
+    const double dx = (f->x1 - f->x0) / (double)nxg, dy = (f->y1 - f->y0) / (double)nyg;
+    const double ld = sqrt(dx * dx + dy * dy);
+    for (int32_t j = 0; j < nyg; j++)
+        for (int32_t i = 0; i < nxg; i++) {
+            const double mx = f->x0 + ((double)i + 0.5) * dx, my = f->y0 + ((double)j + 0.5) * dy;
+            const double s = or_field_value(f, f->phi, mx, my);
+            cat[(int64_t)j * nxg + i] = (int8_t)(fabs(s) <= ld ? 1 : (s < 0.0 ? 0 : 2));
+        }
+}
+
+/* Contour SDF by brute force over all segments: |sdf(p)| = min over segments of the
+ * distance to the closest point p* (an endpoint or the foot on the segment, Fig. (c)); the sign
+ * is that of -(p - p*).n with n the inward normal of the clockwise loop (right-hand normal of
+ * the direction), averaged over the two incident segments when p* is a shared endpoint (Fig.
+ * (b)).  Ties of the distance: the smallest segment index.  segs: n_seg x (x1, y1, x2, y2),
+ * consecutive and closed (segment k ends where k+1 starts, the last where the first starts).
+ * phi: [ny][nx] at the nodes x_i = x0 + i (x1 - x0)/(nx - 1). */
+static void seg_closest(const double *s, double px, double py, double *d2, double *t_out) {
+    const double ax = s[0], ay = s[1], bx = s[2], by = s[3];
+    const double ex = bx - ax, ey = by - ay;
+    const double t = ((px - ax) * ex + (py - ay) * ey) / (ex * ex + ey * ey);
+    double qx, qy, tt;
+    if (t <= 0.0) { qx = ax; qy = ay; tt = 0.0; }
+    else if (t >= 1.0) { qx = bx; qy = by; tt = 1.0; }
+    else { qx = ax + t * ex; qy = ay + t * ey; tt = t; }
+    const double dx = px - qx, dy = py - qy;
+    *d2 = dx * dx + dy * dy;
+    *t_out = tt;
+}
+static void seg_normal(const double *s, double *nx, double *ny) {
+    const double ex = s[2] - s[0], ey = s[3] - s[1];
+    const double l = sqrt(ex * ex + ey * ey);
+    *nx = ey / l;
+    *ny = -ex / l;
+}
+double or_contour_sdf_point(const double *segs, int64_t n_seg, double px, double py) {
+    int64_t best = -1;
+    double bd = 0.0, bt = 0.0;
+    for (int64_t k = 0; k < n_seg; k++) {
+        double d2, t;
+        seg_closest(segs + 4 * k, px, py, &d2, &t);
+        if (best < 0 || d2 < bd) { best = k; bd = d2; bt = t; }
+    }
+    const double *s = segs + 4 * best;
+    double nx, ny;
+    seg_normal(s, &nx, &ny);
+    double qx, qy;
+    if (bt == 0.0 || bt == 1.0) {  /* endpoint: average with the incident segment */
+        const int64_t o = bt == 0.0 ? (best + n_seg - 1) % n_seg : (best + 1) % n_seg;
+        double mx, my;
+        seg_normal(segs + 4 * o, &mx, &my);
+        nx = (nx + mx) * 0.5;
+        ny = (ny + my) * 0.5;
+        qx = bt == 0.0 ? s[0] : s[2];
+        qy = bt == 0.0 ? s[1] : s[3];
+    } else {
+        const double ex = s[2] - s[0], ey = s[3] - s[1];
+        qx = s[0] + bt * ex;
+        qy = s[1] + bt * ey;
+    }
+    const double d = sqrt(bd);
+    const double side = (px - qx) * nx + (py - qy) * ny;
+    return side > 0.0 ? -d : d;
+}
+void or_contour_sdf(const double *segs, int64_t n_seg, int32_t nx, int32_t ny, double x0, double y0, double x1,
+                    double y1, double *phi) {
+    for (int32_t j = 0; j < ny; j++)
+        for (int32_t i = 0; i < nx; i++) {
+            const double px = x0 + (double)i * ((x1 - x0) / (double)(nx - 1));
+            const double py = y0 + (double)j * ((y1 - y0) / (double)(ny - 1));
+            phi[(int64_t)j * nx + i] = or_contour_sdf_point(segs, n_seg, px, py);
+        }
+}
+
+/* Point initialisation counts: valid cells = inner cells and the boundary cells whose
+ * midpoint has sdf(m) <= eta min(dx, dy); rho_i = rho~(m) (1 without rho); rho_norm = rho_i /
+ * sum_valid rho (summed in the loop order); n_E = rho_norm N_init.  Floyd-Steinberg (reading L47):
+ * rows from the top (largest y) down, each row left to right; v = n_E + received residual,
+ * count = max(0, floor(v + 1/2)), R = v - count, R / m to each of the m valid not-yet-visited
+ * neighbours among right, below-left, below, below-right.  cat from or_geometry_categories.
+ * counts: [nyg][nxg].  Returns the total. */
+int64_t or_init_counts(const or_fields *f, int32_t nxg, int32_t nyg, const int8_t *cat, double n_init, double eta,
+                       int32_t *counts) {
+    const double dx = (f->x1 - f->x0) / (double)nxg, dy = (f->y1 - f->y0) / (double)nyg;
+    const double band = eta * (dx < dy ? dx : dy);
+    const int64_t nc = (int64_t)nxg * nyg;
+    uint8_t *valid = (uint8_t *)calloc((size_t)nc, 1);
+    double *rho = (double *)calloc((size_t)nc, sizeof(double));
+    double *acc = (double *)calloc((size_t)nc, sizeof(double));
+    double S = 0.0;
+    for (int32_t j = nyg - 1; j >= 0; j--)
+        for (int32_t i = 0; i < nxg; i++) {
+            const int64_t c = (int64_t)j * nxg + i;
+            const double mx = f->x0 + ((double)i + 0.5) * dx, my = f->y0 + ((double)j + 0.5) * dy;
+            int v = cat[c] == 0;
+            if (cat[c] == 1) v = or_field_value(f, f->phi, mx, my) <= band;
+            valid[c] = (uint8_t)v;
+            if (v) {
+                rho[c] = f->rho ? or_field_value(f, f->rho, mx, my) : 1.0;
+                S += rho[c];
+            }
+        }
+    int64_t tot = 0;
+    for (int32_t j = nyg - 1; j >= 0; j--)
+        for (int32_t i = 0; i < nxg; i++) {
+            const int64_t c = (int64_t)j * nxg + i;
+            counts[c] = 0;
+            if (!valid[c]) continue;
+            const double v = (rho[c] / S) * n_init + acc[c];
+            double r = floor(v + 0.5);
+            if (r < 0.0) r = 0.0;
+            counts[c] = (int32_t)r;
+            tot += counts[c];
+            const double R = v - r;
+            const int ni[4] = {i + 1, i - 1, i, i + 1}, nj[4] = {j, j - 1, j - 1, j - 1};
+            int m = 0;
+            for (int q = 0; q < 4; q++)
+                if (ni[q] >= 0 && ni[q] < nxg && nj[q] >= 0 && valid[(int64_t)nj[q] * nxg + ni[q]]) m++;
+            if (m == 0) continue;
+            const double w = R / (double)m;
+            for (int q = 0; q < 4; q++)
+                if (ni[q] >= 0 && ni[q] < nxg && nj[q] >= 0 && valid[(int64_t)nj[q] * nxg + ni[q]])
+                    acc[(int64_t)nj[q] * nxg + ni[q]] += w;
+        }
+    free(valid); free(rho); free(acc);
+    return tot;
+}
+
+/* Counter-based uniform numbers shared by both sides' point generation (reading L47): splitmix64
+ * of seed + (2 k + comp + 1) * 0x9E3779B97F4A7C15, the top 53 bits scaled by 2^-53. */
+static double or_u01(uint64_t seed, uint64_t k, int comp) {
+    uint64_t z = seed + (2u * k + (uint64_t)comp + 1u) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z = z ^ (z >> 31);
+    return (double)(z >> 11) * 1.1102230246251565e-16;
+}
+
+/* The points: counts[c] uniform points in cell c, cells in the loop order of
+ * or_init_counts, point k (global index in that order) at (cx0 + u dx, cy0 + v dy) with
+ * u = or_u01(seed, k, 0), v = or_u01(seed, k, 1).  A point outside the boundary tolerance
+ * (phi~ > geps = fac_geps min(h, h_avg)) is projected onto the boundary by the damped 2x2 Newton
+ * method of the treatment (P:402 -> P:575-605; deps = sqrt(eps) min(h, h_avg)); if that fails it
+ * stays (reading L47).  Returns the number written. */
+int64_t or_init_points(const or_fields *f, const or_params *p, double c, double h_avg, int32_t nxg, int32_t nyg,
+                       const int32_t *counts, uint64_t seed, double *x, double *y) {
+    const double dx = (f->x1 - f->x0) / (double)nxg, dy = (f->y1 - f->y0) / (double)nyg;
+    int64_t k = 0;
+    for (int32_t j = nyg - 1; j >= 0; j--)
+        for (int32_t i = 0; i < nxg; i++) {
+            const int64_t cc = (int64_t)j * nxg + i;
+            const double cx0 = f->x0 + (double)i * dx, cy0 = f->y0 + (double)j * dy;
+            for (int32_t q = 0; q < counts[cc]; q++, k++) {
+                double px = cx0 + or_u01(seed, (uint64_t)k, 0) * dx;
+                double py = cy0 + or_u01(seed, (uint64_t)k, 1) * dy;
+                const double h = h_of(f, c, px, py);
+                const double hm = h < h_avg ? h : h_avg;
+                const double geps = p->fac_geps * hm;
+                if (or_field_value(f, f->phi, px, py) > geps) {
+                    double qx, qy;
+                    if (newton_project(f, p, px, py, geps, 1.4901161193847656e-08 * hm, &qx, &qy)) { px = qx; py = qy; }
+                }
+                x[k] = px;
+                y[k] = py;
+            }
+        }
+    return k;
+}

@@ -148,6 +148,22 @@ int64_t or_move_count(const or_fields *f, const or_params *p, double c, double h
 int64_t or_point_addition(const or_fields *f, double c, int64_t n_tri, const int32_t *tri, const double *x,
                           const double *y, int64_t n_add, double *x_new, double *y_new, double *ratio_out);
 
+/* ---- NEXT-4: set-up pipeline ------------------------------ */
+void or_geometry_grid_dims(int64_t n_total, double n_opt, int32_t fac_grid, double x0, double y0, double x1,
+                           double y1, int32_t *nx, int32_t *ny);
+/* cat[j*nxg+i]: 0 inner, 1 boundary (|phi~(m)| <= l_diag), 2 outer; box = the fields' box */
+void or_geometry_categories(const or_fields *f, int32_t nxg, int32_t nyg, int8_t *cat);
+/* SDF of a closed clockwise segment loop, brute force over the segments */
+double or_contour_sdf_point(const double *segs, int64_t n_seg, double px, double py);
+void or_contour_sdf(const double *segs, int64_t n_seg, int32_t nx, int32_t ny, double x0, double y0, double x1,
+                    double y1, double *phi);
+/* Floyd-Steinberg counts (reading L47); returns the total */
+int64_t or_init_counts(const or_fields *f, int32_t nxg, int32_t nyg, const int8_t *cat, double n_init, double eta,
+                       int32_t *counts);
+/* the initial points of the counts (counter-based generator, projection P:402); returns the count */
+int64_t or_init_points(const or_fields *f, const or_params *p, double c, double h_avg, int32_t nxg, int32_t nyg,
+                       const int32_t *counts, uint64_t seed, double *x, double *y);
+
 #ifdef __cplusplus
 }
 #endif

@@ -95,7 +95,8 @@ EXPORTED = ["tm_params_default", "tm_create", "tm_destroy", "tm_last_error", "tm
             "tm_migrate_pack", "tm_grid_bin_dc", "tm_halo_pack_dc", "tm_migrate_pack_dc", "tm_append_points",
             "tm_graph_begin", "tm_graph_end", "tm_graph_launch", "tm_graph_destroy", "tm_refresh_positions",
             "tm_retria_check", "tm_move_count", "tm_set_n_total", "tm_point_addition", "tm_control_init",
-            "tm_control_update",
+            "tm_control_update", "tm_geometry_grid_dims", "tm_geometry_categories", "tm_contour_sdf",
+            "tm_sdf_combine", "tm_init_points",
             "tm_host_incircle_exact", "tm_host_cramer", "tm_host_bilinear"]
 
 
@@ -128,6 +129,11 @@ def load_library(path: str = LIB_PATH, build_if_missing: bool = True):
         "tm_adjacency_export": (st, [vp, vp, vp, vp, vp]),
         "tm_work_counts": (st, [vp, ctypes.POINTER(tm_work)]),
         "tm_move_count": (st, [vp, vp, vp, vp, i64, vp]),
+        "tm_geometry_grid_dims": (None, [i64, dbl, i32, dbl, dbl, dbl, dbl, ctypes.POINTER(i32), ctypes.POINTER(i32)]),
+        "tm_geometry_categories": (st, [vp, i32, i32, vp]),
+        "tm_contour_sdf": (st, [vp, vp, i64, i32, i32, dbl, dbl, dbl, dbl, vp]),
+        "tm_sdf_combine": (st, [vp, i32, vp, vp, i64, vp]),
+        "tm_init_points": (st, [vp, i32, i32, vp, dbl, dbl, ctypes.c_uint64, vp, vp, vp, i64, ctypes.POINTER(i64)]),
         "tm_set_n_total": (st, [vp, i64, ctypes.POINTER(dbl), ctypes.POINTER(dbl)]),
         "tm_point_addition": (st, [vp, vp, i64, vp, vp, i64, vp, vp, ctypes.POINTER(dbl)]),
         "tm_control_init": (None, [ctypes.POINTER(tm_control), i64, i64, i32]),
@@ -276,6 +282,23 @@ class Context:
         self._check(self.L.tm_point_addition(self.h, _ptr(tri), int(n_tri), _ptr(x), _ptr(y), int(n_add),
                                              _ptr(x_new), _ptr(y_new), ctypes.byref(r)))
         return r.value
+
+    def tm_geometry_categories(self, nxg: int, nyg: int, cat):
+        self._check(self.L.tm_geometry_categories(self.h, int(nxg), int(nyg), _ptr(cat)))
+
+    def tm_contour_sdf(self, segs, nx: int, ny: int, box, phi):
+        self._check(self.L.tm_contour_sdf(self.h, _ptr(segs), int(segs.shape[0]), int(nx), int(ny), box[0], box[1],
+                                          box[2], box[3], _ptr(phi)))
+
+    def tm_sdf_combine(self, op: int, a, b, out):
+        self._check(self.L.tm_sdf_combine(self.h, int(op), _ptr(a), _ptr(b), int(a.numel()), _ptr(out)))
+
+    def tm_init_points(self, nxg: int, nyg: int, cat, n_init: float, eta: float, seed: int, counts, x=None, y=None,
+                       cap: int = 0) -> int:
+        n = ctypes.c_int64()
+        self._check(self.L.tm_init_points(self.h, int(nxg), int(nyg), _ptr(cat), float(n_init), float(eta), int(seed),
+                                          _ptr(counts), _ptr(x), _ptr(y), int(cap), ctypes.byref(n)))
+        return int(n.value)
 
     def tm_adjacency_export(self, adj, deg, adj_out, deg_out):
         self._check(self.L.tm_adjacency_export(self.h, _ptr(adj), _ptr(deg), _ptr(adj_out), _ptr(deg_out)))
@@ -514,3 +537,25 @@ def mesh(ctx: Context, x, y, n_total: Optional[int] = None, method: str = "hybri
         else:
             x, y, dp = xo, yo, do
     return MeshResult(x, y, tri_last, it, hist)
+
+
+# ---------------------------------------------------------------- NEXT-4
+def geometry_grid_dims(n_total: int, box, n_opt: float = 3.3, fac_grid: int = 5):
+    """P:338-346 (host arithmetic of the library)."""
+    nx, ny = ctypes.c_int32(), ctypes.c_int32()
+    load_library().tm_geometry_grid_dims(int(n_total), float(n_opt), int(fac_grid), box[0], box[1], box[2], box[3],
+                                         ctypes.byref(nx), ctypes.byref(ny))
+    return nx.value, ny.value
+
+
+def initial_points(ctx: Context, n_init: int, nxg: int, nyg: int, eta: float = 0.5, seed: int = 0):
+    """geometry-grid categories, Floyd-Steinberg counts and the initial points (device)."""
+    dev = torch.device("cuda", ctx.device)
+    cat = torch.empty(nyg * nxg, dtype=torch.int8, device=dev)
+    ctx.tm_geometry_categories(nxg, nyg, cat)
+    counts = torch.empty(nyg * nxg, dtype=torch.int32, device=dev)
+    n = ctx.tm_init_points(nxg, nyg, cat, n_init, eta, seed, counts)
+    x = torch.empty(n, dtype=torch.float64, device=dev)
+    y = torch.empty_like(x)
+    ctx.tm_init_points(nxg, nyg, cat, n_init, eta, seed, counts, x, y, n)
+    return x, y, cat.view(nyg, nxg), counts.view(nyg, nxg)

@@ -13,7 +13,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libtrime_gpu.so")
-SOURCES = ["tm_api.cu", "tm_cells.cu", "tm_cells_t.cu", "tm_distmesh.cu", "tm_control.cu"]
+SOURCES = ["tm_api.cu", "tm_cells.cu", "tm_cells_t.cu", "tm_distmesh.cu", "tm_control.cu", "tm_setup.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

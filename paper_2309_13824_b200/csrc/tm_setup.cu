@@ -1,0 +1,371 @@
+// tm_setup.cu -- NEXT-4 of SURVEY §8(f): the set-up pipeline before meshing.
+//   * geometry grid size and cell categories (§3.2);
+//   * contour SDF from a closed clockwise loop of line segments with a segment grid and the
+//     outward layer search (§3.1), and the SDF set operations;
+//   * point initialisation by Floyd-Steinberg dithering of the expected counts (§3.5)
+//     and the projection of outside initial points.
+// Readings L47-L48.  Every floating decision uses the canonical uncontracted
+// operations (cadd/cmul/..., L25), the same operations in the same order as the oracle.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "tm_internal.cuh"
+
+using namespace tmg;
+
+namespace {
+
+struct DevBuf {
+    void *p = nullptr;
+    ~DevBuf() { cudaFree(p); }
+};
+
+// geometry grid cell categories: 1 boundary iff |phi~(m)| <= l_diag, else 0 inner iff phi~(m) < 0,
+// else 2 outer
+__global__ void k_geo_categories(Grid g, const double *__restrict__ phi, int32_t nxg, int32_t nyg, double dx,
+                                 double dy, double ld, int8_t *__restrict__ cat) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= (int64_t)nxg * nyg) return;
+    const int32_t i = (int32_t)(c % nxg), j = (int32_t)(c / nxg);
+    const double mx = cadd(g.x0, cmul(cadd((double)i, 0.5), dx)), my = cadd(g.y0, cmul(cadd((double)j, 0.5), dy));
+    const double s = bilinear(g, phi, mx, my, LdgLoad());
+    cat[c] = (int8_t)(fabs(s) <= ld ? 1 : (s < 0.0 ? 0 : 2));
+}
+
+// ---- contour SDF
+__device__ __forceinline__ void seg_closest(const double *s, double px, double py, double &d2, double &t_out) {
+    const double ax = s[0], ay = s[1], bx = s[2], by = s[3];
+    const double ex = csub(bx, ax), ey = csub(by, ay);
+    const double t = cdiv(cadd(cmul(csub(px, ax), ex), cmul(csub(py, ay), ey)), cadd(cmul(ex, ex), cmul(ey, ey)));
+    double qx, qy, tt;
+    if (t <= 0.0) { qx = ax; qy = ay; tt = 0.0; }
+    else if (t >= 1.0) { qx = bx; qy = by; tt = 1.0; }
+    else { qx = cadd(ax, cmul(t, ex)); qy = cadd(ay, cmul(t, ey)); tt = t; }
+    const double dx = csub(px, qx), dy = csub(py, qy);
+    d2 = cadd(cmul(dx, dx), cmul(dy, dy));
+    t_out = tt;
+}
+
+__device__ __forceinline__ void seg_normal(const double *s, double &nx, double &ny) {
+    const double ex = csub(s[2], s[0]), ey = csub(s[3], s[1]);
+    const double l = sqrt(cadd(cmul(ex, ex), cmul(ey, ey)));
+    nx = cdiv(ey, l);
+    ny = cdiv(-ex, l);
+}
+
+struct SegGrid {
+    int32_t nx, ny;
+    double x0, y0, dx, dy, dmin;  // cell size, min(dx, dy)
+    const int32_t *start, *ids;   // CSR: segments whose bounding box meets the cell
+};
+
+// |sdf| by the outward layer search: layers of cells at Chebyshev distance l around
+// the node's cell until no segment in a further layer can be closer (lower bound (l-1) dmin,
+// strictly: tied segments are still examined); sign from the inward normal, ties by the
+// smallest segment index
+__global__ void k_contour_sdf(const double *__restrict__ segs, int64_t n_seg, SegGrid G, int32_t nx, int32_t ny,
+                              double x0, double y0, double x1, double y1, double *__restrict__ phi) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= (int64_t)nx * ny) return;
+    const int32_t i = (int32_t)(c % nx), j = (int32_t)(c / nx);
+    const double px = cadd(x0, cmul((double)i, cdiv(csub(x1, x0), (double)(nx - 1))));
+    const double py = cadd(y0, cmul((double)j, cdiv(csub(y1, y0), (double)(ny - 1))));
+    int ci = (int)floor((px - G.x0) / G.dx), cj = (int)floor((py - G.y0) / G.dy);
+    ci = ci < 0 ? 0 : (ci >= G.nx ? G.nx - 1 : ci);
+    cj = cj < 0 ? 0 : (cj >= G.ny ? G.ny - 1 : cj);
+    int64_t best = -1;
+    double bd = 0.0, bt = 0.0;
+    const int lmax = max(max(ci, G.nx - 1 - ci), max(cj, G.ny - 1 - cj));
+    for (int l = 0; l <= lmax; l++) {
+        if (best >= 0 && l >= 1) {
+            const double lb = (double)(l - 1) * G.dmin * (1.0 - 1e-12);
+            if (lb * lb > bd) break;
+        }
+        for (int b = cj - l; b <= cj + l; b++) {
+            if (b < 0 || b >= G.ny) continue;
+            const bool edge_row = b == cj - l || b == cj + l;
+            for (int a = ci - l; a <= ci + l; a += edge_row ? 1 : 2 * l) {
+                if (a >= 0 && a < G.nx) {
+                    const int64_t cc = (int64_t)b * G.nx + a;
+                    for (int32_t q = G.start[cc]; q < G.start[cc + 1]; q++) {
+                        const int32_t k = G.ids[q];
+                        double d2, t;
+                        seg_closest(segs + 4 * (int64_t)k, px, py, d2, t);
+                        if (best < 0 || d2 < bd || (d2 == bd && k < best)) { best = k; bd = d2; bt = t; }
+                    }
+                }
+                if (l == 0) break;
+            }
+        }
+    }
+    if (best < 0) {  // no segment at all
+        phi[c] = 0.0;
+        return;
+    }
+    const double *s = segs + 4 * best;
+    double nxv, nyv;
+    seg_normal(s, nxv, nyv);
+    double qx, qy;
+    if (bt == 0.0 || bt == 1.0) {
+        const int64_t o = bt == 0.0 ? (best + n_seg - 1) % n_seg : (best + 1) % n_seg;
+        double mx, my;
+        seg_normal(segs + 4 * o, mx, my);
+        nxv = cmul(cadd(nxv, mx), 0.5);
+        nyv = cmul(cadd(nyv, my), 0.5);
+        qx = bt == 0.0 ? s[0] : s[2];
+        qy = bt == 0.0 ? s[1] : s[3];
+    } else {
+        qx = cadd(s[0], cmul(bt, csub(s[2], s[0])));
+        qy = cadd(s[1], cmul(bt, csub(s[3], s[1])));
+    }
+    const double d = sqrt(bd);
+    const double side = cadd(cmul(csub(px, qx), nxv), cmul(csub(py, qy), nyv));
+    phi[c] = side > 0.0 ? -d : d;
+}
+
+__global__ void k_sdf_combine(int op, const double *__restrict__ a, const double *__restrict__ b, int64_t n,
+                              double *__restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double u = a[i], v = b[i];
+    out[i] = op == 0 ? fmin(u, v) : (op == 1 ? fmax(u, -v) : fmax(u, v));
+}
+
+// ---- point initialisation
+__global__ void k_cell_rho(Grid g, const double *__restrict__ phi, const double *__restrict__ rho, int32_t nxg,
+                           int32_t nyg, double dx, double dy, double *__restrict__ out_phi, double *__restrict__ out_rho) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= (int64_t)nxg * nyg) return;
+    const int32_t i = (int32_t)(c % nxg), j = (int32_t)(c / nxg);
+    const double mx = cadd(g.x0, cmul(cadd((double)i, 0.5), dx)), my = cadd(g.y0, cmul(cadd((double)j, 0.5), dy));
+    out_phi[c] = bilinear(g, phi, mx, my, LdgLoad());
+    out_rho[c] = rho ? bilinear(g, rho, mx, my, LdgLoad()) : 1.0;
+}
+
+__device__ __forceinline__ double u01(uint64_t seed, uint64_t k, int comp) {
+    uint64_t z = seed + (2u * k + (uint64_t)comp + 1u) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z = z ^ (z >> 31);
+    return cmul((double)(z >> 11), 1.1102230246251565e-16);
+}
+
+// point k of the loop order: its cell by binary search over the exclusive prefix of the counts
+// (cells in the loop order), then the cell-uniform position and, outside the tolerance, the
+// projection onto the boundary (the treatment's 2x2 damped Newton, P:402 -> P:575-605)
+__global__ void k_init_points(int64_t n_pts, const int64_t *__restrict__ off, int64_t n_cells,
+                              const int32_t *__restrict__ cell_of_rank, Grid g, const double *__restrict__ phi,
+                              const double *__restrict__ mu, double c, double h_avg, double fac_geps, double damping,
+                              int newton_max, int32_t nxg, double dx, double dy, uint64_t seed,
+                              double *__restrict__ x, double *__restrict__ y) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n_pts) return;
+    int64_t lo = 0, hi = n_cells - 1;  // last rank r with off[r] <= k
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (off[mid] <= k) lo = mid; else hi = mid - 1;
+    }
+    const int32_t cc = cell_of_rank[lo];
+    const int32_t i = cc % nxg, j = cc / nxg;
+    const double cx0 = cadd(g.x0, cmul((double)i, dx)), cy0 = cadd(g.y0, cmul((double)j, dy));
+    double px = cadd(cx0, cmul(u01(seed, (uint64_t)k, 0), dx));
+    double py = cadd(cy0, cmul(u01(seed, (uint64_t)k, 1), dy));
+    const double h = mu ? cmul(c, bilinear(g, mu, px, py, LdgLoad())) : c;
+    const double hm = h < h_avg ? h : h_avg;
+    const double geps = cmul(fac_geps, hm);
+    if (bilinear(g, phi, px, py, LdgLoad()) > geps) {
+        double qx, qy;
+        if (newton_project(g, phi, px, py, geps, cmul(1.4901161193847656e-08, hm), damping, newton_max, qx, qy,
+                           LdgLoad())) {
+            px = qx;
+            py = qy;
+        }
+    }
+    x[k] = px;
+    y[k] = py;
+}
+
+}  // namespace
+
+extern "C" void tm_geometry_grid_dims(int64_t n_total, double n_opt, int32_t fac_grid, double x0, double y0,
+                                      double x1, double y1, int32_t *nx, int32_t *ny) {
+    const double lx = x1 - x0, ly = y1 - y0;
+    const double lam = sqrt((double)n_total / (n_opt * (lx * ly)));
+    *nx = fac_grid * (int32_t)ceil(lam * lx);
+    *ny = fac_grid * (int32_t)ceil(lam * ly);
+}
+
+extern "C" tm_status tm_geometry_categories(tm_ctx *ctx, int32_t nxg, int32_t nyg, int8_t *cat) {
+    if (!ctx) return TM_E_ARG;
+    if (!ctx->have_domain) TM_FAIL(ctx, TM_E_STATE, "tm_geometry_categories before tm_set_domain");
+    if (nxg < 1 || nyg < 1 || !cat) TM_FAIL(ctx, TM_E_ARG, "bad geometry grid %dx%d", nxg, nyg);
+    const Grid &g = ctx->grid;
+    const double dx = cdiv(csub(g.x1, g.x0), (double)nxg), dy = cdiv(csub(g.y1, g.y0), (double)nyg);
+    const double ld = sqrt(cadd(cmul(dx, dx), cmul(dy, dy)));
+    const int64_t n = (int64_t)nxg * nyg;
+    k_geo_categories<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(g, ctx->phi, nxg, nyg, dx, dy, ld, cat);
+    return tm_internal_check_launch(ctx, "k_geo_categories");
+}
+
+extern "C" tm_status tm_contour_sdf(tm_ctx *ctx, const double *segs, int64_t n_seg, int32_t nx, int32_t ny, double x0,
+                                    double y0, double x1, double y1, double *phi) {
+    if (!ctx) return TM_E_ARG;
+    if (ctx->capturing) TM_FAIL(ctx, TM_E_STATE, "tm_contour_sdf while capturing a graph");
+    if (!segs || n_seg < 3 || nx < 2 || ny < 2 || !phi || !(x1 > x0) || !(y1 > y0) || n_seg >= (int64_t)INT32_MAX)
+        TM_FAIL(ctx, TM_E_ARG, "bad arguments to tm_contour_sdf");
+    TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    // segment grid (host; the loop has few segments): n = ceil(L / mean segment length)
+    std::vector<double> hs((size_t)n_seg * 4);
+    TM_CUDA_TRY(ctx, cudaMemcpyAsync(hs.data(), segs, hs.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    TM_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    double bx0 = x0, by0 = y0, bx1 = x1, by1 = y1, lsum = 0.0;
+    for (int64_t k = 0; k < n_seg; k++) {
+        const double *s = &hs[4 * k];
+        bx0 = std::min(bx0, std::min(s[0], s[2])); bx1 = std::max(bx1, std::max(s[0], s[2]));
+        by0 = std::min(by0, std::min(s[1], s[3])); by1 = std::max(by1, std::max(s[1], s[3]));
+        lsum += sqrt((s[2] - s[0]) * (s[2] - s[0]) + (s[3] - s[1]) * (s[3] - s[1]));
+    }
+    const double lbar = lsum / (double)n_seg;
+    if (!(lbar > 0.0)) TM_FAIL(ctx, TM_E_ARG, "degenerate contour");
+    SegGrid G;
+    G.nx = std::max(1, std::min(4096, (int)ceil((bx1 - bx0) / lbar)));
+    G.ny = std::max(1, std::min(4096, (int)ceil((by1 - by0) / lbar)));
+    G.x0 = bx0; G.y0 = by0;
+    G.dx = (bx1 - bx0) / G.nx; G.dy = (by1 - by0) / G.ny;
+    G.dmin = std::min(G.dx, G.dy);
+    const int64_t ncell = (int64_t)G.nx * G.ny;
+    std::vector<int32_t> cnt(ncell + 1, 0);
+    auto cell_range = [&](const double *s, int &a0, int &a1, int &b0, int &b1) {
+        a0 = (int)floor((std::min(s[0], s[2]) - G.x0) / G.dx); a1 = (int)floor((std::max(s[0], s[2]) - G.x0) / G.dx);
+        b0 = (int)floor((std::min(s[1], s[3]) - G.y0) / G.dy); b1 = (int)floor((std::max(s[1], s[3]) - G.y0) / G.dy);
+        a0 = std::max(0, std::min(G.nx - 1, a0 - 1)); a1 = std::max(0, std::min(G.nx - 1, a1 + 1));
+        b0 = std::max(0, std::min(G.ny - 1, b0 - 1)); b1 = std::max(0, std::min(G.ny - 1, b1 + 1));
+    };
+    for (int64_t k = 0; k < n_seg; k++) {
+        int a0, a1, b0, b1;
+        cell_range(&hs[4 * k], a0, a1, b0, b1);
+        for (int b = b0; b <= b1; b++)
+            for (int a = a0; a <= a1; a++) cnt[(int64_t)b * G.nx + a + 1]++;
+    }
+    for (int64_t cc = 0; cc < ncell; cc++) cnt[cc + 1] += cnt[cc];
+    std::vector<int32_t> ids(cnt[ncell]), fill(cnt.begin(), cnt.end() - 1);
+    for (int64_t k = 0; k < n_seg; k++) {
+        int a0, a1, b0, b1;
+        cell_range(&hs[4 * k], a0, a1, b0, b1);
+        for (int b = b0; b <= b1; b++)
+            for (int a = a0; a <= a1; a++) ids[fill[(int64_t)b * G.nx + a]++] = (int32_t)k;
+    }
+    DevBuf dst, dids;
+    TM_CUDA_TRY(ctx, cudaMalloc(&dst.p, cnt.size() * sizeof(int32_t)));
+    TM_CUDA_TRY(ctx, cudaMalloc(&dids.p, std::max<size_t>(1, ids.size()) * sizeof(int32_t)));
+    TM_CUDA_TRY(ctx, cudaMemcpyAsync(dst.p, cnt.data(), cnt.size() * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+    if (!ids.empty())
+        TM_CUDA_TRY(ctx, cudaMemcpyAsync(dids.p, ids.data(), ids.size() * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+    G.start = (const int32_t *)dst.p;
+    G.ids = (const int32_t *)dids.p;
+    const int64_t n = (int64_t)nx * ny;
+    k_contour_sdf<<<(unsigned)((n + 127) / 128), 128, 0, ctx->stream>>>(segs, n_seg, G, nx, ny, x0, y0, x1, y1, phi);
+    tm_status s = tm_internal_check_launch(ctx, "k_contour_sdf");
+    if (s != TM_OK) return s;
+    TM_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));  // the segment grid is freed on return
+    return TM_OK;
+}
+
+extern "C" tm_status tm_sdf_combine(tm_ctx *ctx, int32_t op, const double *a, const double *b, int64_t n, double *out) {
+    if (!ctx) return TM_E_ARG;
+    if (op < 0 || op > 2 || !a || !b || !out || n < 0) TM_FAIL(ctx, TM_E_ARG, "bad arguments to tm_sdf_combine");
+    if (n == 0) return TM_OK;
+    k_sdf_combine<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(op, a, b, n, out);
+    return tm_internal_check_launch(ctx, "k_sdf_combine");
+}
+
+extern "C" tm_status tm_init_points(tm_ctx *ctx, int32_t nxg, int32_t nyg, const int8_t *cat, double n_init,
+                                    double eta, uint64_t seed, int32_t *counts, double *x, double *y, int64_t cap,
+                                    int64_t *n_out) {
+    if (!ctx) return TM_E_ARG;
+    if (!ctx->have_domain) TM_FAIL(ctx, TM_E_STATE, "tm_init_points before tm_set_domain");
+    if (ctx->capturing) TM_FAIL(ctx, TM_E_STATE, "tm_init_points while capturing a graph");
+    if (nxg < 1 || nyg < 1 || !cat || !counts || !n_out || !(n_init >= 0.0) || cap < 0)
+        TM_FAIL(ctx, TM_E_ARG, "bad arguments to tm_init_points");
+    TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    const Grid &g = ctx->grid;
+    const double dx = cdiv(csub(g.x1, g.x0), (double)nxg), dy = cdiv(csub(g.y1, g.y0), (double)nyg);
+    const int64_t nc = (int64_t)nxg * nyg;
+    DevBuf dphi, drho;
+    TM_CUDA_TRY(ctx, cudaMalloc(&dphi.p, nc * sizeof(double)));
+    TM_CUDA_TRY(ctx, cudaMalloc(&drho.p, nc * sizeof(double)));
+    k_cell_rho<<<(unsigned)((nc + 255) / 256), 256, 0, ctx->stream>>>(g, ctx->phi, ctx->rho, nxg, nyg, dx, dy,
+                                                                     (double *)dphi.p, (double *)drho.p);
+    tm_status s = tm_internal_check_launch(ctx, "k_cell_rho");
+    if (s != TM_OK) return s;
+    std::vector<double> hphi(nc), hrho(nc);
+    std::vector<int8_t> hcat(nc);
+    TM_CUDA_TRY(ctx, cudaMemcpyAsync(hphi.data(), dphi.p, nc * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    TM_CUDA_TRY(ctx, cudaMemcpyAsync(hrho.data(), drho.p, nc * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    TM_CUDA_TRY(ctx, cudaMemcpyAsync(hcat.data(), cat, nc, cudaMemcpyDeviceToHost, ctx->stream));
+    TM_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    // Floyd-Steinberg over the valid cells (serial by the method: the residual of a cell is known
+    // only after its predecessors; host code): rows from the top, each left to right (L47)
+    const double band = cmul(eta, dx < dy ? dx : dy);
+    std::vector<uint8_t> valid(nc, 0);
+    double S = 0.0;
+    for (int32_t j = nyg - 1; j >= 0; j--)
+        for (int32_t i = 0; i < nxg; i++) {
+            const int64_t c = (int64_t)j * nxg + i;
+            valid[c] = hcat[c] == 0 || (hcat[c] == 1 && hphi[c] <= band);
+            if (valid[c]) S = cadd(S, hrho[c]);
+        }
+    std::vector<double> acc(nc, 0.0);
+    std::vector<int32_t> hcnt(nc, 0), rank_cell;
+    std::vector<int64_t> off;
+    int64_t tot = 0;
+    for (int32_t j = nyg - 1; j >= 0; j--)
+        for (int32_t i = 0; i < nxg; i++) {
+            const int64_t c = (int64_t)j * nxg + i;
+            if (!valid[c]) continue;
+            const double v = cadd(cmul(cdiv(hrho[c], S), n_init), acc[c]);
+            double r = floor(cadd(v, 0.5));
+            if (r < 0.0) r = 0.0;
+            hcnt[c] = (int32_t)r;
+            if (hcnt[c] > 0) {
+                rank_cell.push_back((int32_t)c);
+                off.push_back(tot);
+            }
+            tot += hcnt[c];
+            const double R = csub(v, r);
+            const int ni[4] = {i + 1, i - 1, i, i + 1}, nj[4] = {j, j - 1, j - 1, j - 1};
+            int m = 0;
+            for (int q = 0; q < 4; q++)
+                if (ni[q] >= 0 && ni[q] < nxg && nj[q] >= 0 && valid[(int64_t)nj[q] * nxg + ni[q]]) m++;
+            if (m == 0) continue;
+            const double w = cdiv(R, (double)m);
+            for (int q = 0; q < 4; q++)
+                if (ni[q] >= 0 && ni[q] < nxg && nj[q] >= 0 && valid[(int64_t)nj[q] * nxg + ni[q]]) {
+                    double &a = acc[(int64_t)nj[q] * nxg + ni[q]];
+                    a = cadd(a, w);
+                }
+        }
+    TM_CUDA_TRY(ctx, cudaMemcpyAsync(counts, hcnt.data(), nc * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+    *n_out = tot;
+    if (tot > cap || !x || !y || tot == 0) {
+        TM_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+        if (x && y && tot > cap) TM_FAIL(ctx, TM_E_CAPACITY, "tm_init_points: %lld points, capacity %lld", (long long)tot,
+                               (long long)cap);
+        return TM_OK;
+    }
+    DevBuf doff, drank;
+    TM_CUDA_TRY(ctx, cudaMalloc(&doff.p, off.size() * sizeof(int64_t)));
+    TM_CUDA_TRY(ctx, cudaMalloc(&drank.p, rank_cell.size() * sizeof(int32_t)));
+    TM_CUDA_TRY(ctx, cudaMemcpyAsync(doff.p, off.data(), off.size() * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+    TM_CUDA_TRY(ctx, cudaMemcpyAsync(drank.p, rank_cell.data(), rank_cell.size() * sizeof(int32_t),
+                                     cudaMemcpyHostToDevice, ctx->stream));
+    k_init_points<<<(unsigned)((tot + 127) / 128), 128, 0, ctx->stream>>>(
+        tot, (const int64_t *)doff.p, (int64_t)off.size(), (const int32_t *)drank.p, g, ctx->phi, ctx->mu, ctx->c,
+        ctx->h_avg, ctx->p.fac_geps, ctx->p.newton_damping, ctx->p.newton_max, nxg, dx, dy, seed, x, y);
+    if ((s = tm_internal_check_launch(ctx, "k_init_points")) != TM_OK) return s;
+    TM_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return TM_OK;
+}
