@@ -384,6 +384,34 @@ tm_status tm_sdf_combine(tm_ctx *ctx, int32_t op, const double *a, const double 
 tm_status tm_init_points(tm_ctx *ctx, int32_t nxg, int32_t nyg, const int8_t *cat, double n_init, double eta,
                          uint64_t seed, int32_t *counts, double *x, double *y, int64_t cap, int64_t *n_out);
 
+/* Automatic sizing (App. A; reading L48).
+ * tm_boundary_points: boundary points of a closed contour (segs as for tm_contour_sdf): every
+ *   segment's start point and, on a segment longer than d_s, the points a + (q/m)(b - a),
+ *   q = 1..m-1, m = floor(len/d_s) + 1; then the serial trimming sweeps of App. A: for each point
+ *   in order, its closest other point whose midpoint with it has |sdf| <= geps_hat is merged into
+ *   the midpoint while closer than d_s; sweeps repeat until nothing changes.  *n_out (host) = the
+ *   count; x, y (device, cap entries) receive the points when given.  synchronises
+ * tm_medial_points: the medial-axis approximation of boundary points x, y (device, n): the
+ *   Delaunay triangles with circumcentre strictly inside the box, from the library's own cell
+ *   kernel with an octagon larger than the box (an unbounded-cell variant of S2); per point the
+ *   farthest circumcentre v1 and the farthest v2 with (v2 - s).(v1 - s) < 0 (ties by the
+ *   triangle's two smallest indices); v1, v2 in point order, kept iff >= n_thres other medial
+ *   points lie strictly within r_nei.  mx, my (device, cap); *n_out (host).  synchronises
+ * tm_sizing_field: lfs(s) = the distance to the nearest medial point, and
+ *   mu = min_s [K |x - s| + lfs(s)] (Eq. sizing field) at the nodes of the [ny][nx] grid
+ *   over the box (device mu; lfs device, ns entries).  Asynchronous. */
+tm_status tm_boundary_points(tm_ctx *ctx, const double *segs, int64_t n_seg, double d_s, double geps_hat, double *x,
+                             double *y, int64_t cap, int64_t *n_out);
+tm_status tm_medial_points(tm_ctx *ctx, const double *x, const double *y, int64_t n, double x0, double y0, double x1,
+                           double y1, double r_nei, int32_t n_thres, double *mx, double *my, int64_t cap,
+                           int64_t *n_out);
+tm_status tm_sizing_field(tm_ctx *ctx, const double *sx, const double *sy, int64_t ns, const double *mx,
+                          const double *my, int64_t nm, double K, int32_t nx, int32_t ny, double x0, double y0,
+                          double x1, double y1, double *mu, double *lfs);
+
+/* rho = 1 / mu^2 elementwise (Eq. density sizing relationship), device arrays. Asynchronous. */
+tm_status tm_density_from_sizing(tm_ctx *ctx, const double *mu, int64_t n, double *rho);
+
 typedef struct tm_graph tm_graph;
 tm_status tm_graph_begin(tm_ctx *ctx);
 tm_status tm_graph_end(tm_ctx *ctx, tm_graph **out);

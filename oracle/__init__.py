@@ -160,6 +160,18 @@ def lib():
         L.or_init_points.argtypes = [ctypes.POINTER(Fields), ctypes.POINTER(Params), ctypes.c_double, ctypes.c_double,
                                      ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_uint64,
                                      ctypes.c_void_p, ctypes.c_void_p]
+        L.or_boundary_points.restype = ctypes.c_int64
+        L.or_boundary_points.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]
+        L.or_medial_points.restype = ctypes.c_int64
+        L.or_medial_points.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
+                                       ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                       ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]
+        L.or_sizing_field.restype = None
+        L.or_sizing_field.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                      ctypes.c_void_p, ctypes.c_double, ctypes.c_int32, ctypes.c_int32,
+                                      ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                      ctypes.c_void_p, ctypes.c_void_p]
         _lib = L
     return _lib
 
@@ -541,3 +553,36 @@ def init_points(fs: FieldSet, counts, seed, c, h_avg, params=None):
     lib().or_init_points(ctypes.byref(fs.c), ctypes.byref(params), c, h_avg, int(nxg), int(nyg), _p(cn), int(seed),
                          _p(x), _p(y))
     return x, y
+
+
+def boundary_points(segs, d_s, geps_hat):
+    """App. A: contour boundary points, trimmed to spacing >= d_s."""
+    s = np.ascontiguousarray(segs, dtype=np.float64)
+    cap = 16
+    while True:
+        x, y = np.empty(cap), np.empty(cap)
+        n = lib().or_boundary_points(_p(s), s.shape[0], float(d_s), float(geps_hat), _p(x), _p(y), cap)
+        if n >= 0:
+            return x[:n].copy(), y[:n].copy()
+        cap = -n
+
+
+def medial_points(x, y, box, r_nei, n_thres=3):
+    """Delaunay poles of the boundary points, trimmed by neighbour counts."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    mx, my = np.empty(2 * len(x) + 16), np.empty(2 * len(x) + 16)
+    m = lib().or_medial_points(len(x), _p(x), _p(y), box[0], box[1], box[2], box[3], float(r_nei), int(n_thres),
+                               _p(mx), _p(my))
+    return mx[:m].copy(), my[:m].copy()
+
+
+def sizing_field(sx, sy, mx, my, K, nx, ny, box):
+    """Eq. sizing field: mu on the node grid and lfs at the boundary points."""
+    sx, sy = np.ascontiguousarray(sx, dtype=np.float64), np.ascontiguousarray(sy, dtype=np.float64)
+    mx, my = np.ascontiguousarray(mx, dtype=np.float64), np.ascontiguousarray(my, dtype=np.float64)
+    mu = np.empty(nx * ny)
+    lfs = np.empty(len(sx))
+    lib().or_sizing_field(len(sx), _p(sx), _p(sy), len(mx), _p(mx), _p(my), float(K), int(nx), int(ny), box[0],
+                          box[1], box[2], box[3], _p(mu), _p(lfs))
+    return mu.reshape(ny, nx), lfs

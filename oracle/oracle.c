@@ -1711,3 +1711,167 @@ int64_t or_init_points(const or_fields *f, const or_params *p, double c, double 
         }
     return k;
 }
+
+/* ---- NEXT-4: automatic sizing (App. A) ---------------------------- */
+/* Boundary points from a contour (App. A): every segment's start point, and on a segment
+ * longer than d_s the points a + (q/m)(b - a), q = 1..m-1, m = floor(len/d_s) + 1 (spacing below
+ * d_s).  Then the trimming loop (reading L48): over the points in their order, find
+ * the closest OTHER point whose midpoint m with p_i has |sdf(m)| <= geps_hat; if it is closer than
+ * d_s, delete it and move p_i to m (and look again), else p_i is done; sweeps repeat until a sweep
+ * changes nothing.  sdf is the contour's (or_contour_sdf_point).  Returns the count (<= cap). */
+int64_t or_boundary_points(const double *segs, int64_t n_seg, double d_s, double geps_hat, double *x, double *y,
+                           int64_t cap) {
+    int64_t n = 0;
+    for (int64_t k = 0; k < n_seg; k++) {
+        const double *s = segs + 4 * k;
+        const double ex = s[2] - s[0], ey = s[3] - s[1];
+        const double len = sqrt(ex * ex + ey * ey);
+        if (n < cap) { x[n] = s[0]; y[n] = s[1]; }
+        n++;
+        if (len > d_s) {
+            const int64_t m = (int64_t)floor(len / d_s) + 1;
+            for (int64_t q = 1; q < m; q++) {
+                const double t = (double)q / (double)m;
+                if (n < cap) { x[n] = s[0] + t * ex; y[n] = s[1] + t * ey; }
+                n++;
+            }
+        }
+    }
+    if (n > cap) return -n;
+    uint8_t *alive = (uint8_t *)malloc((size_t)(n > 0 ? n : 1));
+    for (int64_t i = 0; i < n; i++) alive[i] = 1;
+    for (int changed = 1; changed;) {
+        changed = 0;
+        for (int64_t i = 0; i < n; i++) {
+            while (alive[i]) {
+                int64_t best = -1;
+                double bd = 0.0;
+                for (int64_t j = 0; j < n; j++) {
+                    if (j == i || !alive[j]) continue;
+                    const double dx = x[j] - x[i], dy = y[j] - y[i];
+                    const double d2 = dx * dx + dy * dy;
+                    if (best >= 0 && !(d2 < bd)) continue;
+                    const double mx = (x[i] + x[j]) * 0.5, my = (y[i] + y[j]) * 0.5;
+                    if (!(fabs(or_contour_sdf_point(segs, n_seg, mx, my)) <= geps_hat)) continue;
+                    best = j;
+                    bd = d2;
+                }
+                if (best < 0 || !(bd < d_s * d_s)) break;
+                x[i] = (x[i] + x[best]) * 0.5;
+                y[i] = (y[i] + y[best]) * 0.5;
+                alive[best] = 0;
+                changed = 1;
+            }
+        }
+    }
+    int64_t m = 0;
+    for (int64_t i = 0; i < n; i++)
+        if (alive[i]) { x[m] = x[i]; y[m] = y[i]; m++; }
+    free(alive);
+    return m;
+}
+
+/* Medial-axis approximation (after Amenta et al.): for each boundary point s its
+ * Voronoi vertices are the circumcentres of its Delaunay triangles (canonical Cramer relative to
+ * the smallest index, as the keep rule); v1 = the farthest from s, v2 = the farthest among those
+ * with (v - s).(v1 - s) < 0; distance ties by the smallest (u, v) of the triangle (reading L48).
+ * Only triangles whose circumcentre lies inside the box [x0,x1]x[y0,y1] count (a bounded diagram).
+ * Writes up to 2 points per boundary point into mx/my (v1 then v2, boundary points in order).
+ * Trimming: a medial point is kept iff at least n_thres OTHER medial points lie within
+ * r_nei (strictly closer).  Returns the kept count; med_x/med_y compacted. */
+int64_t or_medial_points(int64_t n, const double *x, const double *y, double x0, double y0, double x1, double y1,
+                         double r_nei, int32_t n_thres, double *mx, double *my) {
+    int64_t cap = 2 * n + 16;
+    int32_t *D = (int32_t *)malloc(sizeof(int32_t) * 3 * (size_t)cap);
+    int64_t nd = or_delaunay(n, x, y, D, cap, NULL);
+    if (nd < 0) { free(D); return -1; }
+    double *cx = (double *)malloc(sizeof(double) * (size_t)(nd > 0 ? nd : 1));
+    double *cy = (double *)malloc(sizeof(double) * (size_t)(nd > 0 ? nd : 1));
+    int32_t *su = (int32_t *)malloc(sizeof(int32_t) * 3 * (size_t)(nd > 0 ? nd : 1));
+    for (int64_t t = 0; t < nd; t++) {
+        int32_t q[3] = {D[3 * t], D[3 * t + 1], D[3 * t + 2]};
+        for (int a = 0; a < 2; a++)
+            for (int b = 0; b < 2 - a; b++)
+                if (q[b] > q[b + 1]) { int32_t s_ = q[b]; q[b] = q[b + 1]; q[b + 1] = s_; }
+        line2 A, B;
+        A.nx = x[q[1]] - x[q[0]]; A.ny = y[q[1]] - y[q[0]]; A.r = 0.5 * (A.nx * A.nx + A.ny * A.ny);
+        B.nx = x[q[2]] - x[q[0]]; B.ny = y[q[2]] - y[q[0]]; B.r = 0.5 * (B.nx * B.nx + B.ny * B.ny);
+        double ox, oy;
+        cramer(A, B, &ox, &oy);
+        cx[t] = x[q[0]] + ox;
+        cy[t] = y[q[0]] + oy;
+        su[3 * t] = q[0]; su[3 * t + 1] = q[1]; su[3 * t + 2] = q[2];
+    }
+    /* per point: the best triangle for v1, then for v2 */
+    int64_t *b1 = (int64_t *)malloc(sizeof(int64_t) * (size_t)n), *b2 = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    double *d1 = (double *)malloc(sizeof(double) * (size_t)n), *d2 = (double *)malloc(sizeof(double) * (size_t)n);
+    for (int64_t i = 0; i < n; i++) { b1[i] = b2[i] = -1; d1[i] = d2[i] = 0.0; }
+#define OR_TKEY(t) (((uint64_t)(uint32_t)su[3 * (t)] << 32) | (uint32_t)su[3 * (t) + 1])
+    for (int pass = 0; pass < 2; pass++)
+        for (int64_t t = 0; t < nd; t++) {
+            if (!(cx[t] > x0 && cx[t] < x1 && cy[t] > y0 && cy[t] < y1)) continue;
+            for (int k = 0; k < 3; k++) {
+                const int32_t s = su[3 * t + k];
+                const double ex = cx[t] - x[s], ey = cy[t] - y[s];
+                const double dd = ex * ex + ey * ey;
+                int64_t *bb = pass ? b2 : b1;
+                double *db = pass ? d2 : d1;
+                if (pass) {
+                    if (b1[s] < 0) continue;
+                    const double fx = cx[b1[s]] - x[s], fy = cy[b1[s]] - y[s];
+                    if (!(ex * fx + ey * fy < 0.0)) continue;
+                }
+                if (bb[s] < 0 || dd > db[s] || (dd == db[s] && OR_TKEY(t) < OR_TKEY(bb[s]))) { bb[s] = t; db[s] = dd; }
+            }
+        }
+#undef OR_TKEY
+    int64_t m = 0;
+    for (int64_t i = 0; i < n; i++) {
+        if (b1[i] >= 0) { mx[m] = cx[b1[i]]; my[m] = cy[b1[i]]; m++; }
+        if (b2[i] >= 0) { mx[m] = cx[b2[i]]; my[m] = cy[b2[i]]; m++; }
+    }
+    uint8_t *keep = (uint8_t *)malloc((size_t)(m > 0 ? m : 1));
+    for (int64_t i = 0; i < m; i++) {
+        int64_t c = 0;
+        for (int64_t j = 0; j < m; j++) {
+            if (j == i) continue;
+            const double dx = mx[j] - mx[i], dy = my[j] - my[i];
+            if (dx * dx + dy * dy < r_nei * r_nei) c++;
+        }
+        keep[i] = c >= n_thres;
+    }
+    int64_t k = 0;
+    for (int64_t i = 0; i < m; i++)
+        if (keep[i]) { mx[k] = mx[i]; my[k] = my[i]; k++; }
+    free(D); free(cx); free(cy); free(su); free(b1); free(b2); free(d1); free(d2); free(keep);
+    return k;
+}
+
+/* Sizing field (Eq. sizing field): lfs(s) = distance from s to the nearest medial point
+ * (P:373); mu(x) = min_s [K |x - s| + lfs(s)] at the nodes of the [ny][nx] grid over the box
+ * (reading L48: the node grid of the bilinear fields instead of geometry-grid midpoints). */
+void or_sizing_field(int64_t ns, const double *sx, const double *sy, int64_t nm, const double *mx, const double *my,
+                     double K, int32_t nx, int32_t ny, double x0, double y0, double x1, double y1, double *mu,
+                     double *lfs) {
+    for (int64_t i = 0; i < ns; i++) {
+        double b = -1.0;
+        for (int64_t j = 0; j < nm; j++) {
+            const double dx = mx[j] - sx[i], dy = my[j] - sy[i];
+            const double d = sqrt(dx * dx + dy * dy);
+            if (b < 0.0 || d < b) b = d;
+        }
+        lfs[i] = b;
+    }
+    for (int32_t j = 0; j < ny; j++)
+        for (int32_t i = 0; i < nx; i++) {
+            const double px = x0 + (double)i * ((x1 - x0) / (double)(nx - 1));
+            const double py = y0 + (double)j * ((y1 - y0) / (double)(ny - 1));
+            double b = -1.0;
+            for (int64_t s = 0; s < ns; s++) {
+                const double dx = px - sx[s], dy = py - sy[s];
+                const double v = K * sqrt(dx * dx + dy * dy) + lfs[s];
+                if (b < 0.0 || v < b) b = v;
+            }
+            mu[(int64_t)j * nx + i] = b;
+        }
+}

@@ -164,6 +164,16 @@ int64_t or_init_counts(const or_fields *f, int32_t nxg, int32_t nyg, const int8_
 int64_t or_init_points(const or_fields *f, const or_params *p, double c, double h_avg, int32_t nxg, int32_t nyg,
                        const int32_t *counts, uint64_t seed, double *x, double *y);
 
+/* automatic sizing (App. A): boundary points of a contour, trimmed (returns the count,
+ * -needed if cap is short); medial points by Delaunay poles, trimmed by neighbour counts; sizing */
+int64_t or_boundary_points(const double *segs, int64_t n_seg, double d_s, double geps_hat, double *x, double *y,
+                           int64_t cap);
+int64_t or_medial_points(int64_t n, const double *x, const double *y, double x0, double y0, double x1, double y1,
+                         double r_nei, int32_t n_thres, double *mx, double *my);
+void or_sizing_field(int64_t ns, const double *sx, const double *sy, int64_t nm, const double *mx, const double *my,
+                     double K, int32_t nx, int32_t ny, double x0, double y0, double x1, double y1, double *mu,
+                     double *lfs);
+
 #ifdef __cplusplus
 }
 #endif

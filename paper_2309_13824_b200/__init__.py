@@ -96,7 +96,8 @@ EXPORTED = ["tm_params_default", "tm_create", "tm_destroy", "tm_last_error", "tm
             "tm_graph_begin", "tm_graph_end", "tm_graph_launch", "tm_graph_destroy", "tm_refresh_positions",
             "tm_retria_check", "tm_move_count", "tm_set_n_total", "tm_point_addition", "tm_control_init",
             "tm_control_update", "tm_geometry_grid_dims", "tm_geometry_categories", "tm_contour_sdf",
-            "tm_sdf_combine", "tm_init_points",
+            "tm_sdf_combine", "tm_init_points", "tm_boundary_points", "tm_medial_points", "tm_sizing_field",
+            "tm_density_from_sizing",
             "tm_host_incircle_exact", "tm_host_cramer", "tm_host_bilinear"]
 
 
@@ -133,6 +134,10 @@ def load_library(path: str = LIB_PATH, build_if_missing: bool = True):
         "tm_geometry_categories": (st, [vp, i32, i32, vp]),
         "tm_contour_sdf": (st, [vp, vp, i64, i32, i32, dbl, dbl, dbl, dbl, vp]),
         "tm_sdf_combine": (st, [vp, i32, vp, vp, i64, vp]),
+        "tm_boundary_points": (st, [vp, vp, i64, dbl, dbl, vp, vp, i64, ctypes.POINTER(i64)]),
+        "tm_medial_points": (st, [vp, vp, vp, i64, dbl, dbl, dbl, dbl, dbl, i32, vp, vp, i64, ctypes.POINTER(i64)]),
+        "tm_density_from_sizing": (st, [vp, vp, i64, vp]),
+        "tm_sizing_field": (st, [vp, vp, vp, i64, vp, vp, i64, dbl, i32, i32, dbl, dbl, dbl, dbl, vp, vp]),
         "tm_init_points": (st, [vp, i32, i32, vp, dbl, dbl, ctypes.c_uint64, vp, vp, vp, i64, ctypes.POINTER(i64)]),
         "tm_set_n_total": (st, [vp, i64, ctypes.POINTER(dbl), ctypes.POINTER(dbl)]),
         "tm_point_addition": (st, [vp, vp, i64, vp, vp, i64, vp, vp, ctypes.POINTER(dbl)]),
@@ -299,6 +304,9 @@ class Context:
         self._check(self.L.tm_init_points(self.h, int(nxg), int(nyg), _ptr(cat), float(n_init), float(eta), int(seed),
                                           _ptr(counts), _ptr(x), _ptr(y), int(cap), ctypes.byref(n)))
         return int(n.value)
+
+    def tm_density_from_sizing(self, mu, rho):
+        self._check(self.L.tm_density_from_sizing(self.h, _ptr(mu), int(mu.numel()), _ptr(rho)))
 
     def tm_adjacency_export(self, adj, deg, adj_out, deg_out):
         self._check(self.L.tm_adjacency_export(self.h, _ptr(adj), _ptr(deg), _ptr(adj_out), _ptr(deg_out)))
@@ -559,3 +567,31 @@ def initial_points(ctx: Context, n_init: int, nxg: int, nyg: int, eta: float = 0
     y = torch.empty_like(x)
     ctx.tm_init_points(nxg, nyg, cat, n_init, eta, seed, counts, x, y, n)
     return x, y, cat.view(nyg, nxg), counts.view(nyg, nxg)
+
+
+def automatic_sizing(ctx: Context, segs, box, nx: int, ny: int, K: float, d_s: float, geps_hat: float,
+                     r_nei: float, n_thres: int = 3):
+    """P:356-373 on the GPU: boundary points of the contour (App. A), their medial-axis poles
+    (trimmed), lfs and the sizing field mu on the (ny, nx) node grid over box.  Returns
+    (mu, (sx, sy), (mx, my), lfs) as device tensors."""
+    dev = segs.device
+    n = ctypes.c_int64()
+    L = ctx.L
+    ctx._check(L.tm_boundary_points(ctx.h, _ptr(segs), int(segs.shape[0]), float(d_s), float(geps_hat), None, None, 0,
+                                    ctypes.byref(n)))
+    sx = torch.empty(n.value, dtype=torch.float64, device=dev)
+    sy = torch.empty_like(sx)
+    ctx._check(L.tm_boundary_points(ctx.h, _ptr(segs), int(segs.shape[0]), float(d_s), float(geps_hat), _ptr(sx),
+                                    _ptr(sy), n.value, ctypes.byref(n)))
+    cap = 2 * sx.shape[0] + 16
+    mx = torch.empty(cap, dtype=torch.float64, device=dev)
+    my = torch.empty_like(mx)
+    m = ctypes.c_int64()
+    ctx._check(L.tm_medial_points(ctx.h, _ptr(sx), _ptr(sy), int(sx.shape[0]), box[0], box[1], box[2], box[3],
+                                  float(r_nei), int(n_thres), _ptr(mx), _ptr(my), cap, ctypes.byref(m)))
+    mx, my = mx[:m.value].contiguous(), my[:m.value].contiguous()
+    mu = torch.empty(ny, nx, dtype=torch.float64, device=dev)
+    lfs = torch.empty_like(sx)
+    ctx._check(L.tm_sizing_field(ctx.h, _ptr(sx), _ptr(sy), int(sx.shape[0]), _ptr(mx), _ptr(my), int(mx.shape[0]),
+                                 float(K), int(nx), int(ny), box[0], box[1], box[2], box[3], _ptr(mu), _ptr(lfs)))
+    return mu, (sx, sy), (mx, my), lfs

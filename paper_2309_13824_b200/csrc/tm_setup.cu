@@ -126,6 +126,11 @@ __global__ void k_contour_sdf(const double *__restrict__ segs, int64_t n_seg, Se
     phi[c] = side > 0.0 ? -d : d;
 }
 
+__global__ void k_density(const double *__restrict__ mu, int64_t n, double *__restrict__ rho) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) rho[i] = cdiv(1.0, cmul(mu[i], mu[i]));  // Eq. density sizing relationship
+}
+
 __global__ void k_sdf_combine(int op, const double *__restrict__ a, const double *__restrict__ b, int64_t n,
                               double *__restrict__ out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -368,4 +373,359 @@ extern "C" tm_status tm_init_points(tm_ctx *ctx, int32_t nxg, int32_t nyg, const
     if ((s = tm_internal_check_launch(ctx, "k_init_points")) != TM_OK) return s;
     TM_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     return TM_OK;
+}
+
+// ---- automatic sizing (App. A)
+namespace {
+
+// poles: per boundary point s the farthest circumcentre of its Delaunay triangles (pass 0), then
+// the farthest in the half-space opposite to v1 (pass 1); ties by the triangle's (u, v) key.
+// Deterministic in two steps: max of the squared distance (bits of a non-negative double order
+// as unsigned integers), then the min key among the triangles attaining it.
+__global__ void k_pole_circ(int64_t nt, const int32_t *__restrict__ tri, const double *__restrict__ x,
+                            const double *__restrict__ y, double *__restrict__ cxy, uint64_t *__restrict__ key,
+                            int32_t *__restrict__ su) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    int32_t q0 = tri[3 * t], q1 = tri[3 * t + 1], q2 = tri[3 * t + 2], s;
+    if (q0 > q1) { s = q0; q0 = q1; q1 = s; }
+    if (q1 > q2) { s = q1; q1 = q2; q2 = s; }
+    if (q0 > q1) { s = q0; q0 = q1; q1 = s; }
+    const Line A = bisector(csub(x[q1], x[q0]), csub(y[q1], y[q0])), B = bisector(csub(x[q2], x[q0]), csub(y[q2], y[q0]));
+    double ox, oy;
+    cramer(A, B, ox, oy);
+    cxy[2 * t] = cadd(x[q0], ox);
+    cxy[2 * t + 1] = cadd(y[q0], oy);
+    key[t] = ((uint64_t)(uint32_t)q0 << 32) | (uint32_t)q1;
+    su[3 * t] = q0; su[3 * t + 1] = q1; su[3 * t + 2] = q2;
+}
+
+__device__ __forceinline__ bool pole_ok(int pass, const double *cxy, int64_t t, const double *x, const double *y,
+                                        int32_t s, const int64_t *b1, double &dd) {
+    const double ex = csub(cxy[2 * t], x[s]), ey = csub(cxy[2 * t + 1], y[s]);
+    dd = cadd(cmul(ex, ex), cmul(ey, ey));
+    if (pass == 0) return true;
+    const int64_t t1 = b1[s];
+    if (t1 < 0) return false;
+    const double fx = csub(cxy[2 * t1], x[s]), fy = csub(cxy[2 * t1 + 1], y[s]);
+    return cadd(cmul(ex, fx), cmul(ey, fy)) < 0.0;
+}
+
+__global__ void k_pole_max(int64_t nt, int pass, const double *__restrict__ cxy, const int32_t *__restrict__ su,
+                           const double *__restrict__ x, const double *__restrict__ y, double bx0, double by0,
+                           double bx1, double by1, const int64_t *__restrict__ b1, unsigned long long *__restrict__ dmax) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    const double cx = cxy[2 * t], cy = cxy[2 * t + 1];
+    if (!(cx > bx0 && cx < bx1 && cy > by0 && cy < by1)) return;
+    for (int k = 0; k < 3; k++) {
+        const int32_t s = su[3 * t + k];
+        double dd;
+        if (pole_ok(pass, cxy, t, x, y, s, b1, dd)) atomicMax(dmax + s, (unsigned long long)__double_as_longlong(dd));
+    }
+}
+
+__global__ void k_pole_arg(int64_t nt, int pass, const double *__restrict__ cxy, const int32_t *__restrict__ su,
+                           const uint64_t *__restrict__ key, const double *__restrict__ x, const double *__restrict__ y,
+                           double bx0, double by0, double bx1, double by1, const int64_t *__restrict__ b1,
+                           const unsigned long long *__restrict__ dmax, unsigned long long *__restrict__ kmin) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    const double cx = cxy[2 * t], cy = cxy[2 * t + 1];
+    if (!(cx > bx0 && cx < bx1 && cy > by0 && cy < by1)) return;
+    for (int k = 0; k < 3; k++) {
+        const int32_t s = su[3 * t + k];
+        double dd;
+        if (pole_ok(pass, cxy, t, x, y, s, b1, dd) && (unsigned long long)__double_as_longlong(dd) == dmax[s])
+            atomicMin(kmin + s, (unsigned long long)key[t]);
+    }
+}
+
+// triangle index of the winning key per point (keys are unique per triangle)
+__global__ void k_pole_pick(int64_t nt, int pass, const double *__restrict__ cxy, const int32_t *__restrict__ su,
+                            const uint64_t *__restrict__ key, const double *__restrict__ x, const double *__restrict__ y,
+                            double bx0, double by0, double bx1, double by1, const int64_t *__restrict__ b1,
+                            const unsigned long long *__restrict__ dmax, const unsigned long long *__restrict__ kmin,
+                            int64_t *__restrict__ best) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    const double cx = cxy[2 * t], cy = cxy[2 * t + 1];
+    if (!(cx > bx0 && cx < bx1 && cy > by0 && cy < by1)) return;
+    for (int k = 0; k < 3; k++) {
+        const int32_t s = su[3 * t + k];
+        double dd;
+        if (pole_ok(pass, cxy, t, x, y, s, b1, dd) && (unsigned long long)__double_as_longlong(dd) == dmax[s] &&
+            kmin[s] == key[t])
+            best[s] = t;
+    }
+}
+
+// medial points kept iff >= n_thres OTHER medial points lie strictly within r_nei (brute force)
+__global__ void k_medial_trim(int64_t m, const double *__restrict__ mx, const double *__restrict__ my, double r2,
+                              int32_t n_thres, uint8_t *__restrict__ keep) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    int64_t c = 0;
+    for (int64_t j = 0; j < m; j++) {
+        if (j == i) continue;
+        const double dx = csub(mx[j], mx[i]), dy = csub(my[j], my[i]);
+        c += cadd(cmul(dx, dx), cmul(dy, dy)) < r2 ? 1 : 0;
+    }
+    keep[i] = c >= n_thres;
+}
+
+__global__ void k_lfs(int64_t ns, const double *__restrict__ sx, const double *__restrict__ sy, int64_t nm,
+                      const double *__restrict__ mx, const double *__restrict__ my, double *__restrict__ lfs) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ns) return;
+    double b = -1.0;
+    for (int64_t j = 0; j < nm; j++) {
+        const double dx = csub(mx[j], sx[i]), dy = csub(my[j], sy[i]);
+        const double d = sqrt(cadd(cmul(dx, dx), cmul(dy, dy)));
+        if (b < 0.0 || d < b) b = d;
+    }
+    lfs[i] = b;
+}
+
+// mu(node) = min_s [K |node - s| + lfs(s)]: the boundary points staged in shared memory by tiles
+__global__ void k_sizing(int64_t ns, const double *__restrict__ sx, const double *__restrict__ sy,
+                         const double *__restrict__ lfs, double K, int32_t nx, int32_t ny, double x0, double y0,
+                         double x1, double y1, double *__restrict__ mu) {
+    __shared__ double tx[256], ty[256], tl[256];
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = c < (int64_t)nx * ny;
+    const int32_t i = live ? (int32_t)(c % nx) : 0, j = live ? (int32_t)(c / nx) : 0;
+    const double px = cadd(x0, cmul((double)i, cdiv(csub(x1, x0), (double)(nx - 1))));
+    const double py = cadd(y0, cmul((double)j, cdiv(csub(y1, y0), (double)(ny - 1))));
+    double b = -1.0;
+    for (int64_t base = 0; base < ns; base += 256) {
+        __syncthreads();
+        const int64_t q = base + threadIdx.x;
+        if (threadIdx.x < 256 && q < ns) { tx[threadIdx.x] = sx[q]; ty[threadIdx.x] = sy[q]; tl[threadIdx.x] = lfs[q]; }
+        __syncthreads();
+        const int m = (int)(ns - base < 256 ? ns - base : 256);
+        for (int k = 0; k < m; k++) {  // in boundary-point order: min is order independent anyway
+            const double dx = csub(px, tx[k]), dy = csub(py, ty[k]);
+            const double v = cadd(cmul(K, sqrt(cadd(cmul(dx, dx), cmul(dy, dy)))), tl[k]);
+            if (b < 0.0 || v < b) b = v;
+        }
+    }
+    if (live) mu[c] = b;
+}
+
+// |sdf| of the contour at one point (host; the trimming loop is serial by the method)
+double host_contour_sdf_abs(const std::vector<double> &S, double px, double py) {
+    const int64_t n = (int64_t)S.size() / 4;
+    double bd = -1.0;
+    for (int64_t k = 0; k < n; k++) {
+        const double *s = &S[4 * k];
+        const double ex = csub(s[2], s[0]), ey = csub(s[3], s[1]);
+        const double t = cdiv(cadd(cmul(csub(px, s[0]), ex), cmul(csub(py, s[1]), ey)), cadd(cmul(ex, ex), cmul(ey, ey)));
+        double qx, qy;
+        if (t <= 0.0) { qx = s[0]; qy = s[1]; }
+        else if (t >= 1.0) { qx = s[2]; qy = s[3]; }
+        else { qx = cadd(s[0], cmul(t, ex)); qy = cadd(s[1], cmul(t, ey)); }
+        const double dx = csub(px, qx), dy = csub(py, qy);
+        const double d2 = cadd(cmul(dx, dx), cmul(dy, dy));
+        if (bd < 0.0 || d2 < bd) bd = d2;
+    }
+    return sqrt(bd);
+}
+
+}  // namespace
+
+extern "C" tm_status tm_boundary_points(tm_ctx *ctx, const double *segs, int64_t n_seg, double d_s, double geps_hat,
+                                        double *x, double *y, int64_t cap, int64_t *n_out) {
+    if (!ctx) return TM_E_ARG;
+    if (ctx->capturing) TM_FAIL(ctx, TM_E_STATE, "tm_boundary_points while capturing a graph");
+    if (!segs || n_seg < 3 || !(d_s > 0.0) || !(geps_hat >= 0.0) || !n_out || cap < 0)
+        TM_FAIL(ctx, TM_E_ARG, "bad arguments to tm_boundary_points");
+    TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    std::vector<double> S((size_t)n_seg * 4);
+    TM_CUDA_TRY(ctx, cudaMemcpyAsync(S.data(), segs, S.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    TM_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    std::vector<double> px, py;
+    for (int64_t k = 0; k < n_seg; k++) {  // App. A: start points, evenly spaced points on long segments
+        const double *s = &S[4 * k];
+        const double ex = csub(s[2], s[0]), ey = csub(s[3], s[1]);
+        const double len = sqrt(cadd(cmul(ex, ex), cmul(ey, ey)));
+        px.push_back(s[0]);
+        py.push_back(s[1]);
+        if (len > d_s) {
+            const int64_t m = (int64_t)floor(cdiv(len, d_s)) + 1;
+            for (int64_t q = 1; q < m; q++) {
+                const double t = cdiv((double)q, (double)m);
+                px.push_back(cadd(s[0], cmul(t, ex)));
+                py.push_back(cadd(s[1], cmul(t, ey)));
+            }
+        }
+    }
+    const int64_t n = (int64_t)px.size();
+    std::vector<uint8_t> alive(n, 1);
+    const double ds2 = cmul(d_s, d_s);
+    for (bool changed = true; changed;) {  // the trimming sweeps (serial by the method)
+        changed = false;
+        for (int64_t i = 0; i < n; i++) {
+            while (alive[i]) {
+                int64_t best = -1;
+                double bd = 0.0;
+                for (int64_t j = 0; j < n; j++) {
+                    if (j == i || !alive[j]) continue;
+                    const double dx = csub(px[j], px[i]), dy = csub(py[j], py[i]);
+                    const double d2 = cadd(cmul(dx, dx), cmul(dy, dy));
+                    if (best >= 0 && !(d2 < bd)) continue;
+                    const double mx = cmul(cadd(px[i], px[j]), 0.5), my = cmul(cadd(py[i], py[j]), 0.5);
+                    if (!(host_contour_sdf_abs(S, mx, my) <= geps_hat)) continue;
+                    best = j;
+                    bd = d2;
+                }
+                if (best < 0 || !(bd < ds2)) break;
+                px[i] = cmul(cadd(px[i], px[best]), 0.5);
+                py[i] = cmul(cadd(py[i], py[best]), 0.5);
+                alive[best] = 0;
+                changed = true;
+            }
+        }
+    }
+    std::vector<double> ox, oy;
+    for (int64_t i = 0; i < n; i++)
+        if (alive[i]) { ox.push_back(px[i]); oy.push_back(py[i]); }
+    *n_out = (int64_t)ox.size();
+    if (!x || !y) return TM_OK;
+    if ((int64_t)ox.size() > cap) TM_FAIL(ctx, TM_E_CAPACITY, "tm_boundary_points: %lld points, capacity %lld",
+                                          (long long)ox.size(), (long long)cap);
+    TM_CUDA_TRY(ctx, cudaMemcpyAsync(x, ox.data(), ox.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    TM_CUDA_TRY(ctx, cudaMemcpyAsync(y, oy.data(), oy.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    TM_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return TM_OK;
+}
+
+extern "C" tm_status tm_medial_points(tm_ctx *ctx, const double *x, const double *y, int64_t n, double x0, double y0,
+                                      double x1, double y1, double r_nei, int32_t n_thres, double *mx, double *my,
+                                      int64_t cap, int64_t *n_out) {
+    if (!ctx) return TM_E_ARG;
+    if (ctx->capturing) TM_FAIL(ctx, TM_E_STATE, "tm_medial_points while capturing a graph");
+    if (!x || !y || n < 3 || !(x1 > x0) || !(y1 > y0) || !mx || !my || !n_out || n >= (int64_t)INT32_MAX / 2)
+        TM_FAIL(ctx, TM_E_ARG, "bad arguments to tm_medial_points");
+    TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    // the Delaunay triangles of the boundary points by the library's own cell kernel on a second
+    // context: phi = -1 on a 2x2 grid over the box, one point's worth of h (c = sqrt(area)) and a
+    // large octagon factor, so cells are Voronoi cells clipped by the box only, and keep_tol =
+    // +inf: every triangle with its circumcentre strictly inside the box ("an
+    // unbounded-cell variant of S2")
+    tm_params p2 = ctx->p;
+    p2.fac_voro_bound = 1e3;
+    p2.keep_tol = 1e300;
+    p2.validity = 0;
+    p2.flags = TM_F_TWO_LEVEL_BINS;
+    tm_ctx *c2 = nullptr;
+    tm_status s = tm_create(ctx->device, ctx->stream, &p2, &c2);
+    if (s != TM_OK) TM_FAIL(ctx, s, "tm_medial_points: context");
+    struct Guard { tm_ctx *c; ~Guard() { tm_destroy(c); } } guard{c2};
+    DevBuf dphi, dtri, dnt;
+    const double m1[4] = {-1.0, -1.0, -1.0, -1.0};
+    TM_CUDA_TRY(ctx, cudaMalloc(&dphi.p, sizeof(m1)));
+    TM_CUDA_TRY(ctx, cudaMemcpyAsync(dphi.p, m1, sizeof(m1), cudaMemcpyHostToDevice, ctx->stream));
+    tm_fields f = {2, 2, x0, y0, x1, y1, (const double *)dphi.p, nullptr, nullptr};
+    if ((s = tm_set_domain(c2, &f, 1, nullptr, nullptr)) != TM_OK) TM_FAIL(ctx, s, "tm_medial_points: %s", c2->err);
+    if ((s = tm_grid_bin(c2, x, y, n, n, nullptr)) != TM_OK) TM_FAIL(ctx, s, "tm_medial_points: %s", c2->err);
+    const int64_t tcap = 2 * n + 64;
+    TM_CUDA_TRY(ctx, cudaMalloc(&dtri.p, tcap * 3 * sizeof(int32_t)));
+    TM_CUDA_TRY(ctx, cudaMalloc(&dnt.p, sizeof(int64_t)));
+    s = tm_voronoi_delaunay(c2, (int32_t *)dtri.p, tcap, (int64_t *)dnt.p, nullptr, nullptr, nullptr, nullptr, nullptr,
+                            nullptr, nullptr);
+    if (s == TM_OK) s = tm_sync(c2);
+    if (s != TM_OK) TM_FAIL(ctx, s, "tm_medial_points: %s", c2->err);
+    int64_t nt = 0;
+    TM_CUDA_TRY(ctx, cudaMemcpy(&nt, dnt.p, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    DevBuf dc, dk, ds, dmax, dkmin, db1, db2;
+    TM_CUDA_TRY(ctx, cudaMalloc(&dc.p, std::max<int64_t>(nt, 1) * 2 * sizeof(double)));
+    TM_CUDA_TRY(ctx, cudaMalloc(&dk.p, std::max<int64_t>(nt, 1) * sizeof(uint64_t)));
+    TM_CUDA_TRY(ctx, cudaMalloc(&ds.p, std::max<int64_t>(nt, 1) * 3 * sizeof(int32_t)));
+    TM_CUDA_TRY(ctx, cudaMalloc(&dmax.p, n * sizeof(unsigned long long)));
+    TM_CUDA_TRY(ctx, cudaMalloc(&dkmin.p, n * sizeof(unsigned long long)));
+    TM_CUDA_TRY(ctx, cudaMalloc(&db1.p, n * sizeof(int64_t)));
+    TM_CUDA_TRY(ctx, cudaMalloc(&db2.p, n * sizeof(int64_t)));
+    const unsigned gt = (unsigned)((std::max<int64_t>(nt, 1) + 255) / 256);
+    auto *cxy = (double *)dc.p;
+    auto *key = (uint64_t *)dk.p;
+    auto *su = (int32_t *)ds.p;
+    if (nt > 0) k_pole_circ<<<gt, 256, 0, ctx->stream>>>(nt, (const int32_t *)dtri.p, x, y, cxy, key, su);
+    int64_t *bb[2] = {(int64_t *)db1.p, (int64_t *)db2.p};
+    for (int pass = 0; pass < 2; pass++) {
+        TM_CUDA_TRY(ctx, cudaMemsetAsync(dmax.p, 0, n * sizeof(unsigned long long), ctx->stream));
+        TM_CUDA_TRY(ctx, cudaMemsetAsync(dkmin.p, 0xff, n * sizeof(unsigned long long), ctx->stream));
+        TM_CUDA_TRY(ctx, cudaMemsetAsync(bb[pass], 0xff, n * sizeof(int64_t), ctx->stream));
+        if (nt > 0) {
+            k_pole_max<<<gt, 256, 0, ctx->stream>>>(nt, pass, cxy, su, x, y, x0, y0, x1, y1, bb[0],
+                                                    (unsigned long long *)dmax.p);
+            k_pole_arg<<<gt, 256, 0, ctx->stream>>>(nt, pass, cxy, su, key, x, y, x0, y0, x1, y1, bb[0],
+                                                    (const unsigned long long *)dmax.p, (unsigned long long *)dkmin.p);
+            k_pole_pick<<<gt, 256, 0, ctx->stream>>>(nt, pass, cxy, su, key, x, y, x0, y0, x1, y1, bb[0],
+                                                     (const unsigned long long *)dmax.p,
+                                                     (const unsigned long long *)dkmin.p, bb[pass]);
+        }
+        if ((s = tm_internal_check_launch(ctx, "k_pole")) != TM_OK) return s;
+    }
+    // gather v1, v2 per boundary point in order (host: a compaction of 2n candidates)
+    std::vector<int64_t> h1(n), h2(n);
+    std::vector<double> hc(2 * std::max<int64_t>(nt, 1));
+    TM_CUDA_TRY(ctx, cudaMemcpyAsync(h1.data(), bb[0], n * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    TM_CUDA_TRY(ctx, cudaMemcpyAsync(h2.data(), bb[1], n * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    if (nt > 0) TM_CUDA_TRY(ctx, cudaMemcpyAsync(hc.data(), cxy, nt * 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    TM_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    std::vector<double> vx, vy;
+    for (int64_t i = 0; i < n; i++) {
+        if (h1[i] >= 0) { vx.push_back(hc[2 * h1[i]]); vy.push_back(hc[2 * h1[i] + 1]); }
+        if (h2[i] >= 0) { vx.push_back(hc[2 * h2[i]]); vy.push_back(hc[2 * h2[i] + 1]); }
+    }
+    const int64_t m = (int64_t)vx.size();
+    int64_t kept = 0;
+    if (m > 0) {
+        DevBuf dvx, dvy, dkeep;
+        TM_CUDA_TRY(ctx, cudaMalloc(&dvx.p, m * sizeof(double)));
+        TM_CUDA_TRY(ctx, cudaMalloc(&dvy.p, m * sizeof(double)));
+        TM_CUDA_TRY(ctx, cudaMalloc(&dkeep.p, m));
+        TM_CUDA_TRY(ctx, cudaMemcpyAsync(dvx.p, vx.data(), m * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        TM_CUDA_TRY(ctx, cudaMemcpyAsync(dvy.p, vy.data(), m * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        k_medial_trim<<<(unsigned)((m + 255) / 256), 256, 0, ctx->stream>>>(m, (const double *)dvx.p, (const double *)dvy.p,
+                                                                           cmul(r_nei, r_nei), n_thres, (uint8_t *)dkeep.p);
+        if ((s = tm_internal_check_launch(ctx, "k_medial_trim")) != TM_OK) return s;
+        std::vector<uint8_t> hk(m);
+        TM_CUDA_TRY(ctx, cudaMemcpyAsync(hk.data(), dkeep.p, m, cudaMemcpyDeviceToHost, ctx->stream));
+        TM_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+        std::vector<double> kx, ky;
+        for (int64_t i = 0; i < m; i++)
+            if (hk[i]) { kx.push_back(vx[i]); ky.push_back(vy[i]); }
+        kept = (int64_t)kx.size();
+        if (kept > cap) TM_FAIL(ctx, TM_E_CAPACITY, "tm_medial_points: %lld points, capacity %lld", (long long)kept,
+                                (long long)cap);
+        if (kept > 0) {
+            TM_CUDA_TRY(ctx, cudaMemcpyAsync(mx, kx.data(), kept * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+            TM_CUDA_TRY(ctx, cudaMemcpyAsync(my, ky.data(), kept * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        }
+        TM_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+    *n_out = kept;
+    return TM_OK;
+}
+
+extern "C" tm_status tm_sizing_field(tm_ctx *ctx, const double *sx, const double *sy, int64_t ns, const double *mx,
+                                     const double *my, int64_t nm, double K, int32_t nx, int32_t ny, double x0,
+                                     double y0, double x1, double y1, double *mu, double *lfs) {
+    if (!ctx) return TM_E_ARG;
+    if (!sx || !sy || ns < 1 || !mx || !my || nm < 1 || nx < 2 || ny < 2 || !mu || !lfs || !(K >= 0.0))
+        TM_FAIL(ctx, TM_E_ARG, "bad arguments to tm_sizing_field");
+    k_lfs<<<(unsigned)((ns + 255) / 256), 256, 0, ctx->stream>>>(ns, sx, sy, nm, mx, my, lfs);
+    const int64_t nn = (int64_t)nx * ny;
+    k_sizing<<<(unsigned)((nn + 255) / 256), 256, 0, ctx->stream>>>(ns, sx, sy, lfs, K, nx, ny, x0, y0, x1, y1, mu);
+    return tm_internal_check_launch(ctx, "k_sizing");
+}
+
+extern "C" tm_status tm_density_from_sizing(tm_ctx *ctx, const double *mu, int64_t n, double *rho) {
+    if (!ctx) return TM_E_ARG;
+    if (!mu || !rho || n < 0) TM_FAIL(ctx, TM_E_ARG, "bad arguments to tm_density_from_sizing");
+    if (n == 0) return TM_OK;
+    k_density<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(mu, n, rho);
+    return tm_internal_check_launch(ctx, "k_density");
 }

@@ -68,28 +68,62 @@ def test_categories_counts_and_points_match_oracle(k, cfg_cache):
 
 
 def test_pipeline_contour_to_mesh():
-    """contour -> SDF (GPU) -> geometry grid -> fac_init * N_total initial points -> hybrid meshing
-    with point addition to termination: every point ends inside or on the boundary, the mesh has
-    N_total points and the triangle count obeys Euler's bound T <= 2N - 2."""
+    """contour -> SDF -> automatic sizing (boundary points, medial axis, lfs, mu; rho = mu^-2) ->
+    geometry grid -> fac_init * N_total initial points -> hybrid meshing with point addition to
+    termination (all on the GPU): every point ends inside or on the boundary, the mesh has N_total
+    points, the triangle count obeys Euler's bound, and the mesh is finer where mu is smaller."""
     import paper_2309_13824_b200 as T
     ctx = T.Context(0, params=T.default_params(validity=1))
     box = (0.0, 0.0, 1.0, 1.0)
     n = 257
+    segs = to_dev(_star())
     phi = torch.empty(n, n, dtype=torch.float64, device="cuda")
-    ctx.tm_contour_sdf(to_dev(_star()), n, n, box, phi)
+    ctx.tm_contour_sdf(segs, n, n, box, phi)
     n_total = 3000
-    n_init = int(0.2 * n_total)
-    ctx.tm_set_domain(box, phi, None, None, n_init)
     nxg, nyg = T.geometry_grid_dims(n_total, box)
+    dxg = 1.0 / nxg
+    mu, _, _, _ = T.automatic_sizing(ctx, segs, box, n, n, K=0.3, d_s=0.5 * dxg, geps_hat=0.01 * dxg,
+                                     r_nei=2 * 3 * 0.5 * dxg)
+    rho = torch.empty_like(mu)
+    ctx.tm_density_from_sizing(mu, rho)
+    n_init = int(0.2 * n_total)
+    ctx.tm_set_domain(box, phi, mu, rho, n_init)
     x, y, cat, counts = T.initial_points(ctx, n_init, nxg, nyg, seed=1)
-    ctx.tm_set_domain(box, phi, None, None, x.shape[0])
+    ctx.tm_set_domain(box, phi, mu, rho, x.shape[0])
     res = T.mesh(ctx, x, y, n_total=n_total, method="hybrid", max_iterations=400)
     acts = [h["action"] for h in res.history]
-    assert acts[-1] in ("terminate_quality", "terminate_moves")
+    assert acts[-1] in ("terminate_quality", "terminate_moves"), acts[-5:]
     assert res.x.shape[0] == n_total
-    fs = O.FieldSet(box, phi.cpu().numpy())
+    fs = O.FieldSet(box, phi.cpu().numpy(), mu=mu.cpu().numpy())
     xs, ys = res.x.cpu().numpy(), res.y.cpu().numpy()
     _, ha = O.domain(fs, n_total)
     worst = max(O.field_value(fs, "phi", a, b) for a, b in zip(xs, ys))
     assert worst <= 0.01 * ha + 1e-12
     assert 0 < res.tri.shape[0] <= 2 * n_total - 2
+    # edge length follows mu: the mean edge over mu at the edge midpoint is nearly constant
+    t = res.tri.cpu().numpy()
+    e = np.concatenate([t[:, [0, 1]], t[:, [1, 2]], t[:, [2, 0]]])
+    L = np.hypot(xs[e[:, 0]] - xs[e[:, 1]], ys[e[:, 0]] - ys[e[:, 1]])
+    m = np.array([O.field_value(fs, "mu", 0.5 * (xs[a] + xs[b]), 0.5 * (ys[a] + ys[b])) for a, b in e])
+    r = L / m
+    lo, hi = m < np.quantile(m, 0.25), m > np.quantile(m, 0.75)
+    assert L[lo].mean() < L[hi].mean() and 0.6 < r[lo].mean() / r[hi].mean() < 1.6
+
+
+def test_automatic_sizing_matches_oracle():
+    """App. A + P:356-373 on the star contour: boundary points, medial points (poles of the
+    library's own Delaunay, trimmed), lfs and the sizing field, bit for bit."""
+    import paper_2309_13824_b200 as T
+    ctx = T.Context(0)
+    box = (0.0, 0.0, 1.0, 1.0)
+    segs = _star()
+    d_s, geps_hat, r_nei, K = 0.008, 5e-4, 2 * 3 * 0.008, 0.1
+    mu, (sx, sy), (mx, my), lfs = T.automatic_sizing(ctx, to_dev(segs), box, 129, 129, K, d_s, geps_hat, r_nei)
+    ox, oy = O.boundary_points(segs, d_s, geps_hat)
+    assert np.array_equal(sx.cpu().numpy(), ox) and np.array_equal(sy.cpu().numpy(), oy)
+    omx, omy = O.medial_points(ox, oy, box, r_nei, 3)
+    assert len(omx) > 10
+    assert np.array_equal(mx.cpu().numpy(), omx) and np.array_equal(my.cpu().numpy(), omy)
+    omu, olfs = O.sizing_field(ox, oy, omx, omy, K, 129, 129, box)
+    assert np.array_equal(lfs.cpu().numpy(), olfs)
+    assert np.array_equal(mu.cpu().numpy(), omu)

@@ -177,3 +177,54 @@ def test_init_points_in_their_cells_and_projected():
                 else:
                     assert abs(O.field_value(fs, "phi", x[k], y[k])) <= geps  # projected
                 k += 1
+
+
+def _circle(n=400, r=0.3, c=(0.5, 0.5)):
+    P = [(c[0] + r * math.cos(-2 * math.pi * k / n), c[1] + r * math.sin(-2 * math.pi * k / n)) for k in range(n)]
+    return np.array([[*P[k], *P[(k + 1) % n]] for k in range(n)])
+
+
+def test_boundary_points_are_trimmed_to_spacing():
+    """App. A: after trimming every point's nearest neighbour is at least d_s away,
+    and a circle of perimeter 2 pi r keeps between 2 pi r / (2 d_s) and 2 pi r / d_s points."""
+    segs = _circle(300)
+    d_s = 0.01
+    x, y = O.boundary_points(segs, d_s, 1e-3)
+    P = np.stack([x, y], 1)
+    D = np.sqrt(((P[:, None, :] - P[None, :, :]) ** 2).sum(-1)) + np.eye(len(x))
+    assert D.min() >= d_s
+    per = 2 * math.pi * 0.3
+    assert per / (2 * d_s) <= len(x) <= per / d_s
+    assert np.abs(np.hypot(x - 0.5, y - 0.5) - 0.3).max() < 1e-3  # on the boundary
+
+
+def test_medial_axis_and_sizing_of_a_circle():
+    """A circle's medial axis is its centre: the poles gather there, lfs(s) = r for every
+    boundary point, and mu(x) = K (r - |x - c|) + r inside (Eq. sizing field)."""
+    segs = _circle(300)
+    x, y = O.boundary_points(segs, 0.01, 1e-3)
+    box = (0.0, 0.0, 1.0, 1.0)
+    mx, my = O.medial_points(x, y, box, r_nei=2 * 3 * 0.01, n_thres=3)
+    assert len(mx) > 0 and np.hypot(mx - 0.5, my - 0.5).max() < 0.01
+    K = 0.2
+    mu, lfs = O.sizing_field(x, y, mx, my, K, 21, 21, box)
+    assert np.abs(lfs - 0.3).max() < 0.01
+    g = configs.node_coords(0, 1, 21)
+    for j in range(21):
+        for i in range(21):
+            rho = math.hypot(g[i] - 0.5, g[j] - 0.5)
+            if rho < 0.25:
+                assert abs(mu[j, i] - (K * (0.3 - rho) + 0.3)) < 0.012, (i, j)
+
+
+def test_lfs_of_a_thin_strip_is_its_half_thickness():
+    """Rectangle [0.1, 0.9] x [0.45, 0.55] (clockwise): the medial axis of the long part is the
+    centre line, so boundary points on the long sides away from the ends have lfs = 0.05."""
+    P = [(0.1, 0.45), (0.1, 0.55), (0.9, 0.55), (0.9, 0.45)]
+    segs = np.array([[*P[k], *P[(k + 1) % 4]] for k in range(4)])
+    x, y = O.boundary_points(segs, 0.01, 1e-3)
+    mx, my = O.medial_points(x, y, (0.0, 0.0, 1.0, 1.0), r_nei=0.06, n_thres=3)
+    _, lfs = O.sizing_field(x, y, mx, my, 0.1, 5, 5, (0.0, 0.0, 1.0, 1.0))
+    mid = (x > 0.3) & (x < 0.7)
+    assert mid.sum() > 20
+    assert np.abs(lfs[mid] - 0.05).max() < 0.006
