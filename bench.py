@@ -339,6 +339,41 @@ def roofline(per, cells_ms, it_ms):
                                       for m in wsum if wsum[m][0]}}
 
 
+# ---------------------------------------------------------------- the paper's E1 (context)
+def run_paper_e1(T, dev, n=1_000_000):
+    """The paper's uniform-square experiment end to end: Floyd-Steinberg initial points
+    (init all), the paper's validity tests and controller, CVD and hybrid meshing to termination
+    (NEXT-2..4).  Time per triangulation = wall time of the meshing loop (its per-iteration
+    controller syncs included) / triangulations: the paper's metric; context for its
+    28-thread 0.221 s (CVD) and 0.251 s (hybrid) per triangulation."""
+    import time
+
+    import torch
+    from inputs import configs
+    box = (0.0, 0.0, 1.0, 1.0)
+    phi = torch.from_numpy(configs.box_phi(box, 1024)).to(dev)
+    nxg, nyg = T.geometry_grid_dims(n, box)
+    out = {"workload": "uniform unit square, N = 1e6, init all (fac_init = 1), validity Tests 1-3, "
+                       "meshing to termination (P:705-745)"}
+    for method in ("cvd", "hybrid"):
+        ctx = T.Context(0, params=T.default_params(validity=1))
+        ctx.tm_set_domain(box, phi, None, None, n)
+        x, y, _, _ = T.initial_points(ctx, n, nxg, nyg, seed=3)
+        ctx.tm_set_domain(box, phi, None, None, x.shape[0])
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = T.mesh(ctx, x, y, n_total=n, method=method, max_iterations=400)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        out[method] = {"triangulations": res.iterations, "seconds": dt, "s_per_triangulation": dt / res.iterations,
+                       "end": res.history[-1]["action"], "n_tri": int(res.tri.shape[0]),
+                       "half_mean_alpha": res.history[-1]["half_alpha"],
+                       "paper_28_threads_s_per_triangulation": {"cvd": 0.220976, "hybrid": 0.250808}[method],
+                       "paper_triangulations": {"cvd": 52, "hybrid": 57}[method]}
+        ctx.close()
+    return out
+
+
 # ---------------------------------------------------------------- cfg5 leg
 def run_cfg5(T, dev, stream, n, iters=20, count=True):
     """North-star scaling workload at N=1: jittered uniform square, n points, `iters` CVD
@@ -408,6 +443,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cfg5", action="store_true")
+    ap.add_argument("--no-paper-e1", action="store_true")
     ap.add_argument("--cfg5-sizes", default="16000000,64000000")
     ap.add_argument("--strips", action="store_true", help="use the x-strip path even at N=1")
     ap.add_argument("--flags", type=int, default=0, help="extra tm_params.flags (A/B)")
@@ -636,6 +672,10 @@ def main():
             cfg5[str(nn)] = run_cfg5(T, dev, stream, nn)
         cfg5["workload"] = "cfg5: jittered uniform unit square, 20 CVD iterations per step (SURVEY §8(d) cfg5)"
 
+    paper_e1 = None
+    if not args.no_paper_e1 and world == 1 and not strip_mode:
+        paper_e1 = run_paper_e1(T, dev)
+
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline and "cvd" in saved:
@@ -665,6 +705,7 @@ def main():
             "ms_per_iteration": {m: (statistics.mean(v) if v else None) for m, v in it_ms.items()},
             "cells_ms_per_launch": {k: (statistics.mean(v) if v else None) for k, v in cells_ms.items()},
             "cfg5": cfg5,
+            "paper_e1": paper_e1,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
