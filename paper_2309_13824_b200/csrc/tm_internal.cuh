@@ -205,39 +205,38 @@ namespace tmg {
 // in the same order as the oracle (canonical, uncontracted: identical bits).
 // Sphere tracing from the inner p_old toward p_new: q <- q + |phi~(q)| u, a step never
 // passing p_new, until |phi~(q)| <= geps, at most trace_max steps (L39).
+// results by value (a reference output would take the caller's variables' addresses: a local-memory
+// frame in every kernel that can reach the treatment, projection used or not)
+struct ProjResult {
+    double x, y;
+    bool ok;
+};
+
 template <typename Load>
-__device__ __noinline__ bool sphere_trace(const Grid &g, const double *phi, double xo, double yo, double xn,
-                                          double yn, double geps, int trace_max, double &qx_out, double &qy_out,
-                                          Load ld) {
+__device__ __noinline__ ProjResult sphere_trace(const Grid &g, const double *phi, double xo, double yo, double xn,
+                                                double yn, double geps, int trace_max, Load ld) {
     const double dx = csub(xn, xo), dy = csub(yn, yo);
     const double len = sqrt(cadd(cmul(dx, dx), cmul(dy, dy)));
     const double ux = cdiv(dx, len), uy = cdiv(dy, len);
     double qx = xo, qy = yo, s = 0.0;
     for (int k = 0; k < trace_max; k++) {
         const double v = bilinear(g, phi, qx, qy, ld);
-        if (fabs(v) <= geps) {
-            qx_out = qx;
-            qy_out = qy;
-            return true;
-        }
+        if (fabs(v) <= geps) return ProjResult{qx, qy, true};
         double r = fabs(v);
         if (cadd(s, r) > len) r = csub(len, s);
         s = cadd(s, r);
         qx = cadd(qx, cmul(r, ux));
         qy = cadd(qy, cmul(r, uy));
     }
-    qx_out = qx;
-    qy_out = qy;
-    return fabs(bilinear(g, phi, qx, qy, ld)) <= geps;
+    return ProjResult{qx, qy, fabs(bilinear(g, phi, qx, qy, ld)) <= geps};
 }
 
 // Damped Newton projection: L(p) = [phi~(p), (p - p_new) x grad phi~(p)] = 0 from
 // p_new, the Jacobian of Eq. projection_Newton_Jacobian with central finite differences of step
 // deps (L36, L41), p <- p - alpha J^-1 L clamped into B, until |phi~| <= geps.
 template <typename Load>
-__device__ __noinline__ bool newton_project(const Grid &g, const double *phi, double xn, double yn, double geps,
-                                            double deps, double damping, int newton_max, double &qx_out,
-                                            double &qy_out, Load ld) {
+__device__ __noinline__ ProjResult newton_project(const Grid &g, const double *phi, double xn, double yn, double geps,
+                                                  double deps, double damping, int newton_max, Load ld) {
     double x = xn, y = yn;
     bool ok = false;
     for (int k = 0; k < newton_max; k++) {
@@ -271,9 +270,7 @@ __device__ __noinline__ bool newton_project(const Grid &g, const double *phi, do
             break;
         }
     }
-    qx_out = x;
-    qy_out = y;
-    return ok;
+    return ProjResult{x, y, ok};
 }
 
 // S5 treatment of one point (L20-L22); returns status.
@@ -302,18 +299,17 @@ __device__ __forceinline__ int treat_point(const Grid &g, const double *phi, dou
     double ph = bilinear(g, phi, qx, qy, ld);
     if (!(ph <= geps) && projection == 1) {
         const double po = bilinear(g, phi, xo, yo, ld);
-        double tx, ty;
-        bool ok;
+        ProjResult r;
         if (po < -geps) {
-            ok = sphere_trace(g, phi, xo, yo, qx, qy, geps, trace_max, tx, ty, ld);
+            r = sphere_trace(g, phi, xo, yo, qx, qy, geps, trace_max, ld);
             status |= 8;
         } else {
-            ok = newton_project(g, phi, qx, qy, geps, cmul(1.4901161193847656e-08, hm), damping, newton_max, tx, ty,
-                                ld);
+            r = newton_project(g, phi, qx, qy, geps, cmul(1.4901161193847656e-08, hm), damping, newton_max, ld);
         }
+        const bool ok = r.ok;
         if (ok) {
-            qx = tx;
-            qy = ty;
+            qx = r.x;
+            qy = r.y;
             status |= 1;
         } else {
             qx = xo;

@@ -182,11 +182,11 @@ __global__ void k_init_points(int64_t n_pts, const int64_t *__restrict__ off, in
     const double hm = h < h_avg ? h : h_avg;
     const double geps = cmul(fac_geps, hm);
     if (bilinear(g, phi, px, py, LdgLoad()) > geps) {
-        double qx, qy;
-        if (newton_project(g, phi, px, py, geps, cmul(1.4901161193847656e-08, hm), damping, newton_max, qx, qy,
-                           LdgLoad())) {
-            px = qx;
-            py = qy;
+        const ProjResult r =
+            newton_project(g, phi, px, py, geps, cmul(1.4901161193847656e-08, hm), damping, newton_max, LdgLoad());
+        if (r.ok) {
+            px = r.x;
+            py = r.y;
         }
     }
     x[k] = px;
