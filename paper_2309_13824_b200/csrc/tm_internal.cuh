@@ -213,7 +213,7 @@ struct ProjResult {
 };
 
 template <typename Load>
-__device__ __noinline__ ProjResult sphere_trace(const Grid &g, const double *phi, double xo, double yo, double xn,
+__device__ __forceinline__ ProjResult sphere_trace(const Grid &g, const double *phi, double xo, double yo, double xn,
                                                 double yn, double geps, int trace_max, Load ld) {
     const double dx = csub(xn, xo), dy = csub(yn, yo);
     const double len = sqrt(cadd(cmul(dx, dx), cmul(dy, dy)));
@@ -235,7 +235,7 @@ __device__ __noinline__ ProjResult sphere_trace(const Grid &g, const double *phi
 // p_new, the Jacobian of Eq. projection_Newton_Jacobian with central finite differences of step
 // deps (L36, L41), p <- p - alpha J^-1 L clamped into B, until |phi~| <= geps.
 template <typename Load>
-__device__ __noinline__ ProjResult newton_project(const Grid &g, const double *phi, double xn, double yn, double geps,
+__device__ __forceinline__ ProjResult newton_project(const Grid &g, const double *phi, double xn, double yn, double geps,
                                                   double deps, double damping, int newton_max, Load ld) {
     double x = xn, y = yn;
     bool ok = false;
