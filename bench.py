@@ -433,6 +433,57 @@ def run_cfg5(T, dev, stream, n, iters=20, count=True):
     return out
 
 
+def run_cfg5_strips(T, dev, stream, n, rank, world, iters=20):
+    """The north-star scaling workload on `world` ranks: cfg5's points split
+    into equal-width x-strips (uniform density), each rank meshing its strip with the ghost-point
+    halo and migration exchanged over NCCL every iteration; one untimed pass, then one timed pass
+    between barriers; the time is the max over ranks (value = all ranks' points x iterations / t)."""
+    import torch
+    import torch.distributed as dist
+    from inputs import configs
+    from paper_2309_13824_b200 import strips as S
+    c = configs.config5(n=n, iters=iters)
+    params = T.default_params()
+    ctx = T.Context(dev.index or 0, stream=stream, params=params)
+    ctx.tm_set_domain(c.box, torch.from_numpy(c.phi).to(dev), None, None, c.n)
+    strips = S.Strips(c.box[0], c.box[2], world)
+    W = S.ghost_width(ctx.c, params.fac_voro_bound, 1.0)
+    x0, y0 = torch.from_numpy(c.x).to(dev), torch.from_numpy(c.y).to(dev)
+    del c
+    cap_own, cap_msg = S.capacities(n, world, int(n * W) + 1)
+    St = S.split_initial(x0, y0, strips, rank, cap_own, cap_msg)
+    del x0, y0
+    xo_, yo_, go_, _ = St.owned()
+    x_own, y_own, g_own = xo_.clone(), yo_.clone(), go_.clone()
+    counts0 = St.counts.clone()
+    comm = S.TorchP2P(rank, world, dev)
+    backend = S.GpuStripBackend(ctx, params.adj_stride)
+
+    def one():
+        St.reset(x_own, y_own, g_own, counts0)
+        for _ in range(iters):
+            S.strip_step(St, strips, backend, comm, W, "cvd")
+    one()
+    ctx.tm_sync()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    one()
+    e1.record(stream)
+    e1.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ctx.tm_sync()
+    tmax = float(t.item())
+    ctx.close()
+    return {"n_points": n, "iterations": iters, "ms_per_iteration": 1e3 * tmax / iters, "value": n * iters / tmax,
+            "unit": UNIT, "ranks": world, "strips": "equal-width x-strips, NCCL halo + migration every iteration",
+            "per_gpu_points": n // world}
+
+
 # ---------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -665,11 +716,12 @@ def main():
         roof = roofline(per, cells_ms, it_ms)
 
     cfg5 = None
-    if not args.no_cfg5 and world == 1 and not strip_mode:
+    if not args.no_cfg5:
         cfg5 = {}
         for nn in [int(v) for v in args.cfg5_sizes.split(",") if v]:
             torch.cuda.empty_cache()
-            cfg5[str(nn)] = run_cfg5(T, dev, stream, nn)
+            cfg5[str(nn)] = (run_cfg5_strips(T, dev, stream, nn, rank, world) if strip_mode
+                             else run_cfg5(T, dev, stream, nn))
         cfg5["workload"] = "cfg5: jittered uniform unit square, 20 CVD iterations per step (SURVEY §8(d) cfg5)"
 
     paper_e1 = None
