@@ -50,6 +50,9 @@ using namespace tmg;
 #ifndef TM_R2_CACHE
 #define TM_R2_CACHE 1  // cache each vertex's r^2 bound in shared memory
 #endif
+#ifndef TM_GROUP_SHIFT
+#define TM_GROUP_SHIFT 2  // measured: 1, 2, 3 all ~5 % faster than per-leaf groups, 2 best; whole-warp 3x slower
+#endif
 #ifndef TM_THREAD_EXACT
 #define TM_THREAD_EXACT 0  // 0: cells with an undecided filter go to the 32-lane group kernel (rare)
 #endif
@@ -792,9 +795,10 @@ __global__ void __launch_bounds__(TB, (MODE & M_WCERT) ? TM_WMINB : TM_TMINB) k_
                 fb = __ballot_sync(0xffffffffu, flq);
             }
         };
-        // groups: runs of lanes with the same home leaf
-        const unsigned long long lkey =
-            ((unsigned long long)rh << 48) | ((unsigned long long)(unsigned)ux << 24) | (unsigned)uy;
+        // groups: runs of lanes with the same home leaf (blocks of 2^TM_GROUP_SHIFT leaves per side)
+        const unsigned long long lkey = ((unsigned long long)rh << 48) |
+                                        ((unsigned long long)(unsigned)(ux >> TM_GROUP_SHIFT) << 24) |
+                                        (unsigned)(uy >> TM_GROUP_SHIFT);
         const unsigned long long lprev = __shfl_up_sync(0xffffffffu, lkey, 1);
         for (unsigned hm = __ballot_sync(0xffffffffu, lane == 0 || lkey != lprev); hm;) {
             const int g0 = __ffs(hm) - 1;
@@ -835,20 +839,42 @@ __global__ void __launch_bounds__(TB, (MODE & M_WCERT) ? TM_WMINB : TM_TMINB) k_
                 const int l = l0 + lane;
                 int st = 0, cnt = 0;
                 if (l < nL) {
-                    const int vy = l / nLx, vx = bxa + (l - vy * nLx);
-                    // any cell of the group within reach (float, conservative: the leaf is widened
-                    // by 1e-5 of its size, the bound carries a 1e-4 margin)
-                    const float ax = lxf + (float)(vx * lsxg), ay = lyf + (float)((bya + vy) * lsyg);
-                    const float wx = (float)lsxg, wy = (float)lsyg, ex = 1e-5f * wx, ey = 1e-5f * wy;
-                    bool need = false;
-                    for (unsigned m = gact; m; m &= m - 1) {
-                        const int c = __ffs(m) - 1;
-                        const float4 q = W.cf[c];
-                        const float gx = fmaxf(fmaxf(ax - ex - q.x, q.x - (ax + wx + ex)), 0.f);
-                        const float gy = fmaxf(fmaxf(ay - ey - q.y, q.y - (ay + wy + ey)), 0.f);
-                        need |= gx * gx + gy * gy < q.z;
+                    const int vy = l / nLx, vx = bxa + (l - vy * nLx), vyy = bya + vy;
+                    // the rectangle to test: the virtual leaf, or -- in a coarser bin -- the whole
+                    // coarse leaf, which vleaf_range returns once, at its virtual leaf closest to the
+                    // group's first home leaf (inside the union box, which holds that leaf); a group
+                    // spanning several home leaves must test the coarse leaf as a whole
+                    int x0l = vx, y0l = vyy, span = 1;
+                    bool canon = true;
+                    {
+                        const int b = (vyy >> rhg) * bg.nbx + (vx >> rhg);
+                        const int rb = b == hbg ? rhg : __ldg(A.rlev + b);
+                        if (rb < rhg) {
+                            const int d = rhg - rb, Lx = vx >> d, Ly = vyy >> d;
+                            const int rx = min(max(uxg, Lx << d), ((Lx + 1) << d) - 1);
+                            const int ry = min(max(uyg, Ly << d), ((Ly + 1) << d) - 1);
+                            canon = rx == vx && ry == vyy;
+                            x0l = Lx << d;
+                            y0l = Ly << d;
+                            span = 1 << d;
+                        }
                     }
-                    if (need) vleaf_range(A, vx, bya + vy, rhg, uxg, uyg, hbg, hoffg, st, cnt);
+                    if (canon) {
+                        // any cell of the group within reach (float, conservative: the leaf is widened
+                        // by 1e-5 of its size, the bound carries a 1e-4 margin)
+                        const float ax = lxf + (float)(x0l * lsxg), ay = lyf + (float)(y0l * lsyg);
+                        const float wx = (float)(span * lsxg), wy = (float)(span * lsyg), ex = 1e-5f * wx,
+                                    ey = 1e-5f * wy;
+                        bool need = false;
+                        for (unsigned m = gact; m; m &= m - 1) {
+                            const int c = __ffs(m) - 1;
+                            const float4 q = W.cf[c];
+                            const float gx = fmaxf(fmaxf(ax - ex - q.x, q.x - (ax + wx + ex)), 0.f);
+                            const float gy = fmaxf(fmaxf(ay - ey - q.y, q.y - (ay + wy + ey)), 0.f);
+                            need |= gx * gx + gy * gy < q.z;
+                        }
+                        if (need) vleaf_range(A, vx, vyy, rhg, uxg, uyg, hbg, hoffg, st, cnt);
+                    }
                 }
                 int incl = cnt;
 #pragma unroll
