@@ -898,23 +898,28 @@ __global__ void __launch_bounds__(TB, (MODE & M_WCERT) ? TM_WMINB : TM_TMINB) k_
                     const int j = stk + (tt - exk);
                     float xjf = 3e38f, yjf = 3e38f;
                     if (valid) { xjf = (float)(__ldg(A.xs + j) - ox); yjf = (float)(__ldg(A.ys + j) - oy); }
+                    // the group's cells near this lane's candidate, as a mask (conservative: a few
+                    // extra pairs are harmless, the ring test decides; the cell's own point and exact
+                    // duplicates are sorted out there) ...
+                    unsigned nm = 0u;
                     for (unsigned m = gact; m; m &= m - 1) {
                         const int c = __ffs(m) - 1;
                         const float4 q = W.cf[c];
                         const float dx = xjf - q.x, dy = yjf - q.y;
-                        // conservative: a few extra pairs are harmless, the ring test decides (the
-                        // cell's own point and exact duplicates are sorted out there)
-                        const bool near = fmaf(dx, dx, dy * dy) < q.z;
-                        const unsigned b = __ballot_sync(0xffffffffu, near);
-                        if (b) {
-                            if (near) {
-                                const int pos = qn + __popc(b & lt);
-                                W.qj[pos] = j;
-                                W.qc[pos] = (uint8_t)c;
-                            }
-                            qn += __popc(b);
-                            if (qn >= 32) flush(32);
+                        nm |= (unsigned)(fmaf(dx, dx, dy * dy) < q.z) << c;
+                    }
+                    // ... queued one pair per lane per round (rounds = the most near cells of a lane)
+                    for (;;) {
+                        const unsigned b = __ballot_sync(0xffffffffu, nm != 0u);
+                        if (!b) break;
+                        if (nm) {
+                            const int pos = qn + __popc(b & lt);
+                            W.qj[pos] = j;
+                            W.qc[pos] = (uint8_t)(__ffs(nm) - 1);
+                            nm &= nm - 1;
                         }
+                        qn += __popc(b);
+                        if (qn >= 32) flush(32);
                     }
                 }
             }
