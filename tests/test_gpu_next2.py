@@ -113,25 +113,10 @@ def _near_threshold(prev, cur, cp, tol=1e-9):
     return any(abs(r - t) <= tol * t for r in rel for t in ths)
 
 
-def test_mesh_to_termination_with_point_addition():
-    """Unit disk, N_total = 2500 from fac_init = 0.2 (P:1091), hybrid DistMesh -> CVD, the paper's
-    validity tests.  Every iteration is checked against the oracle from the GPU's state, every
-    controller decision against the oracle controller fed with the oracle's quality of that state,
-    every point addition against the oracle's on the same mesh; the run must add points up to
-    N_total, switch to CVD and terminate."""
-    import paper_2309_13824_b200 as T
-    box = (-1.1, -1.1, 1.1, 1.1)
-    phi = configs.disk_phi(box, 257)
-    n_total = 2500
-    x0, y0 = _disk(int(0.2 * n_total), 11)
-    ctx = T.Context(0, params=T.default_params(validity=1))
-    ctx.tm_set_domain(box, to_dev(phi), None, None, len(x0))
-    fs = O.FieldSet(box, phi)
-    op = O.default_params(validity=1)
-    octl = O.Controller(n_total, len(x0), method="hybrid")
-    octl.cp.max_iterations = 400
-    st = {"expect_new": None, "ties": 0}
-
+def _checker(ctx, fs, box, op, octl, st):
+    """Per-iteration parity of mesh(): the oracle's iteration from the GPU's state (kept sets exact,
+    positions within the bar, CVD bit for bit), the movement count, the controller decision (fed
+    with the oracle's quality of that state; only exact ties may differ) and the added points."""
     def check(d):
         it, mode = d["it"], d["mode"]
         x, y = d["x"].cpu().numpy(), d["y"].cpu().numpy()
@@ -149,8 +134,7 @@ def test_mesh_to_termination_with_point_addition():
         omc = O.move_count(fs, o.info.c, o.info.h_avg, x, y, o.d_prev)
         assert omc == d["moves"], f"it{it}: move count {d['moves']} vs oracle {omc}"
         prev = octl.prev
-        ost = O.stats(o.tri, x, y)
-        oq = O.quality_of(ost)
+        oq = O.quality_of(O.stats(o.tri, x, y))
         oa = octl.update(*oq, move_count=omc)
         if oa["action"] == "terminate":
             oa["action"] = "terminate_" + {"quality": "quality", "movement": "moves", "max_iterations": "cap"}[oa["reason"]]
@@ -160,10 +144,56 @@ def test_mesh_to_termination_with_point_addition():
         if d["action"] == "add":
             ex, ey, _ = O.point_addition(fs, o.info.c, g["tri"], x, y, d["n_add"])
             st["expect_new"] = (n, ex, ey)
+        st["its"] += 1
+    return check
 
+
+def test_mesh_to_termination_with_point_addition():
+    """Unit disk, N_total = 2500 from fac_init = 0.2 (P:1091), hybrid DistMesh -> CVD, the paper's
+    validity tests.  Every iteration is checked against the oracle from the GPU's state, every
+    controller decision against the oracle controller fed with the oracle's quality of that state,
+    every point addition against the oracle's on the same mesh; the run must add points up to
+    N_total, switch to CVD and terminate."""
+    import paper_2309_13824_b200 as T
+    box = (-1.1, -1.1, 1.1, 1.1)
+    phi = configs.disk_phi(box, 257)
+    n_total = 2500
+    x0, y0 = _disk(int(0.2 * n_total), 11)
+    ctx = T.Context(0, params=T.default_params(validity=1))
+    ctx.tm_set_domain(box, to_dev(phi), None, None, len(x0))
+    fs = O.FieldSet(box, phi)
+    octl = O.Controller(n_total, len(x0), method="hybrid")
+    octl.cp.max_iterations = 400
+    st = {"expect_new": None, "ties": 0, "its": 0}
     res = T.mesh(ctx, to_dev(x0), to_dev(y0), n_total=n_total, method="hybrid", max_iterations=400,
-                 on_iteration=check)
+                 on_iteration=_checker(ctx, fs, box, O.default_params(validity=1), octl, st))
     acts = [h["action"] for h in res.history]
     assert acts[-1] in ("terminate_quality", "terminate_moves"), res.history[-1]
-    assert res.x.shape[0] == n_total and st["ties"] == 0
+    assert res.x.shape[0] == n_total and st["ties"] == 0 and st["its"] == res.iterations
     assert "switch" in acts and acts.count("add") >= 3
+
+
+def test_adaptive_mesh_to_termination(cfg_cache):
+    """cfg3's adaptive annulus fields (rho = mu^-2, mu between 0.002 and 0.02) at N_total = 20000:
+    Floyd-Steinberg initial points for fac_init = 0.2 (NEXT-4), then CVD meshing with point
+    addition to termination, every iteration, decision and added point set checked against the
+    oracle (the R_circ / h(g) ranking with non-uniform h, the rescaled c, the adaptive quadrature)."""
+    import paper_2309_13824_b200 as T
+    c = cfg_cache(3)
+    n_total = 20_000
+    n_init = int(0.2 * n_total)
+    ctx = T.Context(0, params=T.default_params(validity=1))
+    phi, mu, rho = to_dev(c.phi), to_dev(c.mu), to_dev(c.rho)
+    ctx.tm_set_domain(c.box, phi, mu, rho, n_init)
+    nxg, nyg = T.geometry_grid_dims(n_total, c.box)
+    x, y, _, _ = T.initial_points(ctx, n_init, nxg, nyg, seed=9)
+    ctx.tm_set_domain(c.box, phi, mu, rho, x.shape[0])
+    fs = O.FieldSet.from_config(c)
+    octl = O.Controller(n_total, x.shape[0], method="cvd")
+    octl.cp.max_iterations = 300
+    st = {"expect_new": None, "ties": 0, "its": 0}
+    res = T.mesh(ctx, x, y, n_total=n_total, method="cvd", max_iterations=300,
+                 on_iteration=_checker(ctx, fs, c.box, O.default_params(validity=1), octl, st))
+    acts = [h["action"] for h in res.history]
+    assert acts[-1] in ("terminate_quality", "terminate_moves"), acts[-3:]
+    assert res.x.shape[0] == n_total and st["ties"] == 0 and acts.count("add") >= 3
