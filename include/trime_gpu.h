@@ -409,6 +409,21 @@ tm_status tm_sizing_field(tm_ctx *ctx, const double *sx, const double *sy, int64
                           const double *my, int64_t nm, double K, int32_t nx, int32_t ny, double x0, double y0,
                           double x1, double y1, double *mu, double *lfs);
 
+/* Adaptive distance field on the boundary geometry cells (after Frisken et al.; L48):
+ * tm_adf_build: per boundary cell (cat == 1 from tm_geometry_categories on an nxg x nyg grid) a
+ *   top-down quadtree whose nodes hold the contour's exact SDF (segs as tm_contour_sdf) at their
+ *   corners; a node splits into 4 while the largest error of its bilinear interpolant at the 4
+ *   edge midpoints and the centre exceeds E_tol = fac_etol * geps_i * fac_pt (fac_etol 0.1,
+ *   P:1107; geps_i = fac_geps min(h(m_i), h_avg); fac_pt = sqrt(N_current / N_total)) and its
+ *   depth is below max_depth (10).  The trees live in the context; *n_nodes / *n_leaves
+ *   (host, may be NULL) report their size.  synchronises
+ * tm_adf_eval: out[i] (device) = the ADF at (x[i], y[i]) (device): descend to the leaf holding the
+ *   point (x >= a node's mid line goes right / up), bilinear in its corners; NaN outside the
+ *   boundary cells.  Asynchronous. */
+tm_status tm_adf_build(tm_ctx *ctx, const double *segs, int64_t n_seg, int32_t nxg, int32_t nyg, const int8_t *cat,
+                       double fac_etol, double fac_pt, int32_t max_depth, int64_t *n_nodes, int64_t *n_leaves);
+tm_status tm_adf_eval(tm_ctx *ctx, const double *x, const double *y, int64_t n, double *out);
+
 /* rho = 1 / mu^2 elementwise (Eq. density sizing relationship), device arrays. Asynchronous. */
 tm_status tm_density_from_sizing(tm_ctx *ctx, const double *mu, int64_t n, double *rho);
 

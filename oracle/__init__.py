@@ -172,6 +172,15 @@ def lib():
                                       ctypes.c_void_p, ctypes.c_double, ctypes.c_int32, ctypes.c_int32,
                                       ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                       ctypes.c_void_p, ctypes.c_void_p]
+        L.or_adf_build.restype = ctypes.c_void_p
+        L.or_adf_build.argtypes = [ctypes.POINTER(Fields), ctypes.POINTER(Params), ctypes.c_double, ctypes.c_double,
+                                   ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                   ctypes.c_double, ctypes.c_double, ctypes.c_int32,
+                                   ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
+        L.or_adf_eval.restype = ctypes.c_double
+        L.or_adf_eval.argtypes = [ctypes.c_void_p, ctypes.c_double, ctypes.c_double]
+        L.or_adf_free.restype = None
+        L.or_adf_free.argtypes = [ctypes.c_void_p]
         _lib = L
     return _lib
 
@@ -586,3 +595,27 @@ def sizing_field(sx, sy, mx, my, K, nx, ny, box):
     lib().or_sizing_field(len(sx), _p(sx), _p(sy), len(mx), _p(mx), _p(my), float(K), int(nx), int(ny), box[0],
                           box[1], box[2], box[3], _p(mu), _p(lfs))
     return mu.reshape(ny, nx), lfs
+
+
+class ADF:
+    """quadtree ADFs of the contour's SDF on the boundary cells (cat == 1)."""
+
+    def __init__(self, fs: FieldSet, c, h_avg, cat, segs, fac_etol=0.1, fac_pt=1.0, max_depth=10, params=None):
+        params = params or default_params()
+        nyg, nxg = cat.shape
+        self._cat = np.ascontiguousarray(cat, dtype=np.int8)
+        self._segs = np.ascontiguousarray(segs, dtype=np.float64)
+        nn, nl = ctypes.c_int64(), ctypes.c_int64()
+        self.h = lib().or_adf_build(ctypes.byref(fs.c), ctypes.byref(params), c, h_avg, nxg, nyg, _p(self._cat),
+                                    _p(self._segs), self._segs.shape[0], fac_etol, fac_pt, max_depth,
+                                    ctypes.byref(nn), ctypes.byref(nl))
+        self.n_nodes, self.n_leaves = nn.value, nl.value
+
+    def __call__(self, x, y):
+        return lib().or_adf_eval(self.h, float(x), float(y))
+
+    def __del__(self):
+        try:
+            lib().or_adf_free(self.h)
+        except Exception:
+            pass

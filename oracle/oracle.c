@@ -1875,3 +1875,99 @@ void or_sizing_field(int64_t ns, const double *sx, const double *sy, int64_t nm,
             mu[(int64_t)j * nx + i] = b;
         }
 }
+
+/* ---- NEXT-4: adaptive distance field on the boundary cells (after Frisken et al.) --- */
+/* Top-down quadtree per boundary geometry cell: a node holds the exact SDF of the shape input (the
+ * contour, or_contour_sdf_point) at its 4 corners; it is subdivided into 4 children while the
+ * largest error of its bilinear interpolant at the 4 edge midpoints and the centre exceeds E_tol
+ * and its depth (root 0) is below max_depth.  E_tol = fac_etol * geps_i * fac_pt, geps_i =
+ * fac_geps * min(h(m_i), h_avg) at the cell midpoint m_i, fac_pt = sqrt(N_current / N_total).
+ * Evaluation: descend to the leaf holding p (x >= the node's mid line goes right/up), bilinear
+ * interpolation of its corners.  Reading L48. */
+typedef struct { double x0, y0, x1, y1, f[4]; int32_t child; } or_adf_node;
+typedef struct { or_adf_node *nodes; int64_t n, cap; int32_t *root; int32_t nxg, nyg; double x0, y0, dx, dy; } or_adf;
+
+static double adf_lerp2(const double *f, double s, double t) {
+    return lerp(lerp(f[0], f[1], s), lerp(f[2], f[3], s), t);
+}
+static int64_t adf_push(or_adf *A, double x0, double y0, double x1, double y1, const double *segs, int64_t ns) {
+    if (A->n == A->cap) {
+        A->cap = A->cap ? 2 * A->cap : 1024;
+        A->nodes = (or_adf_node *)realloc(A->nodes, sizeof(or_adf_node) * (size_t)A->cap);
+    }
+    or_adf_node *d = &A->nodes[A->n];
+    d->x0 = x0; d->y0 = y0; d->x1 = x1; d->y1 = y1; d->child = -1;
+    d->f[0] = or_contour_sdf_point(segs, ns, x0, y0);
+    d->f[1] = or_contour_sdf_point(segs, ns, x1, y0);
+    d->f[2] = or_contour_sdf_point(segs, ns, x0, y1);
+    d->f[3] = or_contour_sdf_point(segs, ns, x1, y1);
+    return A->n++;
+}
+static void adf_refine(or_adf *A, int64_t k, int depth, double etol, int max_depth, const double *segs, int64_t ns) {
+    or_adf_node nd = A->nodes[k];
+    if (depth >= max_depth) return;
+    const double xm = (nd.x0 + nd.x1) * 0.5, ym = (nd.y0 + nd.y1) * 0.5;
+    const double px[5] = {xm, xm, nd.x0, nd.x1, xm}, py[5] = {nd.y0, nd.y1, ym, ym, ym};
+    const double ps[5] = {0.5, 0.5, 0.0, 1.0, 0.5}, pt[5] = {0.0, 1.0, 0.5, 0.5, 0.5};
+    double err = 0.0;
+    for (int q = 0; q < 5; q++) {
+        const double e = fabs(adf_lerp2(nd.f, ps[q], pt[q]) - or_contour_sdf_point(segs, ns, px[q], py[q]));
+        if (e > err) err = e;
+    }
+    if (!(err > etol)) return;
+    const int64_t c0 = adf_push(A, nd.x0, nd.y0, xm, ym, segs, ns);
+    adf_push(A, xm, nd.y0, nd.x1, ym, segs, ns);
+    adf_push(A, nd.x0, ym, xm, nd.y1, segs, ns);
+    adf_push(A, xm, ym, nd.x1, nd.y1, segs, ns);
+    A->nodes[k].child = (int32_t)c0;
+    for (int q = 0; q < 4; q++) adf_refine(A, c0 + q, depth + 1, etol, max_depth, segs, ns);
+}
+/* builds the ADF of every boundary cell (cat == 1); returns the node count and the leaf count */
+void *or_adf_build(const or_fields *f, const or_params *p, double c, double h_avg, int32_t nxg, int32_t nyg,
+                   const int8_t *cat, const double *segs, int64_t n_seg, double fac_etol, double fac_pt,
+                   int32_t max_depth, int64_t *n_nodes, int64_t *n_leaves) {
+    or_adf *A = (or_adf *)calloc(1, sizeof(or_adf));
+    A->nxg = nxg; A->nyg = nyg; A->x0 = f->x0; A->y0 = f->y0;
+    A->dx = (f->x1 - f->x0) / (double)nxg; A->dy = (f->y1 - f->y0) / (double)nyg;
+    A->root = (int32_t *)malloc(sizeof(int32_t) * (size_t)nxg * (size_t)nyg);
+    for (int32_t j = 0; j < nyg; j++)
+        for (int32_t i = 0; i < nxg; i++) {
+            const int64_t cc = (int64_t)j * nxg + i;
+            A->root[cc] = -1;
+            if (cat[cc] != 1) continue;
+            const double cx0 = f->x0 + (double)i * A->dx, cy0 = f->y0 + (double)j * A->dy;
+            const double cx1 = f->x0 + (double)(i + 1) * A->dx, cy1 = f->y0 + (double)(j + 1) * A->dy;
+            const double mx = f->x0 + ((double)i + 0.5) * A->dx, my = f->y0 + ((double)j + 0.5) * A->dy;
+            const double h = h_of(f, c, mx, my);
+            const double geps = p->fac_geps * (h < h_avg ? h : h_avg);
+            const double etol = fac_etol * geps * fac_pt;
+            const int64_t r = adf_push(A, cx0, cy0, cx1, cy1, segs, n_seg);
+            A->root[cc] = (int32_t)r;
+            adf_refine(A, r, 0, etol, max_depth, segs, n_seg);
+        }
+    int64_t leaves = 0;
+    for (int64_t k = 0; k < A->n; k++) leaves += A->nodes[k].child < 0;
+    *n_nodes = A->n;
+    *n_leaves = leaves;
+    return A;
+}
+/* ADF value at (x, y) if it lies in a boundary cell, else NaN */
+double or_adf_eval(const void *h, double x, double y) {
+    const or_adf *A = (const or_adf *)h;
+    int i = (int)floor((x - A->x0) / A->dx), j = (int)floor((y - A->y0) / A->dy);
+    if (i < 0 || j < 0 || i >= A->nxg || j >= A->nyg) return NAN;
+    int64_t k = A->root[(int64_t)j * A->nxg + i];
+    if (k < 0) return NAN;
+    while (A->nodes[k].child >= 0) {
+        const or_adf_node *d = &A->nodes[k];
+        const double xm = (d->x0 + d->x1) * 0.5, ym = (d->y0 + d->y1) * 0.5;
+        k = d->child + (x >= xm ? 1 : 0) + (y >= ym ? 2 : 0);
+    }
+    const or_adf_node *d = &A->nodes[k];
+    return adf_lerp2(d->f, (x - d->x0) / (d->x1 - d->x0), (y - d->y0) / (d->y1 - d->y0));
+}
+void or_adf_free(void *h) {
+    or_adf *A = (or_adf *)h;
+    if (!A) return;
+    free(A->nodes); free(A->root); free(A);
+}

@@ -174,6 +174,13 @@ void or_sizing_field(int64_t ns, const double *sx, const double *sy, int64_t nm,
                      double K, int32_t nx, int32_t ny, double x0, double y0, double x1, double y1, double *mu,
                      double *lfs);
 
+/* ADF quadtrees on the boundary cells; handle freed by or_adf_free; eval NaN off them */
+void *or_adf_build(const or_fields *f, const or_params *p, double c, double h_avg, int32_t nxg, int32_t nyg,
+                   const int8_t *cat, const double *segs, int64_t n_seg, double fac_etol, double fac_pt,
+                   int32_t max_depth, int64_t *n_nodes, int64_t *n_leaves);
+double or_adf_eval(const void *h, double x, double y);
+void or_adf_free(void *h);
+
 #ifdef __cplusplus
 }
 #endif

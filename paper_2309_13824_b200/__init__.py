@@ -97,7 +97,7 @@ EXPORTED = ["tm_params_default", "tm_create", "tm_destroy", "tm_last_error", "tm
             "tm_retria_check", "tm_move_count", "tm_set_n_total", "tm_point_addition", "tm_control_init",
             "tm_control_update", "tm_geometry_grid_dims", "tm_geometry_categories", "tm_contour_sdf",
             "tm_sdf_combine", "tm_init_points", "tm_boundary_points", "tm_medial_points", "tm_sizing_field",
-            "tm_density_from_sizing",
+            "tm_density_from_sizing", "tm_adf_build", "tm_adf_eval",
             "tm_host_incircle_exact", "tm_host_cramer", "tm_host_bilinear"]
 
 
@@ -137,6 +137,8 @@ def load_library(path: str = LIB_PATH, build_if_missing: bool = True):
         "tm_boundary_points": (st, [vp, vp, i64, dbl, dbl, vp, vp, i64, ctypes.POINTER(i64)]),
         "tm_medial_points": (st, [vp, vp, vp, i64, dbl, dbl, dbl, dbl, dbl, i32, vp, vp, i64, ctypes.POINTER(i64)]),
         "tm_density_from_sizing": (st, [vp, vp, i64, vp]),
+        "tm_adf_build": (st, [vp, vp, i64, i32, i32, vp, dbl, dbl, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+        "tm_adf_eval": (st, [vp, vp, vp, i64, vp]),
         "tm_sizing_field": (st, [vp, vp, vp, i64, vp, vp, i64, dbl, i32, i32, dbl, dbl, dbl, dbl, vp, vp]),
         "tm_init_points": (st, [vp, i32, i32, vp, dbl, dbl, ctypes.c_uint64, vp, vp, vp, i64, ctypes.POINTER(i64)]),
         "tm_set_n_total": (st, [vp, i64, ctypes.POINTER(dbl), ctypes.POINTER(dbl)]),
@@ -304,6 +306,16 @@ class Context:
         self._check(self.L.tm_init_points(self.h, int(nxg), int(nyg), _ptr(cat), float(n_init), float(eta), int(seed),
                                           _ptr(counts), _ptr(x), _ptr(y), int(cap), ctypes.byref(n)))
         return int(n.value)
+
+    def tm_adf_build(self, segs, nxg: int, nyg: int, cat, fac_etol=0.1, fac_pt=1.0, max_depth=10):
+        nn, nl = ctypes.c_int64(), ctypes.c_int64()
+        self._check(self.L.tm_adf_build(self.h, _ptr(segs), int(segs.shape[0]), int(nxg), int(nyg), _ptr(cat),
+                                        float(fac_etol), float(fac_pt), int(max_depth), ctypes.byref(nn),
+                                        ctypes.byref(nl)))
+        return nn.value, nl.value
+
+    def tm_adf_eval(self, x, y, out):
+        self._check(self.L.tm_adf_eval(self.h, _ptr(x), _ptr(y), int(x.shape[0]), _ptr(out)))
 
     def tm_density_from_sizing(self, mu, rho):
         self._check(self.L.tm_density_from_sizing(self.h, _ptr(mu), int(mu.numel()), _ptr(rho)))

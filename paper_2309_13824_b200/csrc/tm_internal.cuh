@@ -171,6 +171,11 @@ struct tm_ctx {
     int64_t cap_tria = 0;
     bool have_tria = false;
     int64_t *scratch_n = nullptr;   // device scratch count (migration source size)
+    // ADF quadtrees on the boundary geometry cells (NEXT-4, tm_setup.cu)
+    void *adf_nodes = nullptr;      // AdfNode pool
+    int32_t *adf_root = nullptr;    // per geometry cell: root node or -1
+    int64_t adf_cap = 0, adf_n = 0;
+    int32_t adf_nxg = 0, adf_nyg = 0;
 };
 
 #define TM_CUDA_TRY(ctx, call)                                                                       \

@@ -729,3 +729,216 @@ extern "C" tm_status tm_density_from_sizing(tm_ctx *ctx, const double *mu, int64
     k_density<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(mu, n, rho);
     return tm_internal_check_launch(ctx, "k_density");
 }
+
+// ---- ADF quadtrees on the boundary geometry cells (after Frisken et al.; reading L48)
+namespace {
+
+struct AdfNode {
+    double x0, y0, x1, y1, f[4];  // bounds and the exact SDF at the corners (f00, f10, f01, f11)
+    int32_t child;                 // first of 4 consecutive children, or -1 (leaf)
+    int32_t pad;
+};
+
+// exact SDF of the contour at one point: brute force over the segments, the same operations and
+// tie rule (smallest segment index) as the oracle's or_contour_sdf_point
+__device__ double contour_sdf_bf(const double *__restrict__ segs, int64_t n_seg, double px, double py) {
+    int64_t best = -1;
+    double bd = 0.0, bt = 0.0;
+    for (int64_t k = 0; k < n_seg; k++) {
+        double d2, t;
+        seg_closest(segs + 4 * k, px, py, d2, t);
+        if (best < 0 || d2 < bd) { best = k; bd = d2; bt = t; }
+    }
+    const double *s = segs + 4 * best;
+    double nxv, nyv;
+    seg_normal(s, nxv, nyv);
+    double qx, qy;
+    if (bt == 0.0 || bt == 1.0) {
+        const int64_t o = bt == 0.0 ? (best + n_seg - 1) % n_seg : (best + 1) % n_seg;
+        double mx, my;
+        seg_normal(segs + 4 * o, mx, my);
+        nxv = cmul(cadd(nxv, mx), 0.5);
+        nyv = cmul(cadd(nyv, my), 0.5);
+        qx = bt == 0.0 ? s[0] : s[2];
+        qy = bt == 0.0 ? s[1] : s[3];
+    } else {
+        qx = cadd(s[0], cmul(bt, csub(s[2], s[0])));
+        qy = cadd(s[1], cmul(bt, csub(s[3], s[1])));
+    }
+    const double d = sqrt(bd);
+    return cadd(cmul(csub(px, qx), nxv), cmul(csub(py, qy), nyv)) > 0.0 ? -d : d;
+}
+
+__device__ __forceinline__ double adf_lerp2(const double *f, double s, double t) {
+    return clerp(clerp(f[0], f[1], s), clerp(f[2], f[3], s), t);
+}
+
+__device__ void adf_fill(AdfNode &d, double x0, double y0, double x1, double y1, const double *segs, int64_t ns) {
+    d.x0 = x0; d.y0 = y0; d.x1 = x1; d.y1 = y1; d.child = -1; d.pad = 0;
+    d.f[0] = contour_sdf_bf(segs, ns, x0, y0);
+    d.f[1] = contour_sdf_bf(segs, ns, x1, y0);
+    d.f[2] = contour_sdf_bf(segs, ns, x0, y1);
+    d.f[3] = contour_sdf_bf(segs, ns, x1, y1);
+}
+
+// one thread per boundary cell, depth-first with an explicit stack; nodes from a pool (a node
+// beyond the capacity is counted but not written: the host rebuilds with the exact size)
+__global__ void k_adf_build(int32_t nxg, int32_t nyg, const int8_t *__restrict__ cat, Grid g,
+                            const double *__restrict__ mu, double c, double h_avg, double fac_geps, double dx,
+                            double dy, const double *__restrict__ segs, int64_t n_seg, double fac_etol, double fac_pt,
+                            int max_depth, AdfNode *__restrict__ pool, int64_t cap,
+                            unsigned long long *__restrict__ count, int32_t *__restrict__ root) {
+    const int64_t cc = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (cc >= (int64_t)nxg * nyg) return;
+    root[cc] = -1;
+    if (cat[cc] != 1) return;
+    const int32_t i = (int32_t)(cc % nxg), j = (int32_t)(cc / nxg);
+    const double mx = cadd(g.x0, cmul(cadd((double)i, 0.5), dx)), my = cadd(g.y0, cmul(cadd((double)j, 0.5), dy));
+    const double h = mu ? cmul(c, bilinear(g, mu, mx, my, LdgLoad())) : c;
+    const double etol = cmul(cmul(fac_etol, cmul(fac_geps, h < h_avg ? h : h_avg)), fac_pt);
+    const unsigned long long r = atomicAdd(count, 1ull);
+    if ((int64_t)r >= cap) return;
+    AdfNode nd;
+    adf_fill(nd, cadd(g.x0, cmul((double)i, dx)), cadd(g.y0, cmul((double)j, dy)),
+             cadd(g.x0, cmul((double)(i + 1), dx)), cadd(g.y0, cmul((double)(j + 1), dy)), segs, n_seg);
+    pool[r] = nd;
+    root[cc] = (int32_t)r;
+    int64_t stk[64];
+    int8_t dep[64];
+    int sp = 0;
+    stk[sp] = (int64_t)r;
+    dep[sp++] = 0;
+    while (sp > 0) {
+        const int64_t k = stk[--sp];
+        const int depth = dep[sp];
+        if (depth >= max_depth) continue;
+        const AdfNode d = pool[k];
+        const double xm = cmul(cadd(d.x0, d.x1), 0.5), ym = cmul(cadd(d.y0, d.y1), 0.5);
+        const double px[5] = {xm, xm, d.x0, d.x1, xm}, py[5] = {d.y0, d.y1, ym, ym, ym};
+        const double ps[5] = {0.5, 0.5, 0.0, 1.0, 0.5}, pt[5] = {0.0, 1.0, 0.5, 0.5, 0.5};
+        double err = 0.0;
+        for (int q = 0; q < 5; q++) {
+            const double e = fabs(csub(adf_lerp2(d.f, ps[q], pt[q]), contour_sdf_bf(segs, n_seg, px[q], py[q])));
+            if (e > err) err = e;
+        }
+        if (!(err > etol)) continue;
+        const unsigned long long c0 = atomicAdd(count, 4ull);
+        if ((int64_t)c0 + 4 > cap) continue;
+        AdfNode ch;
+        adf_fill(ch, d.x0, d.y0, xm, ym, segs, n_seg); pool[c0] = ch;
+        adf_fill(ch, xm, d.y0, d.x1, ym, segs, n_seg); pool[c0 + 1] = ch;
+        adf_fill(ch, d.x0, ym, xm, d.y1, segs, n_seg); pool[c0 + 2] = ch;
+        adf_fill(ch, xm, ym, d.x1, d.y1, segs, n_seg); pool[c0 + 3] = ch;
+        pool[k].child = (int32_t)c0;
+        for (int q = 3; q >= 0; q--) {
+            stk[sp] = (int64_t)c0 + q;
+            dep[sp++] = (int8_t)(depth + 1);
+        }
+    }
+}
+
+__global__ void k_adf_eval(int64_t n, const double *__restrict__ x, const double *__restrict__ y, int32_t nxg,
+                           int32_t nyg, double x0, double y0, double dx, double dy, const AdfNode *__restrict__ pool,
+                           const int32_t *__restrict__ root, double *__restrict__ out) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const double px = x[p], py = y[p];
+    const int i = (int)floor(cdiv(csub(px, x0), dx)), j = (int)floor(cdiv(csub(py, y0), dy));
+    double v = __longlong_as_double(0x7ff8000000000000ll);  // NaN: not a boundary cell
+    if (i >= 0 && j >= 0 && i < nxg && j < nyg) {
+        int64_t k = root[(int64_t)j * nxg + i];
+        if (k >= 0) {
+            while (pool[k].child >= 0) {
+                const AdfNode &d = pool[k];
+                const double xm = cmul(cadd(d.x0, d.x1), 0.5), ym = cmul(cadd(d.y0, d.y1), 0.5);
+                k = d.child + (px >= xm ? 1 : 0) + (py >= ym ? 2 : 0);
+            }
+            const AdfNode &d = pool[k];
+            v = adf_lerp2(d.f, cdiv(csub(px, d.x0), csub(d.x1, d.x0)), cdiv(csub(py, d.y0), csub(d.y1, d.y0)));
+        }
+    }
+    out[p] = v;
+}
+
+__global__ void k_adf_leaves(int64_t n, const AdfNode *__restrict__ pool, unsigned long long *__restrict__ leaves) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool leaf = k < n && pool[k].child < 0;
+    const unsigned b = __ballot_sync(0xffffffffu, leaf);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(leaves, (unsigned long long)__popc(b));
+}
+
+}  // namespace
+
+extern "C" tm_status tm_adf_build(tm_ctx *ctx, const double *segs, int64_t n_seg, int32_t nxg, int32_t nyg,
+                                  const int8_t *cat, double fac_etol, double fac_pt, int32_t max_depth,
+                                  int64_t *n_nodes, int64_t *n_leaves) {
+    if (!ctx) return TM_E_ARG;
+    if (!ctx->have_domain) TM_FAIL(ctx, TM_E_STATE, "tm_adf_build before tm_set_domain");
+    if (ctx->capturing) TM_FAIL(ctx, TM_E_STATE, "tm_adf_build while capturing a graph");
+    if (!segs || n_seg < 3 || nxg < 1 || nyg < 1 || !cat || max_depth < 0 || max_depth > 20)
+        TM_FAIL(ctx, TM_E_ARG, "bad arguments to tm_adf_build");
+    TM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    const Grid &g = ctx->grid;
+    const double dx = cdiv(csub(g.x1, g.x0), (double)nxg), dy = cdiv(csub(g.y1, g.y0), (double)nyg);
+    const int64_t nc = (int64_t)nxg * nyg;
+    if (ctx->adf_nxg * (int64_t)ctx->adf_nyg < nc || !ctx->adf_root) {
+        cudaFree(ctx->adf_root);
+        ctx->adf_root = nullptr;
+        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->adf_root, nc * sizeof(int32_t)));
+    }
+    ctx->adf_nxg = nxg;
+    ctx->adf_nyg = nyg;
+    DevBuf dcnt;
+    TM_CUDA_TRY(ctx, cudaMalloc(&dcnt.p, 2 * sizeof(unsigned long long)));
+    // an overflowing build undercounts (the subtrees of unwritten nodes are not explored): grow and
+    // rebuild until the whole forest fits
+    for (int attempt = 0; attempt < 12; attempt++) {
+        if (ctx->adf_cap < 1024) {
+            cudaFree(ctx->adf_nodes);
+            ctx->adf_nodes = nullptr;
+            TM_CUDA_TRY(ctx, cudaMalloc(&ctx->adf_nodes, 65536 * sizeof(AdfNode)));
+            ctx->adf_cap = 65536;
+        }
+        TM_CUDA_TRY(ctx, cudaMemsetAsync(dcnt.p, 0, 2 * sizeof(unsigned long long), ctx->stream));
+        k_adf_build<<<(unsigned)((nc + 127) / 128), 128, 0, ctx->stream>>>(
+            nxg, nyg, cat, g, ctx->mu, ctx->c, ctx->h_avg, ctx->p.fac_geps, dx, dy, segs, n_seg, fac_etol, fac_pt,
+            max_depth, (AdfNode *)ctx->adf_nodes, ctx->adf_cap, (unsigned long long *)dcnt.p, ctx->adf_root);
+        tm_status s = tm_internal_check_launch(ctx, "k_adf_build");
+        if (s != TM_OK) return s;
+        unsigned long long used = 0;
+        TM_CUDA_TRY(ctx, cudaMemcpyAsync(&used, dcnt.p, sizeof(used), cudaMemcpyDeviceToHost, ctx->stream));
+        TM_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+        if ((int64_t)used <= ctx->adf_cap) {
+            ctx->adf_n = (int64_t)used;
+            break;
+        }
+        if (attempt == 11) TM_FAIL(ctx, TM_E_CAPACITY, "tm_adf_build: more than %llu nodes", used);
+        cudaFree(ctx->adf_nodes);
+        ctx->adf_nodes = nullptr;
+        const int64_t cap = 2 * (int64_t)used + 1024;
+        TM_CUDA_TRY(ctx, cudaMalloc(&ctx->adf_nodes, cap * sizeof(AdfNode)));
+        ctx->adf_cap = cap;
+    }
+    k_adf_leaves<<<(unsigned)((ctx->adf_n + 255) / 256), 256, 0, ctx->stream>>>(
+        ctx->adf_n, (const AdfNode *)ctx->adf_nodes, (unsigned long long *)dcnt.p + 1);
+    unsigned long long lv = 0;
+    TM_CUDA_TRY(ctx, cudaMemcpyAsync(&lv, (unsigned long long *)dcnt.p + 1, sizeof(lv), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+    TM_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    if (n_nodes) *n_nodes = ctx->adf_n;
+    if (n_leaves) *n_leaves = (int64_t)lv;
+    return TM_OK;
+}
+
+extern "C" tm_status tm_adf_eval(tm_ctx *ctx, const double *x, const double *y, int64_t n, double *out) {
+    if (!ctx) return TM_E_ARG;
+    if (!ctx->adf_nodes || !ctx->adf_root || ctx->adf_nxg < 1) TM_FAIL(ctx, TM_E_STATE, "tm_adf_eval before tm_adf_build");
+    if (!x || !y || !out || n < 0) TM_FAIL(ctx, TM_E_ARG, "bad arguments to tm_adf_eval");
+    if (n == 0) return TM_OK;
+    const Grid &g = ctx->grid;
+    const double dx = cdiv(csub(g.x1, g.x0), (double)ctx->adf_nxg), dy = cdiv(csub(g.y1, g.y0), (double)ctx->adf_nyg);
+    k_adf_eval<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(n, x, y, ctx->adf_nxg, ctx->adf_nyg, g.x0, g.y0,
+                                                                      dx, dy, (const AdfNode *)ctx->adf_nodes,
+                                                                      ctx->adf_root, out);
+    return tm_internal_check_launch(ctx, "k_adf_eval");
+}

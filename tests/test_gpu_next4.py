@@ -127,3 +127,42 @@ def test_automatic_sizing_matches_oracle():
     omu, olfs = O.sizing_field(ox, oy, omx, omy, K, 129, 129, box)
     assert np.array_equal(lfs.cpu().numpy(), olfs)
     assert np.array_equal(mu.cpu().numpy(), omu)
+
+
+def test_adf_matches_oracle():
+    """ADF quadtrees on the star's boundary cells: the same node and leaf counts as the
+    oracle's, and the same values, bit for bit, at random points of the boundary cells (NaN off
+    them), for the paper's E_tol factor and a finer one."""
+    import paper_2309_13824_b200 as T
+    ctx = T.Context(0)
+    box = (0.0, 0.0, 1.0, 1.0)
+    segs = _star()
+    n = 193
+    phi = torch.empty(n, n, dtype=torch.float64, device="cuda")
+    ctx.tm_contour_sdf(to_dev(segs), n, n, box, phi)
+    ctx.tm_set_domain(box, phi, None, None, 5000)
+    nxg, nyg = T.geometry_grid_dims(5000, box)
+    cat = torch.empty(nyg * nxg, dtype=torch.int8, device="cuda")
+    ctx.tm_geometry_categories(nxg, nyg, cat)
+    fs = O.FieldSet(box, phi.cpu().numpy())
+    oc, oh = O.domain(fs, 5000)
+    ocat = cat.cpu().numpy().reshape(nyg, nxg)
+    rng = np.random.default_rng(4)
+    js, is_ = np.nonzero(ocat == 1)
+    pick = rng.integers(0, len(js), 4000)
+    d = 1.0 / nxg
+    px = (is_[pick] + rng.random(4000)) * d
+    py = (js[pick] + rng.random(4000)) * d
+    px = np.concatenate([px, [0.5, 0.02]])
+    py = np.concatenate([py, [0.5, 0.02]])  # an inner and an outer cell: NaN
+    for fac_etol in (0.1, 0.01):
+        nn, nl = ctx.tm_adf_build(to_dev(segs), nxg, nyg, cat, fac_etol=fac_etol, fac_pt=np.sqrt(0.2))
+        oadf = O.ADF(fs, oc, oh, ocat, segs, fac_etol=fac_etol, fac_pt=np.sqrt(0.2))
+        assert (nn, nl) == (oadf.n_nodes, oadf.n_leaves)
+        out = torch.empty(len(px), dtype=torch.float64, device="cuda")
+        ctx.tm_adf_eval(to_dev(px), to_dev(py), out)
+        g = out.cpu().numpy()
+        o = np.array([oadf(a, b) for a, b in zip(px, py)])
+        assert np.array_equal(np.isnan(g), np.isnan(o))
+        assert np.array_equal(g[~np.isnan(g)], o[~np.isnan(o)])
+    assert np.isnan(g[-1]) and np.isnan(g[-2])

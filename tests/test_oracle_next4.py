@@ -228,3 +228,65 @@ def test_lfs_of_a_thin_strip_is_its_half_thickness():
     mid = (x > 0.3) & (x < 0.7)
     assert mid.sum() > 20
     assert np.abs(lfs[mid] - 0.05).max() < 0.006
+
+
+def test_adf_on_straight_edges_needs_no_refinement_and_caps_depth():
+    """P:457-472.  Inside a square, along an edge away from the corners, the SDF is linear, so the
+    root's bilinear interpolant is exact at the 5 check points and the cell stays a single leaf;
+    where the distance bends (corners) cells refine.  With a vanishing tolerance every boundary cell
+    becomes a full tree of depth max_depth: (4^(d+1) - 1) / 3 nodes each."""
+    segs = _square()
+    box = (-0.5, -0.5, 1.5, 1.5)
+    g = configs.node_coords(-0.5, 1.5, 65)
+    X, Y = np.meshgrid(g, g)
+    phi = O.contour_sdf(segs, 65, 65, box)
+    fs = O.FieldSet(box, phi)
+    nxg = nyg = 40
+    cat = O.geometry_categories(fs, nxg, nyg)
+    c, ha = O.domain(fs, 4000)
+    adf = O.ADF(fs, c, ha, cat, segs)
+    nb = int((cat == 1).sum())
+    assert nb < adf.n_nodes  # some refinement (around the corners)
+    # a boundary cell in the middle of the left edge (x = 0, y = 0.5), inside: a single leaf, exact
+    d = 2.0 / nxg
+    xs = [0.01, 0.02, 0.03]
+    for x in xs:
+        assert abs(adf(x, 0.5) - (-x)) < 1e-15
+    # where the distance is linear the interpolant is exact (error 0 is never > E_tol): with a
+    # vanishing tolerance only the curved cells refine, to the depth cap and no further
+    full = O.ADF(fs, c, ha, cat, segs, fac_etol=1e-300, max_depth=3)
+    assert nb < full.n_nodes <= nb * (1 + 4 + 16 + 64) and (full.n_nodes - nb) % 4 == 0
+    segc = _circle(300)
+    phic = O.contour_sdf(segc, 65, 65, box)
+    fsc = O.FieldSet(box, phic)
+    catc = O.geometry_categories(fsc, nxg, nyg)
+    nbc = int((catc == 1).sum())
+    fullc = O.ADF(fsc, c, ha, catc, segc, fac_etol=1e-300, max_depth=3)
+    assert fullc.n_nodes == nbc * (1 + 4 + 16 + 64) and fullc.n_leaves == nbc * 64
+
+
+def test_adf_error_bounded_on_a_circle():
+    """A circle contour: the ADF agrees with the exact contour SDF within a few E_tol at random points
+    of the boundary cells (E_tol bounds the error at each leaf's 5 check points), and a tighter
+    tolerance refines more."""
+    segs = _circle(300)
+    box = (0.0, 0.0, 1.0, 1.0)
+    phi = O.contour_sdf(segs, 129, 129, box)
+    fs = O.FieldSet(box, phi)
+    nxg = nyg = 50
+    cat = O.geometry_categories(fs, nxg, nyg)
+    c, ha = O.domain(fs, 5000)
+    adf = O.ADF(fs, c, ha, cat, segs)
+    fine = O.ADF(fs, c, ha, cat, segs, fac_etol=0.01)
+    assert fine.n_nodes > adf.n_nodes
+    etol = 0.1 * 0.01 * min(c, ha)
+    rng = np.random.default_rng(2)
+    d = 1.0 / nxg
+    checked = 0
+    for j, i in zip(*np.nonzero(cat == 1)):
+        for _ in range(3):
+            x, y = (i + rng.random()) * d, (j + rng.random()) * d
+            assert abs(adf(x, y) - O.contour_sdf_point(segs, x, y)) <= 4 * etol
+            checked += 1
+    assert checked > 100
+    assert math.isnan(adf(0.5, 0.5))  # an inner cell: no ADF
