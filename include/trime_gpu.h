@@ -276,6 +276,12 @@ tm_status tm_migrate_pack_dc(tm_ctx *ctx, double *x, double *y, int32_t *gid, do
 tm_status tm_append_points(tm_ctx *ctx, double *x, double *y, int32_t *gid, double *d_prev, int64_t *d_count,
                            int64_t cap, const double *msg, const int64_t *msg_count, int64_t msg_cap);
 
+/* Strip re-balancing input (S7): hist[b] (device int64, nb entries) = the number of the first
+ * *d_n (device; NULL: cap) points of x (device) with x in bin b of nb equal bins of [x0, x1)
+ * (clamped into the first / last bin).  Exact counts; asynchronous. */
+tm_status tm_x_histogram(tm_ctx *ctx, const double *x, const int64_t *d_n, int64_t cap, double x0, double x1,
+                         int32_t nb, int64_t *hist);
+
 /* ---- CUDA Graphs: capture a sequence of the calls above once, replay it many times ----
  * tm_graph_begin starts capturing the context's stream (thread-local capture mode);
  * every call until tm_graph_end is recorded instead of run (its status reports argument

@@ -97,7 +97,7 @@ EXPORTED = ["tm_params_default", "tm_create", "tm_destroy", "tm_last_error", "tm
             "tm_retria_check", "tm_move_count", "tm_set_n_total", "tm_point_addition", "tm_control_init",
             "tm_control_update", "tm_geometry_grid_dims", "tm_geometry_categories", "tm_contour_sdf",
             "tm_sdf_combine", "tm_init_points", "tm_boundary_points", "tm_medial_points", "tm_sizing_field",
-            "tm_density_from_sizing", "tm_adf_build", "tm_adf_eval",
+            "tm_density_from_sizing", "tm_adf_build", "tm_adf_eval", "tm_x_histogram",
             "tm_host_incircle_exact", "tm_host_cramer", "tm_host_bilinear"]
 
 
@@ -139,6 +139,7 @@ def load_library(path: str = LIB_PATH, build_if_missing: bool = True):
         "tm_density_from_sizing": (st, [vp, vp, i64, vp]),
         "tm_adf_build": (st, [vp, vp, i64, i32, i32, vp, dbl, dbl, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
         "tm_adf_eval": (st, [vp, vp, vp, i64, vp]),
+        "tm_x_histogram": (st, [vp, vp, vp, i64, dbl, dbl, i32, vp]),
         "tm_sizing_field": (st, [vp, vp, vp, i64, vp, vp, i64, dbl, i32, i32, dbl, dbl, dbl, dbl, vp, vp]),
         "tm_init_points": (st, [vp, i32, i32, vp, dbl, dbl, ctypes.c_uint64, vp, vp, vp, i64, ctypes.POINTER(i64)]),
         "tm_set_n_total": (st, [vp, i64, ctypes.POINTER(dbl), ctypes.POINTER(dbl)]),
@@ -316,6 +317,10 @@ class Context:
 
     def tm_adf_eval(self, x, y, out):
         self._check(self.L.tm_adf_eval(self.h, _ptr(x), _ptr(y), int(x.shape[0]), _ptr(out)))
+
+    def tm_x_histogram(self, x, d_n_addr, cap: int, x0: float, x1: float, hist):
+        self._check(self.L.tm_x_histogram(self.h, _ptr(x), None if d_n_addr is None else ctypes.c_void_p(int(d_n_addr)),
+                                          int(cap), float(x0), float(x1), int(hist.shape[0]), _ptr(hist)))
 
     def tm_density_from_sizing(self, mu, rho):
         self._check(self.L.tm_density_from_sizing(self.h, _ptr(mu), int(mu.numel()), _ptr(rho)))

@@ -1253,3 +1253,27 @@ extern "C" double tm_host_bilinear(int32_t nx, int32_t ny, double x0, double y0,
     g.dy = cdiv(csub(y1, y0), (double)(ny - 1));
     return bilinear(g, F, x, y, PlainLoad());
 }
+
+// ============================================================================ S7: strip re-balancing input
+// histogram of the owned x over nb equal bins of [x0, x1) (x below x0 in bin 0, at or above x1 in the
+// last): integer counts, exact
+__global__ void k_x_histogram(const double *__restrict__ x, const int64_t *__restrict__ d_n, int64_t n_host,
+                              double x0, double x1, int32_t nb, unsigned long long *__restrict__ hist) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n = d_n ? d_n[0] : n_host;
+    if (i >= n) return;
+    int b = (int)floor((x[i] - x0) / (x1 - x0) * (double)nb);
+    b = b < 0 ? 0 : (b >= nb ? nb - 1 : b);
+    atomicAdd(hist + b, 1ull);
+}
+
+extern "C" tm_status tm_x_histogram(tm_ctx *ctx, const double *x, const int64_t *d_n, int64_t cap, double x0,
+                                    double x1, int32_t nb, int64_t *hist) {
+    if (!ctx) return TM_E_ARG;
+    if (!x || !hist || nb < 1 || cap < 0 || !(x1 > x0)) TM_FAIL(ctx, TM_E_ARG, "bad arguments to tm_x_histogram");
+    TM_CUDA_TRY(ctx, cudaMemsetAsync(hist, 0, (size_t)nb * sizeof(int64_t), ctx->stream));
+    if (cap == 0) return TM_OK;
+    k_x_histogram<<<(unsigned)((cap + 255) / 256), 256, 0, ctx->stream>>>(x, d_n, cap, x0, x1, nb,
+                                                                         reinterpret_cast<unsigned long long *>(hist));
+    return tm_internal_check_launch(ctx, "k_x_histogram");
+}

@@ -81,6 +81,55 @@ class Strips:
         return torch.clamp(((x - self.x0) / w).floor().to(torch.int64), 0, self.P - 1)
 
 
+def rebalanced_cuts(strips: "Strips", hist, W: float, max_shift: float = 0.5) -> "Strips":
+    """Re-balanced strips from a global histogram of the owned x (nb equal bins of [x0, x1)): cut k
+    at the k/P quantile (linear inside its bin), each cut moved by at most `max_shift` of the
+    narrower strip beside it -- so every point changes owner to a neighbouring strip only and the
+    migration step can carry it -- and strips kept at least W wide.  Host arithmetic on the
+    (all-reduced, identical on every rank) counts: every rank computes the same cuts."""
+    P = strips.P
+    if P == 1:
+        return strips
+    h = [int(v) for v in hist]
+    nb = len(h)
+    tot = sum(h)
+    old = [strips._cut(k) for k in range(1, P)]
+    edges = [strips.x0] + old + [strips.x1]
+    cum = [0]
+    for v in h:
+        cum.append(cum[-1] + v)
+    new = []
+    b = 0
+    for k in range(1, P):
+        target = tot * k / P
+        while b < nb - 1 and cum[b + 1] < target:
+            b += 1
+        frac = 0.0 if h[b] == 0 else (target - cum[b]) / h[b]
+        q = strips.x0 + (b + min(max(frac, 0.0), 1.0)) * (strips.x1 - strips.x0) / nb
+        lim = max_shift * min(edges[k] - edges[k - 1], edges[k + 1] - edges[k])
+        new.append(min(max(q, old[k - 1] - lim), old[k - 1] + lim))
+    for k in range(1, P - 1):  # keep the interior strips at least W wide (then keep the old cuts)
+        if new[k] - new[k - 1] < W:
+            return strips
+    return Strips(strips.x0, strips.x1, P, new)
+
+
+def rebalance(S: "StripState", strips: "Strips", backend, comm, W: float, nb: int = 1024) -> "Strips":
+    """Periodic strip re-balancing, between iterations: the global histogram of the
+    owned x (one all-reduce of nb counts), new cuts (rebalanced_cuts), then one migration step
+    with the new bounds on the current points.  Synchronises once (the counts to the host)."""
+    hist = backend.x_histogram(S, strips.x0, strips.x1, nb)
+    comm.allreduce_sum(hist)
+    new = rebalanced_cuts(strips, hist.cpu().tolist(), W)
+    lo, hi = new.bounds(S.rank)
+    S.swap()  # the current points into the update's arrays, where migrate_pack works
+    backend.migrate_pack(S, lo, hi)
+    comm.exchange(S.m_send[0], S.m_send[1], S.m_recv[0], S.m_recv[1])
+    backend.append_migrants(S)
+    S.swap()
+    return new
+
+
 def ghost_width(c: float, fac_voro: float = 5.0, mu_max: float = 1.0) -> float:
     """W = 2 S_max, S = fac_voro * h, h = c * mu (reading L34)."""
     return 2.0 * fac_voro * c * mu_max
@@ -269,6 +318,11 @@ class GpuStripBackend:
             self.ctx.tm_append_points(S.Xo, S.Yo, S.G, S.Do, S.counts.data_ptr(), S.cap_own, m.payload_addr(),
                                       m.addr(), m.cap)
 
+    def x_histogram(self, S: StripState, x0: float, x1: float, nb: int) -> torch.Tensor:
+        h = torch.empty(nb, dtype=torch.int64, device=S.X.device)
+        self.ctx.tm_x_histogram(S.X, S.counts.data_ptr(), S.cap_own, x0, x1, h)
+        return h
+
     def triangles(self):
         """This rank's emitted triangles (global ids; synchronises)."""
         nt = int(self.bufs.n_tri.item())
@@ -301,6 +355,23 @@ def _loop_exchange(states: List[StripState], send, recv):
             recv(states[r - 1])[1].buf.copy_(send(S)[0].buf)
         if r < P - 1:
             recv(states[r + 1])[0].buf.copy_(send(S)[1].buf)
+
+
+def loopback_rebalance(states: List[StripState], strips: Strips, backends, W: float, nb: int = 1024) -> Strips:
+    """rebalance() for P logical ranks in one process (the histogram summed in place)."""
+    total = None
+    for r, S in enumerate(states):
+        h = backends[r].x_histogram(S, strips.x0, strips.x1, nb)
+        total = h if total is None else total + h
+    new = rebalanced_cuts(strips, total.cpu().tolist(), W)
+    for r, S in enumerate(states):
+        S.swap()
+        backends[r].migrate_pack(S, *new.bounds(r))
+    _loop_exchange(states, lambda S: S.m_send, lambda S: S.m_recv)
+    for r, S in enumerate(states):
+        backends[r].append_migrants(S)
+        S.swap()
+    return new
 
 
 def loopback_step(states: List[StripState], strips: Strips, backends, W: float, mode: str = "cvd"):

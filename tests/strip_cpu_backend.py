@@ -90,5 +90,10 @@ class CpuStripBackend:
             S.Xo[b:b + k], S.Yo[b:b + k], S.G[b:b + k], S.Do[b:b + k] = x, y, g, d
             S.counts[0] = b + k
 
+    def x_histogram(self, S, x0, x1, nb):
+        n = int(S.counts[0])
+        b = np.clip(np.floor((S.X[:n].numpy() - x0) / (x1 - x0) * nb).astype(np.int64), 0, nb - 1)
+        return torch.from_numpy(np.bincount(b, minlength=nb).astype(np.int64))
+
     def triangles(self):
         return torch.from_numpy(self.tri.astype(np.int32))

@@ -41,17 +41,19 @@ def _make(P, box, phid, n, mu=None, rho=None, adaptive=True):
     return backends, c
 
 
-def _run(P, n, seed, modes, box=(0.0, 0.0, 1.0, 1.0), chained=False):
+def _run(P, n, seed, modes, box=(0.0, 0.0, 1.0, 1.0), chained=False, rebalance=False):
     import paper_2309_13824_b200 as T
     from paper_2309_13824_b200 import strips as S
     phi = configs.box_phi(box, 128)
     fs = O.FieldSet(box, phi)
     x, y = configs.random_points(n, seed, box)
+    if rebalance:
+        x = x * x  # denser towards x = 0: equal-width strips are unbalanced
     strips = S.Strips(box[0], box[2], P)
     dev = torch.device("cuda", 0)
     backends, c = _make(P, box, torch.from_numpy(phi).to(dev), n)
     W = S.ghost_width(c, 5.0)
-    cap_own, cap_msg = S.capacities(n, P, n // P)
+    cap_own, cap_msg = S.capacities(n, P, n // P, slack=2.0 if rebalance else 1.15)
     to = lambda a: torch.from_numpy(a).to(dev)
     states = [S.split_initial(to(x), to(y), strips, r, cap_own, cap_msg) for r in range(P)]
     dp = None
@@ -67,6 +69,17 @@ def _run(P, n, seed, modes, box=(0.0, 0.0, 1.0, 1.0), chained=False):
         assert err <= 1e-12 * diam, f"P={P} it={it} {mode}: position error {err:.3e}"
         if mode == "cvd":
             assert np.array_equal(xs, ref.x) and np.array_equal(ys, ref.y), f"P={P} it={it}: CVD not bit-identical"
+        if rebalance:  # re-balance the strips on the ranks' state, then check ownership and balance
+            strips = S.loopback_rebalance(states, strips, backends, W, nb=512)
+            backends[0].ctx.tm_sync()
+            owned = [int(st.counts[0].item()) for st in states]
+            assert sum(owned) == n
+            for r, st in enumerate(states):
+                lo, hi = strips.bounds(r)
+                xo = st.owned()[0].cpu().numpy()
+                assert ((xo >= lo) & (xo < hi)).all()
+            if it == len(modes) - 1:  # equal-width strips of x^2 hold ~58/24/18 %
+                assert max(owned) < 1.15 * n / P, owned
         if chained:  # continue from the ranks' own state (migration, warm start across iterations)
             x, y, dp = xs, ys, ds
         else:        # continue from the oracle's state so that both sides start identically
@@ -85,6 +98,13 @@ def test_gpu_strips_chained_iterations(P):
     key on global ids, and every iteration still equals the oracle run on the gathered
     state (the parity protocol of SURVEY §8(c), per iteration)."""
     _run(P, 30000, 41 + P, ["cvd", "cvd", "dm", "cvd", "cvd"], chained=True)
+
+
+def test_gpu_strips_rebalancing():
+    """Skewed points (x^2) on equal-width strips, re-balanced after every iteration (histogram,
+    quantile cuts limited to half a strip, one migration step): every iteration still equals the
+    oracle, every point stays owned once and inside its new strip, and the ranks even out."""
+    _run(3, 20000, 5, ["cvd"] * 5, chained=True, rebalance=True)
 
 
 def test_gpu_strips_capacity_overflow_is_loud():
