@@ -495,6 +495,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cfg5", action="store_true")
     ap.add_argument("--no-paper-e1", action="store_true")
+    ap.add_argument("--no-count", action="store_true",
+                    help="skip the untimed work-counting pass of the roofline (ncu launch lists of the step alone)")
     ap.add_argument("--cfg5-sizes", default="16000000,64000000")
     ap.add_argument("--strips", action="store_true", help="use the x-strip path even at N=1")
     ap.add_argument("--flags", type=int, default=0, help="extra tm_params.flags (A/B)")
@@ -711,7 +713,7 @@ def main():
                "d2h": "final points (x, y), triangle count, final triangle list (int32 x3)"}
 
     roof = None
-    if rank == 0 and ev_cells:
+    if rank == 0 and ev_cells and not args.no_count:
         per = count_work(T, c, local, schedule, dev)
         roof = roofline(per, cells_ms, it_ms)
 
