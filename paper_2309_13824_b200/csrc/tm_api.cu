@@ -84,7 +84,7 @@ extern "C" void tm_destroy(tm_ctx *ctx) {
     cudaFree(ctx->mig_keep); cudaFree(ctx->mig_cnt); cudaFree(ctx->mig_off);
     cudaFree(ctx->nbr); cudaFree(ctx->nbr_cnt); cudaFree(ctx->inv_id);
     cudaFree(ctx->ring_v); cudaFree(ctx->ring_la); cudaFree(ctx->ring_n);
-    cudaFree(ctx->deep_list); cudaFree(ctx->deep_cnt); cudaFree(ctx->scratch_n);
+    cudaFree(ctx->deep_list); cudaFree(ctx->deep_xy); cudaFree(ctx->deep_cnt); cudaFree(ctx->scratch_n);
     cudaFree(ctx->xs_tria); cudaFree(ctx->ys_tria); cudaFree(ctx->hs_tria);
     cudaFree(ctx->adf_nodes); cudaFree(ctx->adf_root);
     delete ctx;

@@ -179,7 +179,8 @@ __device__ __forceinline__ void quad_leaf(const double Q[3][2], const CellArgs &
 // are taken two at a time with their density loads in flight together (the kernel is
 // bound by the latency of those loads); below level 1 the two are siblings, so the
 // descent to their parent is shared.
-// Levels beyond `lmax` (< quad_max) are left to a later pass: returns false then (cx, cy unset).
+// Levels beyond `lmax` (< quad_max) are left to a later pass: returns false then, with (cx, cy) the
+// centroid of level lmax (the later pass's previous level).
 static __device__ bool quad_centroid_g(const double2 *rv, int64_t ns, int nv, double px, double py, double area,
                                        double h, double dprev, const CellArgs &A, double &cx, double &cy,
                                        unsigned long long &nq, int lmax) {
@@ -189,7 +190,11 @@ static __device__ bool quad_centroid_g(const double2 *rv, int64_t ns, int nv, do
     double prevx = 0.0, prevy = 0.0;
     bool done = false;
     for (int L = 1; L <= A.quad_max; L++) {
-        if (L > lmax) return false;
+        if (L > lmax) {  // the last level's centroid: the later pass continues from it
+            cx = prevx;
+            cy = prevy;
+            return false;
+        }
         const int depth = L - 1;
         const int64_t ntot = (int64_t)nv << depth;
         double sw = 0.0, swx = 0.0, swy = 0.0;

@@ -1188,7 +1188,7 @@ __device__ __forceinline__ void cell_update(const CellArgs &A, int32_t orig, dou
 // (bit-identical), with the long serial chain of lookups of a deep cell cut G-fold
 template <int MODE, int G>
 __global__ void __launch_bounds__(128) k_output_deep(CellArgs A, RingBuf R, const int32_t *list,
-                                                     const unsigned long long *cnt) {
+                                                     const double2 *list_xy, const unsigned long long *cnt) {
     const int64_t n = (int64_t)*cnt;
     const int gl = threadIdx.x % G;  // lane in the group
     const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
@@ -1210,9 +1210,11 @@ __global__ void __launch_bounds__(128) k_output_deep(CellArgs A, RingBuf R, cons
         double eps = dprev >= 0.0 ? cdiv(dprev, h) : A.fac_pt;
         if (eps < A.fac_end) eps = A.fac_end;
         const double E = cmul(sqrt(cmul(0.5, S2)), eps);
-        double prevx = 0.0, prevy = 0.0;
+        // levels 1..TM_QLEV1 were summed by k_output_t (same operations): continue from its centroid
+        const double2 pv = list_xy[it];
+        double prevx = pv.x, prevy = pv.y;
         unsigned long long nq = 0;
-        for (int L = 1; L <= A.quad_max; L++) {
+        for (int L = TM_QLEV1 + 1; L <= A.quad_max; L++) {
             const int depth = L - 1;
             const int64_t ntot = (int64_t)nv << depth;
             double sw = 0.0, swx = 0.0, swy = 0.0;
@@ -1257,7 +1259,7 @@ __global__ void __launch_bounds__(128) k_output_deep(CellArgs A, RingBuf R, cons
 
 template <int MODE>
 __global__ void __launch_bounds__(128, TM_OUT_MINB) k_output_t(CellArgs A, RingBuf R, int32_t *deep_list,
-                                                               unsigned long long *deep_cnt) {
+                                                               double2 *deep_xy, unsigned long long *deep_cnt) {
     const int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const int nv = cell < A.n_local ? (int)R.n[cell] : 0;
@@ -1380,11 +1382,13 @@ __global__ void __launch_bounds__(128, TM_OUT_MINB) k_output_t(CellArgs A, RingB
         unsigned long long nq1 = 0;
         const bool done = ring_centroid(rv0, ns, nv, px, py, h, A.d_prev ? __ldg(A.d_prev + orig) : -1.0, A, cx, cy,
                                         nq1, deep_list ? TM_QLEV1 : (1 << 30));
+        nq += nq1;
         if (done) {
-            nq += nq1;
             cell_update<MODE>(A, orig, px, py, h, cx, cy);
         } else {
-            deep_list[atomicAdd(deep_cnt, 1ull)] = (int32_t)cell;
+            const unsigned long long k = atomicAdd(deep_cnt, 1ull);
+            deep_list[k] = (int32_t)cell;
+            deep_xy[k] = make_double2(cx, cy);  // the level-TM_QLEV1 centroid
         }
     }    if ((MODE & M_COUNT) && live) {
         float R2f = 0.f;
@@ -1456,17 +1460,22 @@ static tm_status launch_cells_thread_impl(tm_ctx *ctx, const CellArgs &a) {
         if (!ctx->deep_cnt) TM_CUDA_TRY(ctx, cudaMalloc(&ctx->deep_cnt, sizeof(unsigned long long)));
         if (ctx->cap_deep < ctx->n_local) {
             cudaFree(ctx->deep_list);
+            cudaFree(ctx->deep_xy);
             ctx->deep_list = nullptr;
+            ctx->deep_xy = nullptr;
+            ctx->cap_deep = 0;
             TM_CUDA_TRY(ctx, cudaMalloc(&ctx->deep_list, ctx->cap_ring * sizeof(int32_t)));
+            TM_CUDA_TRY(ctx, cudaMalloc(&ctx->deep_xy, ctx->cap_ring * sizeof(double2)));
             ctx->cap_deep = ctx->cap_ring;
         }
         TM_CUDA_TRY(ctx, cudaMemsetAsync(ctx->deep_cnt, 0, sizeof(unsigned long long), ctx->stream));
     }
     k_output_t<OMODE><<<(unsigned)((ctx->n_local + 127) / 128), 128, 0, ctx->stream>>>(
-        b, R, deep ? ctx->deep_list : nullptr, ctx->deep_cnt);
+        b, R, deep ? ctx->deep_list : nullptr, ctx->deep_xy, ctx->deep_cnt);
     s = tm_internal_check_launch(ctx, "k_output_t");
     if (s != TM_OK || !deep) return s;
-    k_output_deep<OMODE, TM_DEEP_G><<<148 * 8, 128, 0, ctx->stream>>>(b, R, ctx->deep_list, ctx->deep_cnt);
+    k_output_deep<OMODE, TM_DEEP_G><<<148 * 8, 128, 0, ctx->stream>>>(b, R, ctx->deep_list, ctx->deep_xy,
+                                                                      ctx->deep_cnt);
     return tm_internal_check_launch(ctx, "k_output_deep");
 }
 

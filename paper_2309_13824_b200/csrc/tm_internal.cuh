@@ -154,6 +154,7 @@ struct tm_ctx {
     int64_t cap_ring = 0;
     // cells whose adaptive quadrature goes deeper than k_output_t's levels (k_output_deep)
     int32_t *deep_list = nullptr;
+    double2 *deep_xy = nullptr;  // their level-TM_QLEV1 centroid (k_output_deep continues from it)
     unsigned long long *deep_cnt = nullptr;
     int64_t cap_deep = 0;
     // strip migration scratch (stable partition)
