@@ -590,6 +590,10 @@ def main():
         lo_, hi_ = strips.bounds(rank)
         S.GpuStripBackend(ctx, params.adj_stride).halo_pack(S0, lo_, hi_, W)
         ghosts0 = max(S0.h_send[0].count(), S0.h_send[1].count())
+        if world > 1:  # messages are fixed-size: every rank must size them alike (send/recv counts match)
+            g_all = torch.tensor([ghosts0], dtype=torch.int64, device=dev)
+            dist.all_reduce(g_all, op=dist.ReduceOp.MAX)
+            ghosts0 = int(g_all.item())
         cap_msg = min(cap_own, 4 * ghosts0 + 4096)
         S0 = S.split_initial(x0, y0, strips, rank, cap_own, cap_msg)
         xo_, yo_, go_, _ = S0.owned()
