@@ -236,7 +236,7 @@ def load(k: int, cache: bool = True, **kw) -> Config:
             pass
     c = _BUILDERS[k]()
     os.makedirs(_cache_dir(), exist_ok=True)
-    tmp = path + ".tmp.npz"
+    tmp = path + f".tmp{os.getpid()}.npz"  # per process: the ranks of a multi-GPU run may build it at once
     np.savez(tmp, name=c.name, x=c.x, y=c.y, box=np.array(c.box), phi=c.phi,
              mu=c.mu if c.mu is not None else np.zeros(1),
              rho=c.rho if c.rho is not None else np.zeros(1),
