@@ -71,6 +71,12 @@ __host__ __device__ constexpr bool split_rings(int mode) {
 
 constexpr int TB = TM_TB;
 constexpr int VMAX = TM_VMAX;
+// TM_HISLOT: slots >= VLO are tested only by threads whose ring uses one (slots are handed out
+// lowest-free first, so rings rarely reach them); the masks below make this exactly equivalent
+#ifndef TM_HISLOT
+#define TM_HISLOT 0
+#endif
+constexpr int VLO = (TM_HISLOT && VMAX > 8) ? 8 : VMAX;
 static_assert(VMAX <= 31, "slot masks are 32-bit");
 static_assert(VMAX <= TM_NBR, "warm-start rows hold at most TM_NBR neighbours per point (ADVICE r1)");
 static_assert(TB <= 256 && (TB & (TB - 1)) == 0, "balancing keys hold the lane slot in 8 bits");
@@ -181,12 +187,22 @@ __device__ __forceinline__ int clip_t(TPoly &P, int code, const Line &L, const C
     }
     if (is_bis) {
 #pragma unroll
-        for (int k = 0; k < VMAX; k++) {  // point-point filter on every slot (masked below)
+        for (int k = 0; k < VLO; k++) {  // point-point filter on every slot (masked below)
             const double2 vv = P.v[k * TB];
             const double del = fma(L.nx, vv.x, L.ny * vv.y) - L.r;
             const double B = fma(n1, (double)P.K[k * TB], c8);
             out |= (unsigned)(del > B) << k;
             unc |= (unsigned)(del <= B && del >= -B) << k;
+        }
+        if (VLO < VMAX && (P.used >> VLO)) {
+#pragma unroll
+            for (int k = VLO; k < VMAX; k++) {
+                const double2 vv = P.v[k * TB];
+                const double del = fma(L.nx, vv.x, L.ny * vv.y) - L.r;
+                const double B = fma(n1, (double)P.K[k * TB], c8);
+                out |= (unsigned)(del > B) << k;
+                unc |= (unsigned)(del <= B && del >= -B) << k;
+            }
         }
     }
     // wall vertices (and every vertex when L is a wall): the canonical test (L25); interior
@@ -750,13 +766,24 @@ __global__ void __launch_bounds__(TB, (MODE & M_WCERT) ? TM_WMINB : TM_TMINB) k_
                     const unsigned wallq = W.wall[cq];
                     unsigned hit = 0u, isl = 0u;
 #pragma unroll
-                    for (int k = 0; k < VMAX; k++) {  // all slots, masked: no divergence between rings
+                    for (int k = 0; k < VLO; k++) {  // all slots, masked: no divergence between rings
                         const double2 vv = Pq.v[k * TB];
                         isl |= (unsigned)(Pq.la[k * TB] == jq) << k;
                         const double del = fma(L.nx, vv.x, L.ny * vv.y) - L.r;
                         const bool o = ((wallq >> k) & 1u) ? wall_out(L, vv.x, vv.y)
                                                            : del > -fma(n1, (double)Pq.K[k * TB], c8);
                         hit |= (unsigned)o << k;
+                    }
+                    if (VLO < VMAX && (usedq >> VLO)) {
+#pragma unroll
+                        for (int k = VLO; k < VMAX; k++) {
+                            const double2 vv = Pq.v[k * TB];
+                            isl |= (unsigned)(Pq.la[k * TB] == jq) << k;
+                            const double del = fma(L.nx, vv.x, L.ny * vv.y) - L.r;
+                            const bool o = ((wallq >> k) & 1u) ? wall_out(L, vv.x, vv.y)
+                                                               : del > -fma(n1, (double)Pq.K[k * TB], c8);
+                            hit |= (unsigned)o << k;
+                        }
                     }
                     // cut or undecided, and not a line of the ring (a line already bounding it never cuts)
                     flq = (hit & usedq) && !(isl & usedq);
