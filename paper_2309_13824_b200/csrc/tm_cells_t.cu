@@ -73,6 +73,9 @@ constexpr int TB = TM_TB;
 constexpr int VMAX = TM_VMAX;
 // TM_HISLOT: slots >= VLO are tested only by threads whose ring uses one (slots are handed out
 // lowest-free first, so rings rarely reach them); the masks below make this exactly equivalent
+#ifndef TM_BLOCK_ORDER
+#define TM_BLOCK_ORDER 0
+#endif
 #ifndef TM_HISLOT
 #define TM_HISLOT 0
 #endif
@@ -481,7 +484,14 @@ __global__ void __launch_bounds__(TB, (MODE & M_WCERT) ? TM_WMINB : TM_TMINB) k_
     constexpr bool TSPLIT = split_tris(MODE);
     extern __shared__ __align__(16) unsigned char tsmem[];
     const int tid = threadIdx.x;
-    const int64_t cell = (int64_t)blockIdx.x * TB + tid;
+    // TM_BLOCK_ORDER=1: blocks taken from both ends of the sorted order first (the first and last
+    // bin rows hold the boundary arcs, whose octagon-bounded cells are the slow ones), the middle last
+#if TM_BLOCK_ORDER == 1
+    const unsigned bid = (blockIdx.x & 1u) ? gridDim.x - 1u - (blockIdx.x >> 1) : (blockIdx.x >> 1);
+#else
+    const unsigned bid = blockIdx.x;
+#endif
+    const int64_t cell = (int64_t)bid * TB + tid;
     const int lane = tid & 31;
     TPoly P = tpoly_bind(tsmem, tid);
     bool live = false;
@@ -751,7 +761,7 @@ __global__ void __launch_bounds__(TB, (MODE & M_WCERT) ? TM_WMINB : TM_TMINB) k_
             if (lane < m) {
                 jq = W.qj[lane];
                 cq = W.qc[lane];
-                const unsigned usedq = (int64_t)jq != (int64_t)blockIdx.x * TB + wbase + cq ? W.used[cq] : 0u;
+                const unsigned usedq = (int64_t)jq != (int64_t)bid * TB + wbase + cq ? W.used[cq] : 0u;
                 if (usedq) {
                     dxq = csub(__ldg(A.xs + jq), W.cx[cq]);
                     dyq = csub(__ldg(A.ys + jq), W.cy[cq]);
@@ -810,7 +820,7 @@ __global__ void __launch_bounds__(TB, (MODE & M_WCERT) ? TM_WMINB : TM_TMINB) k_
                     Pc.wall = W.wall[cq];
                     if (Pc.used) {
                         const double roc =
-                            cmul(cmul(A.fac_voro, __ldg(A.hs + (int64_t)blockIdx.x * TB + ct)), COS_PI8);
+                            cmul(cmul(A.fac_voro, __ldg(A.hs + (int64_t)bid * TB + ct)), COS_PI8);
                         const CellGeom gc = {W.cx[cq], W.cy[cq], roc, A.grid.x0, A.grid.y0, A.grid.x1, A.grid.y1};
                         const int fc = clip_t(Pc, jq, bisector(dxq, dyq), gc, A, cs);
                         W.used[cq] = fc ? 0u : Pc.used;  // 0: the cell failed, its code in wall
